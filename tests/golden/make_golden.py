@@ -1,0 +1,221 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+The reference package is imported read-only from /root/reference/pkg/src.  Its
+``runners/scoring.py`` imports a ``runners/buffer.py`` that the reference never
+shipped; we inject a stub module carrying only the two fields
+``lane_scores`` reads (``score_fn``, ``maxmc_discounted``, runners/scoring.py:52,59).
+
+Nothing at test time reads /root/reference: the tests read only the .npz files
+written here.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import types
+from dataclasses import dataclass
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _import_reference():
+    sys.path.insert(0, REF)
+    stub = types.ModuleType("autocurricula.runners.buffer")
+
+    @dataclass
+    class PlrConfig:  # fields read by runners/scoring.py:52,59
+        score_fn: str = "maxmc"
+        maxmc_discounted: bool = False
+
+    stub.PlrConfig = PlrConfig
+    sys.modules["autocurricula.runners.buffer"] = stub
+    import autocurricula  # noqa: F401
+    from autocurricula import amaze, env, rng
+    import importlib
+
+    gae = importlib.import_module("autocurricula.agents.gae")
+    rollout = importlib.import_module("autocurricula.agents.rollout")
+    scoring = importlib.import_module("autocurricula.runners.scoring")
+
+    return types.SimpleNamespace(amaze=amaze, env=env, rng=rng, gae=gae, rollout=rollout,
+                                 scoring=scoring, PlrConfig=PlrConfig)
+
+
+def pack(levels, H, W):
+    """MazeLevel list -> [N, 9] int64 rows: 4 mask words, agent r, c, dir, goal r, c."""
+    rows = []
+    for lv in levels:
+        inner = np.asarray(lv.walls)[1:-1, 1:-1].reshape(-1).astype(np.uint64)
+        bits = np.zeros(128, dtype=np.uint64)
+        bits[: inner.size] = inner
+        words = [int((bits[32 * k: 32 * k + 32] << np.arange(32, dtype=np.uint64)).sum()) for k in range(4)]
+        rows.append(words + [lv.agent_pos[0], lv.agent_pos[1], lv.agent_dir, lv.goal_pos[0], lv.goal_pos[1]])
+    return np.array(rows, dtype=np.int64)
+
+
+def gen_levels(R):
+    out = {}
+    cases = [  # (name, H, W, budget, seed, n)
+        ("default", 13, 13, 60, 0, 600),
+        ("seed12345", 13, 13, 60, 12345, 200),
+        ("budget0", 13, 13, 0, 3, 100),
+        ("budget1", 13, 13, 1, 4, 100),
+        ("budget119", 13, 13, 119, 5, 200),
+        ("small9", 9, 9, 25, 6, 200),
+    ]
+    for name, H, W, budget, seed, n in cases:
+        P = R.env.StaticParams(height=H, width=W, wall_budget=budget)
+        root = R.rng.RngStream.from_seed(seed)
+        # lane keys (seed, (0, i)) -- the VectorBatchEnv.reset lane streams
+        levels = [R.amaze.sample_random_level(k, P) for k in root.fold_in(0).split(n)]
+        out[f"lv_{name}"] = pack(levels, H, W)
+        out[f"lv_{name}_meta"] = np.array([H, W, budget, seed, n], dtype=np.int64)
+        # mutation keys (seed, (7, i)); 20 edits and 1 edit
+        for ne in (1, 20):
+            muts = [R.amaze.mutate_level(root.fold_in(7).fold_in(i), lv, ne, P) for i, lv in enumerate(levels)]
+            out[f"mut{ne}_{name}"] = pack(muts, H, W)
+    # large seeds exercise the multi-word entropy path
+    P = R.env.StaticParams()
+    root = R.rng.RngStream.from_seed(2**40 + 17)
+    levels = [R.amaze.sample_random_level(k, P) for k in root.fold_in(0).split(100)]
+    out["lv_bigseed"] = pack(levels, 13, 13)
+    out["lv_bigseed_meta"] = np.array([13, 13, 60, 2**40 + 17, 100], dtype=np.int64)
+    return out
+
+
+def gen_rollout(R, name, shape, mode, T, seed, act_seed, see_through=True, levels_from=None):
+    P = R.env.StaticParams(see_through_walls=see_through)
+    menv = R.amaze.MazeEnv()
+    benv = R.env.batch_lift(menv, R.env.BatchShape(*shape))
+    wrap = R.env.AutoResetWrapper(benv, mode)
+    root = R.rng.RngStream.from_seed(seed)
+    if levels_from is None:
+        res = wrap.reset(root, P)
+    else:
+        res = wrap.reset_to_levels(root, levels_from, P)
+    B = int(np.prod(shape))
+    flat = R.rollout.flatten_obs
+    acts = np.stack([R.rng.RngStream.from_seed(act_seed).fold_in(t).generator().integers(0, 3, size=B)
+                     for t in range(T)])
+    obs = flat(res.observation)
+    o = {f"{name}_view0": obs["view"], f"{name}_dir0": obs["dir"]}
+    views, dirs, rews, dones, solved, times = [], [], [], [], [], []
+    state, extras = res.state, res.extras
+    for t in range(T):
+        r = wrap.step(None, state, acts[t].reshape(shape[0], -1), P, extras)
+        ob = flat(r.observation)
+        views.append(ob["view"]); dirs.append(ob["dir"])
+        rews.append(r.reward.reshape(-1)); dones.append(r.done.reshape(-1))
+        solved.append(r.info["solved"].reshape(-1)); times.append(r.info["time"].reshape(-1))
+        state, extras = r.state, r.extras
+    o.update({
+        f"{name}_actions": acts.astype(np.uint8),
+        f"{name}_view": np.stack(views), f"{name}_dir": np.stack(dirs).astype(np.uint8),
+        f"{name}_reward": np.stack(rews), f"{name}_done": np.stack(dones),
+        f"{name}_solved": np.stack(solved), f"{name}_time": np.stack(times).astype(np.int32),
+        f"{name}_meta": np.array([shape[0], shape[1], shape[2], T, seed, act_seed,
+                                  int(mode == "home"), int(see_through)], dtype=np.int64),
+        f"{name}_final_levels": pack(benv.lane_levels(state), 13, 13),
+    })
+    return o
+
+
+def gen_scores(R):
+    rng = np.random.default_rng(0)
+    T, B = 256, 96
+    V = rng.uniform(0.0, 1.0, (T, B))
+    d = rng.uniform(size=(T, B)) < 1.0 / 40
+    r = np.where(d & (rng.uniform(size=(T, B)) < 0.5), 1.0 - 0.9 * rng.integers(1, 251, (T, B)) / 250, 0.0)
+    # a few lanes with nonzero rewards off done steps (generic GAE inputs)
+    r[:, :8] += rng.normal(0, 0.1, (T, 8))
+    last = rng.uniform(0, 1, B)
+    prior = np.where(rng.uniform(size=B) < 0.5, rng.uniform(0, 1, B), 0.0)
+    out = {"sc_r": r, "sc_v": V, "sc_d": d, "sc_last": last, "sc_prior": prior}
+    for tag, g, lam in (("a", 0.999, 0.98), ("b", 0.995, 0.95), ("c", 1.0, 1.0)):
+        adv, ret = R.gae.compute_gae(r, V, d, last, g, lam)
+        out[f"sc_{tag}_adv"], out[f"sc_{tag}_ret"] = adv, ret
+        out[f"sc_{tag}_gl"] = np.array([g, lam])
+        tb = R.rollout.TrajectoryBatch({}, np.zeros((T, B), np.int64), np.zeros((T, B)), V, r, d,
+                                       np.zeros((T, B, 1)))
+        for fn in ("maxmc", "pvl"):
+            for disc in (False, True):
+                cfg = R.PlrConfig(score_fn=fn, maxmc_discounted=disc)
+                s, m = R.scoring.lane_scores(tb, adv, prior, cfg, gamma=g)
+                out[f"sc_{tag}_{fn}_{int(disc)}_score"], out[f"sc_{tag}_{fn}_{int(disc)}_maxret"] = s, m
+        st = R.rollout.per_lane_episode_stats(r, d, gamma=g)
+        for k, v in st.items():
+            out[f"sc_{tag}_stats_{k}"] = v
+    # SPEC known answers (runners/scoring.py)
+    out["ka_pvl"] = np.array([R.scoring.score_pvl(np.array([0.5, -0.2, 0.3]))])
+    out["ka_maxmc"] = np.array([R.scoring.score_maxmc(np.full(7, 0.2), 1.0)])
+    return out
+
+
+def gen_assets(R):
+    names = R.amaze.asset_names()
+    levels = [R.amaze.load_asset(n) for n in names]
+    out = {"asset_levels": pack(levels, 13, 13),
+           "asset_names": np.array(names)}
+    for st in (True, False):
+        P = R.env.StaticParams(see_through_walls=st)
+        obs = [R.amaze.observe(R.amaze.EnvState.from_level(lv), P) for lv in levels]
+        out[f"asset_view_st{int(st)}"] = np.stack([o.view for o in obs])
+    return out
+
+
+def gen_states(R):
+    """Random (level, pose) states observed with and without occlusion (scalar path)."""
+    rng = np.random.default_rng(1)
+    P = R.env.StaticParams()
+    root = R.rng.RngStream.from_seed(99)
+    levels = [R.amaze.sample_random_level(k, P) for k in root.split(400)]
+    poses = []
+    out = {}
+    for st in (True, False):
+        P2 = R.env.StaticParams(see_through_walls=st)
+        views = []
+        for i, lv in enumerate(levels):
+            if st:
+                free = np.argwhere(~lv.walls)
+                rc = free[rng.integers(len(free))]
+                poses.append([rc[0], rc[1], rng.integers(4)])
+            pr, pc, pd = poses[i]
+            s = R.amaze.EnvState(lv, (int(pr), int(pc)), int(pd), 0, False)
+            views.append(R.amaze.observe(s, P2).view)
+        out[f"st_view_st{int(st)}"] = np.stack(views)
+    out["st_levels"] = pack(levels, 13, 13)
+    out["st_poses"] = np.array(poses, dtype=np.int64)
+    return out
+
+
+def main():
+    R = _import_reference()
+    fx = {}
+    fx.update(gen_levels(R))
+    np.savez_compressed(os.path.join(OUT, "levels.npz"), **fx)
+    ro = {}
+    ro.update(gen_rollout(R, "cfg1", (1, 1, 32), "resample", 256, 0, 1))
+    ro.update(gen_rollout(R, "hier", (2, 3, 4), "resample", 300, 7, 8))
+    ro.update(gen_rollout(R, "occl", (1, 1, 48), "resample", 260, 11, 12, see_through=False))
+    assets = [R.amaze.load_asset(n) for n in R.amaze.asset_names()]
+    ro.update(gen_rollout(R, "home", (1, 2, 10), "home", 300, 5, 6, levels_from=assets))
+    np.savez_compressed(os.path.join(OUT, "rollouts.npz"), **ro)
+    np.savez_compressed(os.path.join(OUT, "scores.npz"), **gen_scores(R))
+    misc = {}
+    misc.update(gen_assets(R))
+    misc.update(gen_states(R))
+    np.savez_compressed(os.path.join(OUT, "views.npz"), **misc)
+    for f in ("levels", "rollouts", "scores", "views"):
+        print(f, os.path.getsize(os.path.join(OUT, f + ".npz")))
+
+
+if __name__ == "__main__":
+    main()
