@@ -1,0 +1,409 @@
+"""Benchmark of the AMaze + PLR hot path (BASELINE.json configs[1] by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one pass of the hot path over one batch of synthetic input (config 2,
+"AMaze 13x13 DR with PPO rollout batch 4096 envs x 256 steps and GAE on 1xB200"):
+  1. DR level generation for every lane (keys (seed, (0, lane))),
+  2. reset_to_levels of every lane,
+  3. 256 fused env steps with RESAMPLE auto-reset driven by a uint8 [T, B] action
+     stream resident in HBM (the policy is out of scope; its values are a resident
+     float64 [T, B] tensor),
+  4. GAE (gamma 0.995, lambda 0.95) + MaxMC regret scores + running max returns.
+metric = env-steps/s = lanes * T / step time (whole job, all ranks).
+
+Under torchrun each rank runs its own lane shard (global lane ids rank*B + i, so the
+keys equal a 1-GPU run over N*B lanes): weak scaling, no data-path collective.
+
+--impl reference times the oracle port of the reference (oracle/amaze_np.py, numpy,
+lane-sharded over all host cores; the reference itself is pure Python and cannot be
+installed on the GPU box) on the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+ENV_BYTES_PER_STEP = 36  # action u8 + view 25 u8 + dir u8 + reward f64 + done u8
+GAE_BYTES_PER_ELEM = 33  # r f64 + V f64 + done u8 in, A f64 + R f64 out
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------------------------
+# CPU reference (oracle port), lane-sharded over processes
+# ------------------------------------------------------------------------------------
+def _cpu_shard(args):
+    lane0, n, T, seed, act_seed, gamma, lam = args
+    import numpy as np
+
+    from oracle import amaze_np as onp
+
+    p = onp.Params()
+    env = onp.AutoReset(n, p, "resample", lane_offset=lane0)
+    t0 = time.perf_counter()
+    obs = env.reset(seed)
+    rng = np.random.default_rng(act_seed + lane0)
+    acts = rng.integers(0, 3, (T, n)).astype(np.uint8)
+    values = rng.uniform(0, 1, (T, n))
+    view, dirs, rew, dn, fobs = onp.rollout(env, obs, acts)
+    adv, ret = onp.gae(rew, values, dn, values[-1], gamma, lam)
+    sc, mx, _ = onp.lane_scores(values, adv, rew, dn, np.zeros(n))
+    return time.perf_counter() - t0
+
+
+def cpu_reference_step(B, T, seed, workers, pool):
+    """One full step of the workload on the host: returns wall seconds."""
+    shards = []
+    per = (B + workers - 1) // workers
+    for w in range(workers):
+        lo = w * per
+        n = min(per, B - lo)
+        if n > 0:
+            shards.append((lo, n, T, seed, 17, 0.995, 0.95))
+    t0 = time.perf_counter()
+    if pool is None:
+        for s in shards:
+            _cpu_shard(s)
+    else:
+        pool.map(_cpu_shard, shards)
+    return time.perf_counter() - t0
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------------------------
+# clocks sampler
+# ------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+        self.active = False
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            if self.active:
+                self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx = float(s[1])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, s[2:6]):
+                if v.lower() in ("active", "yes", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------
+# GPU workload
+# ------------------------------------------------------------------------------------
+class Workload:
+    """Config 2 on one device: DR reset + fused T-step rollout + GAE/MaxMC."""
+
+    def __init__(self, B, T, seed, lane_offset, device):
+        import torch
+
+        import paper_2311_12716_b200 as amz
+
+        self.amz, self.torch = amz, torch
+        self.B, self.T, self.seed, self.dev = B, T, seed, device
+        self.p = amz.StaticParams()
+        self.benv = amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B), device=device,
+                                       lane_offset=lane_offset)
+        self.env = amz.AutoResetWrapper(self.benv, amz.RESAMPLE)
+        self.lane_offset = lane_offset
+        g = torch.Generator(device=device)
+        g.manual_seed(1234 + lane_offset)
+        self.actions = torch.randint(0, 3, (T, B), generator=g, device=device, dtype=torch.uint8)
+        self.values = torch.rand((T, B), generator=g, device=device, dtype=torch.float64)
+        self.last = torch.rand((B,), generator=g, device=device, dtype=torch.float64)
+        v = self.p.agent_view_size
+        self.out = {"view": torch.empty((T, B, v, v), dtype=torch.uint8, device=device),
+                    "dir": torch.empty((T, B), dtype=torch.uint8, device=device),
+                    "rewards": torch.empty((T, B), dtype=torch.float64, device=device),
+                    "dones": torch.empty((T, B), dtype=torch.bool, device=device),
+                    "final_view": torch.empty((B, v, v), dtype=torch.uint8, device=device),
+                    "final_dir": torch.empty((B,), dtype=torch.uint8, device=device)}
+        self.root = amz.RngStream.from_seed(seed)
+        self.launches_per_step = 4  # sample_levels, env_reset, env_rollout, gae_score
+        self.ev_roll = None
+
+    def step(self, it, actions=None, values=None, last=None, timing=None):
+        amz, torch = self.amz, self.torch
+        rng = self.root.fold_in(it)
+        rng_env, rng_wrap = rng.split(2)
+        levels = amz.sample_levels(rng_env, self.B, self.p, lane0=self.lane_offset, device=self.dev)
+        res = self.benv.reset_to_levels(None, levels, self.p)
+        res = self.env._attach(res, rng_wrap)
+        if timing is not None:
+            timing[0].record()
+        traj, cur = amz.rollout_actions(self.env, res, self.actions if actions is None else actions, self.p,
+                                        out=self.out)
+        if timing is not None:
+            timing[1].record()
+        o = amz.gae_and_scores(traj.rewards, self.values if values is None else values, traj.dones,
+                               self.last if last is None else last, 0.995, 0.95)
+        if timing is not None:
+            timing[2].record()
+        return o
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B, T = args.lanes, args.T
+    wl = Workload(B, T, args.seed, rank * B, dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for i in range(args.warmup):
+        wl.step(i)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    clocks.active = True
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record()
+        wl.step(args.warmup + i, timing=kev[i])
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks.active = False
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    roll_ms = [k[0].elapsed_time(k[1]) for k in kev]
+    gae_ms = [k[1].elapsed_time(k[2]) for k in kev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(t.item())
+
+    # ---- e2e through the public API: pinned host inputs in, scores out ----
+    h_act = torch.empty((T, B), dtype=torch.uint8, pin_memory=True)
+    h_act.copy_(wl.actions.cpu())
+    h_val = torch.empty((T, B), dtype=torch.float64, pin_memory=True)
+    h_val.copy_(wl.values.cpu())
+    h_last = torch.empty((B,), dtype=torch.float64, pin_memory=True)
+    h_last.copy_(wl.last.cpu())
+    h_sc = torch.empty((B,), dtype=torch.float64, pin_memory=True)
+    h_mx = torch.empty((B,), dtype=torch.float64, pin_memory=True)
+    d_act = torch.empty_like(wl.actions)
+    d_val = torch.empty_like(wl.values)
+    d_last = torch.empty_like(wl.last)
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        e2e_ev[i][0].record()
+        d_act.copy_(h_act, non_blocking=True)
+        d_val.copy_(h_val, non_blocking=True)
+        d_last.copy_(h_last, non_blocking=True)
+        o = wl.step(10_000 + i, actions=d_act, values=d_val, last=d_last)
+        h_sc.copy_(o["scores"], non_blocking=True)
+        h_mx.copy_(o["max_returns"], non_blocking=True)
+        e2e_ev[i][1].record()
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    clocks.stop()
+    csum = clocks.summary()
+
+    if rank != 0:
+        return None
+    peaks, src = _peaks()
+    units = B * T * world
+    roll = statistics.mean(roll_ms)
+    gae = statistics.mean(gae_ms)
+    roll_gbs = ENV_BYTES_PER_STEP * B * T / (roll * 1e-3) / 1e9
+    gae_gbs = GAE_BYTES_PER_ELEM * B * T / (gae * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    line = {
+        "metric": "AMaze env steps/sec (DR reset + 256-step RESAMPLE rollout + GAE/MaxMC)",
+        "value": units / (total_ms * 1e-3 / args.steps),
+        "unit": "env-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8/int32 env, f64 GAE",
+        "data": "synthetic: DR levels from (seed, lane) keys, uniform random actions and values resident in HBM",
+        "config": {"workload": "configs[1]: AMaze 13x13 DR, 4096 envs x 256 steps, RESAMPLE auto-reset, GAE+MaxMC",
+                   "lanes_per_gpu": B, "T": T, "gamma": 0.995, "lambda": 0.95, "l2": "flushed (256 MB write) "
+                   "before every timed step", "parallelism": f"lane-sharded x{world}"},
+        "e2e": {"value": units / (e2e_ms * 1e-3 / args.steps), "unit": "env-steps/s",
+                "h2d_bytes_per_step": T * B * (1 + 8) + B * 8, "d2h_bytes_per_step": 2 * B * 8},
+        "gpu_launches": wl.launches_per_step * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": roll_gbs / peak, "traffic": None, "peak_source": src,
+                     "algorithmic_bytes": f"{ENV_BYTES_PER_STEP} B/env-step x {B * T} env-steps per launch",
+                     "kernel_ms": roll},
+        "kernels": {"k_env_rollout_ms": roll, "k_gae_score_ms": gae, "k_gae_score_GBs": gae_gbs,
+                    "k_gae_score_frac": gae_gbs / peak,
+                    "levels_scored_per_s": B * world / (gae * 1e-3)},
+        "clocks": {k: csum[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = measure_cpu_baseline(args)
+    return line
+
+
+def measure_cpu_baseline(args, steps=1):
+    import multiprocessing as mp
+
+    cores = _cores()
+    B, T = args.lanes, args.T
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        secs = [cpu_reference_step(B, T, args.seed, cores, pool) for _ in range(steps)]
+    s = statistics.mean(secs)
+    return {"value": B * T / s, "unit": "env-steps/s", "cores": cores, "kind": "port",
+            "sample": f"one full step ({B} lanes x {T} steps DR reset + rollout + GAE/MaxMC) with the numpy oracle "
+                      f"port, lanes sharded over {cores} processes; host: {_cpu_model()}"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import multiprocessing as mp
+
+    cores = _cores()
+    B, T = args.lanes, args.T
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            cpu_reference_step(B, T, args.seed, cores, pool)
+        secs = [cpu_reference_step(B, T, args.seed, cores, pool) for _ in range(args.steps)]
+    s = statistics.mean(secs)
+    val = B * T / s
+    return {
+        "impl": "reference",
+        "metric": "AMaze env steps/sec (DR reset + 256-step RESAMPLE rollout + GAE/MaxMC)",
+        "value": val, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64 env, f64 GAE", "data": "synthetic (same workload, numpy random actions/values)",
+        "config": {"workload": "configs[1]: AMaze 13x13 DR, 4096 envs x 256 steps, RESAMPLE auto-reset, GAE+MaxMC",
+                   "lanes": B, "T": T},
+        "cpu_baseline": {"value": val, "unit": "env-steps/s", "cores": cores, "kind": "port",
+                         "sample": f"full config-2 step per timed step, numpy oracle port of the reference, "
+                                   f"lanes sharded over {cores} processes; host: {_cpu_model()}"},
+        "e2e": {"value": val, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--lanes", type=int, default=4096)
+    ap.add_argument("--T", type=int, default=256)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        import torch
+
+        if world > 1:
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl")
+        line = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

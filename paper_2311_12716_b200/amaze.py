@@ -1,0 +1,149 @@
+"""DR level generation, ACCEL mutation and the maze-env marker object, on the GPU.
+
+Drop-in for ``amaze/generator.py:36-84`` (``sample_random_level``, ``mutate_level``)
+and the lane-protocol parts of ``amaze/env.py:163-234`` (``MazeEnv``).  Batched entry
+points take a parent ``RngStream`` and give level i the key ``parent.key + (lane0 + i,)``
+-- the same keys ``VectorBatchEnv.reset`` (``env/batch.py:43-44,86-89``) and the
+auto-reset wrapper (``env/wrappers.py:64-67``) derive -- so every level is bit-identical
+to the reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .core import StaticParams, as_params
+from .errors import ContractViolation, LevelError
+from .level import MazeLevel, pack_levels, records_to_tensor, tensor_to_records, unpack_levels
+from .rng import RngStream, as_stream
+
+N_ACTIONS = 3  # TURN_LEFT, TURN_RIGHT, FORWARD (amaze/env.py:23-26)
+TILE_EMPTY, TILE_WALL, TILE_GOAL, TILE_OOB = 0, 1, 2, 3
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _split_key(rng: RngStream):
+    """A stream's own key as (prefix stream, last word) for single-level calls."""
+    if not rng.key:
+        raise ContractViolation("single-level generation needs a non-empty stream key "
+                                "(use split/fold_in, as the batched env does)")
+    return RngStream(rng.entropy, rng.key[:-1]), rng.key[-1]
+
+
+def sample_levels(rng, n: int, params: StaticParams, lane0: int = 0, lane_ids=None, device=None):
+    """Levels for keys rng.key + (lane0 + i,) (or + (lane_ids[i],)) -> int32 [n, 8] on device."""
+    torch = _torch()
+    p = as_params(params).validate()
+    rng = as_stream(rng)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty((n, 8), dtype=torch.int32, device=dev)
+    ids = None
+    if lane_ids is not None:
+        ids = torch.as_tensor(lane_ids, device=dev).to(torch.int32).contiguous()
+        if ids.numel() != n:
+            raise ContractViolation("lane_ids must have n entries")
+    seed = rng.seed_prefix()
+    _lib.call("amz_sample_levels", ctypes.byref(p.c_struct()), ctypes.byref(seed), ctypes.c_uint32(lane0),
+              _lib.ptr(ids), n, _lib.ptr(out), _lib.stream_handle(dev))
+    return out
+
+
+def mutate_levels(rng, parents, n_edits: int, params: StaticParams, lane0: int = 0, parent_idx=None, n=None):
+    """ACCEL edits: out[i] = mutate(parents[parent_idx[i]] or parents[i], key rng.key + (lane0+i,))."""
+    torch = _torch()
+    p = as_params(params).validate()
+    rng = as_stream(rng)
+    if n_edits < 1:
+        raise ContractViolation(f"n_mutations must be >= 1, got {n_edits}")
+    idx = None
+    if parent_idx is not None:
+        idx = torch.as_tensor(parent_idx, device=parents.device).to(torch.int32).contiguous()
+        n = idx.numel()
+    elif n is None:
+        n = parents.shape[0]
+    out = torch.empty((n, 8), dtype=torch.int32, device=parents.device)
+    seed = rng.seed_prefix()
+    _lib.call("amz_mutate_levels", ctypes.byref(p.c_struct()), ctypes.byref(seed), ctypes.c_uint32(lane0), n,
+              _lib.ptr(parents.contiguous()), _lib.ptr(idx), int(n_edits), _lib.ptr(out),
+              _lib.stream_handle(parents.device))
+    return out
+
+
+def check_levels(levels, params: StaticParams) -> None:
+    """Raise LevelError if any packed level breaks MazeLevel invariants (synchronous)."""
+    p = as_params(params).validate()
+    bad = ctypes.c_int64(-1)
+    _lib.call("amz_check_levels", ctypes.byref(p.c_struct()), _lib.ptr(levels.contiguous()), levels.shape[0],
+              ctypes.byref(bad), _lib.stream_handle(levels.device))
+    if bad.value >= 0:
+        raise LevelError(f"level {bad.value} violates the MazeLevel invariants")
+
+
+def to_device_levels(levels, params: StaticParams, device=None):
+    """MazeLevel-like list (ours or the reference's) or an int32 [N, 8] tensor -> device tensor."""
+    torch = _torch()
+    if isinstance(levels, torch.Tensor):
+        return levels.to(device or levels.device).to(torch.int32).contiguous()
+    ml = [MazeLevel.from_any(lv).validate() for lv in levels]
+    p = as_params(params)
+    return records_to_tensor(pack_levels(ml, p.height, p.width), device or "cuda")
+
+
+def to_host_levels(levels, params: StaticParams) -> list:
+    p = as_params(params)
+    return unpack_levels(tensor_to_records(levels), p.height, p.width)
+
+
+def sample_random_level(rng, params: StaticParams) -> MazeLevel:
+    """Drop-in for amaze/generator.py:36-52 (one level; synchronous)."""
+    parent, last = _split_key(as_stream(rng))
+    return to_host_levels(sample_levels(parent, 1, params, lane0=last), params)[0]
+
+
+def mutate_level(rng, level, n_mutations: int, params: StaticParams) -> MazeLevel:
+    """Drop-in for amaze/generator.py:55-84 (one level; synchronous)."""
+    if n_mutations < 1:
+        raise ContractViolation(f"n_mutations must be >= 1, got {n_mutations}")
+    parent, last = _split_key(as_stream(rng))
+    par = to_device_levels([level], params)
+    return to_host_levels(mutate_levels(parent, par, n_mutations, params, lane0=last), params)[0]
+
+
+class MazeEnv:
+    """The vector-lane maze environment (amaze/env.py:163-234).  Stepping happens in
+    ``batch.VectorBatchEnv``; this object carries the static facts the batching layer
+    and callers query."""
+
+    step_uses_rng = False
+
+    def action_count(self, params=None) -> int:
+        return N_ACTIONS
+
+    def observation_spec(self, params) -> dict:
+        v = as_params(params).agent_view_size
+        return {"view": ((v, v), 4), "dir": ((), 4)}
+
+    def sample_level(self, rng, params) -> MazeLevel:
+        return sample_random_level(rng, params)
+
+    # make_batch/step_batch presence lets batch_lift pick the vector path
+    def make_batch(self, levels):  # pragma: no cover - protocol marker
+        raise NotImplementedError("use batch.VectorBatchEnv")
+
+    def step_batch(self, *a, **k):  # pragma: no cover - protocol marker
+        raise NotImplementedError("use batch.VectorBatchEnv")
+
+
+def levels_equal(a, b) -> bool:
+    """Exact equality of two packed level tensors (walls + pose bytes)."""
+    ra, rb = tensor_to_records(a), tensor_to_records(b)
+    fields = ("walls", "agent_r", "agent_c", "agent_dir", "goal_r", "goal_c")
+    return all(np.array_equal(ra[f], rb[f]) for f in fields)

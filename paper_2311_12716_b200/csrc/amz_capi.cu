@@ -1,0 +1,278 @@
+// amz_capi.cu -- extern "C" entry points of libamaze_b200.so (include/amaze_b200.h).
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+
+#include "amz_internal.h"
+
+using namespace amz;
+
+static thread_local char g_err[512];
+
+static int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+static int cuda_status(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(AMZ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return 0;
+}
+
+#define AMZ_CHECK_CUDA(call, what)                                                      \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) return fail(AMZ_ECUDA, "%s: %s", what, cudaGetErrorString(e_)); \
+    } while (0)
+
+struct amz_env {
+    amz_params_t p;
+    Geo G;
+    EnvDev E;
+    int *term;  // [2] terminal-lane counters (mode NONE)
+    int parity;
+};
+
+extern "C" {
+
+int amz_abi_version(void) { return AMZ_ABI_VERSION; }
+
+const char *amz_last_error(void) { return g_err; }
+
+int amz_validate_params(const amz_params_t *p) {
+    if (!p) return fail(AMZ_ECONFIG, "null params");
+    // StaticParams.validate (env/core.py:35-48)
+    if (p->height < 3 || p->width < 3)
+        return fail(AMZ_ECONFIG, "grid must be at least 3x3, got %dx%d", p->height, p->width);
+    if (p->agent_view_size < 3 || p->agent_view_size % 2 == 0)
+        return fail(AMZ_ECONFIG, "agent_view_size must be odd and >= 3, got %d", p->agent_view_size);
+    if (p->max_episode_steps < 1)
+        return fail(AMZ_ECONFIG, "max_episode_steps must be >= 1, got %d", p->max_episode_steps);
+    const int max_walls = (p->height - 2) * (p->width - 2) - 2;
+    if (p->wall_budget < 0 || p->wall_budget > max_walls)
+        return fail(AMZ_ECONFIG, "wall_budget must be in [0, %d] for a %dx%d grid, got %d", max_walls, p->height,
+                    p->width, p->wall_budget);
+    // limits of this implementation
+    if (p->height > 16 || p->width > 16 || (p->height - 2) * (p->width - 2) > 128)
+        return fail(AMZ_ECONFIG, "grid %dx%d exceeds the 16x16 / 128-interior-cell limit", p->height, p->width);
+    if (p->agent_view_size > 9) return fail(AMZ_ECONFIG, "agent_view_size %d > 9 unsupported", p->agent_view_size);
+    if (p->max_episode_steps > 65535)
+        return fail(AMZ_ECONFIG, "max_episode_steps %d > 65535 unsupported", p->max_episode_steps);
+    return 0;
+}
+
+int amz_seed_prefix(const uint32_t *run, int n_run, const uint32_t *key, int n_key, amz_seed_t *out) {
+    if (!out || n_run < 1 || (n_key > 0 && !key) || !run) return fail(AMZ_ECONFIG, "bad seed prefix arguments");
+    seed_prefix_host(run, n_run, key, n_key, *out);
+    return 0;
+}
+
+int amz_sample_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t lane0, const uint32_t *lane_ids,
+                      int64_t n, amz_level_t *out, void *stream) {
+    int rc = amz_validate_params(p);
+    if (rc) return rc;
+    if (!prefix || (n > 0 && !out)) return fail(AMZ_ECONFIG, "null argument");
+    rc = launch_sample_levels(make_geo(*p), *prefix, lane0, lane_ids, n, out, (cudaStream_t)stream);
+    return rc ? rc : cuda_status("sample_levels");
+}
+
+int amz_mutate_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t lane0, int64_t n,
+                      const amz_level_t *parents, const int32_t *pidx, int n_edits, amz_level_t *out, void *stream) {
+    int rc = amz_validate_params(p);
+    if (rc) return rc;
+    if (n_edits < 1) return fail(AMZ_ECONTRACT, "n_mutations must be >= 1, got %d", n_edits);
+    if (!prefix || (n > 0 && (!out || !parents))) return fail(AMZ_ECONFIG, "null argument");
+    rc = launch_mutate_levels(make_geo(*p), *prefix, lane0, n, parents, pidx, n_edits, out, (cudaStream_t)stream);
+    return rc ? rc : cuda_status("mutate_levels");
+}
+
+int amz_check_levels(const amz_params_t *p, const amz_level_t *lv, int64_t n, int64_t *bad, void *stream) {
+    int rc = amz_validate_params(p);
+    if (rc) return rc;
+    if (!bad) return fail(AMZ_ECONFIG, "null argument");
+    *bad = -1;
+    if (n <= 0) return 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *d = nullptr, h = ~0ull;
+    AMZ_CHECK_CUDA(cudaMallocAsync((void **)&d, sizeof(h), s), "check_levels alloc");
+    cudaMemcpyAsync(d, &h, sizeof(h), cudaMemcpyHostToDevice, s);
+    launch_check_levels(make_geo(*p), lv, n, d, s);
+    cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    AMZ_CHECK_CUDA(cudaStreamSynchronize(s), "check_levels");
+    *bad = h == ~0ull ? -1 : (int64_t)h;
+    return 0;
+}
+
+int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
+    int rc = amz_validate_params(p);
+    if (rc) return rc;
+    if (!out || n_lanes < 1) return fail(AMZ_ESHAPE, "n_lanes must be >= 1, got %lld", (long long)n_lanes);
+    amz_env *e = new (std::nothrow) amz_env();
+    if (!e) return fail(AMZ_EFAULT, "out of host memory");
+    e->p = *p;
+    e->G = make_geo(*p);
+    e->E.B = n_lanes;
+    e->E.lane_offset = 0;
+    e->parity = 0;
+    size_t b = (size_t)n_lanes;
+    cudaError_t err = cudaMalloc((void **)&e->E.st, b * sizeof(uint4));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.mask, b * sizeof(uint4));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.board, b * 16 * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.err, 4 * sizeof(int));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->term, 2 * sizeof(int));
+    if (err == cudaSuccess) err = cudaMemset(e->E.err, 0, 4 * sizeof(int));
+    if (err == cudaSuccess) err = cudaMemset(e->term, 0, 2 * sizeof(int));
+    if (err == cudaSuccess) err = cudaMemset(e->E.st, 0, b * sizeof(uint4));
+    if (err == cudaSuccess) err = cudaDeviceSynchronize();
+    if (err != cudaSuccess) {
+        amz_env_destroy(e);
+        return fail(AMZ_ECUDA, "env alloc: %s", cudaGetErrorString(err));
+    }
+    *out = e;
+    return 0;
+}
+
+int amz_env_destroy(amz_env_t *e) {
+    if (!e) return 0;
+    cudaFree(e->E.st);
+    cudaFree(e->E.mask);
+    cudaFree(e->E.board);
+    cudaFree(e->E.err);
+    cudaFree(e->term);
+    delete e;
+    return 0;
+}
+
+int64_t amz_env_lanes(const amz_env_t *e) { return e ? e->E.B : -1; }
+
+int amz_env_set_lane_offset(amz_env_t *e, uint32_t offset) {
+    if (!e) return fail(AMZ_ECONFIG, "null env");
+    e->E.lane_offset = offset;
+    return 0;
+}
+
+int amz_env_reset_to_levels(amz_env_t *e, const amz_level_t *lv, const int64_t *lanes, int64_t n, uint8_t *view,
+                            int64_t *dirs, void *stream) {
+    if (!e || !lv) return fail(AMZ_ECONFIG, "null argument");
+    if (!lanes && n != e->E.B) return fail(AMZ_ESHAPE, "expected %lld levels, got %lld", (long long)e->E.B, (long long)n);
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = launch_env_reset(e->G, e->E, lv, lanes, n, view, dirs, s);
+    if (rc) return fail(rc, "reset: unsupported agent_view_size");
+    if (!lanes) cudaMemsetAsync(e->term, 0, 2 * sizeof(int), s);
+    return cuda_status("env_reset");
+}
+
+int amz_env_step(amz_env_t *e, const void *actions, int adtype, int mode, const amz_seed_t *wrap, uint32_t step_idx,
+                 uint8_t *view, int64_t *dirs, double *reward, uint8_t *done, double *solved, int64_t *times,
+                 void *stream) {
+    if (!e || !actions) return fail(AMZ_ECONFIG, "null argument");
+    if (adtype < 0 || adtype > 2) return fail(AMZ_ECONTRACT, "bad action dtype code %d", adtype);
+    if (mode < AMZ_RESET_NONE || mode > AMZ_RESET_HOME) return fail(AMZ_ECONTRACT, "unknown auto-reset mode %d", mode);
+    if (mode == AMZ_RESET_RESAMPLE && !wrap) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
+    cudaStream_t s = (cudaStream_t)stream;
+    amz_seed_t w = wrap ? *wrap : amz_seed_t{};
+    int *tin = e->term + e->parity, *tout = e->term + (e->parity ^ 1);
+    if (mode == AMZ_RESET_NONE) {
+        cudaMemsetAsync(tout, 0, sizeof(int), s);
+        e->parity ^= 1;
+    }
+    int rc = launch_env_step(e->G, e->E, actions, adtype, mode, w, step_idx, view, dirs, reward, done, solved, times,
+                             tin, tout, s);
+    if (rc) return fail(rc, "step: unsupported agent_view_size");
+    return cuda_status("env_step");
+}
+
+int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const amz_seed_t *wrap, uint32_t step0,
+                    uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done, uint8_t *fview, uint8_t *fdir,
+                    void *stream) {
+    if (!e || !actions || !view || !dirs || !reward || !done) return fail(AMZ_ECONFIG, "null argument");
+    if (T < 1) return fail(AMZ_ECONTRACT, "rollout length must be >= 1, got %d", T);
+    if (mode != AMZ_RESET_RESAMPLE && mode != AMZ_RESET_HOME)
+        return fail(AMZ_ECONTRACT, "rollout needs an auto-resetting env (mode %d)", mode);
+    if (mode == AMZ_RESET_RESAMPLE && !wrap) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
+    amz_seed_t w = wrap ? *wrap : amz_seed_t{};
+    int rc = launch_env_rollout(e->G, e->E, T, actions, mode, w, step0, view, dirs, reward, done, fview, fdir,
+                                (cudaStream_t)stream);
+    if (rc) return fail(rc, "rollout: unsupported agent_view_size");
+    return cuda_status("env_rollout");
+}
+
+int amz_env_observe(amz_env_t *e, uint8_t *view, int64_t *dirs, void *stream) {
+    if (!e) return fail(AMZ_ECONFIG, "null env");
+    int rc = launch_env_observe(e->G, e->E, view, dirs, (cudaStream_t)stream);
+    if (rc) return fail(rc, "observe: unsupported agent_view_size");
+    return cuda_status("env_observe");
+}
+
+int amz_env_levels(amz_env_t *e, amz_level_t *out, void *stream) {
+    if (!e || !out) return fail(AMZ_ECONFIG, "null argument");
+    launch_env_levels(e->E, out, (cudaStream_t)stream);
+    return cuda_status("env_levels");
+}
+
+int amz_env_state(amz_env_t *e, int32_t *out, void *stream) {
+    if (!e || !out) return fail(AMZ_ECONFIG, "null argument");
+    launch_env_state(e->E, out, (cudaStream_t)stream);
+    return cuda_status("env_state");
+}
+
+int amz_env_set_state(amz_env_t *e, const int32_t *in, void *stream) {
+    if (!e || !in) return fail(AMZ_ECONFIG, "null argument");
+    launch_env_set_state(e->E, in, (cudaStream_t)stream);
+    return cuda_status("env_set_state");
+}
+
+int amz_env_check(amz_env_t *e, void *stream) {
+    if (!e) return fail(AMZ_ECONFIG, "null env");
+    cudaStream_t s = (cudaStream_t)stream;
+    int h = 0;
+    AMZ_CHECK_CUDA(cudaMemcpyAsync(&h, e->E.err, sizeof(int), cudaMemcpyDeviceToHost, s), "env_check");
+    AMZ_CHECK_CUDA(cudaStreamSynchronize(s), "env_check");
+    if (h) {
+        cudaMemsetAsync(e->E.err, 0, sizeof(int), s);
+        cudaStreamSynchronize(s);
+        return fail(AMZ_ECONTRACT, "step_batch called with terminal lanes");
+    }
+    return 0;
+}
+
+int amz_gae_score(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *last,
+                  double gamma, double lam, const double *prior, int score_fn, int disc, double *adv, double *ret,
+                  double *scores, double *maxret, const amz_episode_stats_t *stats, void *stream) {
+    if (T < 1) return fail(AMZ_ECONTRACT, "cannot score an empty trajectory slice");
+    if (B < 0) return fail(AMZ_ESHAPE, "negative lane count");
+    if (!r || !v || !d || !last || !adv || !ret) return fail(AMZ_ECONFIG, "null argument");
+    if ((score_fn & 0xFF) != AMZ_SCORE_MAXMC && (score_fn & 0xFF) != AMZ_SCORE_PVL)
+        return fail(AMZ_ECONFIG, "unknown score_fn %d", score_fn);
+    if ((score_fn & AMZ_SCORE_PRIOR_FINAL) && !prior) return fail(AMZ_ECONFIG, "PRIOR_FINAL needs prior_max");
+    int rc = launch_gae_score(T, B, r, v, d, last, gamma, lam, prior, score_fn, disc, adv, ret, scores, maxret, stats,
+                              (cudaStream_t)stream);
+    if (rc) return fail(rc, "gae_score: T=%d too long for the pairwise schedule", T);
+    return cuda_status("gae_score");
+}
+
+int amz_lane_scores(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *adv,
+                    double gamma, const double *prior, int score_fn, int disc, double *scores, double *maxret,
+                    const amz_episode_stats_t *stats, void *stream) {
+    if (T < 1) return fail(AMZ_ECONTRACT, "cannot score an empty trajectory slice");
+    if (B < 0) return fail(AMZ_ESHAPE, "negative lane count");
+    if (!r || !v || !d || !scores || !maxret || (score_fn == AMZ_SCORE_PVL && !adv))
+        return fail(AMZ_ECONFIG, "null argument");
+    if ((score_fn & 0xFF) != AMZ_SCORE_MAXMC && (score_fn & 0xFF) != AMZ_SCORE_PVL)
+        return fail(AMZ_ECONFIG, "unknown score_fn %d", score_fn);
+    if ((score_fn & AMZ_SCORE_PRIOR_FINAL) && !prior) return fail(AMZ_ECONFIG, "PRIOR_FINAL needs prior_max");
+    int rc = launch_gae_score(T, B, r, v, d, nullptr, gamma, 1.0, prior, score_fn, disc, (double *)adv, nullptr,
+                              scores, maxret, stats, (cudaStream_t)stream, 0);
+    if (rc) return fail(rc, "lane_scores: T=%d too long for the pairwise schedule", T);
+    return cuda_status("lane_scores");
+}
+
+}  // extern "C"

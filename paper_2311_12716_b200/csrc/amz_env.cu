@@ -1,0 +1,491 @@
+// amz_env.cu -- level generation / mutation kernels and the batched AMaze environment.
+//
+// Lane state (SoA, resident in HBM, owned by amz_env_t):
+//   st[B]    uint4   x = r | c<<8 | d<<16 | terminal<<24
+//                    y = goal_r | goal_c<<8 | home_r<<16 | home_c<<24
+//                    z = home_dir | time<<8
+//   mask[B]  uint4   the lane's level (interior wall bits)
+//   board    u32 [16][B]  rendering form of the level (amz_level.cuh)
+// The per-step kernel reads st/board from HBM; the fused rollout kernel keeps st in
+// registers and the boards in shared memory for all T steps.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "amz_internal.h"
+#include "amz_render.cuh"
+
+namespace amz {
+
+// ---------------------------------------------------------------------------------
+// level generation / mutation / validation
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_sample_levels(Geo G, amz_seed_t prefix, uint32_t lane0,
+                                                       const uint32_t *__restrict__ lane_ids, int64_t n,
+                                                       amz_level_t *__restrict__ out) {
+    extern __shared__ uint8_t perm_smem[];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    amz_seed_t s = prefix;
+    seed_absorb(s, lane_ids ? lane_ids[i] : lane0 + (uint32_t)i);
+    Stream g;
+    g.init(s);
+    Mask m;
+    int ar, ac, ad, gr, gc;
+    sample_level_dev(g, G, perm_smem + threadIdx.x, blockDim.x, m, ar, ac, ad, gr, gc);
+    store_level(out + i, m, ar, ac, ad, gr, gc);
+}
+
+__global__ void __launch_bounds__(128) k_mutate_levels(Geo G, amz_seed_t prefix, uint32_t lane0, int64_t n,
+                                                       const amz_level_t *__restrict__ parents,
+                                                       const int32_t *__restrict__ pidx, int n_edits,
+                                                       amz_level_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    amz_seed_t s = prefix;
+    seed_absorb(s, lane0 + (uint32_t)i);
+    Stream g;
+    g.init(s);
+    Mask m;
+    int ar, ac, ad, gr, gc;
+    load_level(parents + (pidx ? pidx[i] : i), m, ar, ac, ad, gr, gc);
+    mutate_level_dev(g, G, n_edits, m, ar, ac, gr, gc);
+    store_level(out + i, m, ar, ac, ad, gr, gc);
+}
+
+// MazeLevel.validate (amaze/level.py:50-66) on packed levels
+__device__ __forceinline__ bool level_ok(const Geo &G, const amz_level_t *lv) {
+    Mask m;
+    int ar, ac, ad, gr, gc;
+    load_level(lv, m, ar, ac, ad, gr, gc);
+    if (ar < 1 || ar > G.H - 2 || ac < 1 || ac > G.W - 2) return false;
+    if (gr < 1 || gr > G.H - 2 || gc < 1 || gc > G.W - 2) return false;
+    if (ad > 3) return false;
+    if (ar == gr && ac == gc) return false;
+    if (mask_bit(m, (ar - 1) * G.iw + ac - 1) || mask_bit(m, (gr - 1) * G.iw + gc - 1)) return false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        int lo = k * 32;
+        uint32_t valid = G.ni >= lo + 32 ? 0xFFFFFFFFu : (G.ni > lo ? (1u << (G.ni - lo)) - 1u : 0u);
+        if (m.w[k] & ~valid) return false;
+    }
+    return true;
+}
+
+__global__ void k_check_levels(Geo G, const amz_level_t *__restrict__ lv, int64_t n,
+                               unsigned long long *__restrict__ first_bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && !level_ok(G, lv + i)) atomicMin(first_bad, (unsigned long long)i);
+}
+
+// ---------------------------------------------------------------------------------
+// lane state helpers
+// ---------------------------------------------------------------------------------
+struct LaneRec {
+    LaneDyn s;
+    int gr, gc, hr, hc, hd;
+    bool term;
+};
+
+__device__ __forceinline__ LaneRec unpack_st(uint4 v) {
+    LaneRec L;
+    L.s.r = v.x & 0xFF;
+    L.s.c = (v.x >> 8) & 0xFF;
+    L.s.d = (v.x >> 16) & 0xFF;
+    L.term = (v.x >> 24) != 0;
+    L.gr = v.y & 0xFF;
+    L.gc = (v.y >> 8) & 0xFF;
+    L.hr = (v.y >> 16) & 0xFF;
+    L.hc = v.y >> 24;
+    L.hd = v.z & 0xFF;
+    L.s.time = (int)(v.z >> 8);
+    return L;
+}
+
+__device__ __forceinline__ uint4 pack_st(const LaneRec &L) {
+    return make_uint4((uint32_t)L.s.r | ((uint32_t)L.s.c << 8) | ((uint32_t)L.s.d << 16) |
+                          ((uint32_t)L.term << 24),
+                      (uint32_t)L.gr | ((uint32_t)L.gc << 8) | ((uint32_t)L.hr << 16) | ((uint32_t)L.hc << 24),
+                      (uint32_t)L.hd | ((uint32_t)L.s.time << 8), 0u);
+}
+
+// Copy a warp's staged V*V-byte records (stage = 32*VV bytes) to dst[0 .. nvalid*VV).
+__device__ __forceinline__ void warp_flush(const uint8_t *stage, uint8_t *dst, int nbytes, int lane) {
+    if ((((uintptr_t)dst) & 15u) == 0 && (nbytes & 15) == 0) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(stage);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        for (int k = lane; k < (nbytes >> 4); k += 32) d4[k] = s4[k];
+    } else {
+        for (int k = lane; k < nbytes; k += 32) dst[k] = stage[k];
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// reset_to_levels / observe / accessors
+// ---------------------------------------------------------------------------------
+template <int V>
+__global__ void __launch_bounds__(128) k_env_reset(Geo G, EnvDev E, const amz_level_t *__restrict__ levels,
+                                                   const int64_t *__restrict__ lanes, int64_t n,
+                                                   uint8_t *__restrict__ view, int64_t *__restrict__ dirs) {
+    __shared__ uint8_t stage[128 * V * V];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    uint8_t *my = stage + threadIdx.x * V * V;
+    if (i < n) {
+        const int64_t l = lanes ? lanes[i] : i;
+        Mask m;
+        LaneRec L;
+        load_level(levels + i, m, L.s.r, L.s.c, L.s.d, L.gr, L.gc);
+        L.hr = L.s.r;
+        L.hc = L.s.c;
+        L.hd = L.s.d;
+        L.s.time = 0;
+        L.term = false;
+        E.st[l] = pack_st(L);
+        E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+        build_board(m, G, E.board + l, (int)E.B);
+        if (dirs) dirs[i] = L.s.d;
+        if (view) lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, E.board + l, (int)E.B, my);
+    }
+    if (view) {
+        __syncwarp();
+        if (wbase < n) {
+            int nv = (int)(((n - wbase) < 32) ? (n - wbase) : 32);
+            warp_flush(stage + (threadIdx.x & ~31) * V * V, view + wbase * V * V, nv * V * V, lane);
+        }
+    }
+}
+
+template <int V>
+__global__ void __launch_bounds__(128) k_env_observe(Geo G, EnvDev E, uint8_t *__restrict__ view,
+                                                     int64_t *__restrict__ dirs) {
+    __shared__ uint8_t stage[128 * V * V];
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    if (l < E.B) {
+        LaneRec L = unpack_st(E.st[l]);
+        if (dirs) dirs[l] = L.s.d;
+        lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, E.board + l, (int)E.B,
+                       stage + threadIdx.x * V * V);
+    }
+    __syncwarp();
+    if (wbase < E.B && view) {
+        int nv = (int)(((E.B - wbase) < 32) ? (E.B - wbase) : 32);
+        warp_flush(stage + (threadIdx.x & ~31) * V * V, view + wbase * V * V, nv * V * V, lane);
+    }
+}
+
+__global__ void k_env_levels(EnvDev E, amz_level_t *__restrict__ out) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= E.B) return;
+    LaneRec L = unpack_st(E.st[l]);
+    uint4 w = E.mask[l];
+    Mask m;
+    m.w[0] = w.x;
+    m.w[1] = w.y;
+    m.w[2] = w.z;
+    m.w[3] = w.w;
+    store_level(out + l, m, L.hr, L.hc, L.hd, L.gr, L.gc);
+}
+
+__global__ void k_env_state(EnvDev E, int32_t *__restrict__ out) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= E.B) return;
+    LaneRec L = unpack_st(E.st[l]);
+    out[l * 5 + 0] = L.s.r;
+    out[l * 5 + 1] = L.s.c;
+    out[l * 5 + 2] = L.s.d;
+    out[l * 5 + 3] = L.s.time;
+    out[l * 5 + 4] = L.term;
+}
+
+__global__ void k_env_set_state(EnvDev E, const int32_t *__restrict__ in) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= E.B) return;
+    LaneRec L = unpack_st(E.st[l]);
+    L.s.r = in[l * 5 + 0];
+    L.s.c = in[l * 5 + 1];
+    L.s.d = in[l * 5 + 2];
+    L.s.time = in[l * 5 + 3];
+    L.term = in[l * 5 + 4] != 0;
+    E.st[l] = pack_st(L);
+}
+
+// ---------------------------------------------------------------------------------
+// one step of every lane (+ fused auto-reset)
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ int load_action(const void *a, int dtype, int64_t i) {
+    if (dtype == 0) return reinterpret_cast<const uint8_t *>(a)[i];
+    if (dtype == 1) {
+        int v = reinterpret_cast<const int32_t *>(a)[i];
+        return (v < 0 || v > 2) ? 3 : v;
+    }
+    long long v = reinterpret_cast<const int64_t *>(a)[i];
+    return (v < 0 || v > 2) ? 3 : (int)v;
+}
+
+// Fresh episode for a finished lane: RESAMPLE draws key wrap ++ [step, global lane];
+// HOME restarts the lane's own level (env/wrappers.py:64-71).
+__device__ __forceinline__ void lane_autoreset(const Geo &G, int mode, const amz_seed_t &wrap, uint32_t step,
+                                               uint32_t glane, LaneRec &L, Mask &m, uint8_t *perm, int pstride,
+                                               uint32_t *board, int bstride, bool &new_level) {
+    new_level = false;
+    if (mode == AMZ_RESET_RESAMPLE) {
+        amz_seed_t s = wrap;
+        seed_absorb(s, step);
+        seed_absorb(s, glane);
+        Stream g;
+        g.init(s);
+        int ar, ac, ad, gr, gc;
+        sample_level_dev(g, G, perm, pstride, m, ar, ac, ad, gr, gc);
+        build_board(m, G, board, bstride);
+        L.hr = ar;
+        L.hc = ac;
+        L.hd = ad;
+        L.gr = gr;
+        L.gc = gc;
+        new_level = true;
+    }
+    L.s.r = L.hr;
+    L.s.c = L.hc;
+    L.s.d = L.hd;
+    L.s.time = 0;
+    L.term = false;
+}
+
+template <int V>
+__global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *__restrict__ actions, int adtype,
+                                                  int mode, amz_seed_t wrap, uint32_t step_idx,
+                                                  uint8_t *__restrict__ view, int64_t *__restrict__ dirs,
+                                                  double *__restrict__ reward, uint8_t *__restrict__ done,
+                                                  double *__restrict__ solved, int64_t *__restrict__ times,
+                                                  const int *__restrict__ term_in, int *__restrict__ term_out) {
+    extern __shared__ uint8_t smem[];
+    uint8_t *stage = smem;                    // 128 * V * V
+    uint8_t *perm = smem + 128 * V * V;       // ni * 128
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    if (mode == AMZ_RESET_NONE && *term_in > 0) {
+        // step_batch raises on terminal lanes before touching anything (amaze/env.py:325-326)
+        if (l == 0) {
+            *term_out = *term_in;
+            atomicOr(E.err, 1);
+        }
+        return;
+    }
+    bool d_out = false;
+    if (l < E.B) {
+        LaneRec L = unpack_st(E.st[l]);
+        const int a = load_action(actions, adtype, l);
+        uint32_t *bd = E.board + l;
+        const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, (int)E.B);
+        const bool dn = reached || L.s.time >= G.tep;
+        d_out = dn;
+        if (reward) reward[l] = reached ? goal_reward(L.s.time, G.tep) : 0.0;
+        if (done) done[l] = dn;
+        if (solved) solved[l] = reached ? 1.0 : 0.0;
+        if (times) times[l] = L.s.time;
+        if (dn) {
+            if (mode == AMZ_RESET_NONE) {
+                L.term = true;
+            } else {
+                Mask m;
+                bool nl;
+                lane_autoreset(G, mode, wrap, step_idx, E.lane_offset + (uint32_t)l, L, m, perm + threadIdx.x,
+                               blockDim.x, bd, (int)E.B, nl);
+                if (nl) E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+            }
+        }
+        E.st[l] = pack_st(L);
+        if (dirs) dirs[l] = L.s.d;
+        if (view) lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, (int)E.B,
+                                 stage + threadIdx.x * V * V);
+    }
+    if (mode == AMZ_RESET_NONE) {
+        unsigned b = __ballot_sync(0xFFFFFFFFu, d_out);
+        if (lane == 0 && b) atomicAdd(term_out, __popc(b));
+    }
+    if (view) {
+        __syncwarp();
+        if (wbase < E.B) {
+            int nv = (int)(((E.B - wbase) < 32) ? (E.B - wbase) : 32);
+            warp_flush(stage + (threadIdx.x & ~31) * V * V, view + wbase * V * V, nv * V * V, lane);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// fused T-step rollout: lane state in registers, boards in shared memory
+// ---------------------------------------------------------------------------------
+template <int V>
+__global__ void __launch_bounds__(128) k_env_rollout(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions,
+                                                     int mode, amz_seed_t wrap, uint32_t step0,
+                                                     uint8_t *__restrict__ view, uint8_t *__restrict__ dirs,
+                                                     double *__restrict__ reward, uint8_t *__restrict__ done,
+                                                     uint8_t *__restrict__ fview, uint8_t *__restrict__ fdir) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    constexpr int VV = V * V;
+    uint32_t *board = reinterpret_cast<uint32_t *>(smem);  // [16][128]
+    uint8_t *stage = smem + 16 * 128 * 4;                  // [128][VV]
+    uint8_t *perm = stage + 128 * VV;                      // [ni][128]
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + tid;
+    const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (tid & ~31);
+    const int64_t B = E.B;
+    const bool live = l < B;
+    const int nv = wbase < B ? (int)(((B - wbase) < 32) ? (B - wbase) : 32) : 0;
+    uint8_t *mystage = stage + tid * VV;
+    uint8_t *wstage = stage + (tid & ~31) * VV;
+    uint32_t *bd = board + tid;
+
+    LaneRec L;
+    Mask m;
+    bool lvl_changed = false;
+    if (live) {
+        L = unpack_st(E.st[l]);
+#pragma unroll
+        for (int k = 0; k < 16; k++) bd[k * 128] = E.board[k * B + l];
+    }
+    int a_next = (live && T > 0) ? actions[l] : 0;
+    for (int t = 0; t < T; t++) {
+        const int a = a_next;
+        if (live && t + 1 < T) a_next = actions[(int64_t)(t + 1) * B + l];
+        // observation before step t
+        if (live) {
+            lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, 128, mystage);
+            dirs[(int64_t)t * B + l] = (uint8_t)L.s.d;
+        }
+        __syncwarp();
+        if (nv) warp_flush(wstage, view + ((int64_t)t * B + wbase) * VV, nv * VV, lane);
+        if (live) {
+            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, 128);
+            const bool dn = reached || L.s.time >= G.tep;
+            reward[(int64_t)t * B + l] = reached ? goal_reward(L.s.time, G.tep) : 0.0;
+            done[(int64_t)t * B + l] = dn;
+            if (dn) {
+                bool nl;
+                lane_autoreset(G, mode, wrap, step0 + (uint32_t)t, E.lane_offset + (uint32_t)l, L, m, perm + tid,
+                               128, bd, 128, nl);
+                lvl_changed |= nl;
+            }
+        }
+        __syncwarp();
+    }
+    // cursor observation + state write-back
+    if (live) {
+        lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, 128, mystage);
+        if (fdir) fdir[l] = (uint8_t)L.s.d;
+        E.st[l] = pack_st(L);
+        if (lvl_changed) {
+            E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+#pragma unroll
+            for (int k = 0; k < 16; k++) E.board[k * B + l] = bd[k * 128];
+        }
+    }
+    __syncwarp();
+    if (nv && fview) warp_flush(wstage, fview + wbase * VV, nv * VV, lane);
+}
+
+// ---------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------
+static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, const uint32_t *ids, int64_t n,
+                         amz_level_t *out, cudaStream_t s) {
+    if (n <= 0) return 0;
+    k_sample_levels<<<blocks_for(n, 128), 128, 128 * G.ni, s>>>(G, prefix, lane0, ids, n, out);
+    return 0;
+}
+
+int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
+                         const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s) {
+    if (n <= 0) return 0;
+    k_mutate_levels<<<blocks_for(n, 128), 128, 0, s>>>(G, prefix, lane0, n, par, pidx, n_edits, out);
+    return 0;
+}
+
+int launch_check_levels(const Geo &G, const amz_level_t *lv, int64_t n, unsigned long long *first_bad,
+                        cudaStream_t s) {
+    if (n <= 0) return 0;
+    k_check_levels<<<blocks_for(n, 256), 256, 0, s>>>(G, lv, n, first_bad);
+    return 0;
+}
+
+#define AMZ_DISPATCH_V(V_, ...)                                            \
+    switch (V_) {                                                         \
+        case 3: { constexpr int VT = 3; __VA_ARGS__; } break;             \
+        case 5: { constexpr int VT = 5; __VA_ARGS__; } break;             \
+        case 7: { constexpr int VT = 7; __VA_ARGS__; } break;             \
+        case 9: { constexpr int VT = 9; __VA_ARGS__; } break;             \
+        default: return AMZ_ECONFIG;                                      \
+    }
+
+int launch_env_reset(const Geo &G, const EnvDev &E, const amz_level_t *lv, const int64_t *lanes, int64_t n,
+                     uint8_t *view, int64_t *dirs, cudaStream_t s) {
+    if (n <= 0) return 0;
+    AMZ_DISPATCH_V(G.V, (k_env_reset<VT><<<blocks_for(n, 128), 128, 0, s>>>(G, E, lv, lanes, n, view, dirs)));
+    return 0;
+}
+
+int launch_env_observe(const Geo &G, const EnvDev &E, uint8_t *view, int64_t *dirs, cudaStream_t s) {
+    if (E.B <= 0) return 0;
+    AMZ_DISPATCH_V(G.V, (k_env_observe<VT><<<blocks_for(E.B, 128), 128, 0, s>>>(G, E, view, dirs)));
+    return 0;
+}
+
+int launch_env_levels(const EnvDev &E, amz_level_t *out, cudaStream_t s) {
+    if (E.B > 0) k_env_levels<<<blocks_for(E.B, 256), 256, 0, s>>>(E, out);
+    return 0;
+}
+
+int launch_env_state(const EnvDev &E, int32_t *out, cudaStream_t s) {
+    if (E.B > 0) k_env_state<<<blocks_for(E.B, 256), 256, 0, s>>>(E, out);
+    return 0;
+}
+
+int launch_env_set_state(const EnvDev &E, const int32_t *in, cudaStream_t s) {
+    if (E.B > 0) k_env_set_state<<<blocks_for(E.B, 256), 256, 0, s>>>(E, in);
+    return 0;
+}
+
+int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adtype, int mode,
+                    const amz_seed_t &wrap, uint32_t step_idx, uint8_t *view, int64_t *dirs, double *reward,
+                    uint8_t *done, double *solved, int64_t *times, const int *term_in, int *term_out,
+                    cudaStream_t s) {
+    if (E.B <= 0) return 0;
+    const int V = G.V;
+    size_t sm = 128 * V * V + (mode == AMZ_RESET_RESAMPLE ? 128 * G.ni : 0);
+    AMZ_DISPATCH_V(V, (k_env_step<VT><<<blocks_for(E.B, 128), 128, sm, s>>>(G, E, actions, adtype, mode, wrap,
+                                                                          step_idx, view, dirs, reward, done,
+                                                                          solved, times, term_in, term_out)));
+    return 0;
+}
+
+template <int V>
+static int rollout_smem_setup(size_t sm) {
+    static bool done_attr = false;
+    if (!done_attr) {
+        cudaFuncSetAttribute(k_env_rollout<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        done_attr = true;
+    }
+    return 0;
+}
+
+int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
+                       const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
+                       uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
+    if (E.B <= 0) return 0;
+    const int V = G.V;
+    size_t sm = 16 * 128 * 4 + 128 * V * V + (mode == AMZ_RESET_RESAMPLE ? 128 * G.ni : 0);
+    sm = (sm + 15) & ~(size_t)15;
+    AMZ_DISPATCH_V(V, (rollout_smem_setup<VT>(64 * 1024),
+                       k_env_rollout<VT><<<blocks_for(E.B, 128), 128, sm, s>>>(G, E, T, actions, mode, wrap, step0,
+                                                                            view, dirs, reward, done, fview,
+                                                                            fdir)));
+    return 0;
+}
+
+}  // namespace amz

@@ -1,0 +1,56 @@
+// amz_internal.h -- declarations shared by the .cu translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/amaze_b200.h"
+#include "amz_level.cuh"
+
+namespace amz {
+
+// device view of an amz_env_t
+struct EnvDev {
+    int64_t B;
+    uint32_t lane_offset;
+    uint4 *st;
+    uint4 *mask;
+    uint32_t *board;  // [16][B]
+    int *err;
+};
+
+// numpy pairwise summation schedule (numpy/_core/src/umath/loops_utils.h.src
+// pairwise_sum): leaves of <= 128 elements, summed with 8 accumulators, combined
+// bottom-up.  adds[i] = combines to perform after pushing leaf i.
+constexpr int kMaxLeaves = 64;
+struct PairwisePlan {
+    int n_leaves;
+    int leaf_end[kMaxLeaves];
+    uint8_t adds[kMaxLeaves];
+};
+int make_pairwise_plan(int n, PairwisePlan &plan);
+
+int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, const uint32_t *ids, int64_t n,
+                         amz_level_t *out, cudaStream_t s);
+int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
+                         const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s);
+int launch_check_levels(const Geo &G, const amz_level_t *lv, int64_t n, unsigned long long *first_bad,
+                        cudaStream_t s);
+int launch_env_reset(const Geo &G, const EnvDev &E, const amz_level_t *lv, const int64_t *lanes, int64_t n,
+                     uint8_t *view, int64_t *dirs, cudaStream_t s);
+int launch_env_observe(const Geo &G, const EnvDev &E, uint8_t *view, int64_t *dirs, cudaStream_t s);
+int launch_env_levels(const EnvDev &E, amz_level_t *out, cudaStream_t s);
+int launch_env_state(const EnvDev &E, int32_t *out, cudaStream_t s);
+int launch_env_set_state(const EnvDev &E, const int32_t *in, cudaStream_t s);
+int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adtype, int mode,
+                    const amz_seed_t &wrap, uint32_t step_idx, uint8_t *view, int64_t *dirs, double *reward,
+                    uint8_t *done, double *solved, int64_t *times, const int *term_in, int *term_out,
+                    cudaStream_t s);
+int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
+                       const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
+                       uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s);
+int launch_gae_score(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *last,
+                     double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
+                     double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
+                     cudaStream_t s, int do_gae = 1);
+
+}  // namespace amz
