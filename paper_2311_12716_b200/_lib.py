@@ -58,6 +58,7 @@ _SIGS = {
     "amz_env_check": ([P, VP], I32),
     "amz_gae_score": ([I32, I64, P, P, P, P, D, D, P, I32, I32, P, P, P, P,
                        ctypes.POINTER(AmzEpisodeStats), VP], I32),
+    "amz_lane_scores": ([I32, I64, P, P, P, P, D, P, I32, I32, P, P, ctypes.POINTER(AmzEpisodeStats), VP], I32),
 }
 
 _lib = None

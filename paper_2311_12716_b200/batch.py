@@ -155,13 +155,18 @@ class VectorBatchEnv:
         return a.to(torch.int64).contiguous(), 2
 
     def _zeros_result(self, obs, state):
+        """reset results carry zero reward/done/info (env/batch.py:91-96); the zero
+        tensors are allocated once per env and shared read-only across resets."""
         torch = _torch()
-        n = self.n_lanes
-        z = torch.zeros(n, dtype=torch.float64, device=self.device)
-        info = {"solved": self._reshape(torch.zeros(n, dtype=torch.float64, device=self.device)),
-                "time": self._reshape(torch.zeros(n, dtype=torch.int64, device=self.device))}
-        return StepResult({k: self._reshape(v) for k, v in obs.items()}, state, self._reshape(z),
-                          self._reshape(torch.zeros(n, dtype=torch.bool, device=self.device)), info)
+        if getattr(self, "_zeros", None) is None or self._zeros[0].numel() != self.n_lanes:
+            n = self.n_lanes
+            self._zeros = (torch.zeros(n, dtype=torch.float64, device=self.device),
+                           torch.zeros(n, dtype=torch.bool, device=self.device),
+                           torch.zeros(n, dtype=torch.int64, device=self.device))
+        zf, zb, zi = self._zeros
+        info = {"solved": self._reshape(zf), "time": self._reshape(zi)}
+        return StepResult({k: self._reshape(v) for k, v in obs.items()}, state, self._reshape(zf),
+                          self._reshape(zb), info)
 
     # -- reference API ---------------------------------------------------------
     def reset(self, rng, params) -> StepResult:

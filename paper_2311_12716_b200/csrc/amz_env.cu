@@ -327,9 +327,10 @@ __global__ void __launch_bounds__(128) k_env_rollout(Geo G, EnvDev E, int T, con
                                                      uint8_t *__restrict__ fview, uint8_t *__restrict__ fdir) {
     extern __shared__ __align__(16) uint8_t smem[];
     constexpr int VV = V * V;
-    uint32_t *board = reinterpret_cast<uint32_t *>(smem);  // [16][128]
-    uint8_t *stage = smem + 16 * 128 * 4;                  // [128][VV]
-    uint8_t *perm = stage + 128 * VV;                      // [ni][128]
+    const int nt = blockDim.x;
+    uint32_t *board = reinterpret_cast<uint32_t *>(smem);  // [16][nt]
+    uint8_t *stage = smem + 16 * nt * 4;                   // [nt][VV]
+    uint8_t *perm = stage + nt * VV;                       // [ni][nt]
     const int tid = threadIdx.x, lane = tid & 31;
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (tid & ~31);
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(128) k_env_rollout(Geo G, EnvDev E, int T, con
     if (live) {
         L = unpack_st(E.st[l]);
 #pragma unroll
-        for (int k = 0; k < 16; k++) bd[k * 128] = E.board[k * B + l];
+        for (int k = 0; k < 16; k++) bd[k * nt] = E.board[k * B + l];
     }
     int a_next = (live && T > 0) ? actions[l] : 0;
     for (int t = 0; t < T; t++) {
@@ -354,20 +355,20 @@ __global__ void __launch_bounds__(128) k_env_rollout(Geo G, EnvDev E, int T, con
         if (live && t + 1 < T) a_next = actions[(int64_t)(t + 1) * B + l];
         // observation before step t
         if (live) {
-            lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, 128, mystage);
+            lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, nt, mystage);
             dirs[(int64_t)t * B + l] = (uint8_t)L.s.d;
         }
         __syncwarp();
         if (nv) warp_flush(wstage, view + ((int64_t)t * B + wbase) * VV, nv * VV, lane);
         if (live) {
-            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, 128);
+            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, nt);
             const bool dn = reached || L.s.time >= G.tep;
             reward[(int64_t)t * B + l] = reached ? goal_reward(L.s.time, G.tep) : 0.0;
             done[(int64_t)t * B + l] = dn;
             if (dn) {
                 bool nl;
                 lane_autoreset(G, mode, wrap, step0 + (uint32_t)t, E.lane_offset + (uint32_t)l, L, m, perm + tid,
-                               128, bd, 128, nl);
+                               nt, bd, nt, nl);
                 lvl_changed |= nl;
             }
         }
@@ -375,13 +376,13 @@ __global__ void __launch_bounds__(128) k_env_rollout(Geo G, EnvDev E, int T, con
     }
     // cursor observation + state write-back
     if (live) {
-        lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, 128, mystage);
+        lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, nt, mystage);
         if (fdir) fdir[l] = (uint8_t)L.s.d;
         E.st[l] = pack_st(L);
         if (lvl_changed) {
             E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
 #pragma unroll
-            for (int k = 0; k < 16; k++) E.board[k * B + l] = bd[k * 128];
+            for (int k = 0; k < 16; k++) E.board[k * B + l] = bd[k * nt];
         }
     }
     __syncwarp();
@@ -393,17 +394,27 @@ __global__ void __launch_bounds__(128) k_env_rollout(Geo G, EnvDev E, int T, con
 // ---------------------------------------------------------------------------------
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Threads per block for one-lane-per-thread kernels: spread small batches over all
+// 148 SMs (one warp per SM for B <= 4736) instead of packing them into a few CTAs.
+static inline int lanes_per_cta(int64_t n) {
+    const int64_t per_sm = (n + 147) / 148;
+    int t = (int)(((per_sm + 31) / 32) * 32);
+    return t < 32 ? 32 : (t > 128 ? 128 : t);
+}
+
 int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, const uint32_t *ids, int64_t n,
                          amz_level_t *out, cudaStream_t s) {
     if (n <= 0) return 0;
-    k_sample_levels<<<blocks_for(n, 128), 128, 128 * G.ni, s>>>(G, prefix, lane0, ids, n, out);
+    const int nt = lanes_per_cta(n);
+    k_sample_levels<<<blocks_for(n, nt), nt, nt * G.ni, s>>>(G, prefix, lane0, ids, n, out);
     return 0;
 }
 
 int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
                          const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s) {
     if (n <= 0) return 0;
-    k_mutate_levels<<<blocks_for(n, 128), 128, 0, s>>>(G, prefix, lane0, n, par, pidx, n_edits, out);
+    const int nt = lanes_per_cta(n);
+    k_mutate_levels<<<blocks_for(n, nt), nt, 0, s>>>(G, prefix, lane0, n, par, pidx, n_edits, out);
     return 0;
 }
 
@@ -457,8 +468,9 @@ int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adty
                     cudaStream_t s) {
     if (E.B <= 0) return 0;
     const int V = G.V;
-    size_t sm = 128 * V * V + (mode == AMZ_RESET_RESAMPLE ? 128 * G.ni : 0);
-    AMZ_DISPATCH_V(V, (k_env_step<VT><<<blocks_for(E.B, 128), 128, sm, s>>>(G, E, actions, adtype, mode, wrap,
+    const int nt = lanes_per_cta(E.B);
+    size_t sm = 128 * V * V + (mode == AMZ_RESET_RESAMPLE ? nt * G.ni : 0);
+    AMZ_DISPATCH_V(V, (k_env_step<VT><<<blocks_for(E.B, nt), nt, sm, s>>>(G, E, actions, adtype, mode, wrap,
                                                                           step_idx, view, dirs, reward, done,
                                                                           solved, times, term_in, term_out)));
     return 0;
@@ -479,10 +491,11 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
                        uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
     if (E.B <= 0) return 0;
     const int V = G.V;
-    size_t sm = 16 * 128 * 4 + 128 * V * V + (mode == AMZ_RESET_RESAMPLE ? 128 * G.ni : 0);
+    const int nt = lanes_per_cta(E.B);
+    size_t sm = 16 * nt * 4 + nt * V * V + (mode == AMZ_RESET_RESAMPLE ? nt * G.ni : 0);
     sm = (sm + 15) & ~(size_t)15;
     AMZ_DISPATCH_V(V, (rollout_smem_setup<VT>(64 * 1024),
-                       k_env_rollout<VT><<<blocks_for(E.B, 128), 128, sm, s>>>(G, E, T, actions, mode, wrap, step0,
+                       k_env_rollout<VT><<<blocks_for(E.B, nt), nt, sm, s>>>(G, E, T, actions, mode, wrap, step0,
                                                                             view, dirs, reward, done, fview,
                                                                             fdir)));
     return 0;

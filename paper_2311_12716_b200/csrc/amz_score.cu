@@ -202,7 +202,7 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
     PairwisePlan P;
     if (make_pairwise_plan(T, P)) return AMZ_ECONFIG;
     const double gl = gamma * lam;  // Python evaluates gamma * lam first (agents/gae.py:35)
-    const int threads = 64;
+    const int threads = B >= 148 * 64 ? 64 : 32;
     k_gae_score<<<(unsigned)((B + threads - 1) / threads), threads, 0, s>>>(
         T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
         stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
