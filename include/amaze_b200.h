@@ -184,6 +184,44 @@ int amz_lane_scores(int T, int64_t B, const double *rewards_dev, const double *v
                     int score_fn, int maxmc_discounted, double *scores_dev, double *max_ret_dev,
                     const amz_episode_stats_t *stats, void *stream);
 
+/* ---- PLR level buffer (device-resident; oracle/plr_np.py) ----
+ * Capacity K <= 4096 (paper: 4000).  Slots 0..size-1 are valid. */
+int amz_plr_create(int64_t capacity, amz_plr_t **out);
+int amz_plr_destroy(amz_plr_t *plr);
+
+/* buffer_update: for each of the n candidates IN ORDER: an identical
+ * level (walls + pose) present -> score/max_return updated in place; else insert while
+ * not full; else replace the (score, last_sampled, seq)-minimum iff score > its score.
+ * New entries get last_sampled = insert iteration = iter. */
+int amz_plr_update(amz_plr_t *plr, const amz_level_t *levels_dev, const double *scores_dev,
+                   const double *max_ret_dev, int64_t n, int64_t iter, void *stream);
+
+/* buffer_sample_levels, rank prioritisation: n draws with replacement
+ * = numpy Generator(key).choice(size, n, p=P), P = (1-rho) P_S + rho P_C,
+ * P_S = w/sum(w), w = rank_lut_dev[rank-1] ((1/rank)^(1/beta), ranks by score desc then
+ * older insertion), P_C = (iter-last_sampled)/sum (P = P_S if that sum is 0).  key = the
+ * stream's full SeedSequence state (no suffix word).  Outputs slots [n] i32 and the
+ * drawn levels / max returns / scores (each optional); drawn entries get
+ * last_sampled = iter.  An empty buffer raises AMZ_ECONTRACT at amz_plr_size(). */
+int amz_plr_sample(amz_plr_t *plr, const amz_seed_t *key, int64_t n, double rho, const double *rank_lut_dev,
+                   int64_t iter, int32_t *slots_dev, amz_level_t *levels_dev, double *max_ret_dev,
+                   double *score_dev, void *stream);
+
+/* ACCEL parent choice: indices of the q highest scores (ties -> lower index). */
+int amz_plr_top_q(const double *scores_dev, int64_t n, int q, int32_t *out_dev, void *stream);
+
+/* Synchronous: current size; reports a deferred empty-buffer sampling error. */
+int amz_plr_size(amz_plr_t *plr, int64_t *size_host, void *stream);
+
+/* Device-to-device copy of the whole buffer state (checkpoint / drift checks):
+ * levels [K], score [K], max_return [K], last_sampled [K] i64, seq [K] i64,
+ * meta [2] i64 = (size, next_seq).  Any output may be NULL for export. */
+int amz_plr_export(amz_plr_t *plr, amz_level_t *levels_dev, double *score_dev, double *max_ret_dev,
+                   int64_t *last_sampled_dev, int64_t *seq_dev, int64_t *meta_dev, void *stream);
+int amz_plr_import(amz_plr_t *plr, const amz_level_t *levels_dev, const double *score_dev,
+                   const double *max_ret_dev, const int64_t *last_sampled_dev, const int64_t *seq_dev,
+                   const int64_t *meta_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

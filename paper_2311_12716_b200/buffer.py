@@ -1,0 +1,167 @@
+"""PLR level buffer resident on the GPU.
+
+The reference imports ``runners/buffer.py`` (``runners/scoring.py:14``) but never
+shipped it; ``SPEC.md:332-377,427-433`` describe it.  This is that buffer on the
+device: ``update`` = SPEC's ``buffer_update``, ``sample`` = ``buffer_sample_levels``
+(rank prioritisation + staleness), ``decision`` = ``buffer_sample_decision``.  The open
+choices SPEC leaves are pinned identically in the oracle (oracle/plr_np.py docstring)
+and in DESIGN.md.  Both kernels are single-CTA (csrc/amz_plr.cu) and exact: the
+sampler reproduces numpy ``Generator.choice`` bit for bit, the update reproduces the
+sequential per-candidate rule.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, ContractViolation
+from .rng import as_stream
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass(frozen=True)
+class PlrConfig:
+    """SPEC.md:336-339 PlrConfig (+ the two fields runners/scoring.py reads)."""
+
+    replay_rate: float = 0.5
+    buffer_size: int = 4000
+    score_fn: str = "maxmc"
+    prioritization: str = "rank"
+    temperature: float = 0.3
+    staleness_coef: float = 0.3
+    robust: bool = True
+    maxmc_discounted: bool = False
+
+    def validate(self) -> "PlrConfig":
+        if not 0.0 <= self.replay_rate <= 1.0:
+            raise ConfigError(f"replay_rate must be in [0, 1], got {self.replay_rate}")
+        if not self.temperature > 0.0:
+            raise ConfigError(f"temperature must be > 0, got {self.temperature}")
+        if not 0.0 <= self.staleness_coef <= 1.0:
+            raise ConfigError(f"staleness_coef must be in [0, 1], got {self.staleness_coef}")
+        if self.score_fn not in ("maxmc", "pvl"):
+            raise ConfigError(f"unknown score_fn {self.score_fn!r}")
+        if self.prioritization != "rank":
+            raise ConfigError("only rank prioritisation is implemented on the GPU (paper Table 4)")
+        if not 1 <= self.buffer_size <= 4096:
+            raise ConfigError(f"buffer_size must be in [1, 4096], got {self.buffer_size}")
+        return self
+
+
+@dataclass(frozen=True)
+class AccelConfig:
+    """SPEC.md:340-343."""
+
+    n_mutations: int = 20
+    subsample_size: int = 4
+
+
+def rank_weights(K: int, beta: float) -> np.ndarray:
+    """(1/rank)^(1/beta), ranks 1..K, computed by numpy (host LUT)."""
+    ranks = np.arange(1, K + 1, dtype=np.float64)
+    return np.power(1.0 / ranks, 1.0 / beta)
+
+
+class LevelBuffer:
+    """Device PLR buffer of capacity K (slots 0..size-1 valid)."""
+
+    def __init__(self, cfg: PlrConfig, device=None):
+        torch = _torch()
+        self.cfg = cfg.validate()
+        self.K = cfg.buffer_size
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(self.device):
+            h = ctypes.c_void_p()
+            _lib.call("amz_plr_create", self.K, ctypes.byref(h))
+        self.handle = h
+        self.lut = torch.from_numpy(rank_weights(self.K, cfg.temperature)).to(self.device)
+        self.nonempty = False  # host-side knowledge: the first update always inserts
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib._lib is not None:
+            _lib._lib.amz_plr_destroy(h)
+            self.handle = None
+
+    def _stream(self):
+        return _lib.stream_handle(self.device)
+
+    def update(self, levels, scores, max_returns, it: int) -> None:
+        torch = _torch()
+        n = levels.shape[0]
+        lv = levels.to(self.device).to(torch.int32).contiguous()
+        sc = scores.to(self.device).to(torch.float64).contiguous()
+        mx = max_returns.to(self.device).to(torch.float64).contiguous()
+        _lib.call("amz_plr_update", self.handle, _lib.ptr(lv), _lib.ptr(sc), _lib.ptr(mx), n, int(it), self._stream())
+        if n > 0:
+            self.nonempty = True
+
+    def sample(self, rng, n: int, it: int):
+        """n replay draws -> dict(slots i32, levels [n, 8], max_returns f64, scores f64)."""
+        torch = _torch()
+        if not self.nonempty:
+            raise ContractViolation("cannot sample from an empty level buffer")
+        out = {"slots": torch.empty(n, dtype=torch.int32, device=self.device),
+               "levels": torch.empty((n, 8), dtype=torch.int32, device=self.device),
+               "max_returns": torch.empty(n, dtype=torch.float64, device=self.device),
+               "scores": torch.empty(n, dtype=torch.float64, device=self.device)}
+        seed = as_stream(rng).seed_prefix()
+        _lib.call("amz_plr_sample", self.handle, ctypes.byref(seed), n, float(self.cfg.staleness_coef),
+                  _lib.ptr(self.lut), int(it), _lib.ptr(out["slots"]), _lib.ptr(out["levels"]),
+                  _lib.ptr(out["max_returns"]), _lib.ptr(out["scores"]), self._stream())
+        return out
+
+    def decision(self, rng) -> bool:
+        """buffer_sample_decision: replay w.p. p iff non-empty.  The
+        single uniform is drawn on the host from the same numpy stream definition."""
+        if not self.nonempty:
+            return False
+        s = as_stream(rng)
+        g = np.random.Generator(np.random.Philox(np.random.SeedSequence(entropy=s.entropy, spawn_key=s.key)))
+        return bool(g.random() < self.cfg.replay_rate)
+
+    def size(self) -> int:
+        v = ctypes.c_int64(0)
+        _lib.call("amz_plr_size", self.handle, ctypes.byref(v), self._stream())
+        return int(v.value)
+
+    def export(self) -> dict:
+        torch = _torch()
+        K, dev = self.K, self.device
+        st = {"levels": torch.empty((K, 8), dtype=torch.int32, device=dev),
+              "score": torch.empty(K, dtype=torch.float64, device=dev),
+              "max_return": torch.empty(K, dtype=torch.float64, device=dev),
+              "last_sampled": torch.empty(K, dtype=torch.int64, device=dev),
+              "seq": torch.empty(K, dtype=torch.int64, device=dev),
+              "meta": torch.empty(2, dtype=torch.int64, device=dev)}
+        _lib.call("amz_plr_export", self.handle, *(_lib.ptr(st[k]) for k in
+                                                   ("levels", "score", "max_return", "last_sampled", "seq", "meta")),
+                  self._stream())
+        return st
+
+    def load(self, st: dict) -> None:
+        torch = _torch()
+        t = {k: v.to(self.device).contiguous() for k, v in st.items()}
+        _lib.call("amz_plr_import", self.handle, *(_lib.ptr(t[k]) for k in
+                                                   ("levels", "score", "max_return", "last_sampled", "seq", "meta")),
+                  self._stream())
+        self.nonempty = bool(int(t["meta"][0].item()) > 0)
+        del torch
+
+
+def top_q(scores, q: int):
+    """Indices of the q highest scores (ties -> lower index), on device."""
+    torch = _torch()
+    out = torch.empty(q, dtype=torch.int32, device=scores.device)
+    s = scores.to(torch.float64).contiguous()
+    _lib.call("amz_plr_top_q", _lib.ptr(s), s.numel(), int(q), _lib.ptr(out), _lib.stream_handle(scores.device))
+    return out

@@ -40,6 +40,34 @@ struct amz_env {
     int parity;
 };
 
+struct amz_plr {
+    PlrDev D;
+    UpdScratch W;
+    int *err;
+};
+
+static int plr_scratch(amz_plr *b, int64_t n, cudaStream_t s) {
+    if (n <= b->W.cap) return 0;
+    int64_t cap = 1024;
+    while (cap < n) cap <<= 1;
+    cudaFreeAsync(b->W.init_match, s);
+    cudaFreeAsync(b->W.twin_first, s);
+    cudaFreeAsync(b->W.keyslot, s);
+    cudaFreeAsync(b->W.rel, s);
+    cudaFreeAsync(b->W.chash, s);
+    cudaError_t e = cudaMallocAsync((void **)&b->W.init_match, cap * 4, s);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&b->W.twin_first, cap * 4, s);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&b->W.keyslot, cap * 4, s);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&b->W.rel, cap * 4, s);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&b->W.chash, cap * 2 * 4, s);
+    if (e != cudaSuccess) {
+        b->W.cap = 0;
+        return fail(AMZ_ECUDA, "plr scratch: %s", cudaGetErrorString(e));
+    }
+    b->W.cap = cap;
+    return 0;
+}
+
 extern "C" {
 
 int amz_abi_version(void) { return AMZ_ABI_VERSION; }
@@ -273,6 +301,127 @@ int amz_lane_scores(int T, int64_t B, const double *r, const double *v, const ui
                               scores, maxret, stats, (cudaStream_t)stream, 0);
     if (rc) return fail(rc, "lane_scores: T=%d too long for the pairwise schedule", T);
     return cuda_status("lane_scores");
+}
+
+int amz_plr_create(int64_t capacity, amz_plr_t **out) {
+    if (!out) return fail(AMZ_ECONFIG, "null argument");
+    if (capacity < 1 || capacity > 4096) return fail(AMZ_ECONFIG, "buffer_size must be in [1, 4096], got %lld",
+                                                     (long long)capacity);
+    amz_plr *b = new (std::nothrow) amz_plr();
+    if (!b) return fail(AMZ_EFAULT, "out of host memory");
+    b->D.K = capacity;
+    size_t K = (size_t)capacity;
+    cudaError_t e = cudaMalloc((void **)&b->D.levels, K * sizeof(amz_level_t));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b->D.score, K * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b->D.maxret, K * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b->D.last, K * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b->D.seq, K * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b->D.meta, 2 * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b->err, 4 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(b->D.meta, 0, 16);
+    if (e == cudaSuccess) e = cudaMemset(b->err, 0, 4 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(b->D.levels, 0, K * sizeof(amz_level_t));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        amz_plr_destroy(b);
+        return fail(AMZ_ECUDA, "plr alloc: %s", cudaGetErrorString(e));
+    }
+    *out = b;
+    return 0;
+}
+
+int amz_plr_destroy(amz_plr_t *b) {
+    if (!b) return 0;
+    cudaDeviceSynchronize();
+    cudaFree(b->D.levels);
+    cudaFree(b->D.score);
+    cudaFree(b->D.maxret);
+    cudaFree(b->D.last);
+    cudaFree(b->D.seq);
+    cudaFree(b->D.meta);
+    cudaFree(b->err);
+    cudaFree(b->W.init_match);
+    cudaFree(b->W.twin_first);
+    cudaFree(b->W.keyslot);
+    cudaFree(b->W.rel);
+    cudaFree(b->W.chash);
+    delete b;
+    return 0;
+}
+
+int amz_plr_update(amz_plr_t *b, const amz_level_t *levels, const double *scores, const double *max_ret, int64_t n,
+                   int64_t iter, void *stream) {
+    if (!b || (n > 0 && (!levels || !scores || !max_ret))) return fail(AMZ_ECONFIG, "null argument");
+    if (n < 0) return fail(AMZ_ESHAPE, "negative candidate count");
+    if (n > ((int64_t)1 << 30)) return fail(AMZ_ESHAPE, "too many candidates");
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = plr_scratch(b, n, s);
+    if (rc) return rc;
+    launch_plr_update(b->D, levels, scores, max_ret, n, iter, b->W, s);
+    return cuda_status("plr_update");
+}
+
+int amz_plr_sample(amz_plr_t *b, const amz_seed_t *key, int64_t n, double rho, const double *lut, int64_t iter,
+                   int32_t *slots, amz_level_t *levels, double *max_ret, double *score, void *stream) {
+    if (!b || !key || !lut || (n > 0 && !slots)) return fail(AMZ_ECONFIG, "null argument");
+    if (rho < 0.0 || rho > 1.0) return fail(AMZ_ECONFIG, "staleness_coef must be in [0, 1], got %g", rho);
+    if (n <= 0) return 0;
+    launch_plr_sample(b->D, *key, n, 1.0 - rho, rho, lut, iter, slots, levels, max_ret, score, b->err,
+                      (cudaStream_t)stream);
+    return cuda_status("plr_sample");
+}
+
+int amz_plr_top_q(const double *scores, int64_t n, int q, int32_t *out, void *stream) {
+    if (!scores || !out) return fail(AMZ_ECONFIG, "null argument");
+    if (q < 1 || q > 64 || q > n) return fail(AMZ_ECONFIG, "subsample size q=%d must be in [1, min(64, %lld)]", q,
+                                              (long long)n);
+    launch_top_q(scores, n, q, out, (cudaStream_t)stream);
+    return cuda_status("plr_top_q");
+}
+
+int amz_plr_size(amz_plr_t *b, int64_t *size, void *stream) {
+    if (!b || !size) return fail(AMZ_ECONFIG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t meta[2];
+    int err = 0;
+    AMZ_CHECK_CUDA(cudaMemcpyAsync(meta, b->D.meta, 16, cudaMemcpyDeviceToHost, s), "plr_size");
+    AMZ_CHECK_CUDA(cudaMemcpyAsync(&err, b->err, sizeof(int), cudaMemcpyDeviceToHost, s), "plr_size");
+    AMZ_CHECK_CUDA(cudaStreamSynchronize(s), "plr_size");
+    *size = meta[0];
+    if (err) {
+        cudaMemsetAsync(b->err, 0, sizeof(int), s);
+        cudaStreamSynchronize(s);
+        return fail(AMZ_ECONTRACT, "sampled from an empty level buffer");
+    }
+    return 0;
+}
+
+int amz_plr_export(amz_plr_t *b, amz_level_t *levels, double *score, double *max_ret, int64_t *last, int64_t *seq,
+                   int64_t *meta, void *stream) {
+    if (!b) return fail(AMZ_ECONFIG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t K = (size_t)b->D.K;
+    if (levels) cudaMemcpyAsync(levels, b->D.levels, K * sizeof(amz_level_t), cudaMemcpyDeviceToDevice, s);
+    if (score) cudaMemcpyAsync(score, b->D.score, K * 8, cudaMemcpyDeviceToDevice, s);
+    if (max_ret) cudaMemcpyAsync(max_ret, b->D.maxret, K * 8, cudaMemcpyDeviceToDevice, s);
+    if (last) cudaMemcpyAsync(last, b->D.last, K * 8, cudaMemcpyDeviceToDevice, s);
+    if (seq) cudaMemcpyAsync(seq, b->D.seq, K * 8, cudaMemcpyDeviceToDevice, s);
+    if (meta) cudaMemcpyAsync(meta, b->D.meta, 16, cudaMemcpyDeviceToDevice, s);
+    return cuda_status("plr_export");
+}
+
+int amz_plr_import(amz_plr_t *b, const amz_level_t *levels, const double *score, const double *max_ret,
+                   const int64_t *last, const int64_t *seq, const int64_t *meta, void *stream) {
+    if (!b || !levels || !score || !max_ret || !last || !seq || !meta) return fail(AMZ_ECONFIG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t K = (size_t)b->D.K;
+    cudaMemcpyAsync(b->D.levels, levels, K * sizeof(amz_level_t), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(b->D.score, score, K * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(b->D.maxret, max_ret, K * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(b->D.last, last, K * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(b->D.seq, seq, K * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(b->D.meta, meta, 16, cudaMemcpyDeviceToDevice, s);
+    return cuda_status("plr_import");
 }
 
 }  // extern "C"

@@ -53,4 +53,29 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
                      double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
                      cudaStream_t s, int do_gae = 1);
 
+// PLR buffer (amz_plr.cu)
+struct PlrDev {
+    int64_t K;
+    amz_level_t *levels;
+    double *score;
+    double *maxret;
+    int64_t *last;
+    int64_t *seq;
+    int64_t *meta;  // [0] size, [1] next_seq
+};
+struct UpdScratch {
+    int32_t *init_match;  // [n]
+    int32_t *twin_first;  // [n]
+    int32_t *keyslot;     // [n] current slot of the key group led by this candidate (or -1)
+    int32_t *rel;         // [n] compacted relevant candidate ids
+    uint32_t *chash;      // [hsize] candidate hash table (index + 1)
+    int64_t cap;
+};
+int launch_plr_sample(const PlrDev &D, const amz_seed_t &key, int64_t n, double omr, double rho, const double *lut,
+                      int64_t iter, int32_t *slots, amz_level_t *levels, double *maxret, double *score, int *err,
+                      cudaStream_t s);
+int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs, const double *cm, int64_t n,
+                      int64_t iter, const UpdScratch &W, cudaStream_t s);
+int launch_top_q(const double *scores, int64_t n, int q, int32_t *out, cudaStream_t s);
+
 }  // namespace amz

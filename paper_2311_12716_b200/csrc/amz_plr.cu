@@ -1,0 +1,611 @@
+// amz_plr.cu -- device-resident PLR level buffer: rank-prioritised replay sampling and
+// the sequential buffer_update of SPEC.md:373-377, made fast without changing its
+// result.  Semantics (and the open choices SPEC leaves, pinned the same way) follow
+// oracle/plr_np.py.
+//
+// Buffer arrays live in HBM (slots 0..size-1 are valid; slots fill in order and are
+// only ever overwritten by eviction).  Both kernels run as ONE CTA: K <= 4096 fits
+// its shared memory, and the sampler's cumsum and the update's candidate loop are
+// inherently ordered.
+//
+// Sampling (k_plr_sample):
+//   1. rank: CUB block radix sort, (seq asc) then stable (score desc)
+//   2. w = LUT[rank]  (host LUT (1/r)^(1/beta), computed by numpy -> bit-exact)
+//   3. sum(w) in numpy's pairwise order (parallel leaves, ordered combine)
+//   4. P = (1-rho) w/sum(w) + rho st/sum(st); cdf = sequential cumsum / cdf[-1]
+//      (numpy Generator.choice), u_i = i-th random() of the key's stream
+//      (counter-based: block i/4 of Philox), slot_i = searchsorted(cdf, u_i, 'right')
+// Update (k_plr_update): see the comment above the kernel.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cub/block/block_radix_sort.cuh>
+
+#include "amz_internal.h"
+
+namespace amz {
+
+constexpr int kPlrThreads = 1024;
+constexpr int kPlrMaxK = 4096;
+constexpr int kHash = 8192;  // smem hash table entries (>= 2 * K)
+
+__device__ __forceinline__ uint32_t level_hash(const uint4 &w, uint32_t pose) {
+    uint32_t h = 0x9E3779B9u;
+    h = (h ^ w.x) * 0x85EBCA6Bu;
+    h = (h ^ w.y) * 0xC2B2AE35u;
+    h = (h ^ w.z) * 0x85EBCA6Bu;
+    h = (h ^ w.w) * 0xC2B2AE35u;
+    h = (h ^ pose) * 0x27D4EB2Fu;
+    return h ^ (h >> 15);
+}
+
+// pose word = agent_r | agent_c<<8 | agent_dir<<16 | goal_r<<24, second word goal_c
+__device__ __forceinline__ void level_key(const amz_level_t *lv, uint4 &w, uint32_t &p0, uint32_t &p1) {
+    w = *reinterpret_cast<const uint4 *>(lv->walls);
+    const uint2 p = *reinterpret_cast<const uint2 *>(&lv->agent_r);
+    p0 = p.x;
+    p1 = p.y & 0xFFu;
+}
+
+__device__ __forceinline__ bool key_eq(const amz_level_t *a, const uint4 &w, uint32_t p0, uint32_t p1) {
+    uint4 x;
+    uint32_t q0, q1;
+    level_key(a, x, q0, q1);
+    return x.x == w.x && x.y == w.y && x.z == w.z && x.w == w.w && q0 == p0 && q1 == p1;
+}
+
+// numpy float64 maximum/ordering helpers
+__device__ __forceinline__ bool entry_less(double sa, int64_t la, int64_t qa, double sb, int64_t lb, int64_t qb) {
+    if (sa != sb) return sa < sb;
+    if (la != lb) return la < lb;
+    return qa < qb;
+}
+
+// ---------------------------------------------------------------------------------
+// numpy pairwise sum of x[0..n) evaluated by a whole CTA (leaves in parallel).
+// Returns the sum in thread 0 (valid after the call in all threads via smem).
+// ---------------------------------------------------------------------------------
+__device__ double block_pairwise_sum(const double *x, int n, double *leafbuf /* >= 64 */, int *leafinfo /* >= 3*64+1 */) {
+    // thread 0 walks numpy's recursion (pw(s, n) = n <= 128 ? leaf : pw(left) + pw(right),
+    // left length n/2 rounded down to a multiple of 8) and records, per leaf, its range
+    // and how many pending sums close after it.
+    if (threadIdx.x == 0) {
+        int fs[24], fn[24], st[24];
+        int fp = 1, nl = 0;
+        fs[0] = 0;
+        fn[0] = n;
+        st[0] = 0;
+        while (fp > 0) {
+            const int i = fp - 1;
+            if (st[i] == 0 && fn[i] <= 128) {
+                leafinfo[1 + 3 * nl] = fs[i];
+                leafinfo[2 + 3 * nl] = fn[i];
+                leafinfo[3 + 3 * nl] = 0;
+                nl++;
+                fp--;
+            } else if (st[i] < 2) {
+                int n2 = fn[i] / 2;
+                n2 -= n2 % 8;
+                const int cs = st[i] == 0 ? fs[i] : fs[i] + n2;
+                const int cn = st[i] == 0 ? n2 : fn[i] - n2;
+                st[i]++;
+                fs[fp] = cs;
+                fn[fp] = cn;
+                st[fp] = 0;
+                fp++;
+            } else {
+                leafinfo[3 + 3 * (nl - 1)]++;
+                fp--;
+            }
+        }
+        leafinfo[0] = nl;
+    }
+    __syncthreads();
+    const int nl = leafinfo[0];
+    for (int li = threadIdx.x; li < nl; li += blockDim.x) {
+        const int s = leafinfo[1 + 3 * li], len = leafinfo[2 + 3 * li];
+        double res;
+        if (len < 8) {
+            res = 0.0;
+            for (int k = 0; k < len; k++) res = res + x[s + k];
+        } else {
+            double r[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) r[k] = x[s + k];
+            int k = 8;
+            const int l8 = len - len % 8;
+            for (; k < l8; k += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) r[j] = r[j] + x[s + k + j];
+            }
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+            for (; k < len; k++) res = res + x[s + k];
+        }
+        leafbuf[li] = res;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double stk[40];
+        int sp = 0;
+        for (int li = 0; li < nl; li++) {
+            stk[sp++] = leafbuf[li];
+            for (int a = 0; a < leafinfo[3 + 3 * li]; a++) {
+                double b = stk[--sp];
+                double c = stk[--sp];
+                stk[sp++] = c + b;
+            }
+        }
+        leafbuf[0] = stk[0];
+    }
+    __syncthreads();
+    return leafbuf[0];
+}
+
+// ---------------------------------------------------------------------------------
+// sampling
+// ---------------------------------------------------------------------------------
+struct SampleSmem {
+    typename cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int>::TempStorage sort;
+    double p[kPlrMaxK];
+    double leaf[64];
+    int leafinfo[3 * 64 + 4];
+    unsigned long long st_total;
+    int rank_slot[kPlrMaxK];
+};
+
+__global__ void __launch_bounds__(kPlrThreads, 1)
+    k_plr_sample(PlrDev D, amz_seed_t key, int64_t n, double one_minus_rho, double rho,
+                 const double *__restrict__ lut, int64_t iter, int32_t *__restrict__ slots_out,
+                 amz_level_t *__restrict__ levels_out, double *__restrict__ maxret_out,
+                 double *__restrict__ score_out, int *__restrict__ err) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    SampleSmem &S = *reinterpret_cast<SampleSmem *>(smraw);
+    const int tid = threadIdx.x;
+    const int size = (int)D.meta[0];
+    if (size <= 0) {
+        if (tid == 0) atomicOr(err, 2);
+        return;
+    }
+    // ---- 1. ranks: sort by seq asc, then stable by score desc ----
+    using Sort = cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int>;
+    unsigned long long keys[4];
+    int vals[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int i = tid * 4 + k;
+        keys[k] = i < size ? (unsigned long long)D.seq[i] : ~0ull;
+        vals[k] = i;
+    }
+    Sort(S.sort).Sort(keys, vals);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int i = vals[k];
+        // descending score = ascending bitwise-inverted key; non-negative doubles order like their bits
+        unsigned long long b = 0ull;
+        if (i < size) {
+            double s = D.score[i];
+            s = s == 0.0 ? 0.0 : s;  // -0.0 ties with 0.0, as in numpy's sort
+            unsigned long long u = (unsigned long long)__double_as_longlong(s);
+            // total order for all doubles: flip negatives entirely, positives' sign bit
+            u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+            b = ~u;
+        } else {
+            b = ~0ull;
+        }
+        keys[k] = b;
+    }
+    Sort(S.sort).Sort(keys, vals);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int pos = tid * 4 + k;
+        if (vals[k] < size) S.rank_slot[vals[k]] = pos;  // rank - 1
+    }
+    if (tid == 0) S.st_total = 0ull;
+    __syncthreads();
+    // ---- 2./3. weights and their pairwise sum (slot order) ----
+    unsigned long long my_st = 0ull;
+    for (int i = tid; i < size; i += blockDim.x) {
+        S.p[i] = lut[S.rank_slot[i]];
+        my_st += (unsigned long long)(iter - D.last[i]);
+    }
+    // staleness total (exact integer sum)
+    for (int o = 16; o > 0; o >>= 1) my_st += __shfl_down_sync(0xFFFFFFFFu, my_st, o);
+    if ((tid & 31) == 0) atomicAdd(&S.st_total, my_st);
+    const double wsum = block_pairwise_sum(S.p, size, S.leaf, S.leafinfo);
+    const long long tot = (long long)S.st_total;
+    // ---- 4. P, cdf ----
+    for (int i = tid; i < size; i += blockDim.x) {
+        const double ps = S.p[i] / wsum;
+        if (tot == 0) {
+            S.p[i] = ps;
+        } else {
+            const double pc = (double)(iter - D.last[i]) / (double)tot;
+            S.p[i] = one_minus_rho * ps + rho * pc;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < size; i++) {
+            acc = acc + S.p[i];
+            S.p[i] = acc;
+        }
+    }
+    __syncthreads();
+    const double last_cdf = S.p[size - 1];
+    __syncthreads();
+    for (int i = tid; i < size; i += blockDim.x) S.p[i] = S.p[i] / last_cdf;
+    __syncthreads();
+    // ---- draws ----
+    uint64_t k0, k1;
+    seed_key(key, k0, k1);
+    for (int64_t d = tid; d < n; d += blockDim.x) {
+        uint64_t o[4];
+        philox_block((uint64_t)(d >> 2) + 1ull, k0, k1, o[0], o[1], o[2], o[3]);
+        const uint64_t r = o[d & 3];
+        const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
+        // searchsorted(cdf, u, side='right'): first index with cdf[idx] > u
+        int lo = 0, hi = size;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (S.p[mid] <= u)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        const int slot = lo < size ? lo : size - 1;
+        slots_out[d] = slot;
+        if (levels_out) levels_out[d] = D.levels[slot];
+        if (maxret_out) maxret_out[d] = D.maxret[slot];
+        if (score_out) score_out[d] = D.score[slot];
+    }
+    __syncthreads();
+    // sampled entries: last_sampled = iter (after every probability used the old values)
+    for (int64_t d = tid; d < n; d += blockDim.x) D.last[slots_out[d]] = iter;
+}
+
+// ---------------------------------------------------------------------------------
+// update
+//
+// Exact sequential semantics, cheap in practice:
+//   A  (all threads)  smem hash of the current buffer keys; each candidate looks up
+//                     its initial slot (init_match) and its first in-batch twin
+//                     (twin_first, via a global hash with atomicMin)
+//   B  (all threads)  m_low = min(current min score, scores of candidates that can
+//                     update in place).  If the buffer starts full, a candidate with
+//                     no key match and score <= m_low can never enter (the min never
+//                     drops below m_low), so it is skipped; everything else is
+//                     "relevant" and compacted in order.
+//   C  (warp 0)       replays the relevant candidates in order: in-place updates,
+//                     fill inserts, evictions of the (score, last_sampled, seq)
+//                     minimum (recomputed lazily by the warp when a candidate needs it).
+// ---------------------------------------------------------------------------------
+struct UpdSmem {
+    double score[kPlrMaxK];
+    int64_t last[kPlrMaxK];
+    int64_t seq[kPlrMaxK];
+    uint32_t hash[kHash];
+    int owner[kPlrMaxK];      // first-candidate index of the key now in the slot, -1 = initial entry
+    uint32_t replaced[kPlrMaxK / 32];
+    double mlow;
+    int n_rel;
+    int full;
+};
+
+__global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
+                                int64_t hsize) {
+    // twin detection over candidates: global open-addressing table keeps min index
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        uint4 w;
+        uint32_t p0, p1;
+        level_key(cand + c, w, p0, p1);
+        uint32_t h = level_hash(w, p0 ^ (p1 << 24)) & (uint32_t)(hsize - 1);
+        while (true) {
+            uint32_t cur = W.chash[h];
+            if (cur == 0u) {
+                uint32_t prev = atomicCAS(&W.chash[h], 0u, (uint32_t)(c + 1));
+                if (prev == 0u) break;
+                cur = prev;
+            }
+            if (key_eq(cand + (cur - 1), w, p0, p1)) {
+                atomicMin(&W.chash[h], (uint32_t)(c + 1));
+                break;
+            }
+            h = (h + 1) & (uint32_t)(hsize - 1);
+        }
+        W.keyslot[c] = -1;
+    }
+}
+
+__global__ void k_plr_cand_twin(const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W, int64_t hsize) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        uint4 w;
+        uint32_t p0, p1;
+        level_key(cand + c, w, p0, p1);
+        uint32_t h = level_hash(w, p0 ^ (p1 << 24)) & (uint32_t)(hsize - 1);
+        while (true) {
+            uint32_t cur = W.chash[h];
+            if (cur != 0u && key_eq(cand + (cur - 1), w, p0, p1)) {
+                W.twin_first[c] = (int32_t)(cur - 1);
+                break;
+            }
+            h = (h + 1) & (uint32_t)(hsize - 1);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPlrThreads, 1)
+    k_plr_update(PlrDev D, const amz_level_t *__restrict__ cand, const double *__restrict__ cscore,
+                 const double *__restrict__ cmax, int64_t n, int64_t iter, UpdScratch W) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    UpdSmem &S = *reinterpret_cast<UpdSmem *>(smraw);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int K = (int)D.K;
+    int size = (int)D.meta[0];
+    // ---- A: load buffer scalars + key hash ----
+    for (int i = tid; i < kHash; i += blockDim.x) S.hash[i] = 0u;
+    for (int i = tid; i < kPlrMaxK / 32; i += blockDim.x) S.replaced[i] = 0u;
+    if (tid == 0) {
+        S.n_rel = 0;
+        S.full = size >= K;
+    }
+    __syncthreads();
+    double my_min = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+    for (int i = tid; i < size; i += blockDim.x) {
+        S.score[i] = D.score[i];
+        S.last[i] = D.last[i];
+        S.seq[i] = D.seq[i];
+        S.owner[i] = -1;
+        my_min = fmin(my_min, S.score[i]);
+        uint4 w;
+        uint32_t p0, p1;
+        level_key(D.levels + i, w, p0, p1);
+        uint32_t h = level_hash(w, p0 ^ (p1 << 24)) & (kHash - 1);
+        while (atomicCAS(&S.hash[h], 0u, (uint32_t)(i + 1)) != 0u) h = (h + 1) & (kHash - 1);
+    }
+    __syncthreads();
+    for (int64_t c = tid; c < n; c += blockDim.x) {
+        uint4 w;
+        uint32_t p0, p1;
+        level_key(cand + c, w, p0, p1);
+        uint32_t h = level_hash(w, p0 ^ (p1 << 24)) & (kHash - 1);
+        int m = -1;
+        while (true) {
+            uint32_t cur = S.hash[h];
+            if (cur == 0u) break;
+            if (key_eq(D.levels + (cur - 1), w, p0, p1)) {
+                m = (int)(cur - 1);
+                break;
+            }
+            h = (h + 1) & (kHash - 1);
+        }
+        W.init_match[c] = m;
+        // candidates that can update an entry in place bound the running minimum from below
+        if (m >= 0 || W.twin_first[c] != (int32_t)c) my_min = fmin(my_min, cscore[c]);
+    }
+    // block min
+    for (int o = 16; o > 0; o >>= 1) my_min = fmin(my_min, __shfl_xor_sync(0xFFFFFFFFu, my_min, o));
+    __shared__ double wmin[32];
+    if (lane == 0) wmin[tid >> 5] = my_min;
+    __syncthreads();
+    if (tid == 0) {
+        double m = wmin[0];
+        for (int k = 1; k < (int)(blockDim.x >> 5); k++) m = fmin(m, wmin[k]);
+        S.mlow = m;
+    }
+    __syncthreads();
+    // ---- B: relevant candidates, compacted in order (block-wide, chunk by chunk) ----
+    __shared__ int wcount[32];
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t c = base + tid;
+        bool rel = false;
+        if (c < n) {
+            const bool later_twin = W.twin_first[c] != (int32_t)c;
+            rel = !S.full || W.init_match[c] >= 0 || later_twin || !(cscore[c] <= S.mlow);
+        }
+        unsigned b = __ballot_sync(0xFFFFFFFFu, rel);
+        if (lane == 0) wcount[tid >> 5] = __popc(b);
+        __syncthreads();
+        if (tid == 0) {
+            int acc = S.n_rel;
+            for (int k = 0; k < (int)(blockDim.x >> 5); k++) {
+                int v = wcount[k];
+                wcount[k] = acc;
+                acc += v;
+            }
+            S.n_rel = acc;
+        }
+        __syncthreads();
+        if (rel) W.rel[wcount[tid >> 5] + __popc(b & ((1u << lane) - 1u))] = (int32_t)c;
+        __syncthreads();
+    }
+    // A skipped first occurrence is never inserted (score <= mlow), so its later twins,
+    // which are always relevant, correctly find no entry for the key (keyslot = -1).
+    if (tid >= 32) return;
+
+    // ---- C: ordered replay by warp 0 ----
+    const int nrel = S.n_rel;
+    int64_t next_seq = D.meta[1];
+    int minslot = -1;
+    bool minvalid = false;
+    auto recompute_min = [&]() {
+        double bs = 0.0;
+        int64_t bl = 0, bq = 0;
+        int bi = -1;
+        for (int i = lane; i < size; i += 32) {
+            const double s = S.score[i];
+            const int64_t l = S.last[i], q = S.seq[i];
+            if (bi < 0 || entry_less(s, l, q, bs, bl, bq)) {
+                bs = s;
+                bl = l;
+                bq = q;
+                bi = i;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double s2 = __shfl_xor_sync(0xFFFFFFFFu, bs, o);
+            const long long l2 = __shfl_xor_sync(0xFFFFFFFFu, (long long)bl, o);
+            const long long q2 = __shfl_xor_sync(0xFFFFFFFFu, (long long)bq, o);
+            const int i2 = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+            if (i2 >= 0 && (bi < 0 || entry_less(s2, l2, q2, bs, bl, bq))) {
+                bs = s2;
+                bl = l2;
+                bq = q2;
+                bi = i2;
+            }
+        }
+        minslot = bi;
+        minvalid = true;
+    };
+    for (int r = 0; r < nrel; r++) {
+        const int c = W.rel[r];
+        const double sc = cscore[c];
+        const double mr = cmax[c];
+        const int f = W.twin_first[c];
+        int present = -1;
+        const int im = W.init_match[c];
+        if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
+        if (present < 0 && f != c) present = W.keyslot[f];
+        __syncwarp();
+        if (present >= 0) {
+            if (lane == 0) {
+                S.score[present] = sc;
+                D.maxret[present] = mr;
+            }
+            __syncwarp();
+            if (minvalid) {
+                if (present == minslot)
+                    minvalid = false;  // its score changed; recompute lazily
+                else if (entry_less(sc, S.last[present], S.seq[present], S.score[minslot], S.last[minslot],
+                                    S.seq[minslot]))
+                    minslot = present;
+            }
+            continue;
+        }
+        int slot;
+        if (size < K) {
+            slot = size++;
+        } else {
+            if (!minvalid) recompute_min();
+            if (!(sc > S.score[minslot])) continue;
+            slot = minslot;
+            minvalid = false;
+            const int ow = S.owner[slot];
+            if (ow >= 0 && lane == 0) W.keyslot[ow] = -1;
+        }
+        if (lane == 0) {
+            S.score[slot] = sc;
+            S.last[slot] = iter;
+            S.seq[slot] = next_seq;
+            S.owner[slot] = f;
+            S.replaced[slot >> 5] |= 1u << (slot & 31);
+            W.keyslot[f] = slot;
+            D.maxret[slot] = mr;
+            D.levels[slot] = cand[c];
+        }
+        next_seq++;
+        __syncwarp();
+        if (minvalid && entry_less(sc, iter, next_seq - 1, S.score[minslot], S.last[minslot], S.seq[minslot]))
+            minslot = slot;
+    }
+    __syncwarp();
+    for (int i = lane; i < size; i += 32) {
+        D.score[i] = S.score[i];
+        D.last[i] = S.last[i];
+        D.seq[i] = S.seq[i];
+    }
+    if (lane == 0) {
+        D.meta[0] = size;
+        D.meta[1] = next_seq;
+    }
+}
+
+// top-q replay lanes by score (ties -> lower lane index), single CTA
+__global__ void k_top_q(const double *__restrict__ scores, int64_t n, int q, int32_t *__restrict__ out) {
+    __shared__ double bs[32];
+    __shared__ int bi[32];
+    __shared__ int chosen[64];
+    for (int k = 0; k < q; k++) {
+        double best = 0.0;
+        int besti = -1;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            bool skip = false;
+            for (int j = 0; j < k; j++) skip |= chosen[j] == (int)i;
+            if (skip) continue;
+            const double s = scores[i];
+            if (besti < 0 || s > best || (s == best && (int)i < besti)) {
+                best = s;
+                besti = (int)i;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double s2 = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+            const int i2 = __shfl_xor_sync(0xFFFFFFFFu, besti, o);
+            if (i2 >= 0 && (besti < 0 || s2 > best || (s2 == best && i2 < besti))) {
+                best = s2;
+                besti = i2;
+            }
+        }
+        if ((threadIdx.x & 31) == 0) {
+            bs[threadIdx.x >> 5] = best;
+            bi[threadIdx.x >> 5] = besti;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double b = 0.0;
+            int ix = -1;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+                if (bi[w] >= 0 && (ix < 0 || bs[w] > b || (bs[w] == b && bi[w] < ix))) {
+                    b = bs[w];
+                    ix = bi[w];
+                }
+            }
+            chosen[k] = ix;
+            out[k] = ix;
+        }
+        __syncthreads();
+    }
+}
+
+size_t plr_sample_smem() { return sizeof(SampleSmem); }
+size_t plr_update_smem() { return sizeof(UpdSmem); }
+
+int launch_plr_sample(const PlrDev &D, const amz_seed_t &key, int64_t n, double omr, double rho, const double *lut,
+                      int64_t iter, int32_t *slots, amz_level_t *levels, double *maxret, double *score, int *err,
+                      cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_plr_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SampleSmem));
+        attr = true;
+    }
+    k_plr_sample<<<1, kPlrThreads, sizeof(SampleSmem), s>>>(D, key, n, omr, rho, lut, iter, slots, levels, maxret,
+                                                             score, err);
+    return 0;
+}
+
+int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs, const double *cm, int64_t n,
+                      int64_t iter, const UpdScratch &W, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_plr_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
+        attr = true;
+    }
+    if (n <= 0) return 0;
+    int64_t hsize = 1;
+    while (hsize < 2 * n) hsize <<= 1;
+    cudaMemsetAsync(W.chash, 0, hsize * sizeof(uint32_t), s);
+    const int g = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+    k_plr_cand_prep<<<g, 256, 0, s>>>(D, cand, n, W, hsize);
+    k_plr_cand_twin<<<g, 256, 0, s>>>(cand, n, W, hsize);
+    k_plr_update<<<1, kPlrThreads, sizeof(UpdSmem), s>>>(D, cand, cs, cm, n, iter, W);
+    return 0;
+}
+
+int launch_top_q(const double *scores, int64_t n, int q, int32_t *out, cudaStream_t s) {
+    k_top_q<<<1, 256, 0, s>>>(scores, n, q, out);
+    return 0;
+}
+
+}  // namespace amz

@@ -1,0 +1,108 @@
+"""Multi-GPU plumbing for the parallel PLR/ACCEL hot path.
+
+Lanes shard by global lane index: rank r of D owns global lanes [r*L/D, (r+1)*L/D) of
+the iteration's lane layout, and every level key is a function of the global index,
+so a D-GPU iteration equals the 1-GPU iteration lane for lane.  The one exchange step
+is the candidate records (level 32 B + score f64 + max return f64 = 48 B per lane),
+all-gathered in global lane order once per iteration; every rank then applies the same
+deterministic buffer update, keeping the buffer replicated.  ``buffer_digest`` +
+``check_replicas`` is the drift check (the analogue of the shard-sync check at
+agents/ppo.py:323-328).
+
+torch.distributed carries the bytes: NCCL (NVLink/NVSwitch) on GPUs, gloo on CPU for
+the host-logic tests.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+from .errors import RunnerFault, ShapeError
+
+RECORD_WORDS = 12  # int32 words per candidate record
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def world():
+    torch = _torch()
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        return torch.distributed.get_rank(), torch.distributed.get_world_size()
+    return 0, 1
+
+
+def shard(n_lanes: int, rank: int, world_size: int) -> tuple[int, int]:
+    """Global [lo, hi) lane range of ``rank`` (equal shards; L must divide evenly)."""
+    if n_lanes % world_size:
+        raise ShapeError(f"{n_lanes} lanes do not split evenly over {world_size} ranks")
+    per = n_lanes // world_size
+    return rank * per, (rank + 1) * per
+
+
+def pack_candidates(levels, scores, max_returns):
+    """[n, 8] int32 levels + f64 scores + f64 max returns -> [n, 12] int32 records."""
+    torch = _torch()
+    n = levels.shape[0]
+    rec = torch.empty((n, RECORD_WORDS), dtype=torch.int32, device=levels.device)
+    rec[:, :8] = levels
+    rec[:, 8:10] = scores.to(torch.float64).contiguous().view(torch.int32).reshape(n, 2)
+    rec[:, 10:12] = max_returns.to(torch.float64).contiguous().view(torch.int32).reshape(n, 2)
+    return rec
+
+
+def unpack_candidates(rec):
+    torch = _torch()
+    n = rec.shape[0]
+    levels = rec[:, :8].contiguous()
+    scores = rec[:, 8:10].contiguous().view(torch.float64).reshape(n)
+    max_returns = rec[:, 10:12].contiguous().view(torch.float64).reshape(n)
+    return levels, scores, max_returns
+
+
+def all_gather_records(rec):
+    """Concatenate every rank's [n, 12] records in rank order (= global lane order)."""
+    torch = _torch()
+    rank, ws = world()
+    if ws == 1:
+        return rec
+    rec = rec.contiguous()
+    if torch.distributed.get_backend() == "nccl":
+        out = torch.empty((rec.shape[0] * ws, rec.shape[1]), dtype=rec.dtype, device=rec.device)
+        torch.distributed.all_gather_into_tensor(out, rec)
+        return out
+    parts = [torch.empty_like(rec) for _ in range(ws)]
+    torch.distributed.all_gather(parts, rec)
+    return torch.cat(parts)
+
+
+def gather_candidates(levels, scores, max_returns):
+    return unpack_candidates(all_gather_records(pack_candidates(levels, scores, max_returns)))
+
+
+def buffer_digest(state: dict) -> int:
+    """64-bit digest of a buffer state (valid slots only)."""
+    size = int(state["meta"][0].item())
+    h = hashlib.blake2b(digest_size=8)
+    for k in ("levels", "score", "max_return", "last_sampled", "seq"):
+        h.update(state[k][:size].detach().cpu().contiguous().numpy().tobytes())
+    h.update(state["meta"].detach().cpu().numpy().tobytes())
+    return int.from_bytes(h.digest(), "little") & 0x7FFFFFFFFFFFFFFF
+
+
+def check_replicas(digest: int, device=None) -> None:
+    """Raise RunnerFault if the ranks' buffers differ (all-reduce MIN and MAX)."""
+    torch = _torch()
+    rank, ws = world()
+    if ws == 1:
+        return
+    dev = device if device is not None and torch.distributed.get_backend() == "nccl" else "cpu"
+    lo = torch.tensor([digest], dtype=torch.int64, device=dev)
+    hi = lo.clone()
+    torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+    torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+    if int(lo.item()) != int(hi.item()):
+        raise RunnerFault(f"PLR buffer replicas diverged (rank {rank})")

@@ -1,0 +1,131 @@
+"""CUDA PLR buffer / sampler / parallel PLR-ACCEL iterations vs the sequential oracle."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import amaze_np as onp  # noqa: E402
+from oracle import plr_np  # noqa: E402
+from tests.helpers import records_to_rows, tensor_rows  # noqa: E402
+
+import paper_2311_12716_b200 as amz  # noqa: E402
+from paper_2311_12716_b200.buffer import AccelConfig, LevelBuffer, PlrConfig, top_q  # noqa: E402
+from paper_2311_12716_b200.level import records_to_tensor  # noqa: E402
+from paper_2311_12716_b200.plr import ParallelPLR  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _pool(n, seed=0):
+    p = onp.Params()
+    return onp.pack_levels([onp.sample_level(seed, (0, i), p) for i in range(n)], p)
+
+
+def _assert_same(gpu: LevelBuffer, ref: plr_np.LevelBuffer):
+    st = gpu.export()
+    size, nxt = (int(x) for x in st["meta"].cpu())
+    assert size == ref.size and nxt == ref.next_seq
+    lv, sc, mx, ls, sq = ref.snapshot()
+    assert np.array_equal(tensor_rows(st["levels"][:size]), records_to_rows(lv))
+    assert np.array_equal(st["score"][:size].cpu().numpy(), sc)
+    assert np.array_equal(st["max_return"][:size].cpu().numpy(), mx)
+    assert np.array_equal(st["last_sampled"][:size].cpu().numpy(), ls)
+    assert np.array_equal(st["seq"][:size].cpu().numpy(), sq)
+
+
+@pytest.mark.parametrize("K,n,pool", [(2, 3, 4), (16, 40, 60), (100, 300, 500), (4000, 8192, 12000)])
+def test_update_tie_heavy_matches_oracle(K, n, pool):
+    rng = np.random.default_rng(K)
+    recs = _pool(pool, seed=K)
+    gpu = LevelBuffer(PlrConfig(buffer_size=K))
+    ref = plr_np.LevelBuffer(K)
+    for it in range(6):
+        idx = rng.integers(0, pool, n)  # in-batch twins and buffer duplicates
+        sc = rng.choice([0.0, 0.0, 0.0, -0.0, 0.05, 0.1, 0.1, 0.3, 0.7], n) + (it % 2) * rng.choice([0.0, 1e-3], n)
+        mx = rng.uniform(0, 1, n)
+        gpu.update(records_to_tensor(recs[idx]), torch.from_numpy(sc), torch.from_numpy(mx), it)
+        ref.update(recs[idx], sc, mx, it)
+        _assert_same(gpu, ref)
+
+
+def test_spec_update_example():
+    recs = _pool(3)
+    gpu = LevelBuffer(PlrConfig(buffer_size=2))
+    gpu.update(records_to_tensor(recs), torch.tensor([5.0, 1.0, 3.0]), torch.zeros(3), 0)
+    st = gpu.export()
+    assert sorted(st["score"][:2].cpu().tolist()) == [3.0, 5.0]
+
+
+@pytest.mark.parametrize("K,rho,beta", [(5, 0.3, 0.3), (100, 0.0, 1.0), (4000, 0.3, 0.3), (4000, 0.5, 0.3),
+                                        (777, 1.0, 0.5)])
+def test_sample_matches_numpy_choice(K, rho, beta):
+    rng = np.random.default_rng(K)
+    recs = _pool(K + 50, seed=1)
+    cfg = PlrConfig(buffer_size=K, staleness_coef=rho, temperature=beta)
+    gpu = LevelBuffer(cfg)
+    ref = plr_np.LevelBuffer(K)
+    for it in range(3):
+        idx = rng.permutation(K + 50)[:K]
+        sc = rng.choice([0.0, 0.2, 0.2, 0.4, 0.9], K) * rng.uniform(0.5, 1, K)
+        gpu.update(records_to_tensor(recs[idx]), torch.from_numpy(sc), torch.from_numpy(sc), it)
+        ref.update(recs[idx], sc, sc, it)
+    ocfg = plr_np.PlrConfig(buffer_size=K, staleness_coef=rho, temperature=beta)
+    for it in range(3, 7):
+        out = gpu.sample(amz.RngStream(11, (it, 2)), 2048, it)
+        want = ref.sample(11, (it, 2), 2048, ocfg, it)
+        assert np.array_equal(out["slots"].cpu().numpy(), want)
+        lv = ref.levels[want]
+        assert np.array_equal(tensor_rows(out["levels"]), records_to_rows(lv))
+        assert np.array_equal(out["scores"].cpu().numpy(), ref.score[want])
+    _assert_same(gpu, ref)
+
+
+def test_top_q():
+    rng = np.random.default_rng(0)
+    s = rng.choice([0.0, 0.5, 0.5, 1.0, 0.25], 1000)
+    got = top_q(torch.from_numpy(s).cuda(), 4).cpu().numpy()
+    assert np.array_equal(got, plr_np.top_q(s, 4))
+
+
+def _oracle_iteration(buf, seed, it, n, accel, cfg, acts, values, last):
+    p = onp.Params()
+    levels, prior, n_rep, _ = plr_np.compose_lanes(buf, seed, (), it, n, p, cfg, accel)
+    L = len(levels)
+    env = onp.AutoReset(L, p, "home")
+    obs = env.reset_to_levels(seed, (it, 4), onp.unpack_levels(levels, p))
+    view, dirs, rew, dn, _ = onp.rollout(env, obs, acts)
+    adv, _ = onp.gae(rew, values, dn, last, 0.995, 0.95)
+    sc, mx, _ = onp.lane_scores(values, adv, rew, dn, prior, cfg.score_fn)
+    buf.update(levels, sc, mx, it)
+    return levels, sc, mx, n_rep
+
+
+@pytest.mark.parametrize("accel", [None, (4, 20)])
+@pytest.mark.parametrize("score_fn", ["maxmc", "pvl"])
+def test_parallel_iterations_match_oracle(accel, score_fn):
+    n, T, K, seed = 48, 40, 64, 5
+    cfg = PlrConfig(buffer_size=K, score_fn=score_fn)
+    ocfg = plr_np.PlrConfig(buffer_size=K, score_fn=score_fn)
+    plr = ParallelPLR(n, amz.StaticParams(), cfg, amz.RngStream.from_seed(seed),
+                      AccelConfig(accel[1], accel[0]) if accel else None)
+    ref = plr_np.LevelBuffer(K)
+    rng = np.random.default_rng(1)
+    L = plr.L
+    for it in range(5):
+        acts = rng.integers(0, 3, (T, L)).astype(np.uint8)
+        values = rng.uniform(0, 0.3, (T, L))
+        last = rng.uniform(0, 0.3, L)
+        res = plr.iteration(it, torch.from_numpy(acts).cuda(), torch.from_numpy(values).cuda(),
+                            torch.from_numpy(last).cuda())
+        lv, sc, mx, n_rep = _oracle_iteration(ref, seed, it, n, accel, ocfg, acts, values, last)
+        assert res.n_replay == n_rep
+        assert np.array_equal(tensor_rows(res.levels), records_to_rows(lv))
+        assert np.array_equal(res.scores.cpu().numpy(), sc)
+        assert np.array_equal(res.max_returns.cpu().numpy(), mx)
+        _assert_same(plr.buffer, ref)
