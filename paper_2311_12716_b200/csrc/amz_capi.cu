@@ -156,6 +156,8 @@ int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.board, b * 16 * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.err, 4 * sizeof(int));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->term, 2 * sizeof(int));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.spec, b * sizeof(amz_level_t));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.spec_step, b * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMemset(e->E.err, 0, 4 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->term, 0, 2 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->E.st, 0, b * sizeof(uint4));
@@ -175,6 +177,8 @@ int amz_env_destroy(amz_env_t *e) {
     cudaFree(e->E.board);
     cudaFree(e->E.err);
     cudaFree(e->term);
+    cudaFree(e->E.spec);
+    cudaFree(e->E.spec_step);
     delete e;
     return 0;
 }

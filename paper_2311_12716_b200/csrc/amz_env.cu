@@ -13,28 +13,13 @@
 
 #include "amz_internal.h"
 #include "amz_render.cuh"
+#include "amz_sampler.cuh"
 
 namespace amz {
 
 // ---------------------------------------------------------------------------------
 // level generation / mutation / validation
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_sample_levels(Geo G, amz_seed_t prefix, uint32_t lane0,
-                                                       const uint32_t *__restrict__ lane_ids, int64_t n,
-                                                       amz_level_t *__restrict__ out) {
-    extern __shared__ uint8_t perm_smem[];
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    amz_seed_t s = prefix;
-    seed_absorb(s, lane_ids ? lane_ids[i] : lane0 + (uint32_t)i);
-    Stream g;
-    g.init(s);
-    Mask m;
-    int ar, ac, ad, gr, gc;
-    sample_level_dev(g, G, perm_smem + threadIdx.x, blockDim.x, m, ar, ac, ad, gr, gc);
-    store_level(out + i, m, ar, ac, ad, gr, gc);
-}
-
 __global__ void __launch_bounds__(128) k_mutate_levels(Geo G, amz_seed_t prefix, uint32_t lane0, int64_t n,
                                                        const amz_level_t *__restrict__ parents,
                                                        const int32_t *__restrict__ pidx, int n_edits,
@@ -80,34 +65,6 @@ __global__ void k_check_levels(Geo G, const amz_level_t *__restrict__ lv, int64_
 // ---------------------------------------------------------------------------------
 // lane state helpers
 // ---------------------------------------------------------------------------------
-struct LaneRec {
-    LaneDyn s;
-    int gr, gc, hr, hc, hd;
-    bool term;
-};
-
-__device__ __forceinline__ LaneRec unpack_st(uint4 v) {
-    LaneRec L;
-    L.s.r = v.x & 0xFF;
-    L.s.c = (v.x >> 8) & 0xFF;
-    L.s.d = (v.x >> 16) & 0xFF;
-    L.term = (v.x >> 24) != 0;
-    L.gr = v.y & 0xFF;
-    L.gc = (v.y >> 8) & 0xFF;
-    L.hr = (v.y >> 16) & 0xFF;
-    L.hc = v.y >> 24;
-    L.hd = v.z & 0xFF;
-    L.s.time = (int)(v.z >> 8);
-    return L;
-}
-
-__device__ __forceinline__ uint4 pack_st(const LaneRec &L) {
-    return make_uint4((uint32_t)L.s.r | ((uint32_t)L.s.c << 8) | ((uint32_t)L.s.d << 16) |
-                          ((uint32_t)L.term << 24),
-                      (uint32_t)L.gr | ((uint32_t)L.gc << 8) | ((uint32_t)L.hr << 16) | ((uint32_t)L.hc << 24),
-                      (uint32_t)L.hd | ((uint32_t)L.s.time << 8), 0u);
-}
-
 // Copy a warp's staged V*V-byte records (stage = 32*VV bytes) to dst[0 .. nvalid*VV).
 __device__ __forceinline__ void warp_flush(const uint8_t *stage, uint8_t *dst, int nbytes, int lane) {
     if ((((uintptr_t)dst) & 15u) == 0 && (nbytes & 15) == 0) {
@@ -261,11 +218,10 @@ __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *_
                                                   double *__restrict__ reward, uint8_t *__restrict__ done,
                                                   double *__restrict__ solved, int64_t *__restrict__ times,
                                                   const int *__restrict__ term_in, int *__restrict__ term_out) {
-    extern __shared__ uint8_t smem[];
-    uint8_t *stage = smem;                    // 128 * V * V
-    uint8_t *perm = smem + 128 * V * V;       // ni * 128
+    __shared__ __align__(16) uint8_t stage[128 * V * V];
+    __shared__ __align__(16) uint32_t sw[4][kWNW];
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     if (mode == AMZ_RESET_NONE && *term_in > 0) {
         // step_batch raises on terminal lanes before touching anything (amaze/env.py:325-326)
@@ -275,27 +231,56 @@ __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *_
         }
         return;
     }
-    bool d_out = false;
-    if (l < E.B) {
-        LaneRec L = unpack_st(E.st[l]);
+    const bool live = l < E.B;
+    bool dn = false;
+    LaneRec L{};
+    uint32_t *bd = E.board + l;
+    if (live) {
+        L = unpack_st(E.st[l]);
         const int a = load_action(actions, adtype, l);
-        uint32_t *bd = E.board + l;
         const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, (int)E.B);
-        const bool dn = reached || L.s.time >= G.tep;
-        d_out = dn;
+        dn = reached || L.s.time >= G.tep;
         if (reward) reward[l] = reached ? goal_reward(L.s.time, G.tep) : 0.0;
         if (done) done[l] = dn;
         if (solved) solved[l] = reached ? 1.0 : 0.0;
         if (times) times[l] = L.s.time;
+    }
+    if (mode == AMZ_RESET_RESAMPLE) {
+        // the warp samples each finished lane's level cooperatively (amz_sampler.cuh)
+        unsigned todo = __ballot_sync(0xFFFFFFFFu, dn);
+        while (todo) {
+            const int tl = __ffs(todo) - 1;
+            todo &= todo - 1;
+            amz_seed_t sd = wrap;
+            seed_absorb(sd, step_idx);
+            seed_absorb(sd, E.lane_offset + (uint32_t)(wbase + tl));
+            uint64_t k0, k1;
+            seed_key(sd, k0, k1);
+            Mask m;
+            int ar, ac, ad, gr, gc;
+            warp_sample_level(k0, k1, G, sw[warp], m, ar, ac, ad, gr, gc);
+            if (lane == tl) {
+                build_board(m, G, bd, (int)E.B);
+                E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+                L.hr = ar;
+                L.hc = ac;
+                L.hd = ad;
+                L.gr = gr;
+                L.gc = gc;
+            }
+            __syncwarp();
+        }
+    }
+    if (live) {
         if (dn) {
             if (mode == AMZ_RESET_NONE) {
                 L.term = true;
             } else {
-                Mask m;
-                bool nl;
-                lane_autoreset(G, mode, wrap, step_idx, E.lane_offset + (uint32_t)l, L, m, perm + threadIdx.x,
-                               blockDim.x, bd, (int)E.B, nl);
-                if (nl) E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+                L.s.r = L.hr;
+                L.s.c = L.hc;
+                L.s.d = L.hd;
+                L.s.time = 0;
+                L.term = false;
             }
         }
         E.st[l] = pack_st(L);
@@ -304,7 +289,7 @@ __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *_
                                  stage + threadIdx.x * V * V);
     }
     if (mode == AMZ_RESET_NONE) {
-        unsigned b = __ballot_sync(0xFFFFFFFFu, d_out);
+        unsigned b = __ballot_sync(0xFFFFFFFFu, dn);
         if (lane == 0 && b) atomicAdd(term_out, __popc(b));
     }
     if (view) {
@@ -314,79 +299,6 @@ __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *_
             warp_flush(stage + (threadIdx.x & ~31) * V * V, view + wbase * V * V, nv * V * V, lane);
         }
     }
-}
-
-// ---------------------------------------------------------------------------------
-// fused T-step rollout: lane state in registers, boards in shared memory
-// ---------------------------------------------------------------------------------
-template <int V>
-__global__ void __launch_bounds__(128) k_env_rollout(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions,
-                                                     int mode, amz_seed_t wrap, uint32_t step0,
-                                                     uint8_t *__restrict__ view, uint8_t *__restrict__ dirs,
-                                                     double *__restrict__ reward, uint8_t *__restrict__ done,
-                                                     uint8_t *__restrict__ fview, uint8_t *__restrict__ fdir) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    constexpr int VV = V * V;
-    const int nt = blockDim.x;
-    uint32_t *board = reinterpret_cast<uint32_t *>(smem);  // [16][nt]
-    uint8_t *stage = smem + 16 * nt * 4;                   // [nt][VV]
-    uint8_t *perm = stage + nt * VV;                       // [ni][nt]
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int64_t l = (int64_t)blockIdx.x * blockDim.x + tid;
-    const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (tid & ~31);
-    const int64_t B = E.B;
-    const bool live = l < B;
-    const int nv = wbase < B ? (int)(((B - wbase) < 32) ? (B - wbase) : 32) : 0;
-    uint8_t *mystage = stage + tid * VV;
-    uint8_t *wstage = stage + (tid & ~31) * VV;
-    uint32_t *bd = board + tid;
-
-    LaneRec L;
-    Mask m;
-    bool lvl_changed = false;
-    if (live) {
-        L = unpack_st(E.st[l]);
-#pragma unroll
-        for (int k = 0; k < 16; k++) bd[k * nt] = E.board[k * B + l];
-    }
-    int a_next = (live && T > 0) ? actions[l] : 0;
-    for (int t = 0; t < T; t++) {
-        const int a = a_next;
-        if (live && t + 1 < T) a_next = actions[(int64_t)(t + 1) * B + l];
-        // observation before step t
-        if (live) {
-            lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, nt, mystage);
-            dirs[(int64_t)t * B + l] = (uint8_t)L.s.d;
-        }
-        __syncwarp();
-        if (nv) warp_flush(wstage, view + ((int64_t)t * B + wbase) * VV, nv * VV, lane);
-        if (live) {
-            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, nt);
-            const bool dn = reached || L.s.time >= G.tep;
-            reward[(int64_t)t * B + l] = reached ? goal_reward(L.s.time, G.tep) : 0.0;
-            done[(int64_t)t * B + l] = dn;
-            if (dn) {
-                bool nl;
-                lane_autoreset(G, mode, wrap, step0 + (uint32_t)t, E.lane_offset + (uint32_t)l, L, m, perm + tid,
-                               nt, bd, nt, nl);
-                lvl_changed |= nl;
-            }
-        }
-        __syncwarp();
-    }
-    // cursor observation + state write-back
-    if (live) {
-        lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, bd, nt, mystage);
-        if (fdir) fdir[l] = (uint8_t)L.s.d;
-        E.st[l] = pack_st(L);
-        if (lvl_changed) {
-            E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
-#pragma unroll
-            for (int k = 0; k < 16; k++) E.board[k * B + l] = bd[k * nt];
-        }
-    }
-    __syncwarp();
-    if (nv && fview) warp_flush(wstage, fview + wbase * VV, nv * VV, lane);
 }
 
 // ---------------------------------------------------------------------------------
@@ -400,14 +312,6 @@ static inline int lanes_per_cta(int64_t n) {
     const int64_t per_sm = (n + 147) / 148;
     int t = (int)(((per_sm + 31) / 32) * 32);
     return t < 32 ? 32 : (t > 128 ? 128 : t);
-}
-
-int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, const uint32_t *ids, int64_t n,
-                         amz_level_t *out, cudaStream_t s) {
-    if (n <= 0) return 0;
-    const int nt = lanes_per_cta(n);
-    k_sample_levels<<<blocks_for(n, nt), nt, nt * G.ni, s>>>(G, prefix, lane0, ids, n, out);
-    return 0;
 }
 
 int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
@@ -468,36 +372,9 @@ int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adty
                     cudaStream_t s) {
     if (E.B <= 0) return 0;
     const int V = G.V;
-    const int nt = lanes_per_cta(E.B);
-    size_t sm = 128 * V * V + (mode == AMZ_RESET_RESAMPLE ? nt * G.ni : 0);
-    AMZ_DISPATCH_V(V, (k_env_step<VT><<<blocks_for(E.B, nt), nt, sm, s>>>(G, E, actions, adtype, mode, wrap,
+    AMZ_DISPATCH_V(V, (k_env_step<VT><<<blocks_for(E.B, 128), 128, 0, s>>>(G, E, actions, adtype, mode, wrap,
                                                                           step_idx, view, dirs, reward, done,
                                                                           solved, times, term_in, term_out)));
-    return 0;
-}
-
-template <int V>
-static int rollout_smem_setup(size_t sm) {
-    static bool done_attr = false;
-    if (!done_attr) {
-        cudaFuncSetAttribute(k_env_rollout<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        done_attr = true;
-    }
-    return 0;
-}
-
-int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
-                       const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
-                       uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
-    if (E.B <= 0) return 0;
-    const int V = G.V;
-    const int nt = lanes_per_cta(E.B);
-    size_t sm = 16 * nt * 4 + nt * V * V + (mode == AMZ_RESET_RESAMPLE ? nt * G.ni : 0);
-    sm = (sm + 15) & ~(size_t)15;
-    AMZ_DISPATCH_V(V, (rollout_smem_setup<VT>(64 * 1024),
-                       k_env_rollout<VT><<<blocks_for(E.B, nt), nt, sm, s>>>(G, E, T, actions, mode, wrap, step0,
-                                                                            view, dirs, reward, done, fview,
-                                                                            fdir)));
     return 0;
 }
 

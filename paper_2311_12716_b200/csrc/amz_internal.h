@@ -16,6 +16,8 @@ struct EnvDev {
     uint4 *mask;
     uint32_t *board;  // [16][B]
     int *err;
+    amz_level_t *spec;    // [B] speculative timeout levels (amz_rollout.cu)
+    uint32_t *spec_step;  // [B] step index of spec[l] (0xFFFFFFFF = none)
 };
 
 // numpy pairwise summation schedule (numpy/_core/src/umath/loops_utils.h.src

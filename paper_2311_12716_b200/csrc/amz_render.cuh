@@ -135,4 +135,32 @@ __device__ __forceinline__ void lane_render(int r, int c, int d, int gr, int gc,
     }
 }
 
+struct LaneRec {
+    LaneDyn s;
+    int gr, gc, hr, hc, hd;
+    bool term;
+};
+
+__device__ __forceinline__ LaneRec unpack_st(uint4 v) {
+    LaneRec L;
+    L.s.r = v.x & 0xFF;
+    L.s.c = (v.x >> 8) & 0xFF;
+    L.s.d = (v.x >> 16) & 0xFF;
+    L.term = (v.x >> 24) != 0;
+    L.gr = v.y & 0xFF;
+    L.gc = (v.y >> 8) & 0xFF;
+    L.hr = (v.y >> 16) & 0xFF;
+    L.hc = v.y >> 24;
+    L.hd = v.z & 0xFF;
+    L.s.time = (int)(v.z >> 8);
+    return L;
+}
+
+__device__ __forceinline__ uint4 pack_st(const LaneRec &L) {
+    return make_uint4((uint32_t)L.s.r | ((uint32_t)L.s.c << 8) | ((uint32_t)L.s.d << 16) |
+                          ((uint32_t)L.term << 24),
+                      (uint32_t)L.gr | ((uint32_t)L.gc << 8) | ((uint32_t)L.hr << 16) | ((uint32_t)L.hc << 24),
+                      (uint32_t)L.hd | ((uint32_t)L.s.time << 8), 0u);
+}
+
 }  // namespace amz
