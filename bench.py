@@ -109,54 +109,68 @@ def _cpu_model():
 # clocks sampler
 # ------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled through NVML while ``active`` is set."""
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def __init__(self, device):
         self.samples = []
-        self.proc = None
         self.active = False
+        self.stop_flag = False
         self.thread = None
+        self.handle = None
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            props = torch.cuda.get_device_properties(device)
+            try:
+                bus = f"{props.pci_domain_id:08X}:{props.pci_bus_id:02X}:{props.pci_device_id:02X}.0"
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(torch.device(device).index or 0)
+            self.nvml = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: report unknown clocks
+            self.err = repr(e)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+        if self.handle is None:
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
+    def _run(self):
+        n = self.nvml
+        while not self.stop_flag:
             if self.active:
-                self.samples.append([x.strip() for x in line.split(",")])
+                try:
+                    sm = n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)
+                    try:
+                        rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                    except AttributeError:
+                        rs = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+                    self.samples.append((sm, rs))
+                except Exception:
+                    pass
+            time.sleep(0.002)
 
     def stop(self):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop_flag = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
-            try:
-                sm.append(float(s[0]))
-                mx = float(s[1])
-            except (ValueError, IndexError):
-                continue
-            for n, v in zip(names, s[2:6]):
-                if v.lower() in ("active", "yes", "1"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [], "samples": 0}
+        reasons = set()
+        for _, rs in self.samples:
+            for bit, name in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
 # ------------------------------------------------------------------------------------
@@ -230,9 +244,8 @@ def run_ours(args, rank, world, local_rank):
         wl.step(i)
     torch.cuda.synchronize()
     barrier()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(dev)
     clocks.start()
-    time.sleep(0.3)
     clocks.active = True
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
@@ -286,12 +299,19 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
     e2e_ms = float(te.item())
+    peaks, src = _peaks()
+    peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    extra = {}
+    if not args.no_extra:
+        extra["plr"] = measure_plr(dev, 2048, T, False, max(3, min(args.steps, 10)), flush, world)
+        extra["accel"] = measure_plr(dev, 2048, T, True, max(3, min(args.steps, 10)), flush, world)
+        if world == 1:
+            extra["large_batch"] = measure_large_batch(dev, 65536, T, 3, flush, peak)
     clocks.stop()
     csum = clocks.summary()
 
     if rank != 0:
         return None
-    peaks, src = _peaks()
     units = B * T * world
     roll = statistics.mean(roll_ms)
     gae = statistics.mean(gae_ms)
@@ -324,11 +344,90 @@ def run_ours(args, rank, world, local_rank):
         "kernels": {"k_env_rollout_ms": roll, "k_gae_score_ms": gae, "k_gae_score_GBs": gae_gbs,
                     "k_gae_score_frac": gae_gbs / peak,
                     "levels_scored_per_s": B * world / (gae * 1e-3)},
-        "clocks": {k: csum[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+        "clocks": {k: csum[k] for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples")},
     }
+    line.update(extra)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = measure_cpu_baseline(args)
     return line
+
+
+def _timed(fn, iters, flush, torch):
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for i in range(iters):
+        flush.fill_(i & 0xFF)
+        evs[i][0].record()
+        fn(i)
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def measure_plr(dev, n_per_gpu, T, accel, iters, flush, world):
+    """Parallel PLR (configs[2]) / ACCEL (configs[3]) iteration, env side: compose lanes
+    (DR + rank-prioritised replay [+ 20-edit mutants]), HOME rollout, GAE + MaxMC,
+    NCCL candidate all-gather (N > 1), buffer update.  Buffer K = 4000."""
+    import torch
+
+    import paper_2311_12716_b200 as amz
+    from paper_2311_12716_b200.buffer import AccelConfig, PlrConfig
+    from paper_2311_12716_b200.plr import ParallelPLR
+
+    cfg = PlrConfig(buffer_size=4000, score_fn="maxmc", temperature=0.3,
+                    staleness_coef=0.5 if accel else 0.3, replay_rate=0.8 if accel else 0.5)
+    plr = ParallelPLR(n_per_gpu * world, amz.StaticParams(), cfg, amz.RngStream.from_seed(7),
+                      AccelConfig(20, 4) if accel else None, device=dev)
+    L = plr.hi - plr.lo
+    g = torch.Generator(device=dev)
+    g.manual_seed(99 + plr.rank)
+    acts = torch.randint(0, 3, (T, L), generator=g, device=dev, dtype=torch.uint8)
+    vals = torch.rand((T, L), generator=g, device=dev, dtype=torch.float64) * 0.2
+    last = torch.rand((L,), generator=g, device=dev, dtype=torch.float64) * 0.2
+    for it in range(3):  # fills the 4000-level buffer (first iteration inserts 4000 of the new levels)
+        plr.iteration(it, acts, vals, last)
+    torch.cuda.synchronize()
+    ms = _timed(lambda i: plr.iteration(3 + i, acts, vals, last), iters, flush, torch)
+    # the two buffer kernels on their own (latency-bound single-CTA kernels)
+    rec_lv = plr.buffer.export()["levels"][:1].repeat(8192, 1)
+    sc = torch.rand(8192, device=dev, dtype=torch.float64)
+    t_upd = _timed(lambda i: plr.buffer.update(rec_lv, sc, sc, 1000 + i), iters, flush, torch)
+    t_smp = _timed(lambda i: plr.buffer.sample(amz.RngStream(5, (i,)), n_per_gpu * world, 2000 + i), iters, flush,
+                   torch)
+    t = torch.tensor([statistics.mean(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    it_ms = float(t.item())
+    lanes = plr.L
+    return {"config": "configs[3] ACCEL-parallel" if accel else "configs[2] PLR-parallel",
+            "lanes_global": lanes, "T": T, "buffer_size": 4000, "iteration_ms": it_ms,
+            "levels_scored_per_s": lanes / (it_ms * 1e-3), "env_steps_per_s": lanes * T / (it_ms * 1e-3),
+            "buffer_update_us_8192_candidates": 1e3 * statistics.mean(t_upd),
+            "buffer_sample_us": 1e3 * statistics.mean(t_smp)}
+
+
+def measure_large_batch(dev, B, T, iters, flush, peak):
+    """Rollout + GAE at a batch that is HBM-sized (trajectory >> L2): the roofline point."""
+    import torch
+
+    wl = Workload(B, T, 3, 0, dev)
+    for i in range(2):
+        wl.step(i)
+    torch.cuda.synchronize()
+    kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(iters)]
+    for i in range(iters):
+        flush.fill_(i & 0xFF)
+        wl.step(10 + i, timing=kev[i])
+    torch.cuda.synchronize()
+    roll = statistics.mean(k[0].elapsed_time(k[1]) for k in kev)
+    gae = statistics.mean(k[1].elapsed_time(k[2]) for k in kev)
+    rg = ENV_BYTES_PER_STEP * B * T / (roll * 1e-3) / 1e9
+    gg = GAE_BYTES_PER_ELEM * B * T / (gae * 1e-3) / 1e9
+    out = {"lanes": B, "T": T, "rollout_ms": roll, "rollout_GBs": rg, "rollout_frac": rg / peak,
+           "rollout_env_steps_per_s": B * T / (roll * 1e-3), "gae_score_ms": gae, "gae_score_GBs": gg,
+           "gae_score_frac": gg / peak, "levels_scored_per_s": B / (gae * 1e-3)}
+    del wl
+    torch.cuda.empty_cache()
+    return out
 
 
 def measure_cpu_baseline(args, steps=1):
@@ -384,6 +483,7 @@ def main():
     ap.add_argument("--T", type=int, default=256)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the PLR/ACCEL and large-batch measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -282,17 +282,31 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 //                     fill inserts, evictions of the (score, last_sampled, seq)
 //                     minimum (recomputed lazily by the warp when a candidate needs it).
 // ---------------------------------------------------------------------------------
+constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses the hash table's space)
+struct CandChunk {
+    double sc[kChunk];
+    double mr[kChunk];
+    int32_t cid[kChunk];
+    int32_t tf[kChunk];
+    int32_t im[kChunk];
+};
 struct UpdSmem {
     double score[kPlrMaxK];
+    uint64_t tb[kPlrMaxK];  // eviction tie-break key (last_sampled << 32) | seq: lexicographic (last, seq)
     int64_t last[kPlrMaxK];
     int64_t seq[kPlrMaxK];
-    uint32_t hash[kHash];
-    int owner[kPlrMaxK];      // first-candidate index of the key now in the slot, -1 = initial entry
+    union {
+        uint32_t hash[kHash];
+        CandChunk chunk;
+    } u;
+    int owner[kPlrMaxK];  // first-candidate index of the key now in the slot, -1 = initial entry
     uint32_t replaced[kPlrMaxK / 32];
+    int gmin[kPlrMaxK / 32];  // per 32-slot group: slot of its (score, tb) minimum
     double mlow;
     int n_rel;
     int full;
 };
+static_assert(sizeof(CandChunk) <= sizeof(uint32_t) * kHash, "chunk must fit in the hash table space");
 
 __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
                                 int64_t hsize) {
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     const int K = (int)D.K;
     int size = (int)D.meta[0];
     // ---- A: load buffer scalars + key hash ----
-    for (int i = tid; i < kHash; i += blockDim.x) S.hash[i] = 0u;
+    for (int i = tid; i < kHash; i += blockDim.x) S.u.hash[i] = 0u;
     for (int i = tid; i < kPlrMaxK / 32; i += blockDim.x) S.replaced[i] = 0u;
     if (tid == 0) {
         S.n_rel = 0;
@@ -357,13 +371,14 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         S.score[i] = D.score[i];
         S.last[i] = D.last[i];
         S.seq[i] = D.seq[i];
+        S.tb[i] = ((uint64_t)S.last[i] << 32) | (uint32_t)S.seq[i];
         S.owner[i] = -1;
         my_min = fmin(my_min, S.score[i]);
         uint4 w;
         uint32_t p0, p1;
         level_key(D.levels + i, w, p0, p1);
         uint32_t h = level_hash(w, p0 ^ (p1 << 24)) & (kHash - 1);
-        while (atomicCAS(&S.hash[h], 0u, (uint32_t)(i + 1)) != 0u) h = (h + 1) & (kHash - 1);
+        while (atomicCAS(&S.u.hash[h], 0u, (uint32_t)(i + 1)) != 0u) h = (h + 1) & (kHash - 1);
     }
     __syncthreads();
     for (int64_t c = tid; c < n; c += blockDim.x) {
@@ -373,7 +388,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         uint32_t h = level_hash(w, p0 ^ (p1 << 24)) & (kHash - 1);
         int m = -1;
         while (true) {
-            uint32_t cur = S.hash[h];
+            uint32_t cur = S.u.hash[h];
             if (cur == 0u) break;
             if (key_eq(D.levels + (cur - 1), w, p0, p1)) {
                 m = (int)(cur - 1);
@@ -423,94 +438,141 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     }
     // A skipped first occurrence is never inserted (score <= mlow), so its later twins,
     // which are always relevant, correctly find no entry for the key (keyslot = -1).
-    if (tid >= 32) return;
 
-    // ---- C: ordered replay by warp 0 ----
+    // ---- C: ordered replay ----
+    // Minimum of (score, tb) kept in two levels: the minimum slot of every 32-slot group
+    // (S.gmin, computed here by all warps) and the overall minimum, recomputed by warp 0
+    // from the group minima only when an insertion needs it and something changed.
+    const int ngroups = (size + 31) / 32;
+    const int warp = tid >> 5;
+    auto key_less = [&](int a, int b) {  // (score, tb) order of two valid slots
+        const double sa = S.score[a], sb = S.score[b];
+        if (sa != sb) return sa < sb;
+        return S.tb[a] < S.tb[b];
+    };
+    auto group_min = [&](int g, int cur_size) {  // whole warp; returns the group's min slot (uniform)
+        const int sl = g * 32 + lane;
+        int bi = sl < cur_size ? sl : -1;
+        for (int o = 16; o > 0; o >>= 1) {
+            const int j = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+            if (j >= 0 && (bi < 0 || key_less(j, bi) || (!key_less(bi, j) && j < bi))) bi = j;
+        }
+        return bi;
+    };
+    for (int g = tid; g < kPlrMaxK / 32; g += blockDim.x) S.gmin[g] = -1;
+    __syncthreads();
+    for (int g = warp; g < ngroups; g += (int)(blockDim.x >> 5)) {
+        const int m = group_min(g, size);
+        if (lane == 0) S.gmin[g] = m;
+    }
+    __syncthreads();
     const int nrel = S.n_rel;
     int64_t next_seq = D.meta[1];
-    int minslot = -1;
-    bool minvalid = false;
-    auto recompute_min = [&]() {
-        double bs = 0.0;
-        int64_t bl = 0, bq = 0;
-        int bi = -1;
-        for (int i = lane; i < size; i += 32) {
-            const double s = S.score[i];
-            const int64_t l = S.last[i], q = S.seq[i];
-            if (bi < 0 || entry_less(s, l, q, bs, bl, bq)) {
-                bs = s;
-                bl = l;
-                bq = q;
-                bi = i;
+    int gslot = -1;                  // cached overall minimum slot
+    bool gvalid = false;
+    uint32_t dirty[kPlrMaxK / 32 / 32];  // dirty group bits (warp-uniform)
+#pragma unroll
+    for (int i = 0; i < kPlrMaxK / 1024; i++) dirty[i] = 0u;
+    auto overall_min = [&]() {
+        // refresh dirty groups, then reduce the group minima (4 per lane)
+        for (int w = 0; w < kPlrMaxK / 1024; w++) {
+            uint32_t bits = dirty[w];
+            while (bits) {
+                const int g = w * 32 + __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int m = group_min(g, size);
+                if (lane == 0) S.gmin[g] = m;
             }
+            dirty[w] = 0u;
+        }
+        __syncwarp();
+        int bi = -1;
+        for (int g = lane; g < (size + 31) / 32; g += 32) {
+            const int j = S.gmin[g];
+            if (j >= 0 && (bi < 0 || key_less(j, bi))) bi = j;
         }
         for (int o = 16; o > 0; o >>= 1) {
-            const double s2 = __shfl_xor_sync(0xFFFFFFFFu, bs, o);
-            const long long l2 = __shfl_xor_sync(0xFFFFFFFFu, (long long)bl, o);
-            const long long q2 = __shfl_xor_sync(0xFFFFFFFFu, (long long)bq, o);
-            const int i2 = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
-            if (i2 >= 0 && (bi < 0 || entry_less(s2, l2, q2, bs, bl, bq))) {
-                bs = s2;
-                bl = l2;
-                bq = q2;
-                bi = i2;
-            }
+            const int j = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+            if (j >= 0 && (bi < 0 || key_less(j, bi) || (!key_less(bi, j) && j < bi))) bi = j;
         }
-        minslot = bi;
-        minvalid = true;
+        gslot = bi;
+        gvalid = true;
     };
-    for (int r = 0; r < nrel; r++) {
-        const int c = W.rel[r];
-        const double sc = cscore[c];
-        const double mr = cmax[c];
-        const int f = W.twin_first[c];
-        int present = -1;
-        const int im = W.init_match[c];
-        if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
-        if (present < 0 && f != c) present = W.keyslot[f];
-        __syncwarp();
-        if (present >= 0) {
+    auto touched = [&](int slot) {  // slot's key changed: mark its group, drop the cached minimum
+        const int g = slot >> 5;
+        const int w = g >> 5;
+#pragma unroll
+        for (int i = 0; i < kPlrMaxK / 1024; i++)
+            if (i == w) dirty[i] |= 1u << (g & 31);
+        gvalid = false;
+    };
+    for (int base = 0; base < nrel; base += kChunk) {
+        const int cn = (nrel - base) < kChunk ? (nrel - base) : kChunk;
+        __syncthreads();
+        for (int i = tid; i < cn; i += blockDim.x) {
+            const int c = W.rel[base + i];
+            S.u.chunk.cid[i] = c;
+            S.u.chunk.sc[i] = cscore[c];
+            S.u.chunk.mr[i] = cmax[c];
+            S.u.chunk.tf[i] = W.twin_first[c];
+            S.u.chunk.im[i] = W.init_match[c];
+        }
+        __syncthreads();
+        if (warp != 0) continue;
+        for (int r = 0; r < cn; r++) {
+            const int c = S.u.chunk.cid[r];
+            const double sc = S.u.chunk.sc[r];
+            const int f = S.u.chunk.tf[r];
+            const int im = S.u.chunk.im[r];
+            int present = -1;
+            if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
+            if (present < 0 && f != c) present = W.keyslot[f];
+            if (present >= 0) {
+                if (lane == 0) {
+                    S.score[present] = sc;
+                    D.maxret[present] = S.u.chunk.mr[r];
+                }
+                __syncwarp();
+                // keep the two-level minimum exact: a decrease can only lower the minima
+                const int g = present >> 5;
+                const int gm = S.gmin[g];
+                if (gm < 0 || gm == present) {
+                    touched(present);
+                } else if (key_less(present, gm)) {
+                    if (lane == 0) S.gmin[g] = present;
+                    __syncwarp();
+                    if (gvalid && gslot >= 0 && key_less(present, gslot)) gslot = present;
+                }
+                continue;
+            }
+            int slot;
+            if (size < K) {
+                slot = size++;
+            } else {
+                if (!gvalid) overall_min();
+                if (!(sc > S.score[gslot])) continue;
+                slot = gslot;
+                const int ow = S.owner[slot];
+                if (ow >= 0 && lane == 0) W.keyslot[ow] = -1;
+            }
             if (lane == 0) {
-                S.score[present] = sc;
-                D.maxret[present] = mr;
+                S.score[slot] = sc;
+                S.last[slot] = iter;
+                S.seq[slot] = next_seq;
+                S.tb[slot] = ((uint64_t)iter << 32) | (uint32_t)next_seq;
+                S.owner[slot] = f;
+                S.replaced[slot >> 5] |= 1u << (slot & 31);
+                W.keyslot[f] = slot;
+                D.maxret[slot] = S.u.chunk.mr[r];
+                D.levels[slot] = cand[c];
             }
+            next_seq++;
             __syncwarp();
-            if (minvalid) {
-                if (present == minslot)
-                    minvalid = false;  // its score changed; recompute lazily
-                else if (entry_less(sc, S.last[present], S.seq[present], S.score[minslot], S.last[minslot],
-                                    S.seq[minslot]))
-                    minslot = present;
-            }
-            continue;
+            touched(slot);
         }
-        int slot;
-        if (size < K) {
-            slot = size++;
-        } else {
-            if (!minvalid) recompute_min();
-            if (!(sc > S.score[minslot])) continue;
-            slot = minslot;
-            minvalid = false;
-            const int ow = S.owner[slot];
-            if (ow >= 0 && lane == 0) W.keyslot[ow] = -1;
-        }
-        if (lane == 0) {
-            S.score[slot] = sc;
-            S.last[slot] = iter;
-            S.seq[slot] = next_seq;
-            S.owner[slot] = f;
-            S.replaced[slot >> 5] |= 1u << (slot & 31);
-            W.keyslot[f] = slot;
-            D.maxret[slot] = mr;
-            D.levels[slot] = cand[c];
-        }
-        next_seq++;
-        __syncwarp();
-        if (minvalid && entry_less(sc, iter, next_seq - 1, S.score[minslot], S.last[minslot], S.seq[minslot]))
-            minslot = slot;
     }
-    __syncwarp();
+    __syncthreads();
+    if (warp != 0) return;
     for (int i = lane; i < size; i += 32) {
         D.score[i] = S.score[i];
         D.last[i] = S.last[i];
