@@ -103,16 +103,21 @@ __device__ __forceinline__ void row_bits(int r, int c, int d, int H, int W, cons
     inb = ib;
 }
 
-// bytes of one view row (codes: hidden/OOB 3, wall 1, goal 2, empty 0) -> out[0..V)
+// bytes of one view row (codes: hidden/OOB 3, wall 1, goal 2, empty 0) -> out[0..V).
+// V <= 5 spreads the wall and hidden bit masks to bytes through a 32-entry table.
 template <int V>
-__device__ __forceinline__ void emit_row(uint32_t wall, uint32_t inb, bool goal_here, int g_vc, const uint64_t *spread,
-                                         uint8_t *o) {
+__device__ __forceinline__ void emit_row(uint32_t wall, uint32_t inb, bool goal_here, int g_vc,
+                                         const uint64_t *spread, uint8_t *o) {
     constexpr uint32_t vm = (1u << V) - 1u;
     if (V <= 5) {
         uint64_t bytes = spread[wall & inb] | (spread[~inb & vm] * 3ull);
         if (goal_here) bytes = (bytes & ~(0xFFull << (8 * g_vc))) | (2ull << (8 * g_vc));
-#pragma unroll
-        for (int j = 0; j < V; j++) o[j] = (uint8_t)(bytes >> (8 * j));
+        const uint32_t lo = (uint32_t)bytes, hi = (uint32_t)(bytes >> 32);
+        o[0] = (uint8_t)lo;
+        if (V > 1) o[1] = (uint8_t)(lo >> 8);
+        if (V > 2) o[2] = (uint8_t)(lo >> 16);
+        if (V > 3) o[3] = (uint8_t)(lo >> 24);
+        if (V > 4) o[4] = (uint8_t)hi;
     } else {
 #pragma unroll
         for (int j = 0; j < V; j++) {
@@ -120,6 +125,16 @@ __device__ __forceinline__ void emit_row(uint32_t wall, uint32_t inb, bool goal_
             if (goal_here && g_vc == j) code = 2u;
             o[j] = (uint8_t)code;
         }
+    }
+}
+
+// 5-bit mask -> 5 bytes of 0/1 (built once per CTA)
+__device__ __forceinline__ void init_spread(uint64_t *spread) {
+    for (int e = threadIdx.x; e < 32; e += blockDim.x) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int j = 0; j < 5; j++) v |= (uint64_t)((e >> j) & 1) << (8 * j);
+        spread[e] = v;
     }
 }
 
@@ -244,15 +259,10 @@ __global__ void __launch_bounds__(32 * WPC) k_rollout(Geo G, EnvDev E, int T, co
     constexpr int VIEWB = 32 * VV;
     using WS = WarpSmem<V, NS>;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t *s_spread = reinterpret_cast<uint64_t *>(smem);  // [32]
+    uint64_t *s_spread = reinterpret_cast<uint64_t *>(smem);  // [32] spread table
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WS &S = reinterpret_cast<WS *>(smem + 256)[warp];
-    {
-        uint64_t v = 0;
-#pragma unroll
-        for (int j = 0; j < 5; j++) v |= (uint64_t)((lane >> j) & 1) << (8 * j);
-        if (warp == 0) s_spread[lane] = v;
-    }
+    init_spread(s_spread);
     __syncthreads();
 
     const int64_t B = E.B;
@@ -448,12 +458,7 @@ __global__ void __launch_bounds__(128) k_rollout_g4(Geo G, EnvDev E, int T, cons
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane >> 2, k = lane & 3;
     WS &S = wsm[warp];
-    if (warp == 0) {
-        uint64_t v = 0;
-#pragma unroll
-        for (int j = 0; j < 5; j++) v |= (uint64_t)((lane >> j) & 1) << (8 * j);
-        s_spread[lane] = v;
-    }
+    init_spread(s_spread);
     __syncthreads();
     const int64_t B = E.B;
     const int64_t lane0 = ((int64_t)blockIdx.x * 4 + warp) * 8;
