@@ -38,6 +38,13 @@ struct amz_env {
     EnvDev E;
     int *term;  // [2] terminal-lane counters (mode NONE)
     int parity;
+    // rollout scratch (grown on demand): per-step pose records, per-epoch level boards
+    uint32_t *poses = nullptr;
+    uint32_t *epochs = nullptr;
+    uint32_t *final_pose = nullptr;
+    amz_level_t *spec = nullptr;   // speculative timeout levels [B]
+    uint32_t *spec_step = nullptr; // [B]
+    int64_t rollout_T = 0;
 };
 
 struct amz_plr {
@@ -156,8 +163,9 @@ int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.board, b * 16 * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.err, 4 * sizeof(int));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->term, 2 * sizeof(int));
-    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.spec, b * sizeof(amz_level_t));
-    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.spec_step, b * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->final_pose, b * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->spec, b * sizeof(amz_level_t));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->spec_step, b * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMemset(e->E.err, 0, 4 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->term, 0, 2 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->E.st, 0, b * sizeof(uint4));
@@ -177,8 +185,11 @@ int amz_env_destroy(amz_env_t *e) {
     cudaFree(e->E.board);
     cudaFree(e->E.err);
     cudaFree(e->term);
-    cudaFree(e->E.spec);
-    cudaFree(e->E.spec_step);
+    cudaFree(e->final_pose);
+    cudaFree(e->spec);
+    cudaFree(e->spec_step);
+    cudaFree(e->poses);
+    cudaFree(e->epochs);
     delete e;
     return 0;
 }
@@ -231,8 +242,23 @@ int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const
         return fail(AMZ_ECONTRACT, "rollout needs an auto-resetting env (mode %d)", mode);
     if (mode == AMZ_RESET_RESAMPLE && !wrap) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
     amz_seed_t w = wrap ? *wrap : amz_seed_t{};
+    cudaStream_t s = (cudaStream_t)stream;
+    if (T > e->rollout_T) {
+        cudaFreeAsync(e->poses, s);
+        cudaFreeAsync(e->epochs, s);
+        e->poses = nullptr;
+        e->epochs = nullptr;
+        const size_t b = (size_t)e->E.B;
+        cudaError_t er = cudaMallocAsync((void **)&e->poses, (size_t)T * b * sizeof(uint32_t), s);
+        if (er == cudaSuccess) er = cudaMallocAsync((void **)&e->epochs, ((size_t)T + 1) * b * 20 * sizeof(uint32_t), s);
+        if (er != cudaSuccess) {
+            e->rollout_T = 0;
+            return fail(AMZ_ECUDA, "rollout scratch: %s", cudaGetErrorString(er));
+        }
+        e->rollout_T = T;
+    }
     int rc = launch_env_rollout(e->G, e->E, T, actions, mode, w, step0, view, dirs, reward, done, fview, fdir,
-                                (cudaStream_t)stream);
+                                e->poses, e->epochs, e->final_pose, e->spec, e->spec_step, s);
     if (rc) return fail(rc, "rollout: unsupported agent_view_size");
     return cuda_status("env_rollout");
 }

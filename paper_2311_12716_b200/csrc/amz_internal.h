@@ -16,8 +16,6 @@ struct EnvDev {
     uint4 *mask;
     uint32_t *board;  // [16][B]
     int *err;
-    amz_level_t *spec;    // [B] speculative timeout levels (amz_rollout.cu)
-    uint32_t *spec_step;  // [B] step index of spec[l] (0xFFFFFFFF = none)
 };
 
 // numpy pairwise summation schedule (numpy/_core/src/umath/loops_utils.h.src
@@ -47,9 +45,11 @@ int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adty
                     const amz_seed_t &wrap, uint32_t step_idx, uint8_t *view, int64_t *dirs, double *reward,
                     uint8_t *done, double *solved, int64_t *times, const int *term_in, int *term_out,
                     cudaStream_t s);
+// poses [T][B], epochs [(T+1)*B][20], final_pose [B]: rollout scratch (amz_rollout.cu)
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
                        const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
-                       uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s);
+                       uint8_t *done, uint8_t *fview, uint8_t *fdir, uint32_t *poses, uint32_t *epochs,
+                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s);
 int launch_gae_score(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *last,
                      double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
                      double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,

@@ -1,21 +1,24 @@
-// amz_rollout.cu -- fused T-step rollout of every lane (the env side of
-// agents/rollout.py:120-179 with an action stream), B200 layout.
+// amz_rollout.cu -- T fused env steps of every lane (the env side of
+// agents/rollout.py:120-179 with an action stream), split into two kernels.
 //
-// One warp owns 32 consecutive lanes (one lane per thread) and is independent of every
-// other warp: no CTA-wide barrier anywhere in the step loop.  Per step a lane renders
-// its observation (V row slices of its wall board in shared memory, expanded to bytes
-// through a 32-entry spread table), applies its action and writes reward/done into a
-// shared-memory staging ring.  Every NS steps lane 0 ships the warp's staged chunk with
-// cp.async.bulk (TMA bulk-copy engine, SASS UBLKCP): for each step one contiguous run
-// per output array (view 32*V*V bytes, dir 32, reward 256, done 32).  Chunks are
-// double-buffered, so the copies of chunk c drain while chunk c+1 is computed.
+// k_dyn (dynamics, sequential per lane).  One thread per lane, LPW lanes per warp,
+// every warp independent.  Per step: transition + reward/done (amaze/env.py:320-349),
+// one 32-bit pose record (row, col, heading, level epoch) and the fused auto-reset
+// (env/wrappers.py:59-78).  The lanes of a warp that finish on the same step get their
+// RESAMPLE levels from one staged SIMT sampler pass (amz_sampler.cuh): the warp
+// computes all their Philox blocks round-robin, then each runs its Fisher-Yates.  Each
+// level a lane plays ("epoch") is published as a 20-word record (wall board + goal) at
+// slot lane + epoch * B.  The action stream is prefetched 32 steps ahead with cp.async.
 //
-// Auto-reset levels.  A RESAMPLE reset draws the level of key wrap ++ [step, lane].
-// Under random or weak policies almost every reset is a timeout, and a lane's timeout
-// step is known before the rollout starts, so k_spec_levels samples those levels up
-// front, fully parallel (one warp per lane, amz_sampler.cuh).  A reset at exactly that
-// step loads the precomputed level (it is the same key, hence the same level); any
-// other reset (a solved episode) is sampled inline by the whole warp cooperatively.
+// k_render (observations, fully parallel over (t, lane)).  Each thread renders the
+// observation before step t of one lane from its pose record and epoch board
+// (observe_batch + apply_occlusion, amaze/env.py:111-137, 352-364) into shared memory;
+// the CTA's 128 consecutive (t, lane) records are one contiguous 128*V*V-byte run of the
+// time-major view tensor and leave with cp.async.bulk (TMA bulk copy, SASS UBLKCP).
+//
+// The split takes the 25-byte render and its stores off the per-lane sequential chain:
+// the dynamics loop is ~20 instructions per step, the render is embarrassingly
+// parallel and HBM-bound.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -204,362 +207,119 @@ __device__ __forceinline__ void render_lane(int r, int c, int d, int gr, int gc,
     }
 }
 
-template <int V, int NS>
-struct WarpSmem {
-    uint8_t act[2][ACH][32];
-    uint8_t view[2 * NS][32 * V * V];
-    double rew[2 * NS][32];
-    uint8_t dir[2 * NS][32];
-    uint8_t done[2 * NS][32];
-    uint32_t board[16][32];
-    uint32_t stream[kWNW];
-};
+
+constexpr int kRec = 20;  // u32 words per epoch record: board[16], goal, pad
 
 }  // namespace
 
 // ---------------------------------------------------------------------------------
-// speculative timeout levels: lane l times out (if it never reaches the goal) at the
-// step where its time reaches max_episode_steps; sample that level now.
+// phase 1: dynamics
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_spec_levels(Geo G, EnvDev E, int T, amz_seed_t wrap, uint32_t step0,
-                                                     amz_level_t *__restrict__ spec, uint32_t *__restrict__ spec_step) {
-    __shared__ __align__(16) uint32_t sw[4][kWNW];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t l = (int64_t)blockIdx.x * 4 + warp;
-    if (l >= E.B) return;
-    const LaneRec L = unpack_st(E.st[l]);
-    const int s_to = G.tep - L.s.time - 1;
-    if (s_to < 0 || s_to >= T) {
-        if (lane == 0) spec_step[l] = 0xFFFFFFFFu;
-        return;
-    }
-    amz_seed_t sd = wrap;
-    seed_absorb(sd, step0 + (uint32_t)s_to);
-    seed_absorb(sd, E.lane_offset + (uint32_t)l);
-    uint64_t k0, k1;
-    seed_key(sd, k0, k1);
-    Mask m;
-    int ar, ac, ad, gr, gc;
-    warp_sample_level(k0, k1, G, sw[warp], m, ar, ac, ad, gr, gc);
-    if (lane == 0) {
-        store_level(spec + l, m, ar, ac, ad, gr, gc);
-        spec_step[l] = step0 + (uint32_t)s_to;
-    }
-}
+template <int LPW>
+struct DynSmem {
+    uint32_t board[16][LPW];
+    uint8_t act[2][ACH][LPW];
+    uint32_t stream[kSNW][LPW];
+    uint64_t key[2 * LPW];
+    uint8_t perm[128][LPW];
+};
 
-template <int V, bool SEE, int NS, int WPC>
-__global__ void __launch_bounds__(32 * WPC) k_rollout(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions,
-                                                      int mode, amz_seed_t wrap, uint32_t step0,
-                                                      uint8_t *__restrict__ view, uint8_t *__restrict__ dirs,
-                                                      double *__restrict__ reward, uint8_t *__restrict__ done,
-                                                      uint8_t *__restrict__ fview, uint8_t *__restrict__ fdir,
-                                                      const amz_level_t *__restrict__ spec,
-                                                      const uint32_t *__restrict__ spec_step, int bulk_ok) {
-    constexpr int VV = V * V;
-    constexpr int VIEWB = 32 * VV;
-    using WS = WarpSmem<V, NS>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t *s_spread = reinterpret_cast<uint64_t *>(smem);  // [32] spread table
+template <int LPW, int WPC>
+__global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions, int mode,
+                                                  amz_seed_t wrap, uint32_t step0, double *__restrict__ reward,
+                                                  uint8_t *__restrict__ done, uint32_t *__restrict__ poses,
+                                                  uint32_t *__restrict__ epochs, uint32_t *__restrict__ final_pose,
+                                                  const amz_level_t *__restrict__ spec,
+                                                  const uint32_t *__restrict__ spec_step, int avec, int use_lut) {
+    extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WS &S = reinterpret_cast<WS *>(smem + 256)[warp];
-    init_spread(s_spread);
+    DynSmem<LPW> &S = reinterpret_cast<DynSmem<LPW> *>(smem)[warp];
+    // goal rewards R[time] = 1 - 0.9*time/T_ep (numpy's op order), tabulated per CTA
+    double *s_rew = reinterpret_cast<double *>(smem + WPC * sizeof(DynSmem<LPW>));
+    if (use_lut)
+        for (int tt = threadIdx.x; tt <= G.tep; tt += blockDim.x) s_rew[tt] = goal_reward(tt, G.tep);
     __syncthreads();
-
     const int64_t B = E.B;
-    const int64_t lane0 = ((int64_t)blockIdx.x * WPC + warp) * 32;
+    const int64_t lane0 = ((int64_t)blockIdx.x * WPC + warp) * LPW;
     if (lane0 >= B) return;
     const int64_t l = lane0 + lane;
-    const bool live = l < B;
-    const int nv = (int)((B - lane0) < 32 ? (B - lane0) : 32);
-    uint32_t *bd = &S.board[0][lane];
+    const bool live = lane < LPW && l < B;
+    const int nv = (int)((B - lane0) < LPW ? (B - lane0) : LPW);
+    uint32_t *bd = &S.board[0][lane < LPW ? lane : 0];
 
-    LaneRec L;
-    Mask m;
-    bool lvl_changed = false;
-    uint32_t my_spec = 0xFFFFFFFFu;
-    if (live) {
-        L = unpack_st(E.st[l]);
-#pragma unroll
-        for (int w = 0; w < 16; w++) bd[w * 32] = E.board[w * B + l];
-        if (mode == AMZ_RESET_RESAMPLE) my_spec = spec_step[l];
-    } else {
-        L = LaneRec{};
-    }
-    const bool avec = bulk_ok && nv == 32;
-    fetch_actions<32>(S.act[0], actions, B, lane0, nv, 0, T, lane, avec);
-    __syncwarp();
-
-    static_assert(ACH % NS == 0, "action chunk must hold whole staging chunks");
-    const int nchunks = (T + NS - 1) / NS;
-    for (int c = 0; c < nchunks; c++) {
-        const int hb = (c & 1) * NS;
-        const int t0 = c * NS;
-        const int ns = (T - t0) < NS ? (T - t0) : NS;
-        if ((t0 % ACH) == 0) {
-            fetch_actions<32>(S.act[((t0 / ACH) + 1) & 1], actions, B, lane0, nv, t0 + ACH, T, lane, avec);
-            cp_wait<1>();
-            __syncwarp();
-        }
-#pragma unroll
-        for (int j = 0; j < NS; j++) {
-            if (j >= ns) break;
-            const int s = hb + j;
-            const int ta = t0 + j;
-            const uint8_t aj = S.act[(ta / ACH) & 1][ta % ACH][lane];
-            bool dn = false;
-            if (live) {
-                render_lane<V, SEE>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, bd, s_spread, &S.view[s][lane * VV]);
-                S.dir[s][lane] = (uint8_t)L.s.d;
-                const bool reached = lane_transition(L.s, aj, L.gr, L.gc, bd, 32);
-                dn = reached || L.s.time >= G.tep;
-                S.rew[s][lane] = reached ? goal_reward(L.s.time, G.tep) : 0.0;
-                S.done[s][lane] = dn;
-            }
-            const unsigned any = __ballot_sync(0xFFFFFFFFu, dn);
-            if (any) {
-                const uint32_t gstep = step0 + (uint32_t)(t0 + j);
-                if (mode == AMZ_RESET_RESAMPLE) {
-                    const bool hit = dn && my_spec == gstep;
-                    if (hit) {
-                        int ar, ac, ad, gr, gc;
-                        load_level(spec + l, m, ar, ac, ad, gr, gc);
-                        build_board(m, G, bd, 32);
-                        L.hr = ar;
-                        L.hc = ac;
-                        L.hd = ad;
-                        L.gr = gr;
-                        L.gc = gc;
-                        lvl_changed = true;
-                    }
-                    unsigned todo = __ballot_sync(0xFFFFFFFFu, dn && !hit);
-                    while (todo) {
-                        const int tl = __ffs(todo) - 1;
-                        todo &= todo - 1;
-                        amz_seed_t sd = wrap;
-                        seed_absorb(sd, gstep);
-                        seed_absorb(sd, E.lane_offset + (uint32_t)(lane0 + tl));
-                        uint64_t k0, k1;
-                        seed_key(sd, k0, k1);
-                        Mask nm;
-                        int ar, ac, ad, gr, gc;
-                        warp_sample_level(k0, k1, G, S.stream, nm, ar, ac, ad, gr, gc);
-                        if (lane == tl) {
-                            m = nm;
-                            build_board(m, G, bd, 32);
-                            L.hr = ar;
-                            L.hc = ac;
-                            L.hd = ad;
-                            L.gr = gr;
-                            L.gc = gc;
-                            lvl_changed = true;
-                        }
-                        __syncwarp();
-                    }
-                }
-                if (dn) {
-                    L.s.r = L.hr;
-                    L.s.c = L.hc;
-                    L.s.d = L.hd;
-                    L.s.time = 0;
-                    L.term = false;
-                }
-                __syncwarp();
-            }
-        }
-        // ---- chunk end: ship the warp's NS staged steps ----
-        __syncwarp();
-        if (bulk_ok) {
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                for (int j = 0; j < ns; j++) {
-                    const int s = hb + j;
-                    const int64_t row = (int64_t)(t0 + j) * B + lane0;
-                    bulk_store(view + row * VV, S.view[s], VIEWB);
-                    bulk_store(dirs + row, S.dir[s], 32);
-                    bulk_store(reward + row, S.rew[s], 256);
-                    bulk_store(done + row, S.done[s], 32);
-                }
-                bulk_commit();
-                bulk_wait_read<1>();  // chunk c-1 finished reading the other half
-            }
-        } else {
-            for (int j = 0; j < ns; j++) {
-                const int s = hb + j;
-                const int64_t row = (int64_t)(t0 + j) * B + lane0;
-                for (int x = lane; x < nv * VV; x += 32) view[row * VV + x] = S.view[s][x];
-                if (lane < nv) {
-                    dirs[row + lane] = S.dir[s][lane];
-                    reward[row + lane] = S.rew[s][lane];
-                    done[row + lane] = S.done[s][lane];
-                }
-            }
-        }
-        __syncwarp();
-    }
-    // ---- cursor observation + state write-back ----
-    if (bulk_ok && lane == 0) bulk_wait_read<0>();
-    __syncwarp();
-    if (live) {
-        render_lane<V, SEE>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, bd, s_spread, &S.view[0][lane * VV]);
-        S.dir[0][lane] = (uint8_t)L.s.d;
-        E.st[l] = pack_st(L);
-        if (lvl_changed) {
-            E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
-#pragma unroll
-            for (int w = 0; w < 16; w++) E.board[w * B + l] = bd[w * 32];
-        }
-    }
-    __syncwarp();
-    if (bulk_ok) {
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-            if (fview) bulk_store(fview + lane0 * VV, S.view[0], VIEWB);
-            if (fdir) bulk_store(fdir + lane0, S.dir[0], 32);
-            bulk_commit();
-            bulk_wait_all();
-        }
-    } else {
-        if (fview)
-            for (int x = lane; x < nv * VV; x += 32) fview[lane0 * VV + x] = S.view[0][x];
-        if (fdir && lane < nv) fdir[lane0 + lane] = S.dir[0][lane];
-    }
-}
-
-
-// ---------------------------------------------------------------------------------
-// small batches: 4 threads per lane, 8 lanes per warp, every warp independent.
-// The group computes its lane's transition redundantly, renders rows k, k+4 of the
-// observation, and the warp writes each step's 8-lane output runs with 8-byte stores.
-// ---------------------------------------------------------------------------------
-template <int V, bool SEE>
-__global__ void __launch_bounds__(128) k_rollout_g4(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions,
-                                                   int mode, amz_seed_t wrap, uint32_t step0,
-                                                   uint8_t *__restrict__ view, uint8_t *__restrict__ dirs,
-                                                   double *__restrict__ reward, uint8_t *__restrict__ done,
-                                                   uint8_t *__restrict__ fview, uint8_t *__restrict__ fdir,
-                                                   const amz_level_t *__restrict__ spec,
-                                                   const uint32_t *__restrict__ spec_step, int vec_ok) {
-    constexpr int VV = V * V;
-    constexpr int VB = 8 * VV;  // view bytes per warp-step
-    constexpr int VBP = (VB + 15) & ~15;
-    struct alignas(16) WS {
-        uint8_t act[2][ACH][8];
-        uint8_t view[VBP];
-        double rew[8];
-        uint8_t dir[8];
-        uint8_t done[8];
-        uint32_t board[16][8];
-        uint32_t stream[kWNW];
-    };
-    __shared__ uint64_t s_spread[32];
-    __shared__ WS wsm[4];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = lane >> 2, k = lane & 3;
-    WS &S = wsm[warp];
-    init_spread(s_spread);
-    __syncthreads();
-    const int64_t B = E.B;
-    const int64_t lane0 = ((int64_t)blockIdx.x * 4 + warp) * 8;
-    if (lane0 >= B) return;
-    const int64_t l = lane0 + grp;
-    const bool live = l < B;
-    const int nv = (int)((B - lane0) < 8 ? (B - lane0) : 8);
-    const bool vec = vec_ok && nv == 8;
-    uint32_t *bd = &S.board[0][grp];
     LaneRec L{};
     Mask m;
     bool lvl_changed = false;
-    uint32_t my_spec = 0xFFFFFFFFu;
+    uint32_t epoch = 0, my_spec = 0xFFFFFFFFu;
     if (live) {
         L = unpack_st(E.st[l]);
-        for (int w = k; w < 16; w += 4) bd[w * 8] = E.board[w * B + l];
+        uint32_t *rec = epochs + (size_t)l * kRec;
+#pragma unroll
+        for (int w = 0; w < 16; w++) {
+            const uint32_t v = E.board[w * B + l];
+            bd[w * LPW] = v;
+            rec[w] = v;
+        }
+        rec[16] = (uint32_t)L.gr | ((uint32_t)L.gc << 8);
         if (mode == AMZ_RESET_RESAMPLE) my_spec = spec_step[l];
     }
-    const bool avec = vec_ok && nv == 8;
-    fetch_actions<8>(S.act[0], actions, B, lane0, nv, 0, T, lane, avec);
+    const bool vec = avec && nv == LPW;
+    fetch_actions<LPW>(S.act[0], actions, B, lane0, nv, 0, T, lane, vec);
     __syncwarp();
+    uint32_t *pp = poses + l;
+    double *rp = reward + l;
+    uint8_t *dp = done + l;
+    const uint8_t *ap = &S.act[0][0][lane < LPW ? lane : 0];
     for (int t = 0; t < T; t++) {
         if ((t % ACH) == 0) {
-            // chunk t/ACH is in flight since one chunk ago; start the next one
-            fetch_actions<8>(S.act[((t / ACH) + 1) & 1], actions, B, lane0, nv, t + ACH, T, lane, avec);
+            fetch_actions<LPW>(S.act[((t / ACH) + 1) & 1], actions, B, lane0, nv, t + ACH, T, lane, vec);
             cp_wait<1>();
             __syncwarp();
         }
-        const uint8_t a = S.act[(t / ACH) & 1][t % ACH][grp];
         bool dn = false;
         if (live) {
-            if (SEE)
-                render_rows_see<V, 4, 8>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, bd, s_spread, k,
-                                         S.view + grp * VV);
-            else
-                render_lane<V, false, 8>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, bd, s_spread,
-                                         S.view + grp * VV, k, 4);
-            if (k == 0) S.dir[grp] = (uint8_t)L.s.d;
-            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, 8);
+            *pp = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 10);
+            const uint8_t a = ap[((t / ACH) & 1) * ACH * LPW + (t % ACH) * LPW];
+            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, LPW);
             dn = reached || L.s.time >= G.tep;
-            if (k == 1) {
-                S.rew[grp] = reached ? goal_reward(L.s.time, G.tep) : 0.0;
-                S.done[grp] = dn;
-            }
+            *rp = reached ? (use_lut ? s_rew[L.s.time] : goal_reward(L.s.time, G.tep)) : 0.0;
+            *dp = dn;
         }
-        __syncwarp();
-        // ship this step's 8-lane runs
-        const int64_t row = (int64_t)t * B + lane0;
-        if (vec) {
-            for (int x = lane; x < VB / 8; x += 32)
-                reinterpret_cast<uint64_t *>(view + row * VV)[x] = reinterpret_cast<const uint64_t *>(S.view)[x];
-            if (lane < 8) reward[row + lane] = S.rew[lane];
-            if (lane == 8) *reinterpret_cast<uint64_t *>(dirs + row) = *reinterpret_cast<const uint64_t *>(S.dir);
-            if (lane == 9) *reinterpret_cast<uint64_t *>(done + row) = *reinterpret_cast<const uint64_t *>(S.done);
-        } else {
-            for (int x = lane; x < nv * VV; x += 32) view[row * VV + x] = S.view[x];
-            if (lane < nv) {
-                reward[row + lane] = S.rew[lane];
-                dirs[row + lane] = S.dir[lane];
-                done[row + lane] = S.done[lane];
-            }
-        }
-        const unsigned any = __ballot_sync(0xFFFFFFFFu, dn && k == 0);
-        if (any) {
-            const uint32_t gstep = step0 + (uint32_t)t;
+        pp += B;
+        rp += B;
+        dp += B;
+        const unsigned fin = __ballot_sync(0xFFFFFFFFu, dn);
+        if (fin) {
             if (mode == AMZ_RESET_RESAMPLE) {
+                const uint32_t gstep = step0 + (uint32_t)t;
                 const bool hit = dn && my_spec == gstep;
-                if (hit) {
-                    int ar, ac, ad, gr, gc;
-                    load_level(spec + l, m, ar, ac, ad, gr, gc);
-                    if (k == 0) build_board(m, G, bd, 8);
+                const unsigned need = __ballot_sync(0xFFFFFFFFu, dn && !hit);
+                int ar = 0, ac = 0, ad = 0, gr = 0, gc = 0;
+                if (need) {
+                    uint64_t k0 = 0, k1 = 0;
+                    if (dn && !hit) {
+                        amz_seed_t sd = wrap;
+                        seed_absorb(sd, gstep);
+                        seed_absorb(sd, E.lane_offset + (uint32_t)l);
+                        seed_key(sd, k0, k1);
+                    }
+                    warp_sample_batch<LPW>(need, k0, k1, G, &S.stream[0][0], &S.perm[0][0], S.key, m, ar, ac, ad, gr,
+                                           gc);
+                }
+                if (hit) load_level(spec + l, m, ar, ac, ad, gr, gc);
+                if (dn) {
+                    build_board(m, G, bd, LPW);
                     L.hr = ar;
                     L.hc = ac;
                     L.hd = ad;
                     L.gr = gr;
                     L.gc = gc;
                     lvl_changed = true;
-                }
-                unsigned todo = __ballot_sync(0xFFFFFFFFu, dn && !hit && k == 0);
-                while (todo) {
-                    const int tl = __ffs(todo) - 1;  // lane index of the group leader
-                    todo &= todo - 1;
-                    amz_seed_t sd = wrap;
-                    seed_absorb(sd, gstep);
-                    seed_absorb(sd, E.lane_offset + (uint32_t)(lane0 + (tl >> 2)));
-                    uint64_t k0, k1;
-                    seed_key(sd, k0, k1);
-                    Mask nm;
-                    int ar, ac, ad, gr, gc;
-                    warp_sample_level(k0, k1, G, S.stream, nm, ar, ac, ad, gr, gc);
-                    if (grp == (tl >> 2)) {
-                        m = nm;
-                        if (k == 0) build_board(m, G, bd, 8);
-                        L.hr = ar;
-                        L.hc = ac;
-                        L.hd = ad;
-                        L.gr = gr;
-                        L.gc = gc;
-                        lvl_changed = true;
-                    }
-                    __syncwarp();
+                    epoch++;
+                    uint32_t *rec = epochs + ((size_t)epoch * B + l) * kRec;
+#pragma unroll
+                    for (int w = 0; w < 16; w++) rec[w] = bd[w * LPW];
+                    rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
                 }
             }
             if (dn) {
@@ -570,122 +330,187 @@ __global__ void __launch_bounds__(128) k_rollout_g4(Geo G, EnvDev E, int T, cons
                 L.term = false;
             }
         }
-        __syncwarp();
     }
-    // cursor observation + state write-back
     if (live) {
-        if (SEE)
-            render_rows_see<V, 4, 8>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, bd, s_spread, k, S.view + grp * VV);
-        else
-            render_lane<V, false, 8>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, bd, s_spread, S.view + grp * VV, k,
-                                     4);
-        if (k == 0) {
-            S.dir[grp] = (uint8_t)L.s.d;
-            E.st[l] = pack_st(L);
-            if (lvl_changed) E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+        final_pose[l] = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 10);
+        E.st[l] = pack_st(L);
+        if (lvl_changed) {
+            E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+#pragma unroll
+            for (int w = 0; w < 16; w++) E.board[w * B + l] = bd[w * LPW];
         }
-        if (lvl_changed)
-            for (int w = k; w < 16; w += 4) E.board[w * B + l] = bd[w * 8];
     }
-    __syncwarp();
-    if (fview)
-        for (int x = lane; x < nv * VV; x += 32) fview[lane0 * VV + x] = S.view[x];
-    if (fdir && lane < nv) fdir[lane0 + lane] = S.dir[lane];
+}
+
+// Speculative timeout levels: a lane that never reaches the goal times out at the step
+// where its time hits max_episode_steps; that level's key is known now, so it is
+// sampled up front with everyone else's (8 lanes per warp, staged SIMT sampler).
+__global__ void __launch_bounds__(128) k_spec_levels(Geo G, EnvDev E, int T, amz_seed_t wrap, uint32_t step0,
+                                                     amz_level_t *__restrict__ spec, uint32_t *__restrict__ spec_step) {
+    constexpr int LPW = 8;
+    __shared__ __align__(16) uint32_t sw[4][kSNW * LPW];
+    __shared__ uint8_t perm[4][128 * LPW];
+    __shared__ uint64_t skey[4][2 * LPW];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t l0 = ((int64_t)blockIdx.x * 4 + warp) * LPW;
+    if (l0 >= E.B) return;
+    const int64_t l = l0 + lane;
+    bool mine = false;
+    uint64_t k0 = 0, k1 = 0;
+    int s_to = -1;
+    if (lane < LPW && l < E.B) {
+        const LaneRec L = unpack_st(E.st[l]);
+        s_to = G.tep - L.s.time - 1;
+        mine = s_to >= 0 && s_to < T;
+        if (mine) {
+            amz_seed_t sd = wrap;
+            seed_absorb(sd, step0 + (uint32_t)s_to);
+            seed_absorb(sd, E.lane_offset + (uint32_t)l);
+            seed_key(sd, k0, k1);
+        } else {
+            spec_step[l] = 0xFFFFFFFFu;
+        }
+    }
+    const unsigned need = __ballot_sync(0xFFFFFFFFu, mine);
+    if (!need) return;
+    Mask m;
+    int ar, ac, ad, gr, gc;
+    warp_sample_batch<LPW>(need, k0, k1, G, sw[warp], perm[warp], skey[warp], m, ar, ac, ad, gr, gc);
+    if (mine) {
+        store_level(spec + l, m, ar, ac, ad, gr, gc);
+        spec_step[l] = step0 + (uint32_t)s_to;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// phase 2: observations
+// ---------------------------------------------------------------------------------
+template <int V, bool SEE>
+__global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, const uint32_t *__restrict__ poses,
+                                                const uint32_t *__restrict__ epochs, uint8_t *__restrict__ view,
+                                                uint8_t *__restrict__ dirs, int bulk_ok) {
+    constexpr int VV = V * V;
+    __shared__ __align__(128) uint8_t s_view[128 * VV];
+    __shared__ __align__(16) uint8_t s_dir[128];
+    __shared__ uint64_t s_spread[32];
+    init_spread(s_spread);
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * 128;
+    const int64_t i = base + threadIdx.x;
+    if (i < n) {
+        const uint32_t pr = poses[i];
+        const int64_t l = i % B;
+        const uint32_t *rec = epochs + ((size_t)(pr >> 10) * B + l) * kRec;
+        const uint32_t gw = rec[16];
+        const int r = pr & 15, c = (pr >> 4) & 15, d = (pr >> 8) & 3;
+        render_lane<V, SEE, 1>(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, s_spread, s_view + threadIdx.x * VV);
+        s_dir[threadIdx.x] = (uint8_t)d;
+    }
+    const int nvalid = (int)((n - base) < 128 ? (n - base) : 128);
+    if (bulk_ok && nvalid == 128) {
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_store(view + base * VV, s_view, 128 * VV);
+            if (dirs) bulk_store(dirs + base, s_dir, 128);
+            bulk_commit();
+            bulk_wait_all();
+        }
+    } else {
+        __syncthreads();
+        for (int x = threadIdx.x; x < nvalid * VV; x += 128) view[base * VV + x] = s_view[x];
+        if (dirs && threadIdx.x < nvalid) dirs[base + threadIdx.x] = s_dir[threadIdx.x];
+    }
+}
+
+template <int LPW, int WPC>
+static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode, const amz_seed_t &wrap,
+                       uint32_t step0, double *reward, uint8_t *done, uint32_t *poses, uint32_t *epochs,
+                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s) {
+    const int use_lut = G.tep <= 4096;
+    const size_t sm = (size_t)WPC * sizeof(DynSmem<LPW>) + (use_lut ? ((size_t)G.tep + 1) * 8 : 0);
+    cudaFuncSetAttribute(k_dyn<LPW, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const int avec = (E.B % 4 == 0) && ((((uintptr_t)actions) & 3u) == 0);
+    if (mode == AMZ_RESET_RESAMPLE)
+        k_spec_levels<<<(unsigned)((E.B + 31) / 32), 128, 0, s>>>(G, E, T, wrap, step0, spec, spec_step);
+    const int64_t warps = (E.B + LPW - 1) / LPW;
+    k_dyn<LPW, WPC><<<(unsigned)((warps + WPC - 1) / WPC), 32 * WPC, sm, s>>>(
+        G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, avec, use_lut);
 }
 
 template <int V, bool SEE>
-static int launch_rollout_g4(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
-                             const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
-                             uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
-    auto al8 = [](const void *p) { return (((uintptr_t)p) & 7u) == 0; };
-    const int vec = (E.B % 8 == 0) && al8(view) && al8(dirs) && al8(reward) && al8(done) &&
-                    ((((uintptr_t)actions) & 3u) == 0);
-    if (mode == AMZ_RESET_RESAMPLE)
-        k_spec_levels<<<(unsigned)((E.B + 3) / 4), 128, 0, s>>>(G, E, T, wrap, step0, E.spec, E.spec_step);
-    const unsigned grid = (unsigned)((E.B + 31) / 32);
-    k_rollout_g4<V, SEE><<<grid, 128, 0, s>>>(G, E, T, actions, mode, wrap, step0, view, dirs, reward, done, fview,
-                                              fdir, E.spec, E.spec_step, vec);
-    return 0;
-}
-
-template <int V, bool SEE, int NS, int WPC>
-static int launch_rollout_t(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
-                            const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
-                            uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
-    const size_t sm = 256 + (size_t)WPC * sizeof(WarpSmem<V, NS>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_rollout<V, SEE, NS, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr = true;
-    }
+static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *poses, const uint32_t *epochs,
+                          uint8_t *view, uint8_t *dirs, cudaStream_t s) {
     auto al16 = [](const void *p) { return p == nullptr || (((uintptr_t)p) & 15u) == 0; };
-    const int bulk = (E.B % 32 == 0) && al16(view) && al16(dirs) && al16(reward) && al16(done) && al16(fview) &&
-                     al16(fdir) && ((((uintptr_t)actions) & 3u) == 0);
-    if (mode == AMZ_RESET_RESAMPLE)
-        k_spec_levels<<<(unsigned)((E.B + 3) / 4), 128, 0, s>>>(G, E, T, wrap, step0, E.spec, E.spec_step);
-    const int64_t warps = (E.B + 31) / 32;
-    const unsigned grid = (unsigned)((warps + WPC - 1) / WPC);
-    k_rollout<V, SEE, NS, WPC><<<grid, 32 * WPC, sm, s>>>(G, E, T, actions, mode, wrap, step0, view, dirs, reward,
-                                                          done, fview, fdir, E.spec, E.spec_step, bulk);
-    return 0;
-}
-
-template <int V, bool SEE>
-static int launch_rollout_v(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
-                            const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
-                            uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
-    // small batches: 4 threads per lane (keeps ~3.5+ warps per SM at 4096 lanes);
-    // large batches: one lane per thread, TMA bulk stores
-    if (E.B <= 148 * 32 * 4)
-        return launch_rollout_g4<V, SEE>(G, E, T, actions, mode, wrap, step0, view, dirs, reward, done, fview, fdir,
-                                         s);
-    return launch_rollout_t<V, SEE, 4, 4>(G, E, T, actions, mode, wrap, step0, view, dirs, reward, done, fview, fdir,
-                                          s);
+    const int bulk = al16(view) && al16(dirs);
+    k_render<V, SEE><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(G, B, n, poses, epochs, view, dirs, bulk);
 }
 
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
                        const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
-                       uint8_t *done, uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
+                       uint8_t *done, uint8_t *fview, uint8_t *fdir, uint32_t *poses, uint32_t *epochs,
+                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s) {
     if (E.B <= 0) return 0;
-#define AMZ_RV(VV_)                                                                                              \
-    case VV_:                                                                                                    \
-        return G.see ? launch_rollout_v<VV_, true>(G, E, T, actions, mode, wrap, step0, view, dirs, reward, done, \
-                                                   fview, fdir, s)                                               \
-                     : launch_rollout_v<VV_, false>(G, E, T, actions, mode, wrap, step0, view, dirs, reward, done, \
-                                                    fview, fdir, s);
+    if (E.B <= 148 * 8 * 16)
+        launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step,
+                         s);
+    else
+        launch_dyn<32, 2>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec,
+                          spec_step, s);
+    const int64_t n = (int64_t)T * E.B;
+#define AMZ_RR(VV_)                                                                                      \
+    case VV_:                                                                                            \
+        if (G.see) {                                                                                     \
+            launch_render<VV_, true>(G, E.B, n, poses, epochs, view, dirs, s);                           \
+            launch_render<VV_, true>(G, E.B, E.B, final_pose, epochs, fview, fdir, s);                   \
+        } else {                                                                                         \
+            launch_render<VV_, false>(G, E.B, n, poses, epochs, view, dirs, s);                          \
+            launch_render<VV_, false>(G, E.B, E.B, final_pose, epochs, fview, fdir, s);                  \
+        }                                                                                                \
+        return 0;
     switch (G.V) {
-        AMZ_RV(3)
-        AMZ_RV(5)
-        AMZ_RV(7)
-        AMZ_RV(9)
+        AMZ_RR(3)
+        AMZ_RR(5)
+        AMZ_RR(7)
+        AMZ_RR(9)
         default:
             return AMZ_ECONFIG;
     }
-#undef AMZ_RV
+#undef AMZ_RR
 }
 
-// DR level generation: one warp per level (amz_sampler.cuh)
-__global__ void __launch_bounds__(128) k_sample_levels_w(Geo G, amz_seed_t prefix, uint32_t lane0,
+// ---------------------------------------------------------------------------------
+// DR level generation: 8 levels per warp through the staged SIMT sampler
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_sample_levels_b(Geo G, amz_seed_t prefix, uint32_t lane0,
                                                          const uint32_t *__restrict__ lane_ids, int64_t n,
                                                          amz_level_t *__restrict__ out) {
-    __shared__ __align__(16) uint32_t sw[4][kWNW];
+    constexpr int LPW = 8;
+    __shared__ __align__(16) uint32_t sw[4][kSNW * LPW];
+    __shared__ uint8_t perm[4][128 * LPW];
+    __shared__ uint64_t skey[4][2 * LPW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * 4 + warp;
-    if (i >= n) return;
-    amz_seed_t s = prefix;
-    seed_absorb(s, lane_ids ? lane_ids[i] : lane0 + (uint32_t)i);
-    uint64_t k0, k1;
-    seed_key(s, k0, k1);
+    const int64_t i0 = ((int64_t)blockIdx.x * 4 + warp) * LPW;
+    if (i0 >= n) return;
+    const int64_t i = i0 + lane;
+    const bool mine = lane < LPW && i < n;
+    uint64_t k0 = 0, k1 = 0;
+    if (mine) {
+        amz_seed_t s = prefix;
+        seed_absorb(s, lane_ids ? lane_ids[i] : lane0 + (uint32_t)i);
+        seed_key(s, k0, k1);
+    }
+    const unsigned need = __ballot_sync(0xFFFFFFFFu, mine);
     Mask m;
     int ar, ac, ad, gr, gc;
-    warp_sample_level(k0, k1, G, sw[warp], m, ar, ac, ad, gr, gc);
-    if (lane == 0) store_level(out + i, m, ar, ac, ad, gr, gc);
+    warp_sample_batch<LPW>(need, k0, k1, G, sw[warp], perm[warp], skey[warp], m, ar, ac, ad, gr, gc);
+    if (mine) store_level(out + i, m, ar, ac, ad, gr, gc);
 }
 
 int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, const uint32_t *ids, int64_t n,
                          amz_level_t *out, cudaStream_t s) {
     if (n <= 0) return 0;
-    k_sample_levels_w<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(G, prefix, lane0, ids, n, out);
+    k_sample_levels_b<<<(unsigned)((n + 31) / 32), 128, 0, s>>>(G, prefix, lane0, ids, n, out);
     return 0;
 }
 
