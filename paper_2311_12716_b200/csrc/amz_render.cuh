@@ -27,19 +27,21 @@ struct LaneDyn {
 
 // One transition; returns reached.  Unknown action codes are no-ops with time + 1,
 // exactly as step_batch treats them.  `board` gives the wall bits of grid row k at
-// board[k * stride] (low 16 bits).
+// board[k * stride] (low 16 bits).  Branch-free: lanes of a warp taking different
+// actions do not serialise.  Turn deltas and heading vectors come from nibble tables:
+// turn (a=0: +3, a=1: +1, else 0) = 0x13 >> 4a; dr+1 per heading = 0x1210 >> 4d,
+// dc+1 per heading = 0x0121 >> 4d (N, E, S, W as amaze/level.py:19-27).
 __device__ __forceinline__ bool lane_transition(LaneDyn &s, int a, int gr, int gc, const uint32_t *board,
                                                 int stride) {
-    int d = s.d;
-    d = a == 0 ? ((d + 3) & 3) : (a == 1 ? ((d + 1) & 3) : d);
-    if (a == 2) {
-        int tr = s.r + dir_dr(d), tc = s.c + dir_dc(d);
-        uint32_t row = board[tr * stride];
-        if (!((row >> tc) & 1u)) {
-            s.r = tr;
-            s.c = tc;
-        }
-    }
+    const uint32_t ua = (uint32_t)a < 3u ? (uint32_t)a : 3u;
+    const int d = (s.d + (int)((0x13u >> (4u * ua)) & 0xFu)) & 3;
+    const bool fwd = ua == 2u;
+    const int dr = (int)((0x1210u >> (4 * d)) & 0xFu) - 1;
+    const int dc = (int)((0x0121u >> (4 * d)) & 0xFu) - 1;
+    const int tr = fwd ? s.r + dr : s.r, tc = fwd ? s.c + dc : s.c;
+    const bool blocked = (board[tr * stride] >> tc) & 1u;
+    s.r = blocked ? s.r : tr;
+    s.c = blocked ? s.c : tc;
     s.d = d;
     s.time += 1;
     return s.r == gr && s.c == gc;

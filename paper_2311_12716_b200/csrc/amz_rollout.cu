@@ -267,72 +267,74 @@ __global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const 
     fetch_actions<LPW>(S.act[0], actions, B, lane0, nv, 0, T, lane, vec);
     __syncwarp();
     uint32_t *pp = poses + l;
-    double *rp = reward + l;
-    uint8_t *dp = done + l;
     const uint8_t *ap = &S.act[0][0][lane < LPW ? lane : 0];
-    for (int t = 0; t < T; t++) {
-        if ((t % ACH) == 0) {
-            fetch_actions<LPW>(S.act[((t / ACH) + 1) & 1], actions, B, lane0, nv, t + ACH, T, lane, vec);
-            cp_wait<1>();
-            __syncwarp();
-        }
-        bool dn = false;
-        if (live) {
-            *pp = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 10);
-            const uint8_t a = ap[((t / ACH) & 1) * ACH * LPW + (t % ACH) * LPW];
-            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, LPW);
-            dn = reached || L.s.time >= G.tep;
-            *rp = reached ? (use_lut ? s_rew[L.s.time] : goal_reward(L.s.time, G.tep)) : 0.0;
-            *dp = dn;
-        }
-        pp += B;
-        rp += B;
-        dp += B;
-        const unsigned fin = __ballot_sync(0xFFFFFFFFu, dn);
-        if (fin) {
-            if (mode == AMZ_RESET_RESAMPLE) {
-                const uint32_t gstep = step0 + (uint32_t)t;
-                const bool hit = dn && my_spec == gstep;
-                const unsigned need = __ballot_sync(0xFFFFFFFFu, dn && !hit);
-                int ar = 0, ac = 0, ad = 0, gr = 0, gc = 0;
-                if (need) {
-                    uint64_t k0 = 0, k1 = 0;
-                    if (dn && !hit) {
-                        amz_seed_t sd = wrap;
-                        seed_absorb(sd, gstep);
-                        seed_absorb(sd, E.lane_offset + (uint32_t)l);
-                        seed_key(sd, k0, k1);
-                    }
-                    warp_sample_batch<LPW>(need, k0, k1, G, &S.stream[0][0], &S.perm[0][0], S.key, m, ar, ac, ad, gr,
-                                           gc);
-                }
-                if (hit) load_level(spec + l, m, ar, ac, ad, gr, gc);
-                if (dn) {
-                    build_board(m, G, bd, LPW);
-                    L.hr = ar;
-                    L.hc = ac;
-                    L.hd = ad;
-                    L.gr = gr;
-                    L.gc = gc;
-                    lvl_changed = true;
-                    epoch++;
-                    uint32_t *rec = epochs + ((size_t)epoch * B + l) * kRec;
-#pragma unroll
-                    for (int w = 0; w < 16; w++) rec[w] = bd[w * LPW];
-                    rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
-                }
+    for (int t0 = 0; t0 < T; t0 += ACH) {
+        fetch_actions<LPW>(S.act[((t0 / ACH) + 1) & 1], actions, B, lane0, nv, t0 + ACH, T, lane, vec);
+        cp_wait<1>();
+        __syncwarp();
+        const uint8_t *ac = ap + ((t0 / ACH) & 1) * ACH * LPW;
+        const int tn = (T - t0) < ACH ? (T - t0) : ACH;
+#pragma unroll 4
+        for (int j = 0; j < tn; j++) {
+            const int t = t0 + j;
+            bool dn = false;
+            if (live) {
+                // step record: pose before the step (its observation), reached, done, epoch
+                const uint32_t pose = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 12);
+                const uint8_t a = ac[j * LPW];
+                const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, LPW);
+                dn = reached || L.s.time >= G.tep;
+                *pp = pose | ((uint32_t)reached << 10) | ((uint32_t)dn << 11);
+                // only goal steps carry a reward; k_render writes the zeros of all other steps
+                if (reached) reward[(int64_t)t * B + l] = use_lut ? s_rew[L.s.time] : goal_reward(L.s.time, G.tep);
             }
-            if (dn) {
-                L.s.r = L.hr;
-                L.s.c = L.hc;
-                L.s.d = L.hd;
-                L.s.time = 0;
-                L.term = false;
+            pp += B;
+            const unsigned fin = __ballot_sync(0xFFFFFFFFu, dn);
+            if (fin) {
+                if (mode == AMZ_RESET_RESAMPLE) {
+                    const uint32_t gstep = step0 + (uint32_t)t;
+                    const bool hit = dn && my_spec == gstep;
+                    const unsigned need = __ballot_sync(0xFFFFFFFFu, dn && !hit);
+                    int ar = 0, acol = 0, ad = 0, gr = 0, gc = 0;
+                    if (need) {
+                        uint64_t k0 = 0, k1 = 0;
+                        if (dn && !hit) {
+                            amz_seed_t sd = wrap;
+                            seed_absorb(sd, gstep);
+                            seed_absorb(sd, E.lane_offset + (uint32_t)l);
+                            seed_key(sd, k0, k1);
+                        }
+                        warp_sample_batch<LPW>(need, k0, k1, G, &S.stream[0][0], &S.perm[0][0], S.key, m, ar, acol, ad,
+                                               gr, gc);
+                    }
+                    if (hit) load_level(spec + l, m, ar, acol, ad, gr, gc);
+                    if (dn) {
+                        build_board(m, G, bd, LPW);
+                        L.hr = ar;
+                        L.hc = acol;
+                        L.hd = ad;
+                        L.gr = gr;
+                        L.gc = gc;
+                        lvl_changed = true;
+                        epoch++;
+                        uint32_t *rec = epochs + ((size_t)epoch * B + l) * kRec;
+#pragma unroll
+                        for (int w = 0; w < 16; w++) rec[w] = bd[w * LPW];
+                        rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
+                    }
+                }
+                if (dn) {
+                    L.s.r = L.hr;
+                    L.s.c = L.hc;
+                    L.s.d = L.hd;
+                    L.s.time = 0;
+                    L.term = false;
+                }
             }
         }
     }
     if (live) {
-        final_pose[l] = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 10);
+        final_pose[l] = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 12);
         E.st[l] = pack_st(L);
         if (lvl_changed) {
             E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
@@ -388,10 +390,12 @@ __global__ void __launch_bounds__(128) k_spec_levels(Geo G, EnvDev E, int T, amz
 template <int V, bool SEE>
 __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, const uint32_t *__restrict__ poses,
                                                 const uint32_t *__restrict__ epochs, uint8_t *__restrict__ view,
-                                                uint8_t *__restrict__ dirs, int bulk_ok) {
+                                                uint8_t *__restrict__ dirs, double *__restrict__ reward,
+                                                uint8_t *__restrict__ done, int bulk_ok) {
     constexpr int VV = V * V;
     __shared__ __align__(128) uint8_t s_view[128 * VV];
     __shared__ __align__(16) uint8_t s_dir[128];
+    __shared__ __align__(16) uint8_t s_done[128];
     __shared__ uint64_t s_spread[32];
     init_spread(s_spread);
     __syncthreads();
@@ -400,11 +404,13 @@ __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, con
     if (i < n) {
         const uint32_t pr = poses[i];
         const int64_t l = i % B;
-        const uint32_t *rec = epochs + ((size_t)(pr >> 10) * B + l) * kRec;
+        const uint32_t *rec = epochs + ((size_t)(pr >> 12) * B + l) * kRec;
         const uint32_t gw = rec[16];
         const int r = pr & 15, c = (pr >> 4) & 15, d = (pr >> 8) & 3;
         render_lane<V, SEE, 1>(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, s_spread, s_view + threadIdx.x * VV);
         s_dir[threadIdx.x] = (uint8_t)d;
+        s_done[threadIdx.x] = (uint8_t)((pr >> 11) & 1u);
+        if (reward && !((pr >> 10) & 1u)) reward[i] = 0.0;
     }
     const int nvalid = (int)((n - base) < 128 ? (n - base) : 128);
     if (bulk_ok && nvalid == 128) {
@@ -413,13 +419,17 @@ __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, con
         if (threadIdx.x == 0) {
             bulk_store(view + base * VV, s_view, 128 * VV);
             if (dirs) bulk_store(dirs + base, s_dir, 128);
+            if (done) bulk_store(done + base, s_done, 128);
             bulk_commit();
             bulk_wait_all();
         }
     } else {
         __syncthreads();
         for (int x = threadIdx.x; x < nvalid * VV; x += 128) view[base * VV + x] = s_view[x];
-        if (dirs && threadIdx.x < nvalid) dirs[base + threadIdx.x] = s_dir[threadIdx.x];
+        if (threadIdx.x < nvalid) {
+            if (dirs) dirs[base + threadIdx.x] = s_dir[threadIdx.x];
+            if (done) done[base + threadIdx.x] = s_done[threadIdx.x];
+        }
     }
 }
 
@@ -440,10 +450,11 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
 
 template <int V, bool SEE>
 static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *poses, const uint32_t *epochs,
-                          uint8_t *view, uint8_t *dirs, cudaStream_t s) {
+                          uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done, cudaStream_t s) {
     auto al16 = [](const void *p) { return p == nullptr || (((uintptr_t)p) & 15u) == 0; };
-    const int bulk = al16(view) && al16(dirs);
-    k_render<V, SEE><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(G, B, n, poses, epochs, view, dirs, bulk);
+    const int bulk = al16(view) && al16(dirs) && al16(done);
+    k_render<V, SEE><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(G, B, n, poses, epochs, view, dirs, reward, done,
+                                                                  bulk);
 }
 
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
@@ -452,7 +463,7 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
                        uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s) {
     if (E.B <= 0) return 0;
     if (E.B <= 148 * 8 * 16)
-        launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step,
+        launch_dyn<4, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step,
                          s);
     else
         launch_dyn<32, 2>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec,
@@ -461,11 +472,11 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
 #define AMZ_RR(VV_)                                                                                      \
     case VV_:                                                                                            \
         if (G.see) {                                                                                     \
-            launch_render<VV_, true>(G, E.B, n, poses, epochs, view, dirs, s);                           \
-            launch_render<VV_, true>(G, E.B, E.B, final_pose, epochs, fview, fdir, s);                   \
+            launch_render<VV_, true>(G, E.B, n, poses, epochs, view, dirs, reward, done, s);             \
+            launch_render<VV_, true>(G, E.B, E.B, final_pose, epochs, fview, fdir, nullptr, nullptr, s); \
         } else {                                                                                         \
-            launch_render<VV_, false>(G, E.B, n, poses, epochs, view, dirs, s);                          \
-            launch_render<VV_, false>(G, E.B, E.B, final_pose, epochs, fview, fdir, s);                  \
+            launch_render<VV_, false>(G, E.B, n, poses, epochs, view, dirs, reward, done, s);            \
+            launch_render<VV_, false>(G, E.B, E.B, final_pose, epochs, fview, fdir, nullptr, nullptr, s); \
         }                                                                                                \
         return 0;
     switch (G.V) {
