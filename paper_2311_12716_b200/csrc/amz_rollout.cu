@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const 
     uint32_t *bd = &S.board[0][lane < LPW ? lane : 0];
 
     LaneRec L{};
+    L.s.r = L.s.c = 1;  // idle lanes step harmlessly inside the grid
     Mask m;
     bool lvl_changed = false;
     uint32_t epoch = 0, my_spec = 0xFFFFFFFFu;
@@ -277,13 +278,13 @@ __global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const 
 #pragma unroll 4
         for (int j = 0; j < tn; j++) {
             const int t = t0 + j;
-            bool dn = false;
+            // step record: pose before the step (its observation), reached, done, epoch.
+            // Idle lanes (lane >= LPW) run the same arithmetic; only their stores are off.
+            const uint32_t pose = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 12);
+            const uint8_t a = ac[j * LPW];
+            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, LPW);
+            const bool dn = live && (reached || L.s.time >= G.tep);
             if (live) {
-                // step record: pose before the step (its observation), reached, done, epoch
-                const uint32_t pose = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 12);
-                const uint8_t a = ac[j * LPW];
-                const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, LPW);
-                dn = reached || L.s.time >= G.tep;
                 *pp = pose | ((uint32_t)reached << 10) | ((uint32_t)dn << 11);
                 // only goal steps carry a reward; k_render writes the zeros of all other steps
                 if (reached) reward[(int64_t)t * B + l] = use_lut ? s_rew[L.s.time] : goal_reward(L.s.time, G.tep);
@@ -462,12 +463,14 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
                        uint8_t *done, uint8_t *fview, uint8_t *fdir, uint32_t *poses, uint32_t *epochs,
                        uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s) {
     if (E.B <= 0) return 0;
+    // few lanes per warp: the per-lane chain is latency-bound, and a warp stalls for
+    // every resample of any of its lanes, so small warps finish sooner
     if (E.B <= 148 * 8 * 16)
         launch_dyn<4, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step,
                          s);
     else
-        launch_dyn<32, 2>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec,
-                          spec_step, s);
+        launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec,
+                         spec_step, s);
     const int64_t n = (int64_t)T * E.B;
 #define AMZ_RR(VV_)                                                                                      \
     case VV_:                                                                                            \
