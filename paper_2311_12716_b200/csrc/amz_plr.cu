@@ -275,38 +275,111 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 //                     (twin_first, via a global hash with atomicMin)
 //   B  (all threads)  m_low = min(current min score, scores of candidates that can
 //                     update in place).  If the buffer starts full, a candidate with
-//                     no key match and score <= m_low can never enter (the min never
+//                     no key match and score <= m_low can never enter (the minimum never
 //                     drops below m_low), so it is skipped; everything else is
 //                     "relevant" and compacted in order.
-//   C  (warp 0)       replays the relevant candidates in order: in-place updates,
-//                     fill inserts, evictions of the (score, last_sampled, seq)
-//                     minimum (recomputed lazily by the warp when a candidate needs it).
+//   C  (one thread)   replays the relevant candidates in order against an indexed
+//                     binary min-heap of (score, tb) in shared memory, tb = last_sampled
+//                     << 32 | seq (the stale-first eviction order): an in-place update is
+//                     one sift, an eviction is replace-top + sift-down, candidate data are
+//                     prefetched into shared memory by the whole CTA chunk by chunk, and
+//                     level / max_return copies are deferred to a parallel epilogue.
 // ---------------------------------------------------------------------------------
 constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses the hash table's space)
 struct CandChunk {
     double sc[kChunk];
-    double mr[kChunk];
     int32_t cid[kChunk];
     int32_t tf[kChunk];
     int32_t im[kChunk];
 };
 struct UpdSmem {
-    double score[kPlrMaxK];
-    uint64_t tb[kPlrMaxK];  // eviction tie-break key (last_sampled << 32) | seq: lexicographic (last, seq)
-    int64_t last[kPlrMaxK];
-    int64_t seq[kPlrMaxK];
+    double hs[kPlrMaxK];    // heap: score
+    uint64_t ht[kPlrMaxK];  // heap: tie-break key (last_sampled << 32) | seq
+    int hslot[kPlrMaxK];    // heap entry -> buffer slot
+    int pos[kPlrMaxK];      // buffer slot -> heap entry
     union {
         uint32_t hash[kHash];
         CandChunk chunk;
     } u;
-    int owner[kPlrMaxK];  // first-candidate index of the key now in the slot, -1 = initial entry
+    int owner[kPlrMaxK];   // first-candidate index of the key now in the slot, -1 = initial entry
+    int src[kPlrMaxK];     // candidate whose level the slot now holds (-1 = unchanged)
+    int mr_src[kPlrMaxK];  // candidate whose max_return the slot now holds (-1 = unchanged)
     uint32_t replaced[kPlrMaxK / 32];
-    int gmin[kPlrMaxK / 32];  // per 32-slot group: slot of its (score, tb) minimum
     double mlow;
+    int64_t next_seq;
     int n_rel;
     int full;
+    int size;
 };
 static_assert(sizeof(CandChunk) <= sizeof(uint32_t) * kHash, "chunk must fit in the hash table space");
+
+// 32-ary min-heap: children of h are 32h+1 .. 32h+32 (4096 entries -> 3 levels), so a
+// sift-down step is one coalesced load of the 32 children by the warp plus a register
+// arg-min, and a sift-up step is one compare.
+__device__ __forceinline__ bool key_lt(double sa, uint64_t ta, double sb, uint64_t tb) {
+    return sa < sb || (sa == sb && ta < tb);
+}
+__device__ __forceinline__ void heap_swap(UpdSmem &S, int a, int b) {  // one thread
+    const double s = S.hs[a];
+    const uint64_t t = S.ht[a];
+    const int x = S.hslot[a], y = S.hslot[b];
+    S.hs[a] = S.hs[b];
+    S.ht[a] = S.ht[b];
+    S.hslot[a] = y;
+    S.hs[b] = s;
+    S.ht[b] = t;
+    S.hslot[b] = x;
+    S.pos[y] = a;
+    S.pos[x] = b;
+}
+// whole warp, uniform control flow
+__device__ __forceinline__ void heap_up_w(UpdSmem &S, int h, int lane) {
+    while (h > 0) {
+        const int p = (h - 1) >> 5;
+        if (!key_lt(S.hs[h], S.ht[h], S.hs[p], S.ht[p])) break;
+        if (lane == 0) heap_swap(S, h, p);
+        __syncwarp();
+        h = p;
+    }
+}
+__device__ __forceinline__ void heap_down_w(UpdSmem &S, int h, int n, int lane) {
+    while (true) {
+        const int c0 = 32 * h + 1;
+        if (c0 >= n) break;
+        const int c = c0 + lane;
+        int ki = c < n ? c : -1;
+        double ks = ki >= 0 ? S.hs[c] : 0.0;
+        uint64_t kt = ki >= 0 ? S.ht[c] : 0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double s2 = __shfl_xor_sync(0xFFFFFFFFu, ks, o);
+            const uint64_t t2 = __shfl_xor_sync(0xFFFFFFFFu, kt, o);
+            const int i2 = __shfl_xor_sync(0xFFFFFFFFu, ki, o);
+            if (i2 >= 0 && (ki < 0 || key_lt(s2, t2, ks, kt))) {
+                ks = s2;
+                kt = t2;
+                ki = i2;
+            }
+        }
+        if (!key_lt(ks, kt, S.hs[h], S.ht[h])) break;
+        if (lane == 0) heap_swap(S, h, ki);
+        __syncwarp();
+        h = ki;
+    }
+}
+// one thread (heapify: disjoint subtrees per level)
+__device__ __forceinline__ void heap_down_t(UpdSmem &S, int h, int n) {
+    while (true) {
+        const int c0 = 32 * h + 1;
+        if (c0 >= n) break;
+        const int ce = c0 + 32 < n ? c0 + 32 : n;
+        int m = c0;
+        for (int c = c0 + 1; c < ce; c++)
+            if (key_lt(S.hs[c], S.ht[c], S.hs[m], S.ht[m])) m = c;
+        if (!key_lt(S.hs[m], S.ht[m], S.hs[h], S.ht[h])) break;
+        heap_swap(S, h, m);
+        h = m;
+    }
+}
 
 __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
                                 int64_t hsize) {
@@ -357,23 +430,26 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     UpdSmem &S = *reinterpret_cast<UpdSmem *>(smraw);
     const int tid = threadIdx.x, lane = tid & 31;
     const int K = (int)D.K;
-    int size = (int)D.meta[0];
-    // ---- A: load buffer scalars + key hash ----
+    const int size0 = (int)D.meta[0];
+    // ---- A: load the buffer into the heap arrays + key hash ----
     for (int i = tid; i < kHash; i += blockDim.x) S.u.hash[i] = 0u;
     for (int i = tid; i < kPlrMaxK / 32; i += blockDim.x) S.replaced[i] = 0u;
     if (tid == 0) {
         S.n_rel = 0;
-        S.full = size >= K;
+        S.full = size0 >= K;
     }
     __syncthreads();
     double my_min = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-    for (int i = tid; i < size; i += blockDim.x) {
-        S.score[i] = D.score[i];
-        S.last[i] = D.last[i];
-        S.seq[i] = D.seq[i];
-        S.tb[i] = ((uint64_t)S.last[i] << 32) | (uint32_t)S.seq[i];
+    for (int i = tid; i < size0; i += blockDim.x) {
+        const double sc = D.score[i];
+        S.hs[i] = sc;
+        S.ht[i] = ((uint64_t)D.last[i] << 32) | (uint32_t)D.seq[i];
+        S.hslot[i] = i;
+        S.pos[i] = i;
         S.owner[i] = -1;
-        my_min = fmin(my_min, S.score[i]);
+        S.src[i] = -1;
+        S.mr_src[i] = -1;
+        my_min = fmin(my_min, sc);
         uint4 w;
         uint32_t p0, p1;
         level_key(D.levels + i, w, p0, p1);
@@ -410,6 +486,16 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         for (int k = 1; k < (int)(blockDim.x >> 5); k++) m = fmin(m, wmin[k]);
         S.mlow = m;
     }
+    // ---- heapify, level-parallel (all sift-downs of one level touch disjoint subtrees) ----
+    // level starts of the 32-ary heap: 0, 1, 33, 1057
+    {
+        const int starts[4] = {0, 1, 33, 1057};
+        for (int lv = 2; lv >= 0; lv--) {
+            __syncthreads();
+            const int lo = starts[lv], hi = min(starts[lv + 1], size0);
+            for (int h = lo + tid; h < hi; h += blockDim.x) heap_down_t(S, h, size0);
+        }
+    }
     __syncthreads();
     // ---- B: relevant candidates, compacted in order (block-wide, chunk by chunk) ----
     __shared__ int wcount[32];
@@ -439,73 +525,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     // A skipped first occurrence is never inserted (score <= mlow), so its later twins,
     // which are always relevant, correctly find no entry for the key (keyslot = -1).
 
-    // ---- C: ordered replay ----
-    // Minimum of (score, tb) kept in two levels: the minimum slot of every 32-slot group
-    // (S.gmin, computed here by all warps) and the overall minimum, recomputed by warp 0
-    // from the group minima only when an insertion needs it and something changed.
-    const int ngroups = (size + 31) / 32;
-    const int warp = tid >> 5;
-    auto key_less = [&](int a, int b) {  // (score, tb) order of two valid slots
-        const double sa = S.score[a], sb = S.score[b];
-        if (sa != sb) return sa < sb;
-        return S.tb[a] < S.tb[b];
-    };
-    auto group_min = [&](int g, int cur_size) {  // whole warp; returns the group's min slot (uniform)
-        const int sl = g * 32 + lane;
-        int bi = sl < cur_size ? sl : -1;
-        for (int o = 16; o > 0; o >>= 1) {
-            const int j = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
-            if (j >= 0 && (bi < 0 || key_less(j, bi) || (!key_less(bi, j) && j < bi))) bi = j;
-        }
-        return bi;
-    };
-    for (int g = tid; g < kPlrMaxK / 32; g += blockDim.x) S.gmin[g] = -1;
-    __syncthreads();
-    for (int g = warp; g < ngroups; g += (int)(blockDim.x >> 5)) {
-        const int m = group_min(g, size);
-        if (lane == 0) S.gmin[g] = m;
-    }
-    __syncthreads();
+    // ---- C: ordered replay by one thread ----
     const int nrel = S.n_rel;
+    int size = size0;
     int64_t next_seq = D.meta[1];
-    int gslot = -1;                  // cached overall minimum slot
-    bool gvalid = false;
-    uint32_t dirty[kPlrMaxK / 32 / 32];  // dirty group bits (warp-uniform)
-#pragma unroll
-    for (int i = 0; i < kPlrMaxK / 1024; i++) dirty[i] = 0u;
-    auto overall_min = [&]() {
-        // refresh dirty groups, then reduce the group minima (4 per lane)
-        for (int w = 0; w < kPlrMaxK / 1024; w++) {
-            uint32_t bits = dirty[w];
-            while (bits) {
-                const int g = w * 32 + __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int m = group_min(g, size);
-                if (lane == 0) S.gmin[g] = m;
-            }
-            dirty[w] = 0u;
-        }
-        __syncwarp();
-        int bi = -1;
-        for (int g = lane; g < (size + 31) / 32; g += 32) {
-            const int j = S.gmin[g];
-            if (j >= 0 && (bi < 0 || key_less(j, bi))) bi = j;
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const int j = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
-            if (j >= 0 && (bi < 0 || key_less(j, bi) || (!key_less(bi, j) && j < bi))) bi = j;
-        }
-        gslot = bi;
-        gvalid = true;
-    };
-    auto touched = [&](int slot) {  // slot's key changed: mark its group, drop the cached minimum
-        const int g = slot >> 5;
-        const int w = g >> 5;
-#pragma unroll
-        for (int i = 0; i < kPlrMaxK / 1024; i++)
-            if (i == w) dirty[i] |= 1u << (g & 31);
-        gvalid = false;
-    };
     for (int base = 0; base < nrel; base += kChunk) {
         const int cn = (nrel - base) < kChunk ? (nrel - base) : kChunk;
         __syncthreads();
@@ -513,12 +536,11 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             const int c = W.rel[base + i];
             S.u.chunk.cid[i] = c;
             S.u.chunk.sc[i] = cscore[c];
-            S.u.chunk.mr[i] = cmax[c];
             S.u.chunk.tf[i] = W.twin_first[c];
             S.u.chunk.im[i] = W.init_match[c];
         }
         __syncthreads();
-        if (warp != 0) continue;
+        if (tid >= 32) continue;
         for (int r = 0; r < cn; r++) {
             const int c = S.u.chunk.cid[r];
             const double sc = S.u.chunk.sc[r];
@@ -527,60 +549,83 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             int present = -1;
             if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
             if (present < 0 && f != c) present = W.keyslot[f];
-            if (present >= 0) {
+            if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
+                const int h = S.pos[present];
+                const double old = S.hs[h];
+                __syncwarp();
                 if (lane == 0) {
-                    S.score[present] = sc;
-                    D.maxret[present] = S.u.chunk.mr[r];
+                    S.hs[h] = sc;
+                    S.mr_src[present] = c;
                 }
                 __syncwarp();
-                // keep the two-level minimum exact: a decrease can only lower the minima
-                const int g = present >> 5;
-                const int gm = S.gmin[g];
-                if (gm < 0 || gm == present) {
-                    touched(present);
-                } else if (key_less(present, gm)) {
-                    if (lane == 0) S.gmin[g] = present;
-                    __syncwarp();
-                    if (gvalid && gslot >= 0 && key_less(present, gslot)) gslot = present;
-                }
+                if (sc < old)
+                    heap_up_w(S, h, lane);
+                else if (sc > old)
+                    heap_down_w(S, h, size, lane);
                 continue;
             }
+            const uint64_t tbn = ((uint64_t)iter << 32) | (uint32_t)next_seq;
             int slot;
-            if (size < K) {
-                slot = size++;
-            } else {
-                if (!gvalid) overall_min();
-                if (!(sc > S.score[gslot])) continue;
-                slot = gslot;
+            if (size < K) {  // fill
+                slot = size;
+                const int h = size++;
+                __syncwarp();
+                if (lane == 0) {
+                    S.hs[h] = sc;
+                    S.ht[h] = tbn;
+                    S.hslot[h] = slot;
+                    S.pos[slot] = h;
+                }
+                __syncwarp();
+                heap_up_w(S, h, lane);
+            } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
+                if (!(sc > S.hs[0])) continue;
+                slot = S.hslot[0];
                 const int ow = S.owner[slot];
-                if (ow >= 0 && lane == 0) W.keyslot[ow] = -1;
+                __syncwarp();
+                if (lane == 0) {
+                    if (ow >= 0) W.keyslot[ow] = -1;
+                    S.hs[0] = sc;
+                    S.ht[0] = tbn;
+                }
+                __syncwarp();
+                heap_down_w(S, 0, size, lane);
             }
             if (lane == 0) {
-                S.score[slot] = sc;
-                S.last[slot] = iter;
-                S.seq[slot] = next_seq;
-                S.tb[slot] = ((uint64_t)iter << 32) | (uint32_t)next_seq;
                 S.owner[slot] = f;
                 S.replaced[slot >> 5] |= 1u << (slot & 31);
+                S.src[slot] = c;
+                S.mr_src[slot] = c;
                 W.keyslot[f] = slot;
-                D.maxret[slot] = S.u.chunk.mr[r];
-                D.levels[slot] = cand[c];
             }
-            next_seq++;
             __syncwarp();
-            touched(slot);
+            next_seq++;
+        }
+        if (lane == 0) {
+            S.size = size;
+            S.next_seq = next_seq;
         }
     }
-    __syncthreads();
-    if (warp != 0) return;
-    for (int i = lane; i < size; i += 32) {
-        D.score[i] = S.score[i];
-        D.last[i] = S.last[i];
-        D.seq[i] = S.seq[i];
+    if (tid == 0 && nrel == 0) {
+        S.size = size;
+        S.next_seq = next_seq;
     }
-    if (lane == 0) {
-        D.meta[0] = size;
-        D.meta[1] = next_seq;
+    __syncthreads();
+    // ---- epilogue: scatter the heap back to slots, deferred level / max_return copies ----
+    const int fsize = S.size;
+    for (int h = tid; h < fsize; h += blockDim.x) {
+        const int slot = S.hslot[h];
+        const uint64_t tb = S.ht[h];
+        D.score[slot] = S.hs[h];
+        D.last[slot] = (int64_t)(tb >> 32);
+        D.seq[slot] = (int64_t)(uint32_t)tb;
+        const int sc_ = slot < size0 ? S.src[slot] : S.src[slot];
+        if (sc_ >= 0) D.levels[slot] = cand[sc_];
+        if (S.mr_src[slot] >= 0) D.maxret[slot] = cmax[S.mr_src[slot]];
+    }
+    if (tid == 0) {
+        D.meta[0] = fsize;
+        D.meta[1] = S.next_seq;
     }
 }
 
