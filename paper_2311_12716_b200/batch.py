@@ -58,9 +58,12 @@ class DeviceLanes:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value and _lib._lib is not None:
-            _lib._lib.amz_env_destroy(h)
-            self.handle = None
+        try:
+            if h is not None and h.value and _lib._lib is not None:
+                _lib._lib.amz_env_destroy(h)
+        except (AttributeError, TypeError):  # interpreter shutdown: module globals already cleared
+            pass
+        self.handle = None
 
     def __len__(self):
         return self.n

@@ -88,9 +88,12 @@ class LevelBuffer:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value and _lib._lib is not None:
-            _lib._lib.amz_plr_destroy(h)
-            self.handle = None
+        try:
+            if h is not None and h.value and _lib._lib is not None:
+                _lib._lib.amz_plr_destroy(h)
+        except (AttributeError, TypeError):  # interpreter shutdown: module globals already cleared
+            pass
+        self.handle = None
 
     def _stream(self):
         return _lib.stream_handle(self.device)

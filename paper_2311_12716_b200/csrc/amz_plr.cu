@@ -278,8 +278,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 //                     no key match and score <= m_low can never enter (the minimum never
 //                     drops below m_low), so it is skipped; everything else is
 //                     "relevant" and compacted in order.
-//   C  (one thread)   replays the relevant candidates in order against an indexed
-//                     binary min-heap of (score, tb) in shared memory, tb = last_sampled
+//   C  (one warp)     replays the relevant candidates in order against an indexed
+//                     32-ary min-heap of (score, tb) in shared memory, tb = last_sampled
 //                     << 32 | seq (the stale-first eviction order): an in-place update is
 //                     one sift, an eviction is replace-top + sift-down, candidate data are
 //                     prefetched into shared memory by the whole CTA chunk by chunk, and
@@ -293,7 +293,7 @@ struct CandChunk {
     int32_t im[kChunk];
 };
 struct UpdSmem {
-    double hs[kPlrMaxK];    // heap: score
+    uint64_t hk[kPlrMaxK];  // heap: order-preserving score key (score_key)
     uint64_t ht[kPlrMaxK];  // heap: tie-break key (last_sampled << 32) | seq
     int hslot[kPlrMaxK];    // heap entry -> buffer slot
     int pos[kPlrMaxK];      // buffer slot -> heap entry
@@ -303,7 +303,7 @@ struct UpdSmem {
     } u;
     int owner[kPlrMaxK];   // first-candidate index of the key now in the slot, -1 = initial entry
     int src[kPlrMaxK];     // candidate whose level the slot now holds (-1 = unchanged)
-    int mr_src[kPlrMaxK];  // candidate whose max_return the slot now holds (-1 = unchanged)
+    int mr_src[kPlrMaxK];  // candidate whose score / max_return the slot now holds (-1 = unchanged)
     uint32_t replaced[kPlrMaxK / 32];
     double mlow;
     int64_t next_seq;
@@ -313,72 +313,92 @@ struct UpdSmem {
 };
 static_assert(sizeof(CandChunk) <= sizeof(uint32_t) * kHash, "chunk must fit in the hash table space");
 
-// 32-ary min-heap: children of h are 32h+1 .. 32h+32 (4096 entries -> 3 levels), so a
-// sift-down step is one coalesced load of the 32 children by the warp plus a register
-// arg-min, and a sift-up step is one compare.
-__device__ __forceinline__ bool key_lt(double sa, uint64_t ta, double sb, uint64_t tb) {
-    return sa < sb || (sa == sb && ta < tb);
+// Scores enter the heap as order-preserving unsigned keys (-0.0 folded onto +0.0, as the
+// float compare of the reference sees them), so every comparison is integer and a warp
+// arg-min is a redux.sync on the high word (ties fall through to the lower words).
+__device__ __forceinline__ uint64_t score_key(double s) {
+    s = s == 0.0 ? 0.0 : s;
+    const uint64_t u = (uint64_t)__double_as_longlong(s);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
-__device__ __forceinline__ void heap_swap(UpdSmem &S, int a, int b) {  // one thread
-    const double s = S.hs[a];
-    const uint64_t t = S.ht[a];
-    const int x = S.hslot[a], y = S.hslot[b];
-    S.hs[a] = S.hs[b];
-    S.ht[a] = S.ht[b];
-    S.hslot[a] = y;
-    S.hs[b] = s;
-    S.ht[b] = t;
-    S.hslot[b] = x;
-    S.pos[y] = a;
-    S.pos[x] = b;
+__device__ __forceinline__ bool ukey_lt(uint64_t ka, uint64_t ta, uint64_t kb, uint64_t tb) {
+    return ka < kb || (ka == kb && ta < tb);
 }
-// whole warp, uniform control flow
-__device__ __forceinline__ void heap_up_w(UpdSmem &S, int h, int lane) {
+__device__ __forceinline__ void heap_put(UpdSmem &S, int h, uint64_t k, uint64_t t, int slot) {
+    S.hk[h] = k;
+    S.ht[h] = t;
+    S.hslot[h] = slot;
+    S.pos[slot] = h;
+}
+// lanes whose bit is set in `eq` compete; narrows `eq` to the lanes holding the minimum of v
+__device__ __forceinline__ unsigned warp_argmin_word(unsigned eq, uint32_t v, int lane) {
+    const bool in = (eq >> lane) & 1u;
+    const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, in ? v : 0xFFFFFFFFu);
+    return __ballot_sync(0xFFFFFFFFu, in && v == m);
+}
+// 32-ary min-heap (children of h are 32h+1 .. 32h+32; 4096 entries -> 3 levels below the
+// root).  The entry x = (xk, xt, xs) is sifted from the hole h: each level is one coalesced
+// load of the 32 children by the warp, a ballot of "child < x" and a redux arg-min; the
+// winning lane moves its child into the hole.  Whole warp, uniform control flow.
+__device__ __forceinline__ void sift_down_w(UpdSmem &S, int h, int n, uint64_t xk, uint64_t xt, int xs, int lane) {
+    while (true) {
+        const int c = 32 * h + 1 + lane;
+        const bool valid = c < n;
+        uint64_t ck = ~0ull, ct = ~0ull;
+        int cs = 0;
+        if (valid) {
+            ck = S.hk[c];
+            ct = S.ht[c];
+            cs = S.hslot[c];
+        }
+        unsigned eq = __ballot_sync(0xFFFFFFFFu, valid && ukey_lt(ck, ct, xk, xt));
+        if (eq == 0u) break;
+        eq = warp_argmin_word(eq, (uint32_t)(ck >> 32), lane);
+        if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)ck, lane);
+        if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)(ct >> 32), lane);
+        if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)ct, lane);
+        const int win = __ffs(eq) - 1;
+        if (lane == win) heap_put(S, h, ck, ct, cs);
+        h = 32 * h + 1 + win;
+    }
+    if (lane == 0) heap_put(S, h, xk, xt, xs);
+    __syncwarp();
+}
+__device__ __forceinline__ void sift_up_w(UpdSmem &S, int h, uint64_t xk, uint64_t xt, int xs, int lane) {
     while (h > 0) {
         const int p = (h - 1) >> 5;
-        if (!key_lt(S.hs[h], S.ht[h], S.hs[p], S.ht[p])) break;
-        if (lane == 0) heap_swap(S, h, p);
-        __syncwarp();
+        const uint64_t pk = S.hk[p], pt = S.ht[p];
+        if (!ukey_lt(xk, xt, pk, pt)) break;
+        const int ps = S.hslot[p];
+        if (lane == 0) heap_put(S, h, pk, pt, ps);
         h = p;
     }
-}
-__device__ __forceinline__ void heap_down_w(UpdSmem &S, int h, int n, int lane) {
-    while (true) {
-        const int c0 = 32 * h + 1;
-        if (c0 >= n) break;
-        const int c = c0 + lane;
-        int ki = c < n ? c : -1;
-        double ks = ki >= 0 ? S.hs[c] : 0.0;
-        uint64_t kt = ki >= 0 ? S.ht[c] : 0ull;
-        for (int o = 16; o > 0; o >>= 1) {
-            const double s2 = __shfl_xor_sync(0xFFFFFFFFu, ks, o);
-            const uint64_t t2 = __shfl_xor_sync(0xFFFFFFFFu, kt, o);
-            const int i2 = __shfl_xor_sync(0xFFFFFFFFu, ki, o);
-            if (i2 >= 0 && (ki < 0 || key_lt(s2, t2, ks, kt))) {
-                ks = s2;
-                kt = t2;
-                ki = i2;
-            }
-        }
-        if (!key_lt(ks, kt, S.hs[h], S.ht[h])) break;
-        if (lane == 0) heap_swap(S, h, ki);
-        __syncwarp();
-        h = ki;
-    }
+    if (lane == 0) heap_put(S, h, xk, xt, xs);
+    __syncwarp();
 }
 // one thread (heapify: disjoint subtrees per level)
 __device__ __forceinline__ void heap_down_t(UpdSmem &S, int h, int n) {
+    const uint64_t xk = S.hk[h], xt = S.ht[h];
+    const int xs = S.hslot[h];
     while (true) {
         const int c0 = 32 * h + 1;
         if (c0 >= n) break;
         const int ce = c0 + 32 < n ? c0 + 32 : n;
         int m = c0;
-        for (int c = c0 + 1; c < ce; c++)
-            if (key_lt(S.hs[c], S.ht[c], S.hs[m], S.ht[m])) m = c;
-        if (!key_lt(S.hs[m], S.ht[m], S.hs[h], S.ht[h])) break;
-        heap_swap(S, h, m);
+        uint64_t mk = S.hk[c0], mt = S.ht[c0];
+        for (int c = c0 + 1; c < ce; c++) {
+            const uint64_t k = S.hk[c], t = S.ht[c];
+            if (ukey_lt(k, t, mk, mt)) {
+                m = c;
+                mk = k;
+                mt = t;
+            }
+        }
+        if (!ukey_lt(mk, mt, xk, xt)) break;
+        heap_put(S, h, mk, mt, S.hslot[m]);
         h = m;
     }
+    heap_put(S, h, xk, xt, xs);
 }
 
 __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
@@ -442,7 +462,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     double my_min = __longlong_as_double(0x7FF0000000000000ll);  // +inf
     for (int i = tid; i < size0; i += blockDim.x) {
         const double sc = D.score[i];
-        S.hs[i] = sc;
+        S.hk[i] = score_key(sc);
         S.ht[i] = ((uint64_t)D.last[i] << 32) | (uint32_t)D.seq[i];
         S.hslot[i] = i;
         S.pos[i] = i;
@@ -549,19 +569,17 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             int present = -1;
             if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
             if (present < 0 && f != c) present = W.keyslot[f];
+            const uint64_t sk = score_key(sc);
             if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
                 const int h = S.pos[present];
-                const double old = S.hs[h];
+                const uint64_t ok = S.hk[h], ot = S.ht[h];
                 __syncwarp();
-                if (lane == 0) {
-                    S.hs[h] = sc;
-                    S.mr_src[present] = c;
-                }
+                if (lane == 0) S.mr_src[present] = c;
+                if (sk < ok)
+                    sift_up_w(S, h, sk, ot, present, lane);
+                else if (sk > ok)
+                    sift_down_w(S, h, size, sk, ot, present, lane);
                 __syncwarp();
-                if (sc < old)
-                    heap_up_w(S, h, lane);
-                else if (sc > old)
-                    heap_down_w(S, h, size, lane);
                 continue;
             }
             const uint64_t tbn = ((uint64_t)iter << 32) | (uint32_t)next_seq;
@@ -570,26 +588,14 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 slot = size;
                 const int h = size++;
                 __syncwarp();
-                if (lane == 0) {
-                    S.hs[h] = sc;
-                    S.ht[h] = tbn;
-                    S.hslot[h] = slot;
-                    S.pos[slot] = h;
-                }
-                __syncwarp();
-                heap_up_w(S, h, lane);
+                sift_up_w(S, h, sk, tbn, slot, lane);
             } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
-                if (!(sc > S.hs[0])) continue;
+                if (!(sk > S.hk[0])) continue;
                 slot = S.hslot[0];
                 const int ow = S.owner[slot];
                 __syncwarp();
-                if (lane == 0) {
-                    if (ow >= 0) W.keyslot[ow] = -1;
-                    S.hs[0] = sc;
-                    S.ht[0] = tbn;
-                }
-                __syncwarp();
-                heap_down_w(S, 0, size, lane);
+                if (lane == 0 && ow >= 0) W.keyslot[ow] = -1;
+                sift_down_w(S, 0, size, sk, tbn, slot, lane);
             }
             if (lane == 0) {
                 S.owner[slot] = f;
@@ -616,12 +622,14 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     for (int h = tid; h < fsize; h += blockDim.x) {
         const int slot = S.hslot[h];
         const uint64_t tb = S.ht[h];
-        D.score[slot] = S.hs[h];
         D.last[slot] = (int64_t)(tb >> 32);
         D.seq[slot] = (int64_t)(uint32_t)tb;
-        const int sc_ = slot < size0 ? S.src[slot] : S.src[slot];
-        if (sc_ >= 0) D.levels[slot] = cand[sc_];
-        if (S.mr_src[slot] >= 0) D.maxret[slot] = cmax[S.mr_src[slot]];
+        if (S.src[slot] >= 0) D.levels[slot] = cand[S.src[slot]];
+        const int mr = S.mr_src[slot];
+        if (mr >= 0) {
+            D.score[slot] = cscore[mr];
+            D.maxret[slot] = cmax[mr];
+        }
     }
     if (tid == 0) {
         D.meta[0] = fsize;
