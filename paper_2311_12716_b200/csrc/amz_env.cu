@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *_
                                                   double *__restrict__ solved, int64_t *__restrict__ times,
                                                   const int *__restrict__ term_in, int *__restrict__ term_out) {
     __shared__ __align__(16) uint8_t stage[128 * V * V];
-    __shared__ __align__(16) uint32_t sw[4][kWNW];
+    __shared__ __align__(16) WarpSampler sw[4];
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);

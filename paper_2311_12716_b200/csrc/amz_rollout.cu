@@ -219,9 +219,7 @@ template <int LPW>
 struct DynSmem {
     uint32_t board[16][LPW];
     uint8_t act[2][ACH][LPW];
-    uint32_t stream[kSNW][LPW];
-    uint64_t key[2 * LPW];
-    uint8_t perm[128][LPW];
+    WarpSampler samp;
 };
 
 template <int LPW, int WPC>
@@ -305,8 +303,7 @@ __global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const 
                             seed_absorb(sd, E.lane_offset + (uint32_t)l);
                             seed_key(sd, k0, k1);
                         }
-                        warp_sample_batch<LPW>(need, k0, k1, G, &S.stream[0][0], &S.perm[0][0], S.key, m, ar, acol, ad,
-                                               gr, gc);
+                        warp_sample_each(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
                     }
                     if (hit) load_level(spec + l, m, ar, acol, ad, gr, gc);
                     if (dn) {
@@ -347,13 +344,12 @@ __global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const 
 
 // Speculative timeout levels: a lane that never reaches the goal times out at the step
 // where its time hits max_episode_steps; that level's key is known now, so it is
-// sampled up front with everyone else's (8 lanes per warp, staged SIMT sampler).
+// sampled up front with everyone else's (kSpecLPW lanes per warp, warp-cooperative).
+constexpr int kSpecLPW = 1;
 __global__ void __launch_bounds__(128) k_spec_levels(Geo G, EnvDev E, int T, amz_seed_t wrap, uint32_t step0,
                                                      amz_level_t *__restrict__ spec, uint32_t *__restrict__ spec_step) {
-    constexpr int LPW = 8;
-    __shared__ __align__(16) uint32_t sw[4][kSNW * LPW];
-    __shared__ uint8_t perm[4][128 * LPW];
-    __shared__ uint64_t skey[4][2 * LPW];
+    constexpr int LPW = kSpecLPW;
+    __shared__ __align__(16) WarpSampler X[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t l0 = ((int64_t)blockIdx.x * 4 + warp) * LPW;
     if (l0 >= E.B) return;
@@ -378,7 +374,7 @@ __global__ void __launch_bounds__(128) k_spec_levels(Geo G, EnvDev E, int T, amz
     if (!need) return;
     Mask m;
     int ar, ac, ad, gr, gc;
-    warp_sample_batch<LPW>(need, k0, k1, G, sw[warp], perm[warp], skey[warp], m, ar, ac, ad, gr, gc);
+    warp_sample_each(need, k0, k1, G, X[warp], m, ar, ac, ad, gr, gc);
     if (mine) {
         store_level(spec + l, m, ar, ac, ad, gr, gc);
         spec_step[l] = step0 + (uint32_t)s_to;
@@ -443,7 +439,8 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
     cudaFuncSetAttribute(k_dyn<LPW, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int avec = (E.B % 4 == 0) && ((((uintptr_t)actions) & 3u) == 0);
     if (mode == AMZ_RESET_RESAMPLE)
-        k_spec_levels<<<(unsigned)((E.B + 31) / 32), 128, 0, s>>>(G, E, T, wrap, step0, spec, spec_step);
+        k_spec_levels<<<(unsigned)((E.B + 4 * kSpecLPW - 1) / (4 * kSpecLPW)), 128, 0, s>>>(G, E, T, wrap, step0, spec,
+                                                                                           spec_step);
     const int64_t warps = (E.B + LPW - 1) / LPW;
     k_dyn<LPW, WPC><<<(unsigned)((warps + WPC - 1) / WPC), 32 * WPC, sm, s>>>(
         G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, avec, use_lut);
@@ -494,15 +491,14 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
 }
 
 // ---------------------------------------------------------------------------------
-// DR level generation: 8 levels per warp through the staged SIMT sampler
+// DR level generation: kGenLPW levels per warp, warp-cooperative sampler
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_sample_levels_b(Geo G, amz_seed_t prefix, uint32_t lane0,
+constexpr int kGenLPW = 1;
+__global__ void __launch_bounds__(128) k_sample_levels_w(Geo G, amz_seed_t prefix, uint32_t lane0,
                                                          const uint32_t *__restrict__ lane_ids, int64_t n,
                                                          amz_level_t *__restrict__ out) {
-    constexpr int LPW = 8;
-    __shared__ __align__(16) uint32_t sw[4][kSNW * LPW];
-    __shared__ uint8_t perm[4][128 * LPW];
-    __shared__ uint64_t skey[4][2 * LPW];
+    constexpr int LPW = kGenLPW;
+    __shared__ __align__(16) WarpSampler X[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i0 = ((int64_t)blockIdx.x * 4 + warp) * LPW;
     if (i0 >= n) return;
@@ -517,14 +513,15 @@ __global__ void __launch_bounds__(128) k_sample_levels_b(Geo G, amz_seed_t prefi
     const unsigned need = __ballot_sync(0xFFFFFFFFu, mine);
     Mask m;
     int ar, ac, ad, gr, gc;
-    warp_sample_batch<LPW>(need, k0, k1, G, sw[warp], perm[warp], skey[warp], m, ar, ac, ad, gr, gc);
+    warp_sample_each(need, k0, k1, G, X[warp], m, ar, ac, ad, gr, gc);
     if (mine) store_level(out + i, m, ar, ac, ad, gr, gc);
 }
 
 int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, const uint32_t *ids, int64_t n,
                          amz_level_t *out, cudaStream_t s) {
     if (n <= 0) return 0;
-    k_sample_levels_b<<<(unsigned)((n + 31) / 32), 128, 0, s>>>(G, prefix, lane0, ids, n, out);
+    k_sample_levels_w<<<(unsigned)((n + 4 * kGenLPW - 1) / (4 * kGenLPW)), 128, 0, s>>>(G, prefix, lane0, ids, n,
+                                                                                          out);
     return 0;
 }
 

@@ -2,18 +2,14 @@
 //
 // One level per warp, bit-identical to numpy's stream consumption:
 //   * the level's Philox4x64-10 blocks are counter-indexed, so lane b computes block
-//     b+1 and the warp stages the first kNB blocks (kNB*8 u32 words) in shared memory;
+//     b+1 and the warp stages the first kWNB blocks (kWNB*8 u32 words) in shared memory;
 //     words past that are computed on demand (numpy's next_uint32 order: lo, hi of each
 //     u64, u64s in block order);
 //   * integers(0, n) (Lemire) draws run as uniform scalar code;
-//   * the Fisher-Yates of permutation(ni) needs, per step i, the first draw at or after
-//     the stream position whose masked value is <= i.  The warp tests 32 consecutive
-//     words at once (ballot + find-first), so a step costs a handful of dependent
-//     instructions instead of a rejection loop;
-//   * instead of materialising the permuted array, every lane tracks the final
-//     positions of its (up to 4) elements under the transpositions (i, j_i); the wall
-//     mask is then "elements whose final position < n_walls" (an OR-reduction), and
-//     the goal/agent are the elements at two final positions (a ballot).
+//   * the Fisher-Yates of permutation(ni) (masked rejection per step) is resolved 32
+//     stream words at a time, and the permuted array is read off the transpositions
+//     without replaying them (see warp_sample_level).
+// A staged SIMT variant (one level per lane, sequential Fisher-Yates) follows.
 #pragma once
 #include <stdint.h>
 
@@ -64,69 +60,146 @@ __device__ __forceinline__ void warp_stage_stream(uint64_t k0, uint64_t k1, uint
     __syncwarp();
 }
 
+// Per-warp shared scratch of warp_sample_level.
+struct WarpSampler {
+    uint32_t sw[kWNW];   // staged stream words
+    uint32_t L[128][4];  // L[q]: bit set of the steps i with j_i == q (128-bit)
+    uint8_t J[128];      // j_i of Fisher-Yates step i (J[0] = 0)
+    uint8_t T[128];      // terminal of the succ chain from i (pointer jumping)
+};
+
+// smallest element > after of the 128-bit set L[q], or -1
+__device__ __forceinline__ int set_next(const WarpSampler &X, int q, int after) {
+    const int s = after + 1;
+    for (int w = s >> 5; w < 4; w++) {
+        uint32_t bits = X.L[q][w];
+        if (w == (s >> 5)) bits &= ~0u << (s & 31);
+        if (bits) return w * 32 + __ffs(bits) - 1;
+    }
+    return -1;
+}
+
 // All 32 lanes call with the same key; every lane returns the same level.
-// `sw` = this warp's 16-byte aligned scratch of kWNW words.
-__device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, const Geo &G, uint32_t *sw, Mask &mask,
+//   1. j_i for every step i (numpy's masked rejection, i = ni-1 .. 1) in windows of 32
+//      stream words.  Word k of a window serves step i - c_k, c_k = accepted words
+//      before it, and is accepted iff (w_k & mask(i - c_k)) <= i - c_k: a triangular
+//      system solved by Jacobi sweeps (ballot + popc) from "all accepted"; it reaches
+//      the unique fixed point in ~4 sweeps, so a window settles ~25 steps at once.
+//   2. the permuted array without replaying the swaps: reading the transpositions
+//      backwards, position k holds the element reached by jumping first to the next
+//      step after k that drew the same j as k (or to j_k itself if there is none), then
+//      along succ(q) = first step after q that drew q.  The succ chains are collapsed by
+//      pointer jumping.
+__device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, const Geo &G, WarpSampler &X, Mask &mask,
                                                   int &ar, int &ac, int &ad, int &gr, int &gc) {
     const int lane = threadIdx.x & 31;
-    warp_stage_stream(k0, k1, sw);
-    const WarpStream S{sw, k0, k1};
+    const int ni = G.ni;
+    for (int x = lane; x < 128; x += 32) reinterpret_cast<uint4 *>(&X.L[0][0])[x] = make_uint4(0u, 0u, 0u, 0u);
+    warp_stage_stream(k0, k1, X.sw);
+    const WarpStream S{X.sw, k0, k1};
     uint32_t p = 0;
     const uint32_t nw = S.below(p, (uint32_t)G.budget + 1u);
-    // final positions of the elements this lane owns (lane, lane+32, lane+64, lane+96)
-    int pos0 = lane, pos1 = lane + 32, pos2 = lane + 64, pos3 = lane + 96;
-    uint32_t wb = p, w = S.word(wb + lane);
-    for (int i = G.ni - 1; i >= 1; i--) {
-        const uint32_t mk = 0xFFFFFFFFu >> __clz(i);
-        int j;
+    // ---- 1. j_i ----
+    const unsigned lt = (1u << lane) - 1u;
+    int i = ni - 1;
+    while (i >= 1) {
+        const uint32_t w = S.word(p + lane);
+        // c = accepted words before this lane; the step this word serves is i - c.
+        // Jacobi sweep from "all accepted" to the (unique) fixed point.
+        int c = lane, ik;
+        bool acc;
+        uint32_t v;
+        unsigned A;
         while (true) {
-            const int o = (int)(p - wb);
-            const bool ok = lane >= o && (w & mk) <= (uint32_t)i;
-            const unsigned b = __ballot_sync(0xFFFFFFFFu, ok);
-            if (b) {
-                const int f = __ffs(b) - 1;
-                j = (int)(__shfl_sync(0xFFFFFFFFu, w, f) & mk);
-                p = wb + f + 1;
-                break;
-            }
-            wb += 32;
-            w = S.word(wb + lane);
+            ik = i - c;
+            v = ik >= 1 ? (w & (0xFFFFFFFFu >> __clz(ik))) : 0xFFFFFFFFu;
+            acc = ik >= 1 && v <= (uint32_t)ik;
+            A = __ballot_sync(0xFFFFFFFFu, acc);
+            const int c2 = __popc(A & lt);
+            if (__all_sync(0xFFFFFFFFu, c2 == c)) break;
+            c = c2;
         }
-        pos0 = pos0 == i ? j : (pos0 == j ? i : pos0);
-        pos1 = pos1 == i ? j : (pos1 == j ? i : pos1);
-        pos2 = pos2 == i ? j : (pos2 == j ? i : pos2);
-        pos3 = pos3 == i ? j : (pos3 == j ? i : pos3);
+        if (acc) X.J[ik] = (uint8_t)v;
+        const int na = __popc(A);
+        p += (i - na >= 1) ? 32u : (uint32_t)(32 - __clz(A));  // through the last accepted word
+        i -= na;
     }
-    // walls: elements whose final position is below n_walls
-    const int ni = G.ni;
-    const uint32_t b0 = (lane < ni && pos0 < (int)nw) ? 1u : 0u;
-    const uint32_t b1 = (lane + 32 < ni && pos1 < (int)nw) ? 1u : 0u;
-    const uint32_t b2 = (lane + 64 < ni && pos2 < (int)nw) ? 1u : 0u;
-    const uint32_t b3 = (lane + 96 < ni && pos3 < (int)nw) ? 1u : 0u;
-    mask.w[0] = __ballot_sync(0xFFFFFFFFu, b0);
-    mask.w[1] = __ballot_sync(0xFFFFFFFFu, b1);
-    mask.w[2] = __ballot_sync(0xFFFFFFFFu, b2);
-    mask.w[3] = __ballot_sync(0xFFFFFFFFu, b3);
+    if (lane == 0) X.J[0] = 0;
+    __syncwarp();
+    // ---- 2. final positions ----
+    for (int k = lane; k < ni; k += 32) atomicOr(&X.L[X.J[k]][k >> 5], 1u << (k & 31));
+    __syncwarp();
+    for (int k = lane; k < ni; k += 32) {
+        const int sn = set_next(X, k, k);
+        X.T[k] = (uint8_t)(sn >= 0 ? sn : k);
+    }
+    __syncwarp();
+    while (true) {  // T[k] <- T[T[k]] until every chain is collapsed
+        bool moved = false;
+        for (int k = lane; k < ni; k += 32) {
+            const int t = X.T[k], tt = X.T[t];
+            if (tt != t) {
+                X.T[k] = (uint8_t)tt;
+                moved = true;
+            }
+        }
+        __syncwarp();
+        if (!__any_sync(0xFFFFFFFFu, moved)) break;
+    }
+    auto element = [&](int k) {
+        const int q = X.J[k];
+        const int sn = set_next(X, q, k);
+        return sn >= 0 ? (int)X.T[sn] : q;
+    };
+    uint32_t m0 = 0u, m1 = 0u, m2 = 0u, m3 = 0u;
+    for (int k = lane; k < (int)nw; k += 32) {
+        const int e = element(k);
+        const uint32_t b = 1u << (e & 31);
+        const int q = e >> 5;
+        m0 |= q == 0 ? b : 0u;
+        m1 |= q == 1 ? b : 0u;
+        m2 |= q == 2 ? b : 0u;
+        m3 |= q == 3 ? b : 0u;
+    }
+    mask.w[0] = __reduce_or_sync(0xFFFFFFFFu, m0);
+    mask.w[1] = __reduce_or_sync(0xFFFFFFFFu, m1);
+    mask.w[2] = __reduce_or_sync(0xFFFFFFFFu, m2);
+    mask.w[3] = __reduce_or_sync(0xFFFFFFFFu, m3);
     // goal = free[gk], agent = (free without goal)[ak]; free = final positions nw..ni-1
     const uint32_t nfree = (uint32_t)ni - nw;
     const uint32_t gk = S.below(p, nfree);
     const uint32_t ak = S.below(p, nfree - 1u);
     ad = (int)S.below(p, 4u);
-    const int pg = (int)(nw + gk), pa = (int)(nw + (ak < gk ? ak : ak + 1u));
-    auto elem_at = [&](int target) {
-        int e = -1;
-        if (lane < ni && pos0 == target) e = lane;
-        if (lane + 32 < ni && pos1 == target) e = lane + 32;
-        if (lane + 64 < ni && pos2 == target) e = lane + 64;
-        if (lane + 96 < ni && pos3 == target) e = lane + 96;
-        const unsigned b = __ballot_sync(0xFFFFFFFFu, e >= 0);
-        return __shfl_sync(0xFFFFFFFFu, e, __ffs(b) - 1);
-    };
-    const int goal = elem_at(pg), agent = elem_at(pa);
+    const int goal = element((int)(nw + gk)), agent = element((int)(nw + (ak < gk ? ak : ak + 1u)));
     gr = goal / G.iw + 1;
     gc = goal % G.iw + 1;
     ar = agent / G.iw + 1;
     ac = agent % G.iw + 1;
+    __syncwarp();
+}
+
+// Every lane whose bit is set in `need` gets the level of its own key (k0, k1), one
+// warp-cooperative sample per requesting lane.
+__device__ __forceinline__ void warp_sample_each(unsigned need, uint64_t k0, uint64_t k1, const Geo &G,
+                                                 WarpSampler &X, Mask &mask, int &ar, int &ac, int &ad, int &gr,
+                                                 int &gc) {
+    const int lane = threadIdx.x & 31;
+    while (need) {
+        const int tl = __ffs(need) - 1;
+        need &= need - 1;
+        const uint64_t a = __shfl_sync(0xFFFFFFFFu, k0, tl), b = __shfl_sync(0xFFFFFFFFu, k1, tl);
+        Mask m;
+        int r0, c0, d0, g0, h0;
+        warp_sample_level(a, b, G, X, m, r0, c0, d0, g0, h0);
+        if (lane == tl) {
+            mask = m;
+            ar = r0;
+            ac = c0;
+            ad = d0;
+            gr = g0;
+            gc = h0;
+        }
+    }
 }
 
 }  // namespace amz
