@@ -249,7 +249,7 @@ int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const
         e->poses = nullptr;
         e->epochs = nullptr;
         const size_t b = (size_t)e->E.B;
-        cudaError_t er = cudaMallocAsync((void **)&e->poses, (size_t)T * b * sizeof(uint32_t), s);
+        cudaError_t er = cudaMallocAsync((void **)&e->poses, (((size_t)T + 3) / 4) * 4 * b * sizeof(uint32_t), s);
         if (er == cudaSuccess) er = cudaMallocAsync((void **)&e->epochs, ((size_t)T + 1) * b * 20 * sizeof(uint32_t), s);
         if (er != cudaSuccess) {
             e->rollout_T = 0;

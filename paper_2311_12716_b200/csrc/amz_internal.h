@@ -45,7 +45,7 @@ int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adty
                     const amz_seed_t &wrap, uint32_t step_idx, uint8_t *view, int64_t *dirs, double *reward,
                     uint8_t *done, double *solved, int64_t *times, const int *term_in, int *term_out,
                     cudaStream_t s);
-// poses [T][B], epochs [(T+1)*B][20], final_pose [B]: rollout scratch (amz_rollout.cu)
+// poses [ceil(T/4)][B][4] (uint4 per lane per 4 steps), epochs [(T+1)*B][20], final_pose [B]: rollout scratch (amz_rollout.cu)
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
                        const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
                        uint8_t *done, uint8_t *fview, uint8_t *fdir, uint32_t *poses, uint32_t *epochs,

@@ -21,6 +21,7 @@
 // parallel and HBM-bound.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "amz_internal.h"
 #include "amz_render.cuh"
@@ -218,12 +219,20 @@ constexpr int kRec = 20;  // u32 words per epoch record: board[16], goal, pad
 template <int LPW>
 struct DynSmem {
     uint32_t board[16][LPW];
+    uint32_t cb[8][LPW];  // column-pair wall bitmap: bit (pos & 31) of word pos >> 5, pos = r | c << 4
     uint8_t act[2][ACH][LPW];
     WarpSampler samp;
 };
 
+// cb[q] = column 2q bits | column 2q+1 bits << 16 (the board words' high halves)
+template <int LPW>
+__device__ __forceinline__ void build_colpairs(const uint32_t *bd, uint32_t *cb) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) cb[q * LPW] = (bd[2 * q * LPW] >> 16) | (bd[(2 * q + 1) * LPW] & 0xFFFF0000u);
+}
+
 template <int LPW, int WPC>
-__global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions, int mode,
+__global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions, int mode,
                                                   amz_seed_t wrap, uint32_t step0, double *__restrict__ reward,
                                                   uint8_t *__restrict__ done, uint32_t *__restrict__ poses,
                                                   uint32_t *__restrict__ epochs, uint32_t *__restrict__ final_pose,
@@ -244,6 +253,7 @@ __global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const 
     const bool live = lane < LPW && l < B;
     const int nv = (int)((B - lane0) < LPW ? (B - lane0) : LPW);
     uint32_t *bd = &S.board[0][lane < LPW ? lane : 0];
+    uint32_t *cb = &S.cb[0][lane < LPW ? lane : 0];
 
     LaneRec L{};
     L.s.r = L.s.c = 1;  // idle lanes step harmlessly inside the grid
@@ -261,78 +271,142 @@ __global__ void __launch_bounds__(32 * WPC) k_dyn(Geo G, EnvDev E, int T, const 
         }
         rec[16] = (uint32_t)L.gr | ((uint32_t)L.gc << 8);
         if (mode == AMZ_RESET_RESAMPLE) my_spec = spec_step[l];
+        build_colpairs<LPW>(bd, cb);
     }
-    const bool vec = avec && nv == LPW;
+    const bool vec = avec && nv == LPW && LPW % 4 == 0;
     fetch_actions<LPW>(S.act[0], actions, B, lane0, nv, 0, T, lane, vec);
     __syncwarp();
-    uint32_t *pp = poses + l;
     const uint8_t *ap = &S.act[0][0][lane < LPW ? lane : 0];
+    // Packed lane state ps = r | c << 4 | heading << 8 | epoch << 12 (the pose record
+    // layout).  A forward move adds a signed nibble offset to ps; a turn rewrites bits
+    // 8-9.  Idle lanes never finish (goal 0xFF is unreachable from (1, 1), tep = inf).
+    uint32_t ps = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8);
+    uint32_t g = live ? ((uint32_t)L.gr | ((uint32_t)L.gc << 4)) : 0xFFu;
+    int time = L.s.time;
+    const int tep = live ? G.tep : 0x7FFFFFFF;
+    uint4 *pq = reinterpret_cast<uint4 *>(poses) + l;  // steps 4q..4q+3 of lane l at pq[q * B]
+
+    // one step; returns its record: pose before the step, reached (bit 10), done (bit 11)
+    auto step = [&](int t, uint32_t a) -> uint32_t {
+        const uint32_t ua = a < 3u ? a : 3u;
+        const uint32_t d = ((ps >> 8) + ((0x13u >> (4u * ua)) & 0xFu)) & 3u;
+        // heading -> (dr + 16 dc + 17): N 0x10, E 0x21, S 0x12, W 0x01
+        const uint32_t mv = ua == 2u ? ((0x01122110u >> (8u * d)) & 0xFFu) - 17u : 0u;
+        const uint32_t nps = ps + mv;
+        const uint32_t word = bd[(nps & 15u) * LPW];
+        const bool blocked = (word >> ((nps >> 4) & 15u)) & 1u;
+        const uint32_t before = ps;
+        ps = ((blocked ? ps : nps) & ~0x300u) | (d << 8);
+        time++;
+        const bool reached = ((ps ^ g) & 0xFFu) == 0u;
+        const bool dn = reached || time >= tep;
+        // only goal steps carry a reward; k_render writes the zeros of all other steps
+        if (reached) reward[(int64_t)t * B + l] = use_lut ? s_rew[time] : goal_reward(time, G.tep);
+        const unsigned fin = __ballot_sync(0xFFFFFFFFu, dn);
+        if (fin) {
+            if (mode == AMZ_RESET_RESAMPLE) {
+                const uint32_t gstep = step0 + (uint32_t)t;
+                const bool hit = dn && my_spec == gstep;
+                const unsigned need = __ballot_sync(0xFFFFFFFFu, dn && !hit);
+                int ar = 0, acol = 0, ad = 0, gr = 0, gc = 0;
+                if (need) {
+                    uint64_t k0 = 0, k1 = 0;
+                    if (dn && !hit) {
+                        amz_seed_t sd = wrap;
+                        seed_absorb(sd, gstep);
+                        seed_absorb(sd, E.lane_offset + (uint32_t)l);
+                        seed_key(sd, k0, k1);
+                    }
+                    warp_sample_each(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
+                }
+                if (hit) load_level(spec + l, m, ar, acol, ad, gr, gc);
+                if (dn) {
+                    build_board(m, G, bd, LPW);
+                    build_colpairs<LPW>(bd, cb);
+                    L.hr = ar;
+                    L.hc = acol;
+                    L.hd = ad;
+                    L.gr = gr;
+                    L.gc = gc;
+                    lvl_changed = true;
+                    epoch++;
+                    uint32_t *rec = epochs + ((size_t)epoch * B + l) * kRec;
+#pragma unroll
+                    for (int w = 0; w < 16; w++) rec[w] = bd[w * LPW];
+                    rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
+                }
+            }
+            if (dn) {
+                ps = (uint32_t)L.hr | ((uint32_t)L.hc << 4) | ((uint32_t)L.hd << 8) | (epoch << 12);
+                g = (uint32_t)L.gr | ((uint32_t)L.gc << 4);
+                time = 0;
+            }
+        }
+        return before | ((uint32_t)reached << 10) | ((uint32_t)dn << 11);
+    };
+
     for (int t0 = 0; t0 < T; t0 += ACH) {
         fetch_actions<LPW>(S.act[((t0 / ACH) + 1) & 1], actions, B, lane0, nv, t0 + ACH, T, lane, vec);
         cp_wait<1>();
         __syncwarp();
         const uint8_t *ac = ap + ((t0 / ACH) & 1) * ACH * LPW;
         const int tn = (T - t0) < ACH ? (T - t0) : ACH;
-#pragma unroll 4
-        for (int j = 0; j < tn; j++) {
-            const int t = t0 + j;
-            // step record: pose before the step (its observation), reached, done, epoch.
-            // Idle lanes (lane >= LPW) run the same arithmetic; only their stores are off.
-            const uint32_t pose = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 12);
-            const uint8_t a = ac[j * LPW];
-            const bool reached = lane_transition(L.s, a, L.gr, L.gc, bd, LPW);
-            const bool dn = live && (reached || L.s.time >= G.tep);
-            if (live) {
-                *pp = pose | ((uint32_t)reached << 10) | ((uint32_t)dn << 11);
-                // only goal steps carry a reward; k_render writes the zeros of all other steps
-                if (reached) reward[(int64_t)t * B + l] = use_lut ? s_rew[L.s.time] : goal_reward(L.s.time, G.tep);
-            }
-            pp += B;
-            const unsigned fin = __ballot_sync(0xFFFFFFFFu, dn);
-            if (fin) {
-                if (mode == AMZ_RESET_RESAMPLE) {
-                    const uint32_t gstep = step0 + (uint32_t)t;
-                    const bool hit = dn && my_spec == gstep;
-                    const unsigned need = __ballot_sync(0xFFFFFFFFu, dn && !hit);
-                    int ar = 0, acol = 0, ad = 0, gr = 0, gc = 0;
-                    if (need) {
-                        uint64_t k0 = 0, k1 = 0;
-                        if (dn && !hit) {
-                            amz_seed_t sd = wrap;
-                            seed_absorb(sd, gstep);
-                            seed_absorb(sd, E.lane_offset + (uint32_t)l);
-                            seed_key(sd, k0, k1);
-                        }
-                        warp_sample_each(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
-                    }
-                    if (hit) load_level(spec + l, m, ar, acol, ad, gr, gc);
-                    if (dn) {
-                        build_board(m, G, bd, LPW);
-                        L.hr = ar;
-                        L.hc = acol;
-                        L.hd = ad;
-                        L.gr = gr;
-                        L.gc = gc;
-                        lvl_changed = true;
-                        epoch++;
-                        uint32_t *rec = epochs + ((size_t)epoch * B + l) * kRec;
+        // Speculative 8-step batches: the position chain alone (heading and move offset
+        // come from the actions, a wall test is one funnel shift of the column-pair
+        // bitmap), no per-step vote.  When any lane of the warp reaches its goal or times
+        // out inside a batch, the next quad runs through the exact per-step path (the
+        // only inlined copy of the reset / resample code) and speculation resumes after.
+        int j = 0;
+        while (j < tn) {
+            if (j + 8 <= tn) {
+                uint32_t pos = ps & 0xFFu, d = (ps >> 8) & 3u;
+                const uint32_t hi = ps & 0xFFFFF000u;
+                uint32_t rec[8];
+                bool hit = time + 8 >= tep;
 #pragma unroll
-                        for (int w = 0; w < 16; w++) rec[w] = bd[w * LPW];
-                        rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
-                    }
+                for (int k = 0; k < 8; k++) {
+                    const uint32_t a = ac[(j + k) * LPW];
+                    const uint32_t ua = a < 3u ? a : 3u;
+                    rec[k] = pos | (d << 8) | hi;
+                    d = (d + ((0x13u >> (4u * ua)) & 0xFu)) & 3u;
+                    const uint32_t mv = ua == 2u ? ((0x01122110u >> (8u * d)) & 0xFFu) - 17u : 0u;
+                    const uint32_t np = pos + mv;
+                    const uint32_t w = cb[(np >> 5) * LPW];
+                    pos = (__funnelshift_r(w, w, np) & 1u) ? pos : np;
+                    hit |= pos == g;
                 }
-                if (dn) {
-                    L.s.r = L.hr;
-                    L.s.c = L.hc;
-                    L.s.d = L.hd;
-                    L.s.time = 0;
-                    L.term = false;
+                if (!__any_sync(0xFFFFFFFFu, hit)) {
+                    ps = pos | (d << 8) | hi;
+                    time += 8;
+                    if (live) {
+                        pq[(size_t)((t0 + j) >> 2) * B] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
+                        pq[(size_t)((t0 + j + 4) >> 2) * B] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
+                    }
+                    j += 8;
+                    continue;
                 }
             }
+            uint32_t r0 = 0u, r1 = 0u, r2 = 0u, r3 = 0u;
+            const int kn = (tn - j) < 4 ? (tn - j) : 4;
+#pragma unroll 1
+            for (int k = 0; k < kn; k++) {
+                const uint32_t v = step(t0 + j + k, ac[(j + k) * LPW]);
+                r0 = k == 0 ? v : r0;
+                r1 = k == 1 ? v : r1;
+                r2 = k == 2 ? v : r2;
+                r3 = k == 3 ? v : r3;
+            }
+            if (live) pq[(size_t)((t0 + j) >> 2) * B] = make_uint4(r0, r1, r2, r3);
+            j += 4;
         }
     }
+    L.s.r = (int)(ps & 15u);
+    L.s.c = (int)((ps >> 4) & 15u);
+    L.s.d = (int)((ps >> 8) & 3u);
+    L.s.time = time;
+    L.term = false;
     if (live) {
-        final_pose[l] = (uint32_t)L.s.r | ((uint32_t)L.s.c << 4) | ((uint32_t)L.s.d << 8) | (epoch << 12);
+        final_pose[l] = ps;
         E.st[l] = pack_st(L);
         if (lvl_changed) {
             E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
@@ -388,7 +462,7 @@ template <int V, bool SEE>
 __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, const uint32_t *__restrict__ poses,
                                                 const uint32_t *__restrict__ epochs, uint8_t *__restrict__ view,
                                                 uint8_t *__restrict__ dirs, double *__restrict__ reward,
-                                                uint8_t *__restrict__ done, int bulk_ok) {
+                                                uint8_t *__restrict__ done, int bulk_ok, int quad) {
     constexpr int VV = V * V;
     __shared__ __align__(128) uint8_t s_view[128 * VV];
     __shared__ __align__(16) uint8_t s_dir[128];
@@ -399,8 +473,9 @@ __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, con
     const int64_t base = (int64_t)blockIdx.x * 128;
     const int64_t i = base + threadIdx.x;
     if (i < n) {
-        const uint32_t pr = poses[i];
-        const int64_t l = i % B;
+        const int64_t t = i / B, l = i - t * B;
+        // quad layout: steps 4q..4q+3 of lane l are the uint4 at (q * B + l)
+        const uint32_t pr = quad ? poses[((t >> 2) * B + l) * 4 + (t & 3)] : poses[i];
         const uint32_t *rec = epochs + ((size_t)(pr >> 12) * B + l) * kRec;
         const uint32_t gw = rec[16];
         const int r = pr & 15, c = (pr >> 4) & 15, d = (pr >> 8) & 3;
@@ -448,11 +523,11 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
 
 template <int V, bool SEE>
 static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *poses, const uint32_t *epochs,
-                          uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done, cudaStream_t s) {
+                          uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done, int quad, cudaStream_t s) {
     auto al16 = [](const void *p) { return p == nullptr || (((uintptr_t)p) & 15u) == 0; };
     const int bulk = al16(view) && al16(dirs) && al16(done);
     k_render<V, SEE><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(G, B, n, poses, epochs, view, dirs, reward, done,
-                                                                  bulk);
+                                                                  bulk, quad);
 }
 
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
@@ -462,7 +537,16 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
     if (E.B <= 0) return 0;
     // few lanes per warp: the per-lane chain is latency-bound, and a warp stalls for
     // every resample of any of its lanes, so small warps finish sooner
-    if (E.B <= 148 * 8 * 16)
+    static const int forced = getenv("AMZ_DYN_LPW") ? atoi(getenv("AMZ_DYN_LPW")) : 0;
+    if (forced == 1)
+        launch_dyn<1, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+    else if (forced == 2)
+        launch_dyn<2, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+    else if (forced == 8)
+        launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+    else if (forced == 16)
+        launch_dyn<16, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+    else if (E.B <= 148 * 8 * 16)
         launch_dyn<4, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step,
                          s);
     else
@@ -472,11 +556,11 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
 #define AMZ_RR(VV_)                                                                                      \
     case VV_:                                                                                            \
         if (G.see) {                                                                                     \
-            launch_render<VV_, true>(G, E.B, n, poses, epochs, view, dirs, reward, done, s);             \
-            launch_render<VV_, true>(G, E.B, E.B, final_pose, epochs, fview, fdir, nullptr, nullptr, s); \
+            launch_render<VV_, true>(G, E.B, n, poses, epochs, view, dirs, reward, done, 1, s);             \
+            launch_render<VV_, true>(G, E.B, E.B, final_pose, epochs, fview, fdir, nullptr, nullptr, 0, s); \
         } else {                                                                                         \
-            launch_render<VV_, false>(G, E.B, n, poses, epochs, view, dirs, reward, done, s);            \
-            launch_render<VV_, false>(G, E.B, E.B, final_pose, epochs, fview, fdir, nullptr, nullptr, s); \
+            launch_render<VV_, false>(G, E.B, n, poses, epochs, view, dirs, reward, done, 1, s);            \
+            launch_render<VV_, false>(G, E.B, E.B, final_pose, epochs, fview, fdir, nullptr, nullptr, 0, s); \
         }                                                                                                \
         return 0;
     switch (G.V) {
