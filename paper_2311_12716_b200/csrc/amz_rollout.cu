@@ -216,19 +216,71 @@ constexpr int kRec = 20;  // u32 words per epoch record: board[16], goal, pad
 // ---------------------------------------------------------------------------------
 // phase 1: dynamics
 // ---------------------------------------------------------------------------------
+#ifdef AMZ_DYN_PROF
+__device__ unsigned long long g_dyn_prof[65536][4];
+__device__ __forceinline__ unsigned smid_() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+#define DYN_MARK(k_)                                                                         \
+    do {                                                                                     \
+        const int64_t wi_ = (int64_t)blockIdx.x * WPC + (threadIdx.x >> 5);                  \
+        if ((threadIdx.x & 31) == 0 && wi_ < 65536) g_dyn_prof[wi_][k_] = clock64() | ((unsigned long long)smid_() << 56); \
+    } while (0)
+#else
+#define DYN_MARK(k_) \
+    do {             \
+    } while (0)
+#endif
+
 template <int LPW>
 struct DynSmem {
     uint32_t board[16][LPW];
-    uint32_t cb[8][LPW];  // column-pair wall bitmap: bit (pos & 31) of word pos >> 5, pos = r | c << 4
+    uint8_t mt[LPW][5][256];  // move table: position after a step, [heading or 4 = no move][pos]
     uint8_t act[2][ACH][LPW];
+    uint32_t aw[LPW][ACH / 4];  // this chunk's actions per lane, 4 steps per word
     WarpSampler samp;
 };
 
-// cb[q] = column 2q bits | column 2q+1 bits << 16 (the board words' high halves)
+// Move table of lane L (whole warp): mt[e][pos], pos = r | c << 4, is the position after
+// a forward move in heading e (unchanged when the target cell is a wall, as
+// lane_transition), and mt[4][pos] = pos (turns / no-ops).  A step of the position
+// chain is then one shared byte load.  A table word holds rows r0..r0+3 of column c:
+// the four wall flags of their targets are one shift of a column's wall bits (board
+// word high halves; off-grid targets count as walls), and the bytes are
+// pos + off * (not blocked), byte-parallel.
 template <int LPW>
-__device__ __forceinline__ void build_colpairs(const uint32_t *bd, uint32_t *cb) {
-#pragma unroll
-    for (int q = 0; q < 8; q++) cb[q * LPW] = (bd[2 * q * LPW] >> 16) | (bd[(2 * q + 1) * LPW] & 0xFFFF0000u);
+__device__ __forceinline__ void build_move_table(const uint32_t *board, int L, uint8_t *mt) {
+    const int lane = threadIdx.x & 31;
+    auto col = [&](int x) -> uint32_t { return (x >= 0 && x < 16) ? (board[x * LPW + L] >> 16) : 0xFFFFu; };
+    for (int w = lane; w < 5 * 64; w += 32) {
+        const int e = w >> 6, c = (w & 63) >> 2, r0 = (w & 3) << 2;
+        const uint32_t base4 = (uint32_t)(r0 | (c << 4)) * 0x01010101u + 0x03020100u;
+        uint32_t out = base4;
+        if (e < 4) {
+            uint32_t m;
+            int off;
+            if (e == 0) {  // N
+                m = ((col(c) << 1) | 1u) >> r0;
+                off = -1;
+            } else if (e == 2) {  // S
+                m = (col(c) | 0x10000u) >> (r0 + 1);
+                off = 1;
+            } else if (e == 1) {  // E
+                m = col(c + 1) >> r0;
+                off = 16;
+            } else {  // W
+                m = col(c - 1) >> r0;
+                off = -16;
+            }
+            const uint32_t open = ~m & 0xFu;
+            const uint32_t spread = (open * 0x00204081u) & 0x01010101u;
+            out = base4 + spread * (uint32_t)off;
+        }
+        reinterpret_cast<uint32_t *>(mt)[w] = out;
+    }
+    __syncwarp();
 }
 
 template <int LPW, int WPC>
@@ -240,6 +292,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                                                   const uint32_t *__restrict__ spec_step, int avec, int use_lut) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    static_assert(LPW % 4 == 0 && LPW <= 32, "lane-major action gather needs LPW a multiple of 4");
     DynSmem<LPW> &S = reinterpret_cast<DynSmem<LPW> *>(smem)[warp];
     // goal rewards R[time] = 1 - 0.9*time/T_ep (numpy's op order), tabulated per CTA
     double *s_rew = reinterpret_cast<double *>(smem + WPC * sizeof(DynSmem<LPW>));
@@ -247,13 +300,14 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
         for (int tt = threadIdx.x; tt <= G.tep; tt += blockDim.x) s_rew[tt] = goal_reward(tt, G.tep);
     __syncthreads();
     const int64_t B = E.B;
+    DYN_MARK(0);
     const int64_t lane0 = ((int64_t)blockIdx.x * WPC + warp) * LPW;
     if (lane0 >= B) return;
     const int64_t l = lane0 + lane;
     const bool live = lane < LPW && l < B;
     const int nv = (int)((B - lane0) < LPW ? (B - lane0) : LPW);
     uint32_t *bd = &S.board[0][lane < LPW ? lane : 0];
-    uint32_t *cb = &S.cb[0][lane < LPW ? lane : 0];
+    const uint8_t *mtl = &S.mt[lane < LPW ? lane : 0][0][0];
 
     LaneRec L{};
     L.s.r = L.s.c = 1;  // idle lanes step harmlessly inside the grid
@@ -263,16 +317,21 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
     if (live) {
         L = unpack_st(E.st[l]);
         uint32_t *rec = epochs + (size_t)l * kRec;
+        // all loads before any store: epochs may alias E.board as far as the compiler
+        // knows, and interleaving would serialise 16 global round trips
+        uint32_t v[16];
+#pragma unroll
+        for (int w = 0; w < 16; w++) v[w] = E.board[w * B + l];
 #pragma unroll
         for (int w = 0; w < 16; w++) {
-            const uint32_t v = E.board[w * B + l];
-            bd[w * LPW] = v;
-            rec[w] = v;
+            bd[w * LPW] = v[w];
+            rec[w] = v[w];
         }
         rec[16] = (uint32_t)L.gr | ((uint32_t)L.gc << 8);
         if (mode == AMZ_RESET_RESAMPLE) my_spec = spec_step[l];
-        build_colpairs<LPW>(bd, cb);
     }
+    __syncwarp();
+    for (int q = 0; q < nv; q++) build_move_table<LPW>(&S.board[0][0], q, &S.mt[q][0][0]);
     const bool vec = avec && nv == LPW && LPW % 4 == 0;
     fetch_actions<LPW>(S.act[0], actions, B, lane0, nv, 0, T, lane, vec);
     __syncwarp();
@@ -322,7 +381,6 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                 if (hit) load_level(spec + l, m, ar, acol, ad, gr, gc);
                 if (dn) {
                     build_board(m, G, bd, LPW);
-                    build_colpairs<LPW>(bd, cb);
                     L.hr = ar;
                     L.hc = acol;
                     L.hd = ad;
@@ -336,6 +394,15 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                     rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
                 }
             }
+            if (mode == AMZ_RESET_RESAMPLE) {
+                __syncwarp();
+                unsigned chg = fin & ((LPW >= 32) ? 0xFFFFFFFFu : ((1u << LPW) - 1u));
+                while (chg) {
+                    const int q = __ffs(chg) - 1;
+                    chg &= chg - 1;
+                    build_move_table<LPW>(&S.board[0][0], q, &S.mt[q][0][0]);
+                }
+            }
             if (dn) {
                 ps = (uint32_t)L.hr | ((uint32_t)L.hc << 4) | ((uint32_t)L.hd << 8) | (epoch << 12);
                 g = (uint32_t)L.gr | ((uint32_t)L.gc << 4);
@@ -345,34 +412,63 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
         return before | ((uint32_t)reached << 10) | ((uint32_t)dn << 11);
     };
 
+    DYN_MARK(1);
     for (int t0 = 0; t0 < T; t0 += ACH) {
         fetch_actions<LPW>(S.act[((t0 / ACH) + 1) & 1], actions, B, lane0, nv, t0 + ACH, T, lane, vec);
         cp_wait<1>();
         __syncwarp();
         const uint8_t *ac = ap + ((t0 / ACH) & 1) * ACH * LPW;
         const int tn = (T - t0) < ACH ? (T - t0) : ACH;
-        // Speculative 8-step batches: the position chain alone (heading and move offset
-        // come from the actions, a wall test is one funnel shift of the column-pair
-        // bitmap), no per-step vote.  When any lane of the warp reaches its goal or times
+        // Speculative 8-step batches: the position chain alone (the heading chain runs
+        // beside it on the actions; a move is one move-table byte load), no per-step vote.  When any lane of the warp reaches its goal or times
         // out inside a batch, the next quad runs through the exact per-step path (the
         // only inlined copy of the reset / resample code) and speculation resumes after.
+        {
+            // lane-major copy of the chunk's actions (4 steps per word) for the batches
+            const int me = lane < LPW ? lane : 0;
+            const uint32_t *row = reinterpret_cast<const uint32_t *>(&S.act[(t0 / ACH) & 1][0][0]) + (me >> 2);
+            const uint32_t sel = (uint32_t)(me & 3) | ((uint32_t)(4 + (me & 3)) << 4);
+            if (lane < LPW) {
+#pragma unroll
+                for (int q = 0; q < ACH / 4; q++) {
+                    const uint32_t lo = __byte_perm(row[(4 * q) * (LPW / 4)], row[(4 * q + 1) * (LPW / 4)], sel);
+                    const uint32_t hi = __byte_perm(row[(4 * q + 2) * (LPW / 4)], row[(4 * q + 3) * (LPW / 4)], sel);
+                    S.aw[me][q] = __byte_perm(lo, hi, 0x5410);
+                }
+            }
+            __syncwarp();
+        }
         int j = 0;
         while (j < tn) {
             if (j + 8 <= tn) {
-                uint32_t pos = ps & 0xFFu, d = (ps >> 8) & 3u;
+                // SWAR decode of the batch's 8 actions (4 per word): turn deltas, forward
+                // flags, headings by a byte prefix sum; then the position chain alone,
+                // one move-table byte load per step.
+                uint32_t pos = ps & 0xFFu;
                 const uint32_t hi = ps & 0xFFFFF000u;
-                uint32_t rec[8];
+                const uint32_t *awl = &S.aw[lane < LPW ? lane : 0][j >> 2];  // j is a multiple of 4, not 8
+                const uint2 A = make_uint2(awl[0], awl[1]);
+                uint32_t d = (ps >> 8) & 3u;
+                uint32_t ew[2], dw[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const uint32_t a = h ? A.y : A.x;
+                    const uint32_t left = __vcmpeq4(a, 0u), right = __vcmpeq4(a, 0x01010101u);
+                    const uint32_t fwd = __vcmpeq4(a, 0x02020202u);
+                    const uint32_t turn = (left & 0x03030303u) | (right & 0x01010101u);
+                    const uint32_t da = (turn * 0x01010101u + d * 0x01010101u) & 0x03030303u;  // after
+                    dw[h] = (da << 8) | d;                                                     // before
+                    ew[h] = (da & fwd) | (0x04040404u & ~fwd);
+                    d = da >> 24;
+                }
                 bool hit = time + 8 >= tep;
+                uint32_t rec[8];
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
-                    const uint32_t a = ac[(j + k) * LPW];
-                    const uint32_t ua = a < 3u ? a : 3u;
-                    rec[k] = pos | (d << 8) | hi;
-                    d = (d + ((0x13u >> (4u * ua)) & 0xFu)) & 3u;
-                    const uint32_t mv = ua == 2u ? ((0x01122110u >> (8u * d)) & 0xFFu) - 17u : 0u;
-                    const uint32_t np = pos + mv;
-                    const uint32_t w = cb[(np >> 5) * LPW];
-                    pos = (__funnelshift_r(w, w, np) & 1u) ? pos : np;
+                    const uint32_t e = (ew[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+                    const uint32_t db = (dw[k >> 2] >> (8 * (k & 3))) & 0x3u;
+                    rec[k] = pos | (db << 8) | hi;
+                    pos = mtl[e * 256u + pos];
                     hit |= pos == g;
                 }
                 if (!__any_sync(0xFFFFFFFFu, hit)) {
@@ -400,6 +496,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             j += 4;
         }
     }
+    DYN_MARK(2);
     L.s.r = (int)(ps & 15u);
     L.s.c = (int)((ps >> 4) & 15u);
     L.s.d = (int)((ps >> 8) & 3u);
@@ -414,7 +511,14 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             for (int w = 0; w < 16; w++) E.board[w * B + l] = bd[w * LPW];
         }
     }
+    DYN_MARK(3);
 }
+
+#ifdef AMZ_DYN_PROF
+extern "C" int amz_debug_dyn_prof(void *out) {
+    return (int)cudaMemcpyFromSymbol(out, g_dyn_prof, sizeof(g_dyn_prof));
+}
+#endif
 
 // Speculative timeout levels: a lane that never reaches the goal times out at the step
 // where its time hits max_episode_steps; that level's key is known now, so it is
@@ -536,13 +640,10 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
                        uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s) {
     if (E.B <= 0) return 0;
     // few lanes per warp: the per-lane chain is latency-bound, and a warp stalls for
-    // every resample of any of its lanes, so small warps finish sooner
+    // every resample of any of its lanes, so small warps finish sooner.  AMZ_DYN_LPW
+    // (4, 8, 16) overrides the choice for tuning runs (tools/dyn_lpw.sh).
     static const int forced = getenv("AMZ_DYN_LPW") ? atoi(getenv("AMZ_DYN_LPW")) : 0;
-    if (forced == 1)
-        launch_dyn<1, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
-    else if (forced == 2)
-        launch_dyn<2, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
-    else if (forced == 8)
+    if (forced == 8)
         launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
     else if (forced == 16)
         launch_dyn<16, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
