@@ -12,7 +12,8 @@ import os
 from .errors import ConfigError, ContractViolation, LevelError, RunnerFault, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libamaze_b200.so")
+# AMZ_LIB_PATH: a differently-built copy of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("AMZ_LIB_PATH") or os.path.join(_HERE, "libamaze_b200.so")
 
 AMZ_RESET_NONE, AMZ_RESET_RESAMPLE, AMZ_RESET_HOME = 0, 1, 2
 AMZ_SCORE_MAXMC, AMZ_SCORE_PVL = 0, 1

@@ -217,7 +217,7 @@ constexpr int kRec = 20;  // u32 words per epoch record: board[16], goal, pad
 // phase 1: dynamics
 // ---------------------------------------------------------------------------------
 #ifdef AMZ_DYN_PROF
-__device__ unsigned long long g_dyn_prof[65536][4];
+__device__ unsigned long long g_dyn_prof[65536][8];
 __device__ __forceinline__ unsigned smid_() {
     unsigned r;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -228,7 +228,19 @@ __device__ __forceinline__ unsigned smid_() {
         const int64_t wi_ = (int64_t)blockIdx.x * WPC + (threadIdx.x >> 5);                  \
         if ((threadIdx.x & 31) == 0 && wi_ < 65536) g_dyn_prof[wi_][k_] = clock64() | ((unsigned long long)smid_() << 56); \
     } while (0)
+#define DYN_T0(v_) const long long v_ = clock64()
+#define DYN_ACC(k_, v_)                                                                                        \
+    do {                                                                                                        \
+        const int64_t wi_ = (int64_t)blockIdx.x * WPC + (threadIdx.x >> 5);                                     \
+        if ((threadIdx.x & 31) == 0 && wi_ < 65536) g_dyn_prof[wi_][k_] += (unsigned long long)(clock64() - v_); \
+    } while (0)
 #else
+#define DYN_T0(v_) \
+    do {           \
+    } while (0)
+#define DYN_ACC(k_, v_) \
+    do {                \
+    } while (0)
 #define DYN_MARK(k_) \
     do {             \
     } while (0)
@@ -363,6 +375,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
         if (reached) reward[(int64_t)t * B + l] = use_lut ? s_rew[time] : goal_reward(time, G.tep);
         const unsigned fin = __ballot_sync(0xFFFFFFFFu, dn);
         if (fin) {
+            DYN_T0(c_evt);
             if (mode == AMZ_RESET_RESAMPLE) {
                 const uint32_t gstep = step0 + (uint32_t)t;
                 const bool hit = dn && my_spec == gstep;
@@ -376,7 +389,12 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                         seed_absorb(sd, E.lane_offset + (uint32_t)l);
                         seed_key(sd, k0, k1);
                     }
+                    DYN_T0(c_smp);
                     warp_sample_each(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
+                    DYN_ACC(5, c_smp);
+#ifdef AMZ_DYN_PROF
+                    if (lane == 0) g_dyn_prof[(int64_t)blockIdx.x * WPC + warp][7] += __popc(need);
+#endif
                 }
                 if (hit) load_level(spec + l, m, ar, acol, ad, gr, gc);
                 if (dn) {
@@ -396,18 +414,21 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             }
             if (mode == AMZ_RESET_RESAMPLE) {
                 __syncwarp();
+                DYN_T0(c_tbl);
                 unsigned chg = fin & ((LPW >= 32) ? 0xFFFFFFFFu : ((1u << LPW) - 1u));
                 while (chg) {
                     const int q = __ffs(chg) - 1;
                     chg &= chg - 1;
                     build_move_table<LPW>(&S.board[0][0], q, &S.mt[q][0][0]);
                 }
+                DYN_ACC(6, c_tbl);
             }
             if (dn) {
                 ps = (uint32_t)L.hr | ((uint32_t)L.hc << 4) | ((uint32_t)L.hd << 8) | (epoch << 12);
                 g = (uint32_t)L.gr | ((uint32_t)L.gc << 4);
                 time = 0;
             }
+            DYN_ACC(4, c_evt);
         }
         return before | ((uint32_t)reached << 10) | ((uint32_t)dn << 11);
     };
@@ -517,6 +538,9 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
 #ifdef AMZ_DYN_PROF
 extern "C" int amz_debug_dyn_prof(void *out) {
     return (int)cudaMemcpyFromSymbol(out, g_dyn_prof, sizeof(g_dyn_prof));
+}
+extern "C" int amz_debug_dyn_prof_reset(const void *zero) {
+    return (int)cudaMemcpyToSymbol(g_dyn_prof, zero, sizeof(g_dyn_prof));
 }
 #endif
 

@@ -17,11 +17,13 @@ p = amz.StaticParams()
 for mode in (amz.HOME, amz.RESAMPLE):
     env = amz.AutoResetWrapper(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B)), mode)
     acts = torch.randint(0, 3, (T, B), dtype=torch.uint8, device="cuda")
-    for i in range(3):
-        res = env.reset(amz.RngStream.from_seed(i), p)
-        tr, cur = amz.rollout_actions(env, res, acts, p)
+    res = env.reset(amz.RngStream.from_seed(1), p)
     torch.cuda.synchronize()
-    buf = np.zeros((65536, 4), dtype=np.uint64)
+    zero = np.zeros((65536, 8), dtype=np.uint64)
+    _l.lib().amz_debug_dyn_prof_reset(ctypes.c_void_p(zero.ctypes.data))
+    tr, cur = amz.rollout_actions(env, res, acts, p)
+    torch.cuda.synchronize()
+    buf = np.zeros((65536, 8), dtype=np.uint64)
     _l.lib().amz_debug_dyn_prof(ctypes.c_void_p(buf.ctypes.data))
     nw = B // 4
     b = buf[:nw]
@@ -36,3 +38,8 @@ for mode in (amz.HOME, amz.RESAMPLE):
     print(mode, "warps", nw, "prologue cyc med/max", int(np.median(pro)), int(pro.max()),
           "loop med/max", int(np.median(loop)), int(loop.max()), "epi med/max", int(np.median(epi)), int(epi.max()),
           "SM span med/max", int(np.median(spans)), int(max(spans)))
+    ev, smp, tbl, q = [b[:, k].astype(np.int64) for k in (4, 5, 6, 7)]
+    w = int(np.argmax(loop))
+    print("   event cyc med/max", int(np.median(ev)), int(ev.max()), "sampler med/max", int(np.median(smp)), int(smp.max()),
+          "table med/max", int(np.median(tbl)), int(tbl.max()), "sampled levels med/max/sum", int(np.median(q)), int(q.max()), int(q.sum()))
+    print("   slowest warp: loop", int(loop[w]), "events", int(ev[w]), "sampler", int(smp[w]), "table", int(tbl[w]), "quads", int(q[w]))
