@@ -204,7 +204,8 @@ class Workload:
                     "final_view": torch.empty((B, v, v), dtype=torch.uint8, device=device),
                     "final_dir": torch.empty((B,), dtype=torch.uint8, device=device)}
         self.root = amz.RngStream.from_seed(seed)
-        self.launches_per_step = 4  # sample_levels, env_reset, env_rollout, gae_score
+        # our kernels per step: k_sample_levels_w, k_env_reset, k_spec_levels, k_dyn, k_render, k_gae_score3
+        self.launches_per_step = 6
         self.ev_roll = None
 
     def step(self, it, actions=None, values=None, last=None, timing=None):
