@@ -39,6 +39,15 @@ ENV_BYTES_PER_STEP = 36  # action u8 + view 25 u8 + dir u8 + reward f64 + done u
 GAE_BYTES_PER_ELEM = 33  # r f64 + V f64 + done u8 in, A f64 + R f64 out
 
 
+def _traffic():
+    """Per-launch DRAM bytes of the roofline kernels from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1c_traffic.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -339,9 +348,15 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": T * B * (1 + 8) + B * 8, "d2h_bytes_per_step": 2 * B * 8},
         "gpu_launches": wl.launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": roll_gbs / peak, "traffic": None, "peak_source": src,
+                     "frac": roll_gbs / peak,
+                     "traffic": _traffic().get("k_env_rollout", {}).get("dram_bytes"),
+                     "traffic_source": "profiles/r1c_traffic.json (ncu --set full, per launch)",
+                     "peak_source": src,
                      "algorithmic_bytes": f"{ENV_BYTES_PER_STEP} B/env-step x {B * T} env-steps per launch",
-                     "kernel_ms": roll},
+                     "kernel_ms": roll,
+                     "note": "k_env_rollout = k_spec_levels + k_dyn + k_render; at 4096 lanes the per-lane "
+                             "256-step dynamics chain (latency) bounds it, not HBM; the HBM point is "
+                             "large_batch (65536 lanes)"},
         "kernels": {"k_env_rollout_ms": roll, "k_gae_score_ms": gae, "k_gae_score_GBs": gae_gbs,
                     "k_gae_score_frac": gae_gbs / peak,
                     "levels_scored_per_s": B * world / (gae * 1e-3)},
