@@ -317,6 +317,7 @@ def run_ours(args, rank, world, local_rank):
         extra["accel"] = measure_plr(dev, 2048, T, True, max(3, min(args.steps, 10)), flush, world)
         if world == 1:
             extra["large_batch"] = measure_large_batch(dev, 65536, T, 3, flush, peak)
+            extra["level_metrics"] = measure_level_metrics(dev, 65536, 5, flush)
     clocks.stop()
     csum = clocks.summary()
 
@@ -444,6 +445,21 @@ def measure_large_batch(dev, B, T, iters, flush, peak):
     del wl
     torch.cuda.empty_cache()
     return out
+
+
+def measure_level_metrics(dev, n, iters, flush):
+    """Curriculum metrics: BFS shortest path + wall stats per level."""
+    import torch
+
+    import paper_2311_12716_b200 as amz
+
+    P = amz.StaticParams()
+    lv = amz.sample_levels(amz.RngStream.from_seed(5), n, P, device=dev)
+    amz.level_metrics(lv, P)
+    torch.cuda.synchronize()
+    ms = _timed(lambda i: amz.level_metrics(lv, P), iters, flush, torch)
+    t = statistics.mean(ms)
+    return {"levels": n, "ms": t, "levels_per_s": n / (t * 1e-3)}
 
 
 def measure_cpu_baseline(args, steps=1):

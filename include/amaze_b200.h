@@ -116,6 +116,13 @@ int amz_mutate_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t 
                       amz_level_t *out_dev, void *stream);
 
 /* Validate levels on device; *bad_index_host = first invalid index or -1 (synchronous). */
+/* Curriculum metrics of n levels (amaze/metrics.py:21-31 env_metrics, BFS of
+ * amaze/pathfinding.py:116-135): interior wall count, agent->goal shortest path length
+ * (0 if unsolvable), solvable flag, passable ratio (float64, bit-exact).  Any output
+ * pointer may be NULL.  Async on `stream`. */
+int amz_level_metrics(const amz_params_t *p, const amz_level_t *levels, int64_t n, int32_t *n_walls,
+                      int32_t *shortest_path, uint8_t *solvable, double *passable, void *stream);
+
 int amz_check_levels(const amz_params_t *p, const amz_level_t *levels_dev, int64_t n,
                      int64_t *bad_index_host, void *stream);
 

@@ -7,7 +7,8 @@ policy.  See DESIGN.md.
 
 __version__ = "0.1.0"
 
-from .amaze import MazeEnv, check_levels, mutate_level, mutate_levels, sample_levels, sample_random_level
+from .amaze import (EnvMetrics, MazeEnv, check_levels, env_metrics, level_metrics, mutate_level, mutate_levels,
+                    sample_levels, sample_random_level)
 from .batch import HOME, RESAMPLE, AutoResetWrapper, VectorBatchEnv, batch_lift
 from .core import BatchShape, StaticParams, StepResult
 from .errors import (AutocurriculaError, ConfigError, ContractViolation, LevelError, LevelParseError, RunnerFault,

@@ -45,6 +45,7 @@ _SIGS = {
     "amz_sample_levels": ([ctypes.POINTER(AmzParams), ctypes.POINTER(AmzSeed), U32, P, I64, P, VP], I32),
     "amz_mutate_levels": ([ctypes.POINTER(AmzParams), ctypes.POINTER(AmzSeed), U32, I64, P, P, I32, P, VP], I32),
     "amz_check_levels": ([ctypes.POINTER(AmzParams), P, I64, ctypes.POINTER(ctypes.c_int64), VP], I32),
+    "amz_level_metrics": ([ctypes.POINTER(AmzParams), P, I64, P, P, P, P, VP], I32),
     "amz_env_create": ([ctypes.POINTER(AmzParams), I64, ctypes.POINTER(ctypes.c_void_p)], I32),
     "amz_env_destroy": ([P], I32),
     "amz_env_lanes": ([P], I64),

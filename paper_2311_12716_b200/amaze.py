@@ -11,6 +11,7 @@ to the reference's.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -85,6 +86,48 @@ def check_levels(levels, params: StaticParams) -> None:
               ctypes.byref(bad), _lib.stream_handle(levels.device))
     if bad.value >= 0:
         raise LevelError(f"level {bad.value} violates the MazeLevel invariants")
+
+
+@dataclass(frozen=True)
+class EnvMetrics:
+    """amaze/metrics.py:13-18."""
+
+    n_walls: int  # interior walls only
+    shortest_path_length: int  # agent -> goal, 0 if unsolvable
+    solvable: bool
+    passable_ratio: float  # fraction of interior cells that are non-wall
+
+
+def level_metrics(levels, params: StaticParams) -> dict:
+    """Batched env_metrics (amaze/metrics.py:21-31) of packed device levels (int32 [N, 8]
+    tensor, or anything ``to_device_levels`` accepts): dict of CUDA tensors
+    ``n_walls`` int32, ``shortest_path_length`` int32, ``solvable`` bool,
+    ``passable_ratio`` float64, each [N]."""
+    torch = _torch()
+    p = as_params(params).validate()
+    lv = to_device_levels(levels, p)
+    n = lv.shape[0]
+    dev = lv.device
+    out = {"n_walls": torch.empty(n, dtype=torch.int32, device=dev),
+           "shortest_path_length": torch.empty(n, dtype=torch.int32, device=dev),
+           "solvable": torch.empty(n, dtype=torch.bool, device=dev),
+           "passable_ratio": torch.empty(n, dtype=torch.float64, device=dev)}
+    _lib.call("amz_level_metrics", ctypes.byref(p.c_struct()), _lib.ptr(lv), n, _lib.ptr(out["n_walls"]),
+              _lib.ptr(out["shortest_path_length"]), _lib.ptr(out["solvable"]), _lib.ptr(out["passable_ratio"]),
+              _lib.stream_handle(dev))
+    return out
+
+
+def env_metrics(level, params: StaticParams | None = None) -> EnvMetrics:
+    """amaze/metrics.py:21 for one level (ours or the reference's MazeLevel); the grid
+    shape comes from the level when ``params`` is omitted."""
+    ml = MazeLevel.from_any(level)
+    if params is None:
+        h, w = np.asarray(ml.walls).shape
+        params = StaticParams(height=int(h), width=int(w), wall_budget=min(60, (int(h) - 2) * (int(w) - 2) - 2))
+    m = level_metrics([ml], params)
+    return EnvMetrics(int(m["n_walls"][0]), int(m["shortest_path_length"][0]), bool(m["solvable"][0]),
+                      float(m["passable_ratio"][0]))
 
 
 def to_device_levels(levels, params: StaticParams, device=None):

@@ -146,6 +146,17 @@ int amz_check_levels(const amz_params_t *p, const amz_level_t *lv, int64_t n, in
     return 0;
 }
 
+int amz_level_metrics(const amz_params_t *p, const amz_level_t *lv, int64_t n, int32_t *n_walls, int32_t *spl,
+                      uint8_t *solvable, double *passable, void *stream) {
+    int rc = amz_validate_params(p);
+    if (rc) return rc;
+    if (n < 0) return fail(AMZ_ESHAPE, "n must be >= 0, got %lld", (long long)n);
+    if (n > 0 && !lv) return fail(AMZ_ECONFIG, "null argument");
+    launch_level_metrics(make_geo(*p), lv, n, n_walls, spl, solvable, passable, (cudaStream_t)stream);
+    AMZ_CHECK_CUDA(cudaGetLastError(), "level_metrics launch");
+    return 0;
+}
+
 int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
     int rc = amz_validate_params(p);
     if (rc) return rc;

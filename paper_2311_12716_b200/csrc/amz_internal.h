@@ -33,6 +33,8 @@ int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0,
                          amz_level_t *out, cudaStream_t s);
 int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
                          const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s);
+int launch_level_metrics(const Geo &G, const amz_level_t *lv, int64_t n, int32_t *n_walls, int32_t *spl,
+                         uint8_t *solvable, double *passable, cudaStream_t s);
 int launch_check_levels(const Geo &G, const amz_level_t *lv, int64_t n, unsigned long long *first_bad,
                         cudaStream_t s);
 int launch_env_reset(const Geo &G, const EnvDev &E, const amz_level_t *lv, const int64_t *lanes, int64_t n,

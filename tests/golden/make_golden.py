@@ -196,7 +196,37 @@ def gen_states(R):
     return out
 
 
+def gen_metrics(R):
+    """env_metrics (amaze/metrics.py:21-31: BFS agent -> goal, amaze/pathfinding.py:116-135)."""
+    out = {}
+    cases = [  # (name, H, W, budget, seed, n)
+        ("default", 13, 13, 60, 21, 400),
+        ("dense", 13, 13, 119, 22, 300),
+        ("small9", 9, 9, 30, 23, 200),
+        ("wide", 11, 15, 70, 24, 200),
+    ]
+    sets = []
+    for name, H, W, budget, seed, n in cases:
+        P = R.env.StaticParams(height=H, width=W, wall_budget=budget)
+        root = R.rng.RngStream.from_seed(seed)
+        sets.append((name, H, W, [R.amaze.sample_random_level(k, P) for k in root.fold_in(0).split(n)]))
+    sets.append(("assets", 13, 13, [R.amaze.load_asset(nm) for nm in R.amaze.asset_names()]))
+    from autocurricula.amaze.metrics import env_metrics
+    for name, H, W, levels in sets:
+        ms = [env_metrics(lv) for lv in levels]
+        out[f"m_{name}_levels"] = pack(levels, H, W)
+        out[f"m_{name}_meta"] = np.array([H, W], dtype=np.int64)
+        out[f"m_{name}_nwalls"] = np.array([m.n_walls for m in ms], dtype=np.int64)
+        out[f"m_{name}_spl"] = np.array([m.shortest_path_length for m in ms], dtype=np.int64)
+        out[f"m_{name}_solvable"] = np.array([m.solvable for m in ms], dtype=bool)
+        out[f"m_{name}_passable"] = np.array([m.passable_ratio for m in ms], dtype=np.float64)
+    return out
+
+
 def main():
+    if "--only-metrics" in sys.argv:
+        np.savez_compressed(os.path.join(OUT, "metrics.npz"), **gen_metrics(_import_reference()))
+        return
     R = _import_reference()
     fx = {}
     fx.update(gen_levels(R))
@@ -213,6 +243,7 @@ def main():
     misc.update(gen_assets(R))
     misc.update(gen_states(R))
     np.savez_compressed(os.path.join(OUT, "views.npz"), **misc)
+    np.savez_compressed(os.path.join(OUT, "metrics.npz"), **gen_metrics(R))
     for f in ("levels", "rollouts", "scores", "views"):
         print(f, os.path.getsize(os.path.join(OUT, f + ".npz")))
 

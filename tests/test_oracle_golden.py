@@ -84,3 +84,17 @@ def test_known_answers(golden):
     assert z["ka_maxmc"][0] == pytest.approx(0.8)
     adv, _ = onp.gae(np.ones((3, 1)), np.zeros((3, 1)), np.zeros((3, 1)), np.zeros(1), 1.0, 1.0)
     assert adv[:, 0].tolist() == [3.0, 2.0, 1.0]
+
+
+@pytest.mark.parametrize("name", ["default", "dense", "small9", "wide", "assets"])
+def test_env_metrics_match_reference(golden, name):
+    """oracle env_metrics == the reference's amaze/metrics.py:21 on fixtures it produced."""
+    z = golden("metrics")
+    H, W = (int(x) for x in z[f"m_{name}_meta"])
+    p = onp.Params(height=H, width=W)
+    levels = _levels_from_rows(z[f"m_{name}_levels"], p)
+    got = np.array([onp.env_metrics(lv) for lv in levels], dtype=object)
+    assert np.array_equal(got[:, 0].astype(np.int64), z[f"m_{name}_nwalls"])
+    assert np.array_equal(got[:, 1].astype(np.int64), z[f"m_{name}_spl"])
+    assert np.array_equal(got[:, 2].astype(bool), z[f"m_{name}_solvable"])
+    assert np.array_equal(got[:, 3].astype(np.float64), z[f"m_{name}_passable"])
