@@ -116,6 +116,17 @@ int amz_mutate_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t 
                       amz_level_t *out_dev, void *stream);
 
 /* Validate levels on device; *bad_index_host = first invalid index or -1 (synchronous). */
+/* Policy hand-off (agents/rollout.py:145-152 sample_actions + agents/ppo.py:82-96,136-138):
+ * logits [B][A] (dtype 0 = f32, 1 = f64; A <= 16) -> action (int64 and/or u8, any NULL)
+ * and its log-softmax probability (f64, may be NULL).  Sampling uses u = the (lane0+i)-th
+ * double of the generator `key` (numpy Generator.random order); greedy = argmax.  With
+ * step_dev == NULL, `key` is the SeedSequence state after the generator's whole key
+ * (e.g. RngStream.fold_in(t)); otherwise `key` is the prefix and the device absorbs the
+ * u32 *step_dev first (CUDA-graph replay with a device step counter). */
+int amz_policy_head(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *key,
+                    const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *actions, uint8_t *actions_u8,
+                    double *log_probs, void *stream);
+
 /* Curriculum metrics of n levels (amaze/metrics.py:21-31 env_metrics, BFS of
  * amaze/pathfinding.py:116-135): interior wall count, agent->goal shortest path length
  * (0 if unsolvable), solvable flag, passable ratio (float64, bit-exact).  Any output

@@ -189,7 +189,11 @@ class VectorBatchEnv:
                   _lib.ptr(dirs), lanes.stream())
         return self._zeros_result({"view": view, "dir": dirs}, lanes)
 
-    def _step(self, state, actions, params, mode: int, wrap: RngStream | None, step_idx: int) -> StepResult:
+    def _step(self, state, actions, params, mode: int, wrap: RngStream | None, step_idx: int,
+              out: dict | None = None) -> StepResult:
+        """``out`` may hold flat-lane destination tensors (``view`` u8 [n,V,V], ``dir``
+        int64 [n], ``reward`` f64 [n], ``done`` bool [n]), e.g. slices of a trajectory
+        store, which the step kernel then writes directly."""
         torch = _torch()
         p = as_params(params)
         lanes = state if isinstance(state, DeviceLanes) else self.lanes
@@ -197,10 +201,15 @@ class VectorBatchEnv:
             raise ContractViolation("step before reset")
         a, code = self._flat_actions(actions)
         n, v = self.n_lanes, p.agent_view_size
-        view = torch.empty((n, v, v), dtype=torch.uint8, device=self.device)
-        dirs = torch.empty((n,), dtype=torch.int64, device=self.device)
-        rew = torch.empty((n,), dtype=torch.float64, device=self.device)
-        done = torch.empty((n,), dtype=torch.bool, device=self.device)
+        o = out or {}
+        view = o["view"] if "view" in o else torch.empty((n, v, v), dtype=torch.uint8, device=self.device)
+        dirs = o["dir"] if "dir" in o else torch.empty((n,), dtype=torch.int64, device=self.device)
+        rew = o["reward"] if "reward" in o else torch.empty((n,), dtype=torch.float64, device=self.device)
+        done = o["done"] if "done" in o else torch.empty((n,), dtype=torch.bool, device=self.device)
+        for name, x, dt in (("view", view, torch.uint8), ("dir", dirs, torch.int64), ("reward", rew, torch.float64),
+                            ("done", done, torch.bool)):
+            if x.dtype != dt or not x.is_contiguous() or x.numel() != (n * v * v if name == "view" else n):
+                raise ShapeError(f"step output {name!r} must be a contiguous {dt} tensor of the lane count")
         solved = torch.empty((n,), dtype=torch.float64, device=self.device)
         times = torch.empty((n,), dtype=torch.int64, device=self.device)
         seed = wrap.seed_prefix() if wrap is not None else None
@@ -274,10 +283,10 @@ class AutoResetWrapper:
         result.extras[self.EXTRAS_KEY] = {"rng": rng_wrap, "step": 0, "home": home}
         return result
 
-    def step(self, rng, state, actions, params, extras: dict) -> StepResult:
+    def step(self, rng, state, actions, params, extras: dict, out: dict | None = None) -> StepResult:
         wrap = extras[self.EXTRAS_KEY]
         res = self.benv._step(state, actions, params, _MODES[self.mode],
-                              wrap["rng"] if self.mode == RESAMPLE else None, int(wrap["step"]))
+                              wrap["rng"] if self.mode == RESAMPLE else None, int(wrap["step"]), out=out)
         res.extras = dict(extras)
         res.extras[self.EXTRAS_KEY] = {**wrap, "step": wrap["step"] + 1}
         return res

@@ -146,6 +146,24 @@ int amz_check_levels(const amz_params_t *p, const amz_level_t *lv, int64_t n, in
     return 0;
 }
 
+int amz_policy_head(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *key, const uint32_t *step_dev,
+                    int greedy, int64_t lane0, int64_t *actions, uint8_t *actions_u8, double *log_probs,
+                    void *stream) {
+    if (B < 0) return fail(AMZ_ESHAPE, "lanes must be >= 0, got %lld", (long long)B);
+    if (A < 1 || A > 16) return fail(AMZ_ESHAPE, "action count must be in [1, 16], got %d", A);
+    if (dtype != 0 && dtype != 1) return fail(AMZ_ECONFIG, "logits dtype code must be 0 (f32) or 1 (f64)");
+    if (B > 0 && !logits) return fail(AMZ_ECONFIG, "null argument");
+    if (!greedy && !key) return fail(AMZ_ECONFIG, "sampling needs a generator key");
+    amz_seed_t pre = key ? *key : amz_seed_t{};
+    uint64_t k0 = 0, k1 = 0;
+    if (key && !step_dev) seed_key(pre, k0, k1);
+    int rc = launch_policy_head(logits, dtype, B, A, k0, k1, pre, step_dev, greedy, lane0, actions, actions_u8,
+                                log_probs, (cudaStream_t)stream);
+    if (rc) return fail(rc, "policy_head: bad shape");
+    AMZ_CHECK_CUDA(cudaGetLastError(), "policy_head launch");
+    return 0;
+}
+
 int amz_level_metrics(const amz_params_t *p, const amz_level_t *lv, int64_t n, int32_t *n_walls, int32_t *spl,
                       uint8_t *solvable, double *passable, void *stream) {
     int rc = amz_validate_params(p);

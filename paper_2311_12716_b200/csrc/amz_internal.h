@@ -33,6 +33,9 @@ int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0,
                          amz_level_t *out, cudaStream_t s);
 int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
                          const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s);
+int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
+                       const amz_seed_t &prefix, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
+                       uint8_t *act8, double *logp, cudaStream_t s);
 int launch_level_metrics(const Geo &G, const amz_level_t *lv, int64_t n, int32_t *n_walls, int32_t *spl,
                          uint8_t *solvable, double *passable, cudaStream_t s);
 int launch_check_levels(const Geo &G, const amz_level_t *lv, int64_t n, unsigned long long *first_bad,

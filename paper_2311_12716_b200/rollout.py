@@ -31,12 +31,13 @@ def _torch():
 class TrajectoryBatch:
     """Time-major rollout storage on the GPU ([T, B, ...] over flat lanes)."""
 
-    obs: dict          # view uint8 [T, B, V, V], dir uint8 [T, B]
-    actions: object    # uint8 [T, B]
+    obs: dict          # view uint8 [T, B, V, V], dir uint8 [T, B] (int64 from the policy rollout)
+    actions: object    # uint8 [T, B] (int64 from the policy rollout)
     rewards: object    # float64 [T, B]
     dones: object      # bool [T, B]
     values: object = None
     log_probs: object = None
+    pre_hidden: object = None  # [T, B, H]: carry fed to the policy at step t
 
     @property
     def length(self) -> int:
@@ -52,6 +53,7 @@ class RolloutCursor:
     obs: dict
     state: object
     extras: dict
+    hidden: object = None
 
 
 def random_actions(rng, T: int, B: int, device=None):

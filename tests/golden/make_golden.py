@@ -223,7 +223,77 @@ def gen_metrics(R):
     return out
 
 
+class _ExactActor:
+    """A policy whose arithmetic is exact in any evaluation order (small integer sums
+    times powers of two), so a torch copy on the GPU reproduces it bit for bit; the
+    action hand-off is the reference's own sample_actions / log_softmax_np."""
+
+    def __init__(self, R):
+        self.R = R
+
+    def initial_hidden(self, n):
+        return np.zeros((n, 2))
+
+    def logits(self, obs):
+        view = obs["view"].astype(np.int64).reshape(obs["dir"].shape[0], -1)
+        d = obs["dir"].astype(np.int64)
+        idx = np.arange(view.shape[1])
+        cols = [(((view + 1) * (a + 2 + idx % 3)) % 5).sum(axis=1) * 0.25 - 0.5 * ((d + a) % 4) for a in range(3)]
+        return np.stack(cols, axis=1).astype(np.float64)
+
+    def act(self, obs, hidden, g=None, greedy=False):
+        import importlib
+
+        ppo = importlib.import_module("autocurricula.agents.ppo")
+        logits = self.logits(obs)
+        B = logits.shape[0]
+        actions = logits.argmax(axis=-1).astype(np.int64) if greedy else self.R.rollout.sample_actions(logits, g)
+        logp = ppo.log_softmax_np(logits)[np.arange(B), actions]
+        view = obs["view"].astype(np.int64).reshape(B, -1)
+        d = obs["dir"].astype(np.int64)
+        values = 0.125 * (view.sum(axis=1) % 11) + 0.5 * d
+        hidden = hidden + np.stack([np.ones(B), d.astype(np.float64)], axis=1)
+        return actions, logp, values, hidden
+
+
+def gen_policy(R):
+    """agents/rollout.py:145-152 sample_actions, agents/ppo.py:136 log_softmax_np, and a
+    full agents/rollout.py:87 rollout() with an exact actor (RESAMPLE, 64 lanes x 40)."""
+    import importlib
+
+    ppo = importlib.import_module("autocurricula.agents.ppo")
+    rng = np.random.default_rng(7)
+    out = {}
+    for tag, A, scale, f32 in (("a3f32", 3, 2.0, True), ("a3", 3, 1.0, False), ("a5", 5, 3.0, False),
+                               ("a8", 8, 2.0, False), ("a11", 11, 4.0, False), ("wide", 3, 300.0, False)):
+        T, B = 4, 400
+        lg = rng.normal(0, scale, (T, B, A))
+        if f32:
+            lg = lg.astype(np.float32).astype(np.float64)
+        lg[:, :10] = np.round(lg[:, :10])  # ties
+        acts = np.stack([R.rollout.sample_actions(lg[t], R.rng.RngStream.from_seed(31).fold_in(t).generator())
+                         for t in range(T)])
+        out[f"pa_{tag}_logits"] = lg
+        out[f"pa_{tag}_actions"] = acts
+        out[f"pa_{tag}_logp"] = np.stack([ppo.log_softmax_np(lg[t]) for t in range(T)])
+    P = R.env.StaticParams()
+    for tag, greedy in (("pr", False), ("prg", True)):
+        benv = R.env.VectorBatchEnv(R.amaze.MazeEnv(), R.env.BatchShape(1, 1, 64))
+        wrap = R.env.AutoResetWrapper(benv, R.env.RESAMPLE)
+        start = wrap.reset(R.rng.RngStream.from_seed(9), P)
+        traj, cur = R.rollout.rollout(R.rng.RngStream.from_seed(5), _ExactActor(R), wrap, start, 40, P, greedy=greedy)
+        out.update({f"{tag}_view": traj.obs["view"], f"{tag}_dir": traj.obs["dir"], f"{tag}_actions": traj.actions,
+                    f"{tag}_log_probs": traj.log_probs, f"{tag}_values": traj.values, f"{tag}_rewards": traj.rewards,
+                    f"{tag}_dones": traj.dones, f"{tag}_pre_hidden": traj.pre_hidden,
+                    f"{tag}_cur_view": cur.obs["view"], f"{tag}_cur_dir": cur.obs["dir"],
+                    f"{tag}_cur_hidden": cur.hidden})
+    return out
+
+
 def main():
+    if "--only-policy" in sys.argv:
+        np.savez_compressed(os.path.join(OUT, "policy.npz"), **gen_policy(_import_reference()))
+        return
     if "--only-metrics" in sys.argv:
         np.savez_compressed(os.path.join(OUT, "metrics.npz"), **gen_metrics(_import_reference()))
         return
@@ -244,6 +314,7 @@ def main():
     misc.update(gen_states(R))
     np.savez_compressed(os.path.join(OUT, "views.npz"), **misc)
     np.savez_compressed(os.path.join(OUT, "metrics.npz"), **gen_metrics(R))
+    np.savez_compressed(os.path.join(OUT, "policy.npz"), **gen_policy(R))
     for f in ("levels", "rollouts", "scores", "views"):
         print(f, os.path.getsize(os.path.join(OUT, f + ".npz")))
 

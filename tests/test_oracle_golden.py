@@ -98,3 +98,13 @@ def test_env_metrics_match_reference(golden, name):
     assert np.array_equal(got[:, 1].astype(np.int64), z[f"m_{name}_spl"])
     assert np.array_equal(got[:, 2].astype(bool), z[f"m_{name}_solvable"])
     assert np.array_equal(got[:, 3].astype(np.float64), z[f"m_{name}_passable"])
+
+
+@pytest.mark.parametrize("tag", ["a3f32", "a3", "a5", "a8", "a11", "wide"])
+def test_sample_actions_oracle_matches_reference(golden, tag):
+    z = golden("policy")
+    lg = z[f"pa_{tag}_logits"]
+    for t in range(lg.shape[0]):
+        g = onp.generator(31, (t,))
+        assert np.array_equal(onp.sample_actions(lg[t], g), z[f"pa_{tag}_actions"][t])
+        assert np.array_equal(onp.log_softmax(lg[t]), z[f"pa_{tag}_logp"][t])
