@@ -318,6 +318,7 @@ def run_ours(args, rank, world, local_rank):
         if world == 1:
             extra["large_batch"] = measure_large_batch(dev, 65536, T, 3, flush, peak)
             extra["level_metrics"] = measure_level_metrics(dev, 65536, 5, flush)
+            extra["policy_rollout"] = measure_policy_rollout(dev, 4096, 64)
     clocks.stop()
     csum = clocks.summary()
 
@@ -460,6 +461,39 @@ def measure_level_metrics(dev, n, iters, flush):
     ms = _timed(lambda i: amz.level_metrics(lv, P), iters, flush, torch)
     t = statistics.mean(ms)
     return {"levels": n, "ms": t, "levels_per_s": n / (t * 1e-3)}
+
+
+def measure_policy_rollout(dev, B, T):
+    """rollout() with a torch student net of the reference's architecture
+    in the loop (fused policy head + device step), eager vs one CUDA-graph replay per step."""
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from policy_rollout_bench import StudentNet
+
+    import paper_2311_12716_b200 as amz
+
+    torch.manual_seed(0)
+    actor = amz.TorchPolicyActor(StudentNet().to(dev).eval())
+    P = amz.StaticParams()
+    out = {"lanes": B, "T": T, "policy": "tile/dir embed -> Linear 128 -> GRUCell 256 -> heads, fp32, random init"}
+    for name in ("eager", "graph"):
+        env = amz.AutoResetWrapper(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B), device=dev), amz.RESAMPLE)
+        start = env.reset(amz.RngStream.from_seed(1), P)
+        gr = amz.GraphRollout(actor, env, T) if name == "graph" else None
+        run = (lambda r, s: gr(r, s, copy=False)) if gr else (lambda r, s: amz.rollout(r, actor, env, s, T, P))
+        _, cur = run(amz.RngStream.from_seed(2), start)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for i in range(2):
+            _, cur = run(amz.RngStream.from_seed(3 + i), cur)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 2
+        out[f"{name}_ms"] = ms
+        out[f"{name}_lane_steps_per_s"] = B * T / (ms * 1e-3)
+    return out
 
 
 def measure_cpu_baseline(args, steps=1):

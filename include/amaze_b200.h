@@ -119,13 +119,18 @@ int amz_mutate_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t 
 /* Policy hand-off (agents/rollout.py:145-152 sample_actions + agents/ppo.py:82-96,136-138):
  * logits [B][A] (dtype 0 = f32, 1 = f64; A <= 16) -> action (int64 and/or u8, any NULL)
  * and its log-softmax probability (f64, may be NULL).  Sampling uses u = the (lane0+i)-th
- * double of the generator `key` (numpy Generator.random order); greedy = argmax.  With
- * step_dev == NULL, `key` is the SeedSequence state after the generator's whole key
- * (e.g. RngStream.fold_in(t)); otherwise `key` is the prefix and the device absorbs the
- * u32 *step_dev first (CUDA-graph replay with a device step counter). */
-int amz_policy_head(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *key,
-                    const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *actions, uint8_t *actions_u8,
-                    double *log_probs, void *stream);
+ * double of the generator whose SeedSequence state after its whole key is `key`
+ * (e.g. RngStream.fold_in(t)), as numpy's Generator.random(B) hands them out;
+ * greedy = argmax (key may be NULL). */
+int amz_policy_head(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *key, int greedy,
+                    int64_t lane0, int64_t *actions, uint8_t *actions_u8, double *log_probs, void *stream);
+
+/* The same for CUDA-graph replay: prefix_dev (device amz_seed_t: the rollout stream's
+ * prefix) and step_dev (device u32 t) are read at run time; the generator is
+ * prefix ++ [t]. */
+int amz_policy_head_dev(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *prefix_dev,
+                        const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *actions, uint8_t *actions_u8,
+                        double *log_probs, void *stream);
 
 /* Curriculum metrics of n levels (amaze/metrics.py:21-31 env_metrics, BFS of
  * amaze/pathfinding.py:116-135): interior wall count, agent->goal shortest path length
@@ -161,6 +166,14 @@ int amz_env_step(amz_env_t *env, const void *actions_dev, int action_dtype, int 
                  const amz_seed_t *wrap, uint32_t step_idx, uint8_t *view_dev, int64_t *dir_dev,
                  double *reward_dev, uint8_t *done_dev, double *solved_dev, int64_t *time_dev,
                  void *stream);
+
+/* amz_env_step for CUDA-graph replay: the auto-reset key prefix (wrap_dev, a device
+ * amz_seed_t) and the env step index (step_dev, a device u32 the captured graph
+ * advances) are read at run time, so one captured step serves every step of every
+ * rollout.  Auto-reset modes only (RESAMPLE / HOME; wrap_dev may be NULL for HOME). */
+int amz_env_step_dev(amz_env_t *env, const void *actions_dev, int action_dtype, int mode,
+                     const amz_seed_t *wrap_dev, const uint32_t *step_dev, uint8_t *view_dev, int64_t *dir_dev,
+                     double *reward_dev, uint8_t *done_dev, double *solved_dev, int64_t *time_dev, void *stream);
 
 /* T fused steps with an action stream actions_dev u8 [T][B] (time-major).
  * Writes the trajectory the way agents/rollout.py stores it: view [T][B][V][V] and

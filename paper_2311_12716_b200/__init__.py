@@ -16,6 +16,6 @@ from .errors import (AutocurriculaError, ConfigError, ContractViolation, LevelEr
 from .gae import compute_gae, gae_and_scores, per_lane_episode_stats
 from .level import MazeLevel, pack_levels, unpack_levels
 from .rng import RngStream
-from .policy import TorchPolicyActor, policy_head, rollout, sample_actions
+from .policy import GraphRollout, TorchPolicyActor, policy_head, rollout, sample_actions
 from .rollout import RolloutCursor, TrajectoryBatch, random_actions, rollout_actions
 from .scoring import lane_scores, score_maxmc, score_pvl

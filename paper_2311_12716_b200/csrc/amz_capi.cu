@@ -146,18 +146,31 @@ int amz_check_levels(const amz_params_t *p, const amz_level_t *lv, int64_t n, in
     return 0;
 }
 
-int amz_policy_head(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *key, const uint32_t *step_dev,
-                    int greedy, int64_t lane0, int64_t *actions, uint8_t *actions_u8, double *log_probs,
-                    void *stream) {
+int amz_policy_head_dev(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *prefix_dev,
+                        const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *actions, uint8_t *actions_u8,
+                        double *log_probs, void *stream) {
+    if (B < 0) return fail(AMZ_ESHAPE, "lanes must be >= 0, got %lld", (long long)B);
+    if (A < 1 || A > 16) return fail(AMZ_ESHAPE, "action count must be in [1, 16], got %d", A);
+    if (dtype != 0 && dtype != 1) return fail(AMZ_ECONFIG, "logits dtype code must be 0 (f32) or 1 (f64)");
+    if (B > 0 && !logits) return fail(AMZ_ECONFIG, "null argument");
+    if (!greedy && (!prefix_dev || !step_dev)) return fail(AMZ_ECONFIG, "sampling needs a key prefix and a step counter");
+    int rc = launch_policy_head(logits, dtype, B, A, 0, 0, prefix_dev, step_dev, greedy, lane0, actions, actions_u8,
+                                log_probs, (cudaStream_t)stream);
+    if (rc) return fail(rc, "policy_head: bad shape");
+    AMZ_CHECK_CUDA(cudaGetLastError(), "policy_head launch");
+    return 0;
+}
+
+int amz_policy_head(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *key, int greedy,
+                    int64_t lane0, int64_t *actions, uint8_t *actions_u8, double *log_probs, void *stream) {
     if (B < 0) return fail(AMZ_ESHAPE, "lanes must be >= 0, got %lld", (long long)B);
     if (A < 1 || A > 16) return fail(AMZ_ESHAPE, "action count must be in [1, 16], got %d", A);
     if (dtype != 0 && dtype != 1) return fail(AMZ_ECONFIG, "logits dtype code must be 0 (f32) or 1 (f64)");
     if (B > 0 && !logits) return fail(AMZ_ECONFIG, "null argument");
     if (!greedy && !key) return fail(AMZ_ECONFIG, "sampling needs a generator key");
-    amz_seed_t pre = key ? *key : amz_seed_t{};
     uint64_t k0 = 0, k1 = 0;
-    if (key && !step_dev) seed_key(pre, k0, k1);
-    int rc = launch_policy_head(logits, dtype, B, A, k0, k1, pre, step_dev, greedy, lane0, actions, actions_u8,
+    if (key) seed_key(*key, k0, k1);
+    int rc = launch_policy_head(logits, dtype, B, A, k0, k1, nullptr, nullptr, greedy, lane0, actions, actions_u8,
                                 log_probs, (cudaStream_t)stream);
     if (rc) return fail(rc, "policy_head: bad shape");
     AMZ_CHECK_CUDA(cudaGetLastError(), "policy_head launch");
@@ -242,13 +255,14 @@ int amz_env_reset_to_levels(amz_env_t *e, const amz_level_t *lv, const int64_t *
     return cuda_status("env_reset");
 }
 
-int amz_env_step(amz_env_t *e, const void *actions, int adtype, int mode, const amz_seed_t *wrap, uint32_t step_idx,
-                 uint8_t *view, int64_t *dirs, double *reward, uint8_t *done, double *solved, int64_t *times,
-                 void *stream) {
+static int env_step_impl(amz_env_t *e, const void *actions, int adtype, int mode, const amz_seed_t *wrap,
+                         uint32_t step_idx, const uint32_t *step_dev, const amz_seed_t *wrap_dev, uint8_t *view,
+                         int64_t *dirs, double *reward, uint8_t *done, double *solved, int64_t *times,
+                         void *stream) {
     if (!e || !actions) return fail(AMZ_ECONFIG, "null argument");
     if (adtype < 0 || adtype > 2) return fail(AMZ_ECONTRACT, "bad action dtype code %d", adtype);
     if (mode < AMZ_RESET_NONE || mode > AMZ_RESET_HOME) return fail(AMZ_ECONTRACT, "unknown auto-reset mode %d", mode);
-    if (mode == AMZ_RESET_RESAMPLE && !wrap) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
+    if (mode == AMZ_RESET_RESAMPLE && !wrap && !wrap_dev) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
     cudaStream_t s = (cudaStream_t)stream;
     amz_seed_t w = wrap ? *wrap : amz_seed_t{};
     int *tin = e->term + e->parity, *tout = e->term + (e->parity ^ 1);
@@ -256,10 +270,28 @@ int amz_env_step(amz_env_t *e, const void *actions, int adtype, int mode, const 
         cudaMemsetAsync(tout, 0, sizeof(int), s);
         e->parity ^= 1;
     }
-    int rc = launch_env_step(e->G, e->E, actions, adtype, mode, w, step_idx, view, dirs, reward, done, solved, times,
+    int rc = launch_env_step(e->G, e->E, actions, adtype, mode, w, step_idx, step_dev, wrap_dev, view, dirs, reward,
+                             done, solved, times,
                              tin, tout, s);
     if (rc) return fail(rc, "step: unsupported agent_view_size");
     return cuda_status("env_step");
+}
+
+int amz_env_step(amz_env_t *e, const void *actions, int adtype, int mode, const amz_seed_t *wrap, uint32_t step_idx,
+                 uint8_t *view, int64_t *dirs, double *reward, uint8_t *done, double *solved, int64_t *times,
+                 void *stream) {
+    return env_step_impl(e, actions, adtype, mode, wrap, step_idx, nullptr, nullptr, view, dirs, reward, done, solved,
+                         times, stream);
+}
+
+int amz_env_step_dev(amz_env_t *e, const void *actions, int adtype, int mode, const amz_seed_t *wrap_dev,
+                     const uint32_t *step_dev, uint8_t *view, int64_t *dirs, double *reward, uint8_t *done,
+                     double *solved, int64_t *times, void *stream) {
+    if (!step_dev) return fail(AMZ_ECONFIG, "null step counter");
+    if (mode == AMZ_RESET_NONE) return fail(AMZ_ECONTRACT, "the device-counter step needs an auto-reset mode");
+    if (mode == AMZ_RESET_RESAMPLE && !wrap_dev) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
+    return env_step_impl(e, actions, adtype, mode, nullptr, 0u, step_dev, wrap_dev, view, dirs, reward, done, solved,
+                         times, stream);
 }
 
 int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const amz_seed_t *wrap, uint32_t step0,

@@ -213,11 +213,16 @@ __device__ __forceinline__ void lane_autoreset(const Geo &G, int mode, const amz
 
 template <int V>
 __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *__restrict__ actions, int adtype,
-                                                  int mode, amz_seed_t wrap, uint32_t step_idx,
+                                                  int mode, amz_seed_t wrap, uint32_t step_base,
+                                                  const uint32_t *__restrict__ step_dev,
+                                                  const amz_seed_t *__restrict__ wrap_dev,
                                                   uint8_t *__restrict__ view, int64_t *__restrict__ dirs,
                                                   double *__restrict__ reward, uint8_t *__restrict__ done,
                                                   double *__restrict__ solved, int64_t *__restrict__ times,
                                                   const int *__restrict__ term_in, int *__restrict__ term_out) {
+    // graph replay: key and step come from device memory the captured graph updates
+    const uint32_t step_idx = step_dev ? *step_dev : step_base;
+    if (wrap_dev) wrap = *wrap_dev;
     __shared__ __align__(16) uint8_t stage[128 * V * V];
     __shared__ __align__(16) WarpSampler sw[4];
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *_
             const int tl = __ffs(todo) - 1;
             todo &= todo - 1;
             amz_seed_t sd = wrap;
-            seed_absorb(sd, step_idx);
+            seed_absorb(sd, step_idx);  // step_base + the device step counter, if any
             seed_absorb(sd, E.lane_offset + (uint32_t)(wbase + tl));
             uint64_t k0, k1;
             seed_key(sd, k0, k1);
@@ -367,13 +372,17 @@ int launch_env_set_state(const EnvDev &E, const int32_t *in, cudaStream_t s) {
 }
 
 int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adtype, int mode,
-                    const amz_seed_t &wrap, uint32_t step_idx, uint8_t *view, int64_t *dirs, double *reward,
+                    const amz_seed_t &wrap, uint32_t step_idx, const uint32_t *step_dev,
+                    const amz_seed_t *wrap_dev, uint8_t *view,
+                    int64_t *dirs, double *reward,
                     uint8_t *done, double *solved, int64_t *times, const int *term_in, int *term_out,
                     cudaStream_t s) {
     if (E.B <= 0) return 0;
     const int V = G.V;
     AMZ_DISPATCH_V(V, (k_env_step<VT><<<blocks_for(E.B, 128), 128, 0, s>>>(G, E, actions, adtype, mode, wrap,
-                                                                          step_idx, view, dirs, reward, done,
+                                                                          step_idx, step_dev, wrap_dev, view, dirs,
+                                                                          reward,
+                                                                          done,
                                                                           solved, times, term_in, term_out)));
     return 0;
 }

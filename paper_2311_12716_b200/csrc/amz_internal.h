@@ -34,7 +34,7 @@ int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0,
 int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
                          const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s);
 int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
-                       const amz_seed_t &prefix, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
+                       const amz_seed_t *prefix_dev, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
                        uint8_t *act8, double *logp, cudaStream_t s);
 int launch_level_metrics(const Geo &G, const amz_level_t *lv, int64_t n, int32_t *n_walls, int32_t *spl,
                          uint8_t *solvable, double *passable, cudaStream_t s);
@@ -47,7 +47,8 @@ int launch_env_levels(const EnvDev &E, amz_level_t *out, cudaStream_t s);
 int launch_env_state(const EnvDev &E, int32_t *out, cudaStream_t s);
 int launch_env_set_state(const EnvDev &E, const int32_t *in, cudaStream_t s);
 int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adtype, int mode,
-                    const amz_seed_t &wrap, uint32_t step_idx, uint8_t *view, int64_t *dirs, double *reward,
+                    const amz_seed_t &wrap, uint32_t step_idx, const uint32_t *step_dev, const amz_seed_t *wrap_dev,
+                    uint8_t *view, int64_t *dirs, double *reward,
                     uint8_t *done, double *solved, int64_t *times, const int *term_in, int *term_out,
                     cudaStream_t s);
 // poses [ceil(T/4)][B][4] (uint4 per lane per 4 steps), epochs [(T+1)*B][20], final_pose [B]: rollout scratch (amz_rollout.cu)

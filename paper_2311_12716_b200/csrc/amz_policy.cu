@@ -37,7 +37,7 @@ __device__ __forceinline__ double np_row_sum(const double *e, int n) {
 
 template <typename TL>
 __global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logits, int64_t B, int A, uint64_t k0,
-                                                     uint64_t k1, amz_seed_t prefix,
+                                                     uint64_t k1, const amz_seed_t *__restrict__ prefix_dev,
                                                      const uint32_t *__restrict__ step_dev, int greedy,
                                                      int64_t lane0, int64_t *__restrict__ act64,
                                                      uint8_t *__restrict__ act8, double *__restrict__ logp) {
@@ -64,9 +64,10 @@ __global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logi
             if (isnan(x[a]) || x[a] > x[act]) act = a;
         }
     } else {
-        if (step_dev) {  // graph replay: the step word is absorbed here
-            seed_absorb(prefix, *step_dev);
-            seed_key(prefix, k0, k1);
+        if (prefix_dev) {  // graph replay: the key prefix and the step word come from device memory
+            amz_seed_t pre = *prefix_dev;
+            seed_absorb(pre, *step_dev);
+            seed_key(pre, k0, k1);
         }
         const uint64_t q = (uint64_t)(lane0 + i);
         uint64_t o0, o1, o2, o3;
@@ -89,16 +90,16 @@ __global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logi
 }
 
 int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
-                       const amz_seed_t &prefix, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
+                       const amz_seed_t *prefix_dev, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
                        uint8_t *act8, double *logp, cudaStream_t s) {
     if (B <= 0) return 0;
     if (A < 1 || A > kMaxActions) return AMZ_ESHAPE;
     const unsigned g = (unsigned)((B + 127) / 128);
     if (dtype == 0)
-        k_policy_head<float><<<g, 128, 0, s>>>((const float *)logits, B, A, k0, k1, prefix, step_dev, greedy, lane0,
+        k_policy_head<float><<<g, 128, 0, s>>>((const float *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy, lane0,
                                                act64, act8, logp);
     else
-        k_policy_head<double><<<g, 128, 0, s>>>((const double *)logits, B, A, k0, k1, prefix, step_dev, greedy, lane0,
+        k_policy_head<double><<<g, 128, 0, s>>>((const double *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy, lane0,
                                                 act64, act8, logp);
     return 0;
 }

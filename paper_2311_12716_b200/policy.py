@@ -31,14 +31,21 @@ def _torch():
     return torch
 
 
-def policy_head(logits, g=None, greedy: bool = False, lane0: int = 0, actions=None, log_probs=None, actions_u8=None,
-                step_dev=None):
+class DeviceStepKey:
+    """``rng.fold_in(t)`` with ``rng``'s SeedSequence prefix and ``t`` in device memory
+    (CUDA-graph replay: the captured kernels read both at run time)."""
+
+    def __init__(self, prefix, step):
+        self.prefix = prefix  # uint8 CUDA tensor holding an amz_seed_t
+        self.step = step      # int32 CUDA scalar tensor (u32 t)
+
+
+def policy_head(logits, g=None, greedy: bool = False, lane0: int = 0, actions=None, log_probs=None, actions_u8=None):
     """logits [B, A] (float32/float64 CUDA) -> (actions int64 [B], log_probs float64 [B]).
 
     ``g``: the step's stream (RngStream or the reference's; e.g. ``rng.fold_in(t)``);
     lane i draws the (lane0 + i)-th double of its generator, as ``g.random(B)[i]``.
-    ``step_dev`` (uint32 CUDA scalar) switches to graph-replay keys: ``g`` is then the
-    rollout stream and the device folds in the step it reads from ``step_dev``."""
+    ``g`` may be a ``DeviceStepKey`` (graph replay: key prefix and step read on device)."""
     torch = _torch()
     if logits.dim() != 2:
         raise ShapeError(f"logits must be [B, A], got {tuple(logits.shape)}")
@@ -53,11 +60,15 @@ def policy_head(logits, g=None, greedy: bool = False, lane0: int = 0, actions=No
         log_probs = torch.empty(B, dtype=torch.float64, device=dev)
     if not greedy and g is None:
         raise ContractViolation("sampling needs a generator stream g")
+    a8 = _lib.ptr(actions_u8) if actions_u8 is not None else None
+    dt = 0 if lg.dtype == torch.float32 else 1
+    if isinstance(g, DeviceStepKey):
+        _lib.call("amz_policy_head_dev", _lib.ptr(lg), dt, B, A, _lib.ptr(g.prefix), _lib.ptr(g.step),
+                  int(bool(greedy)), int(lane0), _lib.ptr(actions), a8, _lib.ptr(log_probs), _lib.stream_handle(dev))
+        return actions, log_probs
     key = as_stream(g).seed_prefix() if g is not None else None
-    _lib.call("amz_policy_head", _lib.ptr(lg), 0 if lg.dtype == torch.float32 else 1, B, A,
-              ctypes.byref(key) if key is not None else None, _lib.ptr(step_dev) if step_dev is not None else None,
-              int(bool(greedy)), int(lane0), _lib.ptr(actions), _lib.ptr(actions_u8) if actions_u8 is not None else None,
-              _lib.ptr(log_probs), _lib.stream_handle(dev))
+    _lib.call("amz_policy_head", _lib.ptr(lg), dt, B, A, ctypes.byref(key) if key is not None else None,
+              int(bool(greedy)), int(lane0), _lib.ptr(actions), a8, _lib.ptr(log_probs), _lib.stream_handle(dev))
     return actions, log_probs
 
 
@@ -139,4 +150,128 @@ def rollout(rng, actor, env, start, length: int, params, hidden=None, greedy: bo
     return traj, RolloutCursor({"view": view[length], "dir": dirs[length]}, state, extras, hidden)
 
 
-__all__ = ["policy_head", "sample_actions", "TorchPolicyActor", "rollout"]
+def _seed_bytes(stream, device):
+    torch = _torch()
+    raw = bytes(as_stream(stream).seed_prefix())
+    return torch.tensor(list(raw), dtype=torch.uint8, device=device)
+
+
+class GraphRollout:
+    """``rollout`` with every step one replay of a captured CUDA graph (SURVEY §8f row
+    1: "CUDA-Graph the rollout() loop").  One step = trajectory slot writes at the device
+    step index, ``actor.act`` (torch, must be capturable: device work only, static
+    shapes), the fused policy head, the device-counter env step, the carry reset.  Keys
+    (the rollout stream's and the auto-reset wrapper's SeedSequence prefixes) and the
+    step counters live in device memory, so the graph captured on the first call serves
+    every later call on the same env (same lanes, same actor).  Results equal
+    ``rollout``'s; the trajectory tensors are cloned unless ``copy=False`` (then they are
+    the graph's buffers, overwritten by the next call)."""
+
+    def __init__(self, actor, env, length: int, greedy: bool = False):
+        if length < 1:
+            raise ContractViolation(f"rollout length must be >= 1, got {length}")
+        self.actor, self.env, self.T, self.greedy = actor, env, length, greedy
+        self.graph = None
+        self.buf = None
+
+    def _alloc(self, obs, hidden, state):
+        torch = _torch()
+        B, v = obs["view"].shape[0], obs["view"].shape[-1]
+        dev = obs["view"].device
+        T = self.T
+        self.buf = {
+            "view": torch.empty((T, B, v, v), dtype=torch.uint8, device=dev),
+            "dir": torch.empty((T, B), dtype=torch.int64, device=dev),
+            "actions": torch.empty((T, B), dtype=torch.int64, device=dev),
+            "log_probs": torch.empty((T, B), dtype=torch.float64, device=dev),
+            "values": torch.empty((T, B), dtype=torch.float64, device=dev),
+            "rewards": torch.empty((T, B), dtype=torch.float64, device=dev),
+            "dones": torch.empty((T, B), dtype=torch.bool, device=dev),
+            "pre_hidden": torch.empty((T, *hidden.shape), dtype=hidden.dtype, device=dev),
+            "cur_view": torch.empty((B, v, v), dtype=torch.uint8, device=dev),
+            "cur_dir": torch.empty((B,), dtype=torch.int64, device=dev),
+            "cur_hidden": torch.empty_like(hidden),
+            "cur_rew": torch.empty((B,), dtype=torch.float64, device=dev),
+            "cur_done": torch.empty((B,), dtype=torch.bool, device=dev),
+            "t32": torch.zeros(1, dtype=torch.int32, device=dev),
+            "s32": torch.zeros(1, dtype=torch.int32, device=dev),
+            "t64": torch.zeros(1, dtype=torch.int64, device=dev),
+            "key": torch.zeros(24, dtype=torch.uint8, device=dev),
+            "wrap": torch.zeros(24, dtype=torch.uint8, device=dev),
+        }
+        self.state = state
+
+    def _body(self):
+        from .batch import RESAMPLE
+
+        b = self.buf
+        t = b["t64"]
+        b["view"].index_copy_(0, t, b["cur_view"].unsqueeze(0))
+        b["dir"].index_copy_(0, t, b["cur_dir"].unsqueeze(0))
+        b["pre_hidden"].index_copy_(0, t, b["cur_hidden"].unsqueeze(0))
+        g = None if self.greedy else DeviceStepKey(b["key"], b["t32"])
+        act, logp, val, h = self.actor.act({"view": b["cur_view"], "dir": b["cur_dir"]}, b["cur_hidden"], g=g,
+                                           greedy=self.greedy)
+        a = act.reshape(-1).to(_torch().int64).contiguous()
+        mode = _lib.AMZ_RESET_RESAMPLE if self.env.mode == RESAMPLE else _lib.AMZ_RESET_HOME
+        _lib.call("amz_env_step_dev", self.state.handle, _lib.ptr(a), 2, mode, _lib.ptr(b["wrap"]), _lib.ptr(b["s32"]),
+                  _lib.ptr(b["cur_view"]), _lib.ptr(b["cur_dir"]), _lib.ptr(b["cur_rew"]), _lib.ptr(b["cur_done"]),
+                  None, None, self.state.stream())
+        b["actions"].index_copy_(0, t, a.unsqueeze(0))
+        b["log_probs"].index_copy_(0, t, logp.reshape(1, -1).double())
+        b["values"].index_copy_(0, t, val.reshape(1, -1).double())
+        b["rewards"].index_copy_(0, t, b["cur_rew"].unsqueeze(0))
+        b["dones"].index_copy_(0, t, b["cur_done"].unsqueeze(0))
+        b["cur_hidden"].copy_(h * (~b["cur_done"]).to(h.dtype).unsqueeze(-1))
+        b["t32"].add_(1)
+        b["s32"].add_(1)
+        b["t64"].add_(1)
+
+    def __call__(self, rng, start, hidden=None, copy: bool = True):
+        torch = _torch()
+        from .batch import AutoResetWrapper
+
+        if isinstance(start, RolloutCursor):
+            obs, state, extras = dict(start.obs), start.state, start.extras
+            hidden = start.hidden if hidden is None else hidden
+        else:
+            obs = _flat(start.observation)
+            state, extras = start.state, start.extras
+        if hidden is None:
+            hidden = self.actor.initial_hidden(obs["view"].shape[0])
+        wrap = extras[AutoResetWrapper.EXTRAS_KEY]
+        if self.buf is None:
+            self._alloc(obs, hidden, state)
+        elif state is not self.state:
+            raise ContractViolation("a GraphRollout is bound to the env state it was captured on")
+        b = self.buf
+        b["cur_view"].copy_(obs["view"])
+        b["cur_dir"].copy_(obs["dir"].to(torch.int64))
+        b["cur_hidden"].copy_(hidden)
+        b["t32"].zero_()
+        b["t64"].zero_()
+        b["s32"].fill_(int(wrap["step"]))
+        b["key"].copy_(_seed_bytes(rng, b["key"].device))
+        if wrap.get("rng") is not None:
+            b["wrap"].copy_(_seed_bytes(wrap["rng"], b["wrap"].device))
+        steps = self.T
+        if self.graph is None:
+            self._body()  # step 0 runs eagerly (also warms up the actor's kernels)
+            steps -= 1
+            if steps > 0:
+                self.graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph):
+                    self._body()
+        for _ in range(steps):
+            self.graph.replay()
+        c = (lambda x: x.clone()) if copy else (lambda x: x)
+        traj = TrajectoryBatch({"view": c(b["view"]), "dir": c(b["dir"])}, c(b["actions"]), c(b["rewards"]),
+                               c(b["dones"]), c(b["values"]), c(b["log_probs"]), c(b["pre_hidden"]))
+        ext = dict(extras)
+        ext[AutoResetWrapper.EXTRAS_KEY] = {**wrap, "step": wrap["step"] + self.T}
+        cur = RolloutCursor({"view": b["cur_view"].clone(), "dir": b["cur_dir"].clone()}, state, ext,
+                            b["cur_hidden"].clone())
+        return traj, cur
+
+
+__all__ = ["policy_head", "sample_actions", "TorchPolicyActor", "rollout", "GraphRollout", "DeviceStepKey"]

@@ -100,3 +100,39 @@ def test_policy_rollout_matches_reference(golden, tag, greedy):
     s2 = env2.reset(amz.RngStream.from_seed(9), P)
     t1, c1 = amz.rollout(amz.RngStream.from_seed(5), TorchExactActor(), env2, s2, 25, P, greedy=greedy)
     assert np.array_equal(c(t1.actions), z[f"{tag}_actions"][:25])
+
+
+@pytest.mark.parametrize("tag,greedy", [("pr", False), ("prg", True)])
+def test_graph_rollout_matches_reference(golden, tag, greedy):
+    """The CUDA-graph replayed rollout equals the reference; a second call (graph
+    already captured) on the continued env equals the eager rollout's continuation."""
+    import paper_2311_12716_b200 as amz
+
+    z = golden("policy")
+    P = amz.StaticParams()
+    c = lambda x: x.cpu().numpy()  # noqa: E731
+    env = amz.AutoResetWrapper(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, 64)), amz.RESAMPLE)
+    start = env.reset(amz.RngStream.from_seed(9), P)
+    gr = amz.GraphRollout(TorchExactActor(), env, 40, greedy=greedy)
+    traj, cur = gr(amz.RngStream.from_seed(5), start)
+    assert np.array_equal(c(traj.obs["view"]), z[f"{tag}_view"])
+    assert np.array_equal(c(traj.obs["dir"]), z[f"{tag}_dir"])
+    assert np.array_equal(c(traj.actions), z[f"{tag}_actions"])
+    assert np.array_equal(c(traj.values), z[f"{tag}_values"])
+    assert np.array_equal(c(traj.rewards), z[f"{tag}_rewards"])
+    assert np.array_equal(c(traj.dones), z[f"{tag}_dones"])
+    assert np.array_equal(c(traj.pre_hidden), z[f"{tag}_pre_hidden"])
+    np.testing.assert_allclose(c(traj.log_probs), z[f"{tag}_log_probs"], rtol=LOGP_RTOL, atol=0)
+    assert np.array_equal(c(cur.obs["view"]), z[f"{tag}_cur_view"])
+    assert np.array_equal(c(cur.hidden), z[f"{tag}_cur_hidden"])
+    # replay path: continue both the graph env and an eager twin for another 40 steps
+    env2 = amz.AutoResetWrapper(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, 64)), amz.RESAMPLE)
+    s2 = env2.reset(amz.RngStream.from_seed(9), P)
+    _, e_cur = amz.rollout(amz.RngStream.from_seed(5), TorchExactActor(), env2, s2, 40, P, greedy=greedy)
+    e_traj, _ = amz.rollout(amz.RngStream.from_seed(6), TorchExactActor(), env2, e_cur, 40, P, greedy=greedy)
+    g_traj, _ = gr(amz.RngStream.from_seed(6), cur)
+    assert gr.graph is not None
+    for name in ("actions", "rewards", "dones", "values", "pre_hidden"):
+        assert np.array_equal(c(getattr(g_traj, name)), c(getattr(e_traj, name))), name
+    assert np.array_equal(c(g_traj.obs["view"]), c(e_traj.obs["view"]))
+    np.testing.assert_allclose(c(g_traj.log_probs), c(e_traj.log_probs), rtol=LOGP_RTOL, atol=0)
