@@ -95,6 +95,7 @@ typedef struct amz_episode_stats {
 
 typedef struct amz_env amz_env_t;
 typedef struct amz_plr amz_plr_t;
+typedef struct amz_teacher amz_teacher_t;
 
 int amz_abi_version(void);
 const char *amz_last_error(void);
@@ -116,6 +117,21 @@ int amz_mutate_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t 
                       amz_level_t *out_dev, void *stream);
 
 /* Validate levels on device; *bad_index_host = first invalid index or -1 (synchronous). */
+/* PAIRED level designer, batched (amaze/teacher.py:36-159): n_lanes design episodes
+ * of wall_budget + 2 steps.  Observations per lane: grid u8 [H][W] tile codes,
+ * phase f32 [4] one-hot, n_placed i64 (phase/n_placed may be NULL); step also writes
+ * done u8 and time i64 (may be NULL).  Actions are int64 interior cell indices
+ * (row-major).  Contract violations (terminal lane, action out of range) are flagged on
+ * the device and raised by amz_teacher_check (synchronous) as AMZ_ECONTRACT.
+ * amz_teacher_levels decodes every (finished) lane into a level record (synchronous). */
+int amz_teacher_create(const amz_params_t *p, int64_t n_lanes, amz_teacher_t **out);
+int amz_teacher_destroy(amz_teacher_t *t);
+int amz_teacher_reset(amz_teacher_t *t, uint8_t *grid_dev, float *phase_dev, int64_t *n_placed_dev, void *stream);
+int amz_teacher_step(amz_teacher_t *t, const int64_t *actions_dev, uint8_t *grid_dev, float *phase_dev,
+                     int64_t *n_placed_dev, uint8_t *done_dev, int64_t *time_dev, void *stream);
+int amz_teacher_check(amz_teacher_t *t, void *stream);
+int amz_teacher_levels(amz_teacher_t *t, amz_level_t *levels_dev, void *stream);
+
 /* Policy hand-off (agents/rollout.py:145-152 sample_actions + agents/ppo.py:82-96,136-138):
  * logits [B][A] (dtype 0 = f32, 1 = f64; A <= 16) -> action (int64 and/or u8, any NULL)
  * and its log-softmax probability (f64, may be NULL).  Sampling uses u = the (lane0+i)-th

@@ -19,3 +19,4 @@ from .rng import RngStream
 from .policy import GraphRollout, TorchPolicyActor, policy_head, rollout, sample_actions
 from .rollout import RolloutCursor, TrajectoryBatch, random_actions, rollout_actions
 from .scoring import lane_scores, score_maxmc, score_pvl
+from .teacher import TeacherBatchEnv, TeacherEnv

@@ -47,6 +47,12 @@ _SIGS = {
     "amz_check_levels": ([ctypes.POINTER(AmzParams), P, I64, ctypes.POINTER(ctypes.c_int64), VP], I32),
     "amz_level_metrics": ([ctypes.POINTER(AmzParams), P, I64, P, P, P, P, VP], I32),
     "amz_policy_head": ([P, I32, I64, I32, ctypes.POINTER(AmzSeed), I32, I64, P, P, P, VP], I32),
+    "amz_teacher_create": ([ctypes.POINTER(AmzParams), I64, ctypes.POINTER(ctypes.c_void_p)], I32),
+    "amz_teacher_destroy": ([P], I32),
+    "amz_teacher_reset": ([P, P, P, P, VP], I32),
+    "amz_teacher_step": ([P, P, P, P, P, P, P, VP], I32),
+    "amz_teacher_check": ([P, VP], I32),
+    "amz_teacher_levels": ([P, P, VP], I32),
     "amz_policy_head_dev": ([P, I32, I64, I32, P, P, I32, I64, P, P, P, VP], I32),
     "amz_env_step_dev": ([P, P, I32, I32, P, P, P, P, P, P, P, P, VP], I32),
     "amz_env_create": ([ctypes.POINTER(AmzParams), I64, ctypes.POINTER(ctypes.c_void_p)], I32),

@@ -35,10 +35,15 @@ def _torch():
 
 
 def batch_lift(env, shape: BatchShape):
-    """env/batch.py:24-28: any maze env with the vector lane protocol -> VectorBatchEnv."""
+    """env/batch.py:24-28: any maze env with the vector lane protocol -> VectorBatchEnv;
+    the PAIRED designer (teacher.TeacherEnv) -> teacher.TeacherBatchEnv."""
     if hasattr(env, "make_batch") and hasattr(env, "step_batch"):
         return VectorBatchEnv(env, shape)
-    raise ShapeError("only the AMaze vector lane protocol is implemented on the GPU")
+    from .teacher import TeacherBatchEnv, TeacherEnv
+
+    if isinstance(env, TeacherEnv):
+        return TeacherBatchEnv(env, shape)
+    raise ShapeError("only the AMaze env and the PAIRED designer are implemented on the GPU")
 
 
 class DeviceLanes:

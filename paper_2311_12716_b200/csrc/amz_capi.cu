@@ -146,6 +146,89 @@ int amz_check_levels(const amz_params_t *p, const amz_level_t *lv, int64_t n, in
     return 0;
 }
 
+// ---- PAIRED level designer (amaze/teacher.py) ----
+struct amz_teacher {
+    amz_params_t p;
+    Geo G;
+    int64_t B;
+    uint4 *mask = nullptr;
+    uint4 *st = nullptr;
+    int *err = nullptr;
+};
+
+int amz_teacher_create(const amz_params_t *p, int64_t n_lanes, amz_teacher_t **out) {
+    int rc = amz_validate_params(p);
+    if (rc) return rc;
+    if (!out || n_lanes < 1) return fail(AMZ_ESHAPE, "n_lanes must be >= 1, got %lld", (long long)n_lanes);
+    amz_teacher *t = new (std::nothrow) amz_teacher();
+    if (!t) return fail(AMZ_EFAULT, "out of host memory");
+    t->p = *p;
+    t->G = make_geo(*p);
+    t->B = n_lanes;
+    cudaError_t err = cudaMalloc((void **)&t->mask, (size_t)n_lanes * sizeof(uint4));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&t->st, (size_t)n_lanes * sizeof(uint4));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&t->err, sizeof(int));
+    if (err == cudaSuccess) err = cudaMemset(t->err, 0, sizeof(int));
+    if (err != cudaSuccess) {
+        cudaFree(t->mask);
+        cudaFree(t->st);
+        cudaFree(t->err);
+        delete t;
+        return fail(AMZ_ECUDA, "teacher alloc: %s", cudaGetErrorString(err));
+    }
+    *out = t;
+    return 0;
+}
+
+int amz_teacher_destroy(amz_teacher_t *t) {
+    if (!t) return 0;
+    cudaFree(t->mask);
+    cudaFree(t->st);
+    cudaFree(t->err);
+    delete t;
+    return 0;
+}
+
+int amz_teacher_reset(amz_teacher_t *t, uint8_t *grid, float *phase, int64_t *n_placed, void *stream) {
+    if (!t || !grid) return fail(AMZ_ECONFIG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(t->err, 0, sizeof(int), s);
+    launch_teacher_reset(t->G, t->B, t->mask, t->st, grid, phase, n_placed, s);
+    return cuda_status("teacher_reset");
+}
+
+int amz_teacher_step(amz_teacher_t *t, const int64_t *actions, uint8_t *grid, float *phase, int64_t *n_placed,
+                     uint8_t *done, int64_t *times, void *stream) {
+    if (!t || !actions || !grid) return fail(AMZ_ECONFIG, "null argument");
+    launch_teacher_step(t->G, t->B, t->mask, t->st, actions, grid, phase, n_placed, done, times, t->err,
+                        (cudaStream_t)stream);
+    return cuda_status("teacher_step");
+}
+
+static int teacher_err(amz_teacher_t *t, cudaStream_t s) {
+    int h = 0;
+    cudaMemcpyAsync(&h, t->err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    AMZ_CHECK_CUDA(cudaStreamSynchronize(s), "teacher check");
+    if (h) cudaMemsetAsync(t->err, 0, sizeof(int), s);
+    if (h & 1) return fail(AMZ_ECONTRACT, "step called on a terminal design state");
+    if (h & 2) return fail(AMZ_ECONTRACT, "design action outside interior range [0, %d)", t->G.ni);
+    if (h & 4) return fail(AMZ_ECONTRACT, "no free cell left for the agent");
+    if (h & 8) return fail(AMZ_ECONTRACT, "design sequence not finished");
+    return 0;
+}
+
+int amz_teacher_check(amz_teacher_t *t, void *stream) {
+    if (!t) return fail(AMZ_ECONFIG, "null argument");
+    return teacher_err(t, (cudaStream_t)stream);
+}
+
+int amz_teacher_levels(amz_teacher_t *t, amz_level_t *out, void *stream) {
+    if (!t || !out) return fail(AMZ_ECONFIG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    launch_teacher_levels(t->B, t->mask, t->st, out, t->err, s);
+    return teacher_err(t, s);
+}
+
 int amz_policy_head_dev(const void *logits, int dtype, int64_t B, int A, const amz_seed_t *prefix_dev,
                         const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *actions, uint8_t *actions_u8,
                         double *log_probs, void *stream) {

@@ -33,6 +33,11 @@ int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0,
                          amz_level_t *out, cudaStream_t s);
 int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, int64_t n, const amz_level_t *par,
                          const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s);
+int launch_teacher_reset(const Geo &G, int64_t B, uint4 *mask, uint4 *st, uint8_t *grid, float *phase,
+                         int64_t *n_placed, cudaStream_t s);
+int launch_teacher_step(const Geo &G, int64_t B, uint4 *mask, uint4 *st, const int64_t *actions, uint8_t *grid,
+                        float *phase, int64_t *n_placed, uint8_t *done, int64_t *times, int *err, cudaStream_t s);
+int launch_teacher_levels(int64_t B, const uint4 *mask, const uint4 *st, amz_level_t *out, int *err, cudaStream_t s);
 int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
                        const amz_seed_t *prefix_dev, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
                        uint8_t *act8, double *logp, cudaStream_t s);

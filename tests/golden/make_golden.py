@@ -290,7 +290,43 @@ def gen_policy(R):
     return out
 
 
+def gen_teacher(R):
+    """amaze/teacher.py via batch_lift (GenericBatchEnv): random design episodes plus the
+    decoded levels; cases 13x13 budget 60 and 9x9 budget 5 (dense aiming -> agent wraps)."""
+    import importlib
+
+    teacher = importlib.import_module("autocurricula.amaze.teacher")
+    out = {}
+    for tag, H, W, budget, seed, B in (("t13", 13, 13, 60, 41, 48), ("t9", 9, 9, 5, 42, 64)):
+        P = R.env.StaticParams(height=H, width=W, wall_budget=budget)
+        env = R.env.batch_lift(teacher.TeacherEnv(), R.env.BatchShape(2, 1, B // 2))
+        res = env.reset(R.rng.RngStream.from_seed(seed), P)
+        T = teacher.TeacherEnv().episode_length(P)
+        g = np.random.default_rng(seed)
+        ni = P.n_interior
+        acts, grids, phases, nps, dones, times = [], [], [], [], [], []
+        state = res.state
+        grids.append(res.observation["grid"]); phases.append(res.observation["phase"])
+        nps.append(res.observation["n_placed"])
+        for t in range(T):
+            # aim at few cells so the no-op / wall-clearing / agent-wrap rules all fire
+            a = g.integers(0, ni if t % 3 else min(ni, 9), size=(2, B // 2))
+            r = env.step(None, state, a, P)
+            state = r.state
+            acts.append(a); grids.append(r.observation["grid"]); phases.append(r.observation["phase"])
+            nps.append(r.observation["n_placed"]); dones.append(r.done); times.append(r.info["time"])
+        levels = [env.env.designed_level(s) for s in state]
+        out.update({f"{tag}_meta": np.array([H, W, budget, seed, B], dtype=np.int64),
+                    f"{tag}_actions": np.stack(acts), f"{tag}_grid": np.stack(grids), f"{tag}_phase": np.stack(phases),
+                    f"{tag}_n_placed": np.stack(nps), f"{tag}_done": np.stack(dones), f"{tag}_time": np.stack(times),
+                    f"{tag}_levels": pack(levels, H, W)})
+    return out
+
+
 def main():
+    if "--only-teacher" in sys.argv:
+        np.savez_compressed(os.path.join(OUT, "teacher.npz"), **gen_teacher(_import_reference()))
+        return
     if "--only-policy" in sys.argv:
         np.savez_compressed(os.path.join(OUT, "policy.npz"), **gen_policy(_import_reference()))
         return
@@ -315,6 +351,7 @@ def main():
     np.savez_compressed(os.path.join(OUT, "views.npz"), **misc)
     np.savez_compressed(os.path.join(OUT, "metrics.npz"), **gen_metrics(R))
     np.savez_compressed(os.path.join(OUT, "policy.npz"), **gen_policy(R))
+    np.savez_compressed(os.path.join(OUT, "teacher.npz"), **gen_teacher(R))
     for f in ("levels", "rollouts", "scores", "views"):
         print(f, os.path.getsize(os.path.join(OUT, f + ".npz")))
 

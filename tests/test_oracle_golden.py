@@ -108,3 +108,28 @@ def test_sample_actions_oracle_matches_reference(golden, tag):
         g = onp.generator(31, (t,))
         assert np.array_equal(onp.sample_actions(lg[t], g), z[f"pa_{tag}_actions"][t])
         assert np.array_equal(onp.log_softmax(lg[t]), z[f"pa_{tag}_logp"][t])
+
+
+@pytest.mark.parametrize("tag", ["t13", "t9"])
+def test_teacher_oracle_matches_reference(golden, tag):
+    z = golden("teacher")
+    H, W, budget, seed, B = (int(x) for x in z[f"{tag}_meta"])
+    p = onp.Params(height=H, width=W, wall_budget=budget)
+    lanes = [onp.Teacher(p) for _ in range(B)]
+    acts = z[f"{tag}_actions"].reshape(z[f"{tag}_actions"].shape[0], -1)
+    for t in range(acts.shape[0] + 1):
+        obs = [ln.observe() for ln in lanes]
+        assert np.array_equal(np.stack([o[0] for o in obs]), z[f"{tag}_grid"][t].reshape(B, H, W))
+        assert np.array_equal(np.stack([o[1] for o in obs]), z[f"{tag}_phase"][t].reshape(B, 4))
+        assert np.array_equal(np.array([o[2] for o in obs]), z[f"{tag}_n_placed"][t].reshape(B))
+        if t < acts.shape[0]:
+            for ln, a in zip(lanes, acts[t]):
+                ln.step(a)
+    assert np.array_equal(onp_rows([ln.level() for ln in lanes], p), z[f"{tag}_levels"])
+
+
+def onp_rows(levels, p):
+    rec = onp.pack_levels(levels, p)
+    return np.stack([rec["walls"][:, 0], rec["walls"][:, 1], rec["walls"][:, 2], rec["walls"][:, 3],
+                     rec["agent_r"], rec["agent_c"], rec["agent_dir"], rec["goal_r"], rec["goal_c"]],
+                    axis=1).astype(np.int64)
