@@ -106,3 +106,63 @@ def check_replicas(digest: int, device=None) -> None:
     torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
     if int(lo.item()) != int(hi.item()):
         raise RunnerFault(f"PLR buffer replicas diverged (rank {rank})")
+
+
+# ------------------------------------------------------------------------------------
+# SDP gradient averaging for PPO shards (agents/ppo.py:267-330)
+# ------------------------------------------------------------------------------------
+
+def _flat(tensors):
+    torch = _torch()
+    return torch.cat([t.reshape(-1) for t in tensors]) if tensors else torch.zeros(0)
+
+
+def sdp_average_gradients(params, exact: bool = False, group=None) -> None:
+    """Replace every parameter's gradient by the mean over ranks (one rank per shard),
+    the in-process shard mean of agents/ppo.py:308-313 (missing gradients count as
+    zeros, :260-263).  ``exact=False``: one all-reduce(SUM) of a flat bucket (NCCL over
+    NVLink on GPUs), then / D -- identical on every rank.  ``exact=True``: all-gather the
+    flat gradients and sum them in rank order from 0 like the reference's Python
+    ``sum(...) / n_shards``, bit-identical to the single-process result for any D."""
+    torch = _torch()
+    dist = torch.distributed
+    params = list(params)
+    grads = [p.grad.detach() if p.grad is not None else torch.zeros_like(p) for p in params]
+    flat = _flat(grads).contiguous()
+    D = dist.get_world_size(group)
+    if D == 1:
+        return
+    if exact:
+        parts = [torch.empty_like(flat) for _ in range(D)]
+        dist.all_gather(parts, flat, group=group)
+        acc = torch.zeros_like(flat)
+        for part in parts:
+            acc = acc + part
+        mean = acc / D
+    else:
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        mean = flat / D
+    off = 0
+    with torch.no_grad():
+        for p in params:
+            n = p.numel()
+            p.grad = mean[off:off + n].view_as(p).clone()
+            off += n
+
+
+def check_param_sync(params, tol: float = 1e-6, group=None) -> float:
+    """agents/ppo.py:322-328 across ranks: max |params - rank 0's params| (all-reduce
+    MAX); raises RunnerFault above ``tol``."""
+    torch = _torch()
+    dist = torch.distributed
+    with torch.no_grad():
+        vec = _flat([p.detach().double() for p in params]).contiguous()
+        ref = vec.clone()
+        dist.broadcast(ref, src=0, group=group)
+        drift = (vec - ref).abs().max() if vec.numel() else torch.zeros((), dtype=torch.float64)
+        d = drift.reshape(1).clone()
+        dist.all_reduce(d, op=dist.ReduceOp.MAX, group=group)
+    val = float(d.item())
+    if val > tol:
+        raise RunnerFault(f"shard parameters diverged by {val:.3e}")
+    return val

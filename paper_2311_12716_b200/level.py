@@ -14,7 +14,11 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import LevelError
+from .errors import LevelError, LevelParseError
+
+# agent heading glyphs, amaze/level.py:29-30
+AGENT_CHARS = {0: "^", 1: ">", 2: "v", 3: "<"}
+CHAR_DIRS = {v: k for k, v in AGENT_CHARS.items()}
 
 RECORD = np.dtype([("walls", "<u4", (4,)), ("agent_r", "u1"), ("agent_c", "u1"), ("agent_dir", "u1"),
                    ("goal_r", "u1"), ("goal_c", "u1"), ("pad", "u1", (3,)), ("pad2", "<u4", (2,))])
@@ -125,3 +129,59 @@ def records_to_tensor(rec: np.ndarray, device="cuda"):
 def tensor_to_records(t) -> np.ndarray:
     arr = t.detach().to("cpu").contiguous().numpy().astype(np.int32, copy=False)
     return arr.reshape(-1).view(RECORD)
+
+
+def encode_level(level) -> str:
+    """Grid text of a level (amaze/level.py:83-97): '#' wall, '.' floor, 'G' goal,
+    '^>v<' the agent by heading; one line per row, trailing newline."""
+    lv = MazeLevel.from_any(level)
+    walls = np.asarray(lv.walls, dtype=bool)
+    h, w = walls.shape
+    grid = np.where(walls, "#", ".").astype("<U1")
+    grid[tuple(lv.goal_pos)] = "G"
+    grid[tuple(lv.agent_pos)] = AGENT_CHARS[int(lv.agent_dir)]
+    return "\n".join("".join(row) for row in grid) + "\n"
+
+
+def decode_level(text: str, expected_shape: tuple | None = None) -> MazeLevel:
+    """Parse grid text (amaze/level.py:100-145): blank lines skipped, ragged rows,
+    wrong shape, illegal characters, duplicate / missing agent or goal raise
+    LevelParseError with the 1-based line/column the reference reports; invariant
+    violations of the parsed level become LevelParseError at (1, 1)."""
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+    if not lines:
+        raise LevelParseError("empty level text", 1, 1)
+    h, w = len(lines), len(lines[0])
+    for i, ln in enumerate(lines):
+        if len(ln) != w:
+            raise LevelParseError(f"row has length {len(ln)}, expected {w}", i + 1, len(ln) + 1)
+    if expected_shape is not None and (h, w) != tuple(expected_shape):
+        raise LevelParseError(f"level is {h}x{w}, expected {expected_shape[0]}x{expected_shape[1]}", 1, 1)
+    walls = np.zeros((h, w), dtype=bool)
+    agent_pos = agent_dir = goal_pos = None
+    for r, ln in enumerate(lines):
+        for c, ch in enumerate(ln):
+            if ch == "#":
+                walls[r, c] = True
+            elif ch == ".":
+                continue
+            elif ch == "G":
+                if goal_pos is not None:
+                    raise LevelParseError("duplicate goal", r + 1, c + 1)
+                goal_pos = (r, c)
+            elif ch in CHAR_DIRS:
+                if agent_pos is not None:
+                    raise LevelParseError("duplicate agent", r + 1, c + 1)
+                agent_pos, agent_dir = (r, c), CHAR_DIRS[ch]
+            else:
+                raise LevelParseError(f"illegal character {ch!r}", r + 1, c + 1)
+    if agent_pos is None:
+        raise LevelParseError("missing agent", h, w)
+    if goal_pos is None:
+        raise LevelParseError("missing goal", h, w)
+    try:
+        return MazeLevel(walls, agent_pos, agent_dir, goal_pos).validate()
+    except LevelParseError:
+        raise
+    except LevelError as e:
+        raise LevelParseError(str(e), 1, 1) from e

@@ -323,7 +323,35 @@ def gen_teacher(R):
     return out
 
 
+def gen_codec(R):
+    """amaze/level.py:83-145: encode_level texts of the shipped assets and DR levels, and
+    the LevelParseError (message, line, col) the reference raises on malformed texts."""
+    lv_mod = R.amaze.level if hasattr(R.amaze, "level") else __import__("autocurricula.amaze.level", fromlist=["x"])
+    names = R.amaze.asset_names()
+    levels = [R.amaze.load_asset(n) for n in names]
+    P = R.env.StaticParams()
+    root = R.rng.RngStream.from_seed(77)
+    levels += [R.amaze.sample_random_level(k, P) for k in root.split(20)]
+    texts = [lv_mod.encode_level(lv) for lv in levels]
+    bad = ["", "\n\n", "#####\n#.G.#\n####\n", "#####\n#^G.#\n#####\n", "#####\n#^Gx#\n#####\n",
+           "#####\n#^G^#\n#####\n", "#####\n#GG>#\n#####\n", "#####\n#...#\n#####\n", "#####\n#.^.#\n#####\n",
+           "#####\n#.^.G\n#####\n", "#####\n\n#^.G#\n\n#####\n", "######\n#^..G#\n######\n"]
+    errs = []
+    for t in bad:
+        try:
+            lv_mod.decode_level(t, expected_shape=(3, 5) if t.startswith("######") else None)
+            errs.append(("ok", 0, 0))
+        except Exception as e:  # noqa: BLE001 - recorded verbatim
+            errs.append((str(e), getattr(e, "line", 0), getattr(e, "col", 0)))
+    return {"codec_levels": pack(levels, 13, 13), "codec_texts": np.array(texts), "codec_bad": np.array(bad),
+            "codec_bad_msg": np.array([e[0] for e in errs]), "codec_bad_line": np.array([e[1] for e in errs]),
+            "codec_bad_col": np.array([e[2] for e in errs])}
+
+
 def main():
+    if "--only-codec" in sys.argv:
+        np.savez_compressed(os.path.join(OUT, "codec.npz"), **gen_codec(_import_reference()))
+        return
     if "--only-teacher" in sys.argv:
         np.savez_compressed(os.path.join(OUT, "teacher.npz"), **gen_teacher(_import_reference()))
         return
@@ -352,6 +380,7 @@ def main():
     np.savez_compressed(os.path.join(OUT, "metrics.npz"), **gen_metrics(R))
     np.savez_compressed(os.path.join(OUT, "policy.npz"), **gen_policy(R))
     np.savez_compressed(os.path.join(OUT, "teacher.npz"), **gen_teacher(R))
+    np.savez_compressed(os.path.join(OUT, "codec.npz"), **gen_codec(R))
     for f in ("levels", "rollouts", "scores", "views"):
         print(f, os.path.getsize(os.path.join(OUT, f + ".npz")))
 

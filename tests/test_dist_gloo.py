@@ -99,3 +99,60 @@ def test_record_pack_roundtrip():
     mx = torch.randn(7, dtype=torch.float64)
     a, b, c = dist.unpack_candidates(dist.pack_candidates(lv, sc, mx))
     assert torch.equal(a, lv) and torch.equal(b, sc) and torch.equal(c, mx)
+
+
+def _grad_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist_.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2311_12716_b200 import dist
+
+        def model_and_grads(r):
+            torch.manual_seed(100)  # identical initial parameters on every shard
+            m = torch.nn.Sequential(torch.nn.Linear(5, 7), torch.nn.Tanh(), torch.nn.Linear(7, 3))
+            torch.manual_seed(200 + r)  # shard-specific minibatch
+            x = torch.randn(11, 5, dtype=torch.float32) * (r + 1)
+            m(x).pow(2).sum().backward()
+            m[2].bias.grad = None  # a parameter without a gradient counts as zeros
+            return m
+
+        out = {}
+        for exact in (True, False):
+            m = model_and_grads(rank)
+            dist.sdp_average_gradients(m.parameters(), exact=exact)
+            out[exact] = [p.grad.clone() for p in m.parameters()]
+        # the reference's in-process mean: sum(g[i] for g in shard_grads) / n_shards
+        shards = [[p.grad.detach() if p.grad is not None else torch.zeros_like(p) for p in model_and_grads(r).parameters()]
+                  for r in range(world)]
+        want = [sum(g[i] for g in shards) / world for i in range(len(shards[0]))]
+        exact_ok = all(torch.equal(a, b) for a, b in zip(out[True], want))
+        close_ok = all(torch.allclose(a, b, rtol=1e-6, atol=1e-7) for a, b in zip(out[False], want))
+        m = model_and_grads(rank)
+        drift0 = dist.check_param_sync(m.parameters())
+        if rank == 1:
+            with torch.no_grad():
+                m[0].weight[0, 0] += 1.0
+        try:
+            dist.check_param_sync(m.parameters())
+            fault = "no-fault"
+        except Exception as e:  # RunnerFault
+            fault = type(e).__name__
+        q.put((rank, exact_ok, close_ok, drift0, fault))
+    finally:
+        dist_.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sdp_gradient_average_matches_reference_mean(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    msgs = sorted(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, exact_ok, close_ok, drift0, fault in msgs:
+        assert exact_ok and close_ok and drift0 == 0.0 and fault == "RunnerFault"
