@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                         seed_key(sd, k0, k1);
                     }
                     DYN_T0(c_smp);
-                    warp_sample_each(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
+                    warp_sample_each<true>(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
                     DYN_ACC(5, c_smp);
 #ifdef AMZ_DYN_PROF
                     if (lane == 0) g_dyn_prof[(int64_t)blockIdx.x * WPC + warp][7] += __popc(need);

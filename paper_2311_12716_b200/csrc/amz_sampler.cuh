@@ -68,6 +68,11 @@ struct WarpSampler {
     uint8_t T[128];      // terminal of the succ chain from i (pointer jumping)
 };
 
+// Phase 2 of warp_sample_level: kTrack = false reads the permutation off the swap lists
+// (fewest instructions: throughput kernels that sample many levels); kTrack = true
+// follows each lane's 4 elements through the 120 transpositions (4 independent select
+// chains: lowest latency for one level on the dynamics' critical path).
+
 // smallest element > after of the 128-bit set L[q], or -1
 __device__ __forceinline__ int set_next(const WarpSampler &X, int q, int after) {
     const int s = after + 1;
@@ -90,11 +95,13 @@ __device__ __forceinline__ int set_next(const WarpSampler &X, int q, int after) 
 //      step after k that drew the same j as k (or to j_k itself if there is none), then
 //      along succ(q) = first step after q that drew q.  The succ chains are collapsed by
 //      pointer jumping.
+template <bool kTrack = false>
 __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, const Geo &G, WarpSampler &X, Mask &mask,
                                                   int &ar, int &ac, int &ad, int &gr, int &gc) {
     const int lane = threadIdx.x & 31;
     const int ni = G.ni;
-    for (int x = lane; x < 128; x += 32) reinterpret_cast<uint4 *>(&X.L[0][0])[x] = make_uint4(0u, 0u, 0u, 0u);
+    if (!kTrack)
+        for (int x = lane; x < 128; x += 32) reinterpret_cast<uint4 *>(&X.L[0][0])[x] = make_uint4(0u, 0u, 0u, 0u);
     warp_stage_stream(k0, k1, X.sw);
     const WarpStream S{X.sw, k0, k1};
     uint32_t p = 0;
@@ -126,60 +133,97 @@ __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, cons
     }
     if (lane == 0) X.J[0] = 0;
     __syncwarp();
-    // ---- 2. final positions ----
-    for (int k = lane; k < ni; k += 32) atomicOr(&X.L[X.J[k]][k >> 5], 1u << (k & 31));
-    __syncwarp();
-    for (int k = lane; k < ni; k += 32) {
-        const int sn = set_next(X, k, k);
-        X.T[k] = (uint8_t)(sn >= 0 ? sn : k);
-    }
-    __syncwarp();
-    while (true) {  // T[k] <- T[T[k]] until every chain is collapsed
-        bool moved = false;
+    if (kTrack) {
+        // ---- 2. final positions of this lane's elements ----
+        int q0 = lane, q1 = lane + 32, q2 = lane + 64, q3 = lane + 96;
+#pragma unroll 4
+        for (int i = ni - 1; i >= 1; i--) {
+            const int j = X.J[i];
+            q0 = q0 == i ? j : (q0 == j ? i : q0);
+            q1 = q1 == i ? j : (q1 == j ? i : q1);
+            q2 = q2 == i ? j : (q2 == j ? i : q2);
+            q3 = q3 == i ? j : (q3 == j ? i : q3);
+        }
+        mask.w[0] = __ballot_sync(0xFFFFFFFFu, lane < ni && q0 < (int)nw);
+        mask.w[1] = __ballot_sync(0xFFFFFFFFu, lane + 32 < ni && q1 < (int)nw);
+        mask.w[2] = __ballot_sync(0xFFFFFFFFu, lane + 64 < ni && q2 < (int)nw);
+        mask.w[3] = __ballot_sync(0xFFFFFFFFu, lane + 96 < ni && q3 < (int)nw);
+        auto element = [&](int target) {  // the element whose final position is target
+            const int e = (lane < ni && q0 == target)        ? lane
+                          : (lane + 32 < ni && q1 == target) ? lane + 32
+                          : (lane + 64 < ni && q2 == target) ? lane + 64
+                          : (lane + 96 < ni && q3 == target) ? lane + 96
+                                                             : -1;
+            const unsigned b = __ballot_sync(0xFFFFFFFFu, e >= 0);
+            return __shfl_sync(0xFFFFFFFFu, e, __ffs(b) - 1);
+        };
+        // goal = free[gk], agent = (free without goal)[ak]; free = final positions nw..ni-1
+        const uint32_t nfree = (uint32_t)ni - nw;
+        const uint32_t gk = S.below(p, nfree);
+        const uint32_t ak = S.below(p, nfree - 1u);
+        ad = (int)S.below(p, 4u);
+        const int goal = element((int)(nw + gk)), agent = element((int)(nw + (ak < gk ? ak : ak + 1u)));
+        gr = goal / G.iw + 1;
+        gc = goal % G.iw + 1;
+        ar = agent / G.iw + 1;
+        ac = agent % G.iw + 1;
+    } else {
+        // ---- 2. final positions ----
+        for (int k = lane; k < ni; k += 32) atomicOr(&X.L[X.J[k]][k >> 5], 1u << (k & 31));
+        __syncwarp();
         for (int k = lane; k < ni; k += 32) {
-            const int t = X.T[k], tt = X.T[t];
-            if (tt != t) {
-                X.T[k] = (uint8_t)tt;
-                moved = true;
-            }
+            const int sn = set_next(X, k, k);
+            X.T[k] = (uint8_t)(sn >= 0 ? sn : k);
         }
         __syncwarp();
-        if (!__any_sync(0xFFFFFFFFu, moved)) break;
+        while (true) {  // T[k] <- T[T[k]] until every chain is collapsed
+            bool moved = false;
+            for (int k = lane; k < ni; k += 32) {
+                const int t = X.T[k], tt = X.T[t];
+                if (tt != t) {
+                    X.T[k] = (uint8_t)tt;
+                    moved = true;
+                }
+            }
+            __syncwarp();
+            if (!__any_sync(0xFFFFFFFFu, moved)) break;
+        }
+        auto element = [&](int k) {
+            const int q = X.J[k];
+            const int sn = set_next(X, q, k);
+            return sn >= 0 ? (int)X.T[sn] : q;
+        };
+        uint32_t m0 = 0u, m1 = 0u, m2 = 0u, m3 = 0u;
+        for (int k = lane; k < (int)nw; k += 32) {
+            const int e = element(k);
+            const uint32_t b = 1u << (e & 31);
+            const int q = e >> 5;
+            m0 |= q == 0 ? b : 0u;
+            m1 |= q == 1 ? b : 0u;
+            m2 |= q == 2 ? b : 0u;
+            m3 |= q == 3 ? b : 0u;
+        }
+        mask.w[0] = __reduce_or_sync(0xFFFFFFFFu, m0);
+        mask.w[1] = __reduce_or_sync(0xFFFFFFFFu, m1);
+        mask.w[2] = __reduce_or_sync(0xFFFFFFFFu, m2);
+        mask.w[3] = __reduce_or_sync(0xFFFFFFFFu, m3);
+        // goal = free[gk], agent = (free without goal)[ak]; free = final positions nw..ni-1
+        const uint32_t nfree = (uint32_t)ni - nw;
+        const uint32_t gk = S.below(p, nfree);
+        const uint32_t ak = S.below(p, nfree - 1u);
+        ad = (int)S.below(p, 4u);
+        const int goal = element((int)(nw + gk)), agent = element((int)(nw + (ak < gk ? ak : ak + 1u)));
+        gr = goal / G.iw + 1;
+        gc = goal % G.iw + 1;
+        ar = agent / G.iw + 1;
+        ac = agent % G.iw + 1;
     }
-    auto element = [&](int k) {
-        const int q = X.J[k];
-        const int sn = set_next(X, q, k);
-        return sn >= 0 ? (int)X.T[sn] : q;
-    };
-    uint32_t m0 = 0u, m1 = 0u, m2 = 0u, m3 = 0u;
-    for (int k = lane; k < (int)nw; k += 32) {
-        const int e = element(k);
-        const uint32_t b = 1u << (e & 31);
-        const int q = e >> 5;
-        m0 |= q == 0 ? b : 0u;
-        m1 |= q == 1 ? b : 0u;
-        m2 |= q == 2 ? b : 0u;
-        m3 |= q == 3 ? b : 0u;
-    }
-    mask.w[0] = __reduce_or_sync(0xFFFFFFFFu, m0);
-    mask.w[1] = __reduce_or_sync(0xFFFFFFFFu, m1);
-    mask.w[2] = __reduce_or_sync(0xFFFFFFFFu, m2);
-    mask.w[3] = __reduce_or_sync(0xFFFFFFFFu, m3);
-    // goal = free[gk], agent = (free without goal)[ak]; free = final positions nw..ni-1
-    const uint32_t nfree = (uint32_t)ni - nw;
-    const uint32_t gk = S.below(p, nfree);
-    const uint32_t ak = S.below(p, nfree - 1u);
-    ad = (int)S.below(p, 4u);
-    const int goal = element((int)(nw + gk)), agent = element((int)(nw + (ak < gk ? ak : ak + 1u)));
-    gr = goal / G.iw + 1;
-    gc = goal % G.iw + 1;
-    ar = agent / G.iw + 1;
-    ac = agent % G.iw + 1;
     __syncwarp();
 }
 
 // Every lane whose bit is set in `need` gets the level of its own key (k0, k1), one
 // warp-cooperative sample per requesting lane.
+template <bool kTrack = false>
 __device__ __forceinline__ void warp_sample_each(unsigned need, uint64_t k0, uint64_t k1, const Geo &G,
                                                  WarpSampler &X, Mask &mask, int &ar, int &ac, int &ad, int &gr,
                                                  int &gc) {
@@ -190,7 +234,7 @@ __device__ __forceinline__ void warp_sample_each(unsigned need, uint64_t k0, uin
         const uint64_t a = __shfl_sync(0xFFFFFFFFu, k0, tl), b = __shfl_sync(0xFFFFFFFFu, k1, tl);
         Mask m;
         int r0, c0, d0, g0, h0;
-        warp_sample_level(a, b, G, X, m, r0, c0, d0, g0, h0);
+        warp_sample_level<kTrack>(a, b, G, X, m, r0, c0, d0, g0, h0);
         if (lane == tl) {
             mask = m;
             ar = r0;
