@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "amz_internal.h"
 
@@ -337,144 +338,93 @@ __global__ void __launch_bounds__(64) k_gae_score2(int T, int64_t B, const doubl
     }
 }
 
-// ---------------------------------------------------------------------------------
-// k_gae_score3: the same three passes for 16 lanes per CTA, with the [T][16] columns
-// streamed through an 8-stage cp.async ring (8 steps per stage) so that every warp has
-// ~64 steps of loads in flight instead of one dependent DRAM round trip per 8 steps.
-// Pass 2 keeps the pass-3 source column (advantages for PVL, values for MaxMC) in
-// shared memory, so pass 3 reads no global memory.  Needs B % 16 == 0 (16-B aligned
-// rows of the done bytes) and T <= kG3MaxT; launch_gae_score falls back otherwise.
-// ---------------------------------------------------------------------------------
-constexpr int kG3LW = 16;     // lanes per CTA
-constexpr int kG3GS = 8;      // steps per stage
-constexpr int kG3NS = 8;      // stages in flight
-constexpr int kG3MaxT = 256;  // pass-3 column kept in shared memory
-struct G3Stage {
-    double r[kG3GS][kG3LW];
-    double v[kG3GS][kG3LW];
-    uint8_t d[kG3GS][kG3LW];
-};
-struct G3Smem {
-    G3Stage ring[2][kG3NS];
-    double src[kG3MaxT][kG3LW];
-    double leaf[kMaxLeaves][kG3LW];
-    double mx[kG3LW];
-};
-
 __device__ __forceinline__ void g3_cp16(void *sdst, const void *gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
                  "l"(gsrc)
                  : "memory");
 }
 
-__global__ void __launch_bounds__(64) k_gae_score3(int T, int64_t B, const double *__restrict__ rw,
-                                                   const double *__restrict__ val, const uint8_t *__restrict__ dn,
-                                                   const double *__restrict__ last, double gamma, double gl,
-                                                   const double *__restrict__ prior, int score_fn, int disc,
-                                                   double *__restrict__ adv, double *__restrict__ ret,
-                                                   double *__restrict__ scores, double *__restrict__ maxret,
-                                                   int64_t *__restrict__ st_eps, double *__restrict__ st_mean,
-                                                   double *__restrict__ st_max, double *__restrict__ st_solved,
-                                                   const PairwisePlan P) {
-    extern __shared__ __align__(16) uint8_t g3raw[];
-    G3Smem &S = *reinterpret_cast<G3Smem *>(g3raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t l0 = (int64_t)blockIdx.x * kG3LW;
-    const int64_t l = l0 + lane;
+// ---------------------------------------------------------------------------------
+// k_gae_score4: 16 lanes per CTA, 4 warps, whole columns in shared memory (T <= 256).
+//   load   all 128 threads stream the CTA's [T][16] rewards / values / dones into shared
+//          memory with cp.async (bandwidth-bound: every warp keeps ~35 16-B copies in
+//          flight);
+//   prep   warps 1-3 compute the data-parallel part of the GAE recurrence,
+//          delta_t = (r_t + (gamma*keep_t) * V_{t+1}) - V_t, while warp 0 runs
+//          per_lane_episode_stats forward over (r, done);
+//   scan   warp 1 runs the reverse recurrence A_t = delta_t + ((gamma*lam)*keep_t) * A_{t+1}
+//          alone: two dependent float64 ops per step;
+//   out    all threads store A and R = A + V and sum the pass-3 leaves from shared memory.
+// Same float64 operations in the same order as the reference (bit-exact).
+// ---------------------------------------------------------------------------------
+constexpr int kG4MaxT = 256;
+template <int kG4LW>
+struct G4Smem {
+    double r[kG4MaxT][kG4LW];    // rewards
+    double v[kG4MaxT][kG4LW];    // values
+    double a[kG4MaxT][kG4LW];    // delta, then advantages (in place)
+    uint8_t d[kG4MaxT][kG4LW];   // dones
+    double leaf[kMaxLeaves][kG4LW];
+    double mx[kG4LW];
+};
+
+__device__ __forceinline__ void g4_cp8(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+
+template <int kG4LW>
+__global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const double *__restrict__ rw,
+                                                    const double *__restrict__ val, const uint8_t *__restrict__ dn,
+                                                    const double *__restrict__ last, double gamma, double gl,
+                                                    const double *__restrict__ prior, int score_fn, int disc,
+                                                    double *__restrict__ adv, double *__restrict__ ret,
+                                                    double *__restrict__ scores, double *__restrict__ maxret,
+                                                    int64_t *__restrict__ st_eps, double *__restrict__ st_mean,
+                                                    double *__restrict__ st_max, double *__restrict__ st_solved,
+                                                    const PairwisePlan P) {
+    extern __shared__ __align__(16) uint8_t g4raw[];
+    G4Smem<kG4LW> &S = *reinterpret_cast<G4Smem<kG4LW> *>(g4raw);
+    constexpr int CR = kG4LW / 2;  // 16-B chunks per row of r (and of v)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t l0 = (int64_t)blockIdx.x * kG4LW;
     const bool noclamp = (score_fn & AMZ_SCORE_NOCLAMP) != 0;
     const bool prior_final = (score_fn & AMZ_SCORE_PRIOR_FINAL) != 0;
     const int fn = score_fn & 0xFF;
     const bool pvl = fn == AMZ_SCORE_PVL;
-    // warp 0: forward (rewards, dones); warp 1: reverse (rewards, values, dones)
-    const bool rev = warp == 1;
-    const int nst = (warp == 0 && prior_final) ? 0 : (T + kG3GS - 1) / kG3GS;
-    G3Stage *ring = S.ring[warp];
-    // stage copy plan (fixed per thread): rewards and values rows j = lane>>3 and
-    // j+4, 16-B chunk q = lane&7; done rows j = lane (lanes 0..7)
-    const int cq = lane & 7, cj = lane >> 3;
-    auto issue = [&](int st) {
-        if (st < nst) {
-            G3Stage &G = ring[st % kG3NS];
-            const int k0 = st * kG3GS;
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int j = cj + 4 * h, k = k0 + j;
-                if (k < T) {
-                    const int64_t row = (int64_t)(rev ? T - 1 - k : k) * B + l0;
-                    g3_cp16(&G.r[j][2 * cq], rw + row + 2 * cq);
-                    if (rev) g3_cp16(&G.v[j][2 * cq], val + row + 2 * cq);
-                }
-            }
-            if (lane < kG3GS && k0 + lane < T)
-                g3_cp16(&G.d[lane][0], dn + (int64_t)(rev ? T - 1 - (k0 + lane) : k0 + lane) * B + l0);
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-#pragma unroll 1
-    for (int st = 0; st < kG3NS - 1; st++) issue(st);
-
-    const bool act = lane < kG3LW;
-    const bool keep_src = pvl;  // MaxMC's source (values) is staged by this warp too
-    // pass 1 state
-    const double g1 = disc ? gamma : 1.0;
-    double acc = 0.0, dsc = 1.0, tot = 0.0, best = 0.0;
-    int cnt = 0, hits = 0;
-    // pass 2 state
-    double nxt = (rev && act) ? last[l] : 0.0, run = 0.0;
-    const double g0 = gamma * 0.0, gl0 = gl * 0.0;  // x * keep for keep = 0.0, sign included
-    int64_t off = (int64_t)(T - 1) * B + l;         // reverse walk over [t][B]
-    // per_lane_episode_stats step: the episode bookkeeping only runs on a done
-    auto fwd_step = [&](double r, bool dd) {
-        acc = acc + dsc * r;
-        dsc = dsc * g1;
-        if (dd) {
-            cnt++;
-            tot = tot + acc;
-            best = np_max(best, acc);
-            hits += acc > 0.0;
-            acc = 0.0;
-        }
-    };
-    auto rev_step = [&](double r, double xv, bool dd, int t) {
-        // gamma * keep and (gamma * lam) * keep with keep in {0.0, 1.0}
-        const double gk = dd ? g0 : gamma, glk = dd ? gl0 : gl;
-        const double delta = (r + gk * nxt) - xv;
-        run = delta + glk * run;
-        adv[off] = run;
-        ret[off] = run + xv;
-        off -= B;
-        nxt = xv;
-        S.src[t][lane] = keep_src ? run : xv;
-    };
-#pragma unroll 1
-    for (int st = 0; st < nst; st++) {
-        issue(st + kG3NS - 1);
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kG3NS - 1) : "memory");
-        __syncwarp();
-        const G3Stage &G = ring[st % kG3NS];
-        const int jn = (T - st * kG3GS) < kG3GS ? (T - st * kG3GS) : kG3GS;
-        if (act) {
-            if (!rev) {
-                if (jn == kG3GS) {
-#pragma unroll
-                    for (int j = 0; j < kG3GS; j++) fwd_step(G.r[j][lane], G.d[j][lane] != 0);
-                } else {
-                    for (int j = 0; j < jn; j++) fwd_step(G.r[j][lane], G.d[j][lane] != 0);
-                }
-            } else {
-                const int tb = T - 1 - st * kG3GS;
-                if (jn == kG3GS) {
-#pragma unroll
-                    for (int j = 0; j < kG3GS; j++) rev_step(G.r[j][lane], G.v[j][lane], G.d[j][lane] != 0, tb - j);
-                } else {
-                    for (int j = 0; j < jn; j++) rev_step(G.r[j][lane], G.v[j][lane], G.d[j][lane] != 0, tb - j);
-                }
-            }
-        }
-        __syncwarp();
+    // ---- load: CR + CR 16-B chunks of r and v per row, one chunk of dones ----
+    for (int x = tid; x < T * (2 * CR + 1); x += 128) {
+        const int t = x / (2 * CR + 1), q = x - t * (2 * CR + 1);
+        const int64_t row = (int64_t)t * B + l0;
+        if (q < CR)
+            g3_cp16(&S.r[t][2 * q], rw + row + 2 * q);
+        else if (q < 2 * CR)
+            g3_cp16(&S.v[t][2 * (q - CR)], val + row + 2 * (q - CR));
+        else if (kG4LW == 16)
+            g3_cp16(&S.d[t][0], dn + row);
+        else
+            g4_cp8(&S.d[t][0], dn + row);
     }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    if (!rev && act) {
+    asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    // ---- pass 1 (warp 0): per_lane_episode_stats forward, beside prep and the scan ----
+    if (warp == 0 && lane < kG4LW) {
+        const int64_t l = l0 + lane;
+        const double g1 = disc ? gamma : 1.0;
+        double acc = 0.0, dsc = 1.0, tot = 0.0, best = 0.0;
+        int cnt = 0, hits = 0;
+        for (int t = 0; t < (prior_final ? 0 : T); t++) {
+            acc = acc + dsc * S.r[t][lane];
+            dsc = dsc * g1;
+            if (S.d[t][lane]) {
+                cnt++;
+                tot = tot + acc;
+                best = np_max(best, acc);
+                hits += acc > 0.0;
+                acc = 0.0;
+            }
+        }
         const double mx = prior_final ? prior[l] : np_max(prior ? prior[l] : 0.0, best);
         S.mx[lane] = mx;
         if (maxret) maxret[l] = mx;
@@ -482,47 +432,65 @@ __global__ void __launch_bounds__(64) k_gae_score3(int T, int64_t B, const doubl
         if (st_mean) st_mean[l] = cnt > 0 ? tot / (double)cnt : 0.0;
         if (st_max) st_max[l] = best;
         if (st_solved) st_solved[l] = cnt > 0 ? (double)hits / (double)cnt : 0.0;
-    }
-    if (!scores) return;
-    __syncthreads();
-    // ---- pass 3 from shared memory: leaves split between the warps ----
-    if (act) {
-        const double mx = S.mx[lane];
-        auto elem = [&](int t) {
-            const double x = S.src[t][lane];
-            return pvl ? np_max(x, 0.0) : mx - x;
-        };
-        int start = 0;
-        for (int li = 0; li < P.n_leaves; li++) {
-            const int end = P.leaf_end[li];
-            if ((li & 1) == warp) {
-                const int len = end - start;
-                double res = 0.0;
-                if (len < 8) {
-                    for (int k = 0; k < len; k++) res = res + elem(start + k);
-                } else {
-                    double r[8];
-#pragma unroll
-                    for (int k = 0; k < 8; k++) r[k] = elem(start + k);
-                    const int l8 = len - len % 8;
-                    for (int k = 8; k < l8; k += 8) {
-#pragma unroll
-                        for (int j = 0; j < 8; j++) r[j] = r[j] + elem(start + k + j);
-                    }
-                    res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-                    for (int k = l8; k < len; k++) res = res + elem(start + k);
-                }
-                S.leaf[li][lane] = res;
+    } else if (warp >= 1) {
+        // ---- prep (warps 1-3): delta_t ----
+        const double g0 = gamma * 0.0;
+        for (int x = tid - 32; x < T * kG4LW; x += 96) {
+            const int t = x / kG4LW, c = x - t * kG4LW;
+            const double nxt = t + 1 < T ? S.v[t + 1][c] : last[l0 + c];
+            const double gk = S.d[t][c] ? g0 : gamma;
+            S.a[t][c] = (S.r[t][c] + gk * nxt) - S.v[t][c];
+        }
+        // warps 1-3 only: pass 1 keeps running in warp 0 meanwhile
+        asm volatile("bar.sync 1, 96;\n" ::: "memory");
+        // ---- pass 2 (warp 1): the reverse scan; A and R = A + V stored as it goes ----
+        if (warp == 1 && lane < kG4LW) {
+            const double gl0 = gl * 0.0;
+            double run = 0.0;
+            double *pa = adv + (int64_t)(T - 1) * B + l0 + lane, *pr = ret + (int64_t)(T - 1) * B + l0 + lane;
+            for (int t = T - 1; t >= 0; t--) {
+                const double glk = S.d[t][lane] ? gl0 : gl;
+                run = S.a[t][lane] + glk * run;  // delta_t, overwritten by A_t
+                S.a[t][lane] = run;
+                *pa = run;
+                *pr = run + S.v[t][lane];
+                pa -= B;
+                pr -= B;
             }
-            start = end;
         }
     }
     __syncthreads();
-    if (warp == 0 && act) {
+    if (!scores) return;
+    // ---- pass 3: pairwise leaves from shared memory, 8 lanes x leaves over the warps ----
+    for (int x = tid; x < P.n_leaves * kG4LW; x += 128) {
+        const int li = x / kG4LW, c = x - li * kG4LW;
+        const int start = li == 0 ? 0 : P.leaf_end[li - 1], end = P.leaf_end[li];
+        const double mx = S.mx[c];
+        auto elem = [&](int t) { return pvl ? np_max(S.a[t][c], 0.0) : mx - S.v[t][c]; };
+        const int len = end - start;
+        double res = 0.0;
+        if (len < 8) {
+            for (int k = 0; k < len; k++) res = res + elem(start + k);
+        } else {
+            double rr[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) rr[k] = elem(start + k);
+            const int l8 = len - len % 8;
+            for (int k = 8; k < l8; k += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) rr[j] = rr[j] + elem(start + k + j);
+            }
+            res = ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
+            for (int k = l8; k < len; k++) res = res + elem(start + k);
+        }
+        S.leaf[li][c] = res;
+    }
+    __syncthreads();
+    if (tid < kG4LW) {
         double stk[16];
         int sp = 0;
         for (int li = 0; li < P.n_leaves; li++) {
-            stk[sp++] = S.leaf[li][lane];
+            stk[sp++] = S.leaf[li][tid];
             for (int k = 0; k < P.adds[li]; k++) {
                 const double b = stk[--sp];
                 const double a = stk[--sp];
@@ -530,7 +498,7 @@ __global__ void __launch_bounds__(64) k_gae_score3(int T, int64_t B, const doubl
             }
         }
         const double sc = stk[0] / (double)T;
-        scores[l] = noclamp ? sc : np_max(sc, 0.0);
+        scores[l0 + tid] = noclamp ? sc : np_max(sc, 0.0);
     }
 }
 
@@ -542,12 +510,22 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
     PairwisePlan P;
     if (make_pairwise_plan(T, P)) return AMZ_ECONFIG;
     const double gl = gamma * lam;  // Python evaluates gamma * lam first (agents/gae.py:35)
-    const bool g3 = do_gae && T <= kG3MaxT && B % kG3LW == 0 && B % 16 == 0 && ((uintptr_t)r & 15u) == 0 &&
+    const bool g3 = do_gae && T <= kG4MaxT && B % 16 == 0 && ((uintptr_t)r & 15u) == 0 &&
                     ((uintptr_t)v & 15u) == 0 && ((uintptr_t)d & 15u) == 0;
+    static const int lw = getenv("AMZ_GAE_LW") ? atoi(getenv("AMZ_GAE_LW")) : 8;
+    if (g3 && lw == 16) {
+        const size_t sm = sizeof(G4Smem<16>);
+        cudaFuncSetAttribute(k_gae_score4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_gae_score4<16><<<(unsigned)(B / 16), 128, sm, s>>>(
+            T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
+            stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
+            stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
+        return 0;
+    }
     if (g3) {
-        const size_t sm = sizeof(G3Smem);
-        cudaFuncSetAttribute(k_gae_score3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_gae_score3<<<(unsigned)(B / kG3LW), 64, sm, s>>>(
+        const size_t sm = sizeof(G4Smem<8>);
+        cudaFuncSetAttribute(k_gae_score4<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_gae_score4<8><<<(unsigned)(B / 8), 128, sm, s>>>(
             T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
             stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
             stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
