@@ -586,74 +586,84 @@ __global__ void __launch_bounds__(128) k_spec_levels(Geo G, EnvDev E, int T, amz
 // ---------------------------------------------------------------------------------
 // phase 2: observations
 // ---------------------------------------------------------------------------------
-// One launch renders the T*B step observations (CTAs [0, g1)) and the B final
-// observations (CTAs [g1, g1 + ceil(B/128))).
+// One persistent launch renders the T*B step observations (tiles [0, g1)) and the B
+// final observations (tiles [g1, g1 + ceil(B/128))), 128 observations per tile.  A CTA
+// loops over tiles with two staging buffers: the bulk store of one tile drains while the
+// next tile renders, and the spread table is built once per CTA.
 template <int V, bool SEE>
 __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, const uint32_t *__restrict__ poses,
                                                 const uint32_t *__restrict__ final_pose,
                                                 const uint32_t *__restrict__ epochs, uint8_t *__restrict__ view,
                                                 uint8_t *__restrict__ dirs, double *__restrict__ reward,
                                                 uint8_t *__restrict__ done, uint8_t *__restrict__ fview,
-                                                uint8_t *__restrict__ fdir, int bulk_ok, int64_t g1) {
+                                                uint8_t *__restrict__ fdir, int bulk_ok, int64_t g1, int64_t ntiles) {
     constexpr int VV = V * V;
-    __shared__ __align__(128) uint8_t s_view[128 * VV];
-    __shared__ __align__(16) uint8_t s_dir[128];
-    __shared__ __align__(16) uint8_t s_done[128];
+    __shared__ __align__(128) uint8_t s_view[2][128 * VV];
+    __shared__ __align__(16) uint8_t s_dir[2][128];
+    __shared__ __align__(16) uint8_t s_done[2][128];
     __shared__ uint64_t s_spread[32];
     __shared__ int64_t s_t0;
-    const bool fin = (int64_t)blockIdx.x >= g1;
-    const int64_t base = (fin ? (int64_t)blockIdx.x - g1 : (int64_t)blockIdx.x) * 128;
-    const int64_t cnt = fin ? B : n;
     init_spread(s_spread);
-    if (threadIdx.x == 0) s_t0 = fin ? 0 : base / B;  // one 64-bit division per CTA
-    __syncthreads();
-    uint8_t *vout = fin ? fview : view;
-    uint8_t *dout = fin ? fdir : dirs;
-    uint8_t *nout = fin ? nullptr : done;
-    const int64_t i = base + threadIdx.x;
-    if (i < cnt) {
-        uint32_t pr;
-        int64_t l;
-        if (fin) {
-            l = i;
-            pr = final_pose[l];
-        } else {
-            int64_t t = s_t0;
-            l = i - t * B;
-            while (l >= B) {
-                l -= B;
-                t++;
-            }
-            // quad layout: steps 4q..4q+3 of lane l are the uint4 at (q * B + l)
-            pr = poses[((t >> 2) * B + l) * 4 + (t & 3)];
-        }
-        const uint32_t *rec = epochs + ((size_t)(pr >> 12) * B + l) * kRec;
-        const uint32_t gw = rec[16];
-        const int r = pr & 15, c = (pr >> 4) & 15, d = (pr >> 8) & 3;
-        render_lane<V, SEE, 1>(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, s_spread, s_view + threadIdx.x * VV);
-        s_dir[threadIdx.x] = (uint8_t)d;
-        s_done[threadIdx.x] = (uint8_t)((pr >> 11) & 1u);
-        if (!fin && reward && !((pr >> 10) & 1u)) reward[i] = 0.0;
-    }
-    const int nvalid = (int)((cnt - base) < 128 ? (cnt - base) : 128);
-    if (bulk_ok && nvalid == 128) {
-        fence_proxy_async();
-        __syncthreads();
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        const int buf = it & 1;
+        const bool fin = tile >= g1;
+        const int64_t base = (fin ? tile - g1 : tile) * 128;
+        const int64_t cnt = fin ? B : n;
         if (threadIdx.x == 0) {
-            bulk_store(vout + base * VV, s_view, 128 * VV);
-            if (dout) bulk_store(dout + base, s_dir, 128);
-            if (nout) bulk_store(nout + base, s_done, 128);
-            bulk_commit();
-            bulk_wait_all();
+            s_t0 = fin ? 0 : base / B;  // one 64-bit division per tile
+            if (bulk_ok) bulk_wait_read<1>();  // this buffer's previous bulk store has been read
         }
-    } else {
         __syncthreads();
-        for (int x = threadIdx.x; x < nvalid * VV; x += 128) vout[base * VV + x] = s_view[x];
-        if (threadIdx.x < nvalid) {
-            if (dout) dout[base + threadIdx.x] = s_dir[threadIdx.x];
-            if (nout) nout[base + threadIdx.x] = s_done[threadIdx.x];
+        uint8_t *vout = fin ? fview : view;
+        uint8_t *dout = fin ? fdir : dirs;
+        uint8_t *nout = fin ? nullptr : done;
+        const int64_t i = base + threadIdx.x;
+        if (i < cnt) {
+            uint32_t pr;
+            int64_t l;
+            if (fin) {
+                l = i;
+                pr = final_pose[l];
+            } else {
+                int64_t t = s_t0;
+                l = i - t * B;
+                while (l >= B) {
+                    l -= B;
+                    t++;
+                }
+                // quad layout: steps 4q..4q+3 of lane l are the uint4 at (q * B + l)
+                pr = poses[((t >> 2) * B + l) * 4 + (t & 3)];
+            }
+            const uint32_t *rec = epochs + ((size_t)(pr >> 12) * B + l) * kRec;
+            const uint32_t gw = rec[16];
+            const int r = pr & 15, c = (pr >> 4) & 15, d = (pr >> 8) & 3;
+            render_lane<V, SEE, 1>(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, s_spread,
+                                   s_view[buf] + threadIdx.x * VV);
+            s_dir[buf][threadIdx.x] = (uint8_t)d;
+            s_done[buf][threadIdx.x] = (uint8_t)((pr >> 11) & 1u);
+            if (!fin && reward && !((pr >> 10) & 1u)) reward[i] = 0.0;
+        }
+        const int nvalid = (int)((cnt - base) < 128 ? (cnt - base) : 128);
+        if (bulk_ok && nvalid == 128) {
+            fence_proxy_async();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                bulk_store(vout + base * VV, s_view[buf], 128 * VV);
+                if (dout) bulk_store(dout + base, s_dir[buf], 128);
+                if (nout) bulk_store(nout + base, s_done[buf], 128);
+                bulk_commit();
+            }
+        } else {
+            __syncthreads();
+            for (int x = threadIdx.x; x < nvalid * VV; x += 128) vout[base * VV + x] = s_view[buf][x];
+            if (threadIdx.x < nvalid) {
+                if (dout) dout[base + threadIdx.x] = s_dir[buf][threadIdx.x];
+                if (nout) nout[base + threadIdx.x] = s_done[buf][threadIdx.x];
+            }
         }
     }
+    if (threadIdx.x == 0 && bulk_ok) bulk_wait_all();
 }
 
 template <int LPW, int WPC>
@@ -678,9 +688,10 @@ static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *po
                           uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
     auto al16 = [](const void *p) { return p == nullptr || (((uintptr_t)p) & 15u) == 0; };
     const int bulk = al16(view) && al16(dirs) && al16(done) && al16(fview) && al16(fdir);
-    const int64_t g1 = (n + 127) / 128, g2 = fview ? (B + 127) / 128 : 0;
-    k_render<V, SEE><<<(unsigned)(g1 + g2), 128, 0, s>>>(G, B, n, poses, final_pose, epochs, view, dirs, reward, done,
-                                                         fview, fdir, bulk, g1);
+    const int64_t g1 = (n + 127) / 128, g2 = fview ? (B + 127) / 128 : 0, nt = g1 + g2;
+    const int64_t grid = nt < 148 * 12 ? nt : 148 * 12;
+    k_render<V, SEE><<<(unsigned)grid, 128, 0, s>>>(G, B, n, poses, final_pose, epochs, view, dirs, reward, done, fview,
+                                                    fdir, bulk, g1, nt);
 }
 
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
