@@ -405,10 +405,15 @@ def measure_plr(dev, n_per_gpu, T, accel, iters, flush, world):
         plr.iteration(it, acts, vals, last)
     torch.cuda.synchronize()
     ms = _timed(lambda i: plr.iteration(3 + i, acts, vals, last), iters, flush, torch)
-    # the two buffer kernels on their own (latency-bound single-CTA kernels)
-    rec_lv = plr.buffer.export()["levels"][:1].repeat(8192, 1)
-    sc = torch.rand(8192, device=dev, dtype=torch.float64)
-    t_upd = _timed(lambda i: plr.buffer.update(rec_lv, sc, sc, 1000 + i), iters, flush, torch)
+    # the two buffer kernels on their own (latency-bound single-CTA kernels): an update
+    # with 4096 distinct new levels (scores U(0,1): most evict -- the worst case) and one
+    # with 4096 replays of buffered levels (in-place updates)
+    new_lv = amz.sample_levels(amz.RngStream(99, (0,)), 4096, amz.StaticParams(), device=dev)
+    sc = torch.rand(4096, device=dev, dtype=torch.float64)
+    old_lv = plr.buffer.export()["levels"][:4000]
+    sc2 = torch.rand(4000, device=dev, dtype=torch.float64)
+    t_upd = _timed(lambda i: plr.buffer.update(new_lv, sc, sc, 1000 + i), iters, flush, torch)
+    t_rep = _timed(lambda i: plr.buffer.update(old_lv, sc2, sc2, 1000 + i), iters, flush, torch)
     t_smp = _timed(lambda i: plr.buffer.sample(amz.RngStream(5, (i,)), n_per_gpu * world, 2000 + i), iters, flush,
                    torch)
     t = torch.tensor([statistics.mean(ms)], dtype=torch.float64, device=dev)
@@ -419,7 +424,8 @@ def measure_plr(dev, n_per_gpu, T, accel, iters, flush, world):
     return {"config": "configs[3] ACCEL-parallel" if accel else "configs[2] PLR-parallel",
             "lanes_global": lanes, "T": T, "buffer_size": 4000, "iteration_ms": it_ms,
             "levels_scored_per_s": lanes / (it_ms * 1e-3), "env_steps_per_s": lanes * T / (it_ms * 1e-3),
-            "buffer_update_us_8192_candidates": 1e3 * statistics.mean(t_upd),
+            "buffer_update_us_4096_new_levels": 1e3 * statistics.mean(t_upd),
+            "buffer_update_us_4000_replays": 1e3 * statistics.mean(t_rep),
             "buffer_sample_us": 1e3 * statistics.mean(t_smp)}
 
 
