@@ -251,7 +251,8 @@ struct DynSmem {
     uint32_t board[16][LPW];
     uint8_t mt[LPW][5][256];  // move table: position after a step, [heading or 4 = no move][pos]
     uint8_t act[2][ACH][LPW];
-    uint32_t aw[LPW][ACH / 4];  // this chunk's actions per lane, 4 steps per word
+    uint32_t aw[LPW][ACH / 4 + 2];  // this chunk's actions per lane, 4 steps per word (+2 zero pad)
+    uint32_t rec[LPW][ACH];         // this chunk's step records per lane
     WarpSampler samp;
 };
 
@@ -357,22 +358,9 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
     const int tep = live ? G.tep : 0x7FFFFFFF;
     uint4 *pq = reinterpret_cast<uint4 *>(poses) + l;  // steps 4q..4q+3 of lane l at pq[q * B]
 
-    // one step; returns its record: pose before the step, reached (bit 10), done (bit 11)
-    auto step = [&](int t, uint32_t a) -> uint32_t {
-        const uint32_t ua = a < 3u ? a : 3u;
-        const uint32_t d = ((ps >> 8) + ((0x13u >> (4u * ua)) & 0xFu)) & 3u;
-        // heading -> (dr + 16 dc + 17): N 0x10, E 0x21, S 0x12, W 0x01
-        const uint32_t mv = ua == 2u ? ((0x01122110u >> (8u * d)) & 0xFFu) - 17u : 0u;
-        const uint32_t nps = ps + mv;
-        const uint32_t word = bd[(nps & 15u) * LPW];
-        const bool blocked = (word >> ((nps >> 4) & 15u)) & 1u;
-        const uint32_t before = ps;
-        ps = ((blocked ? ps : nps) & ~0x300u) | (d << 8);
-        time++;
-        const bool reached = ((ps ^ g) & 0xFFu) == 0u;
-        const bool dn = reached || time >= tep;
-        // only goal steps carry a reward; k_render writes the zeros of all other steps
-        if (reached) reward[(int64_t)t * B + l] = use_lut ? s_rew[time] : goal_reward(time, G.tep);
+    // Episode ends at step t of the lanes with dn: RESAMPLE levels (prepared timeout level
+    // or the warp-cooperative sampler), board + move table, epoch record, reset.
+    auto episode_end = [&](int t, bool dn) {
         const unsigned fin = __ballot_sync(0xFFFFFFFFu, dn);
         if (fin) {
             DYN_T0(c_evt);
@@ -430,7 +418,6 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             }
             DYN_ACC(4, c_evt);
         }
-        return before | ((uint32_t)reached << 10) | ((uint32_t)dn << 11);
     };
 
     DYN_MARK(1);
@@ -438,14 +425,9 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
         fetch_actions<LPW>(S.act[((t0 / ACH) + 1) & 1], actions, B, lane0, nv, t0 + ACH, T, lane, vec);
         cp_wait<1>();
         __syncwarp();
-        const uint8_t *ac = ap + ((t0 / ACH) & 1) * ACH * LPW;
         const int tn = (T - t0) < ACH ? (T - t0) : ACH;
-        // Speculative 8-step batches: the position chain alone (the heading chain runs
-        // beside it on the actions; a move is one move-table byte load), no per-step vote.  When any lane of the warp reaches its goal or times
-        // out inside a batch, the next quad runs through the exact per-step path (the
-        // only inlined copy of the reset / resample code) and speculation resumes after.
         {
-            // lane-major copy of the chunk's actions (4 steps per word) for the batches
+            // lane-major copy of the chunk's actions (4 steps per word)
             const int me = lane < LPW ? lane : 0;
             const uint32_t *row = reinterpret_cast<const uint32_t *>(&S.act[(t0 / ACH) & 1][0][0]) + (me >> 2);
             const uint32_t sel = (uint32_t)(me & 3) | ((uint32_t)(4 + (me & 3)) << 4);
@@ -456,66 +438,79 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                     const uint32_t hi = __byte_perm(row[(4 * q + 2) * (LPW / 4)], row[(4 * q + 3) * (LPW / 4)], sel);
                     S.aw[me][q] = __byte_perm(lo, hi, 0x5410);
                 }
+                S.aw[me][ACH / 4] = S.aw[me][ACH / 4 + 1] = 0u;
             }
             __syncwarp();
         }
+        // Speculative batches of up to 8 steps: the position chain alone (heading by byte
+        // prefix sums of the SWAR-decoded actions, a move = one move-table byte load).  The
+        // warp keeps the steps up to the first episode end of any of its lanes (exact for
+        // every lane), handles that end, and continues from the next step -- nothing is
+        // recomputed.
         int j = 0;
         while (j < tn) {
-            if (j + 8 <= tn) {
-                // SWAR decode of the batch's 8 actions (4 per word): turn deltas, forward
-                // flags, headings by a byte prefix sum; then the position chain alone,
-                // one move-table byte load per step.
-                uint32_t pos = ps & 0xFFu;
-                const uint32_t hi = ps & 0xFFFFF000u;
-                const uint32_t *awl = &S.aw[lane < LPW ? lane : 0][j >> 2];  // j is a multiple of 4, not 8
-                const uint2 A = make_uint2(awl[0], awl[1]);
-                uint32_t d = (ps >> 8) & 3u;
-                uint32_t ew[2], dw[2];
+            const int n = (tn - j) < 8 ? (tn - j) : 8;
+            const int me = lane < LPW ? lane : 0;
+            const uint32_t *awl = &S.aw[me][j >> 2];
+            const int sh = 8 * (j & 3);
+            const uint32_t a0 = __funnelshift_r(awl[0], awl[1], sh), a1 = __funnelshift_r(awl[1], awl[2], sh);
+            uint32_t pos = ps & 0xFFu, d = (ps >> 8) & 3u;
+            const uint32_t hi = ps & 0xFFFFF000u;
+            uint32_t ew[2], dw[2];
 #pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const uint32_t a = h ? A.y : A.x;
-                    const uint32_t left = __vcmpeq4(a, 0u), right = __vcmpeq4(a, 0x01010101u);
-                    const uint32_t fwd = __vcmpeq4(a, 0x02020202u);
-                    const uint32_t turn = (left & 0x03030303u) | (right & 0x01010101u);
-                    const uint32_t da = (turn * 0x01010101u + d * 0x01010101u) & 0x03030303u;  // after
-                    dw[h] = (da << 8) | d;                                                     // before
-                    ew[h] = (da & fwd) | (0x04040404u & ~fwd);
-                    d = da >> 24;
-                }
-                bool hit = time + 8 >= tep;
-                uint32_t rec[8];
+            for (int h = 0; h < 2; h++) {
+                const uint32_t a = h ? a1 : a0;
+                const uint32_t left = __vcmpeq4(a, 0u), right = __vcmpeq4(a, 0x01010101u);
+                const uint32_t fwd = __vcmpeq4(a, 0x02020202u);
+                const uint32_t turn = (left & 0x03030303u) | (right & 0x01010101u);
+                const uint32_t da = (turn * 0x01010101u + d * 0x01010101u) & 0x03030303u;  // after
+                dw[h] = (da << 8) | d;                                                     // before
+                ew[h] = (da & fwd) | (0x04040404u & ~fwd);
+                d = da >> 24;
+            }
+            uint32_t rec[8], pk[8];
+            unsigned ev = (time + n >= tep) ? (1u << (tep - time - 1)) : 0u;  // timeout step, if inside
 #pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    const uint32_t e = (ew[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-                    const uint32_t db = (dw[k >> 2] >> (8 * (k & 3))) & 0x3u;
-                    rec[k] = pos | (db << 8) | hi;
-                    pos = mtl[e * 256u + pos];
-                    hit |= pos == g;
-                }
-                if (!__any_sync(0xFFFFFFFFu, hit)) {
-                    ps = pos | (d << 8) | hi;
-                    time += 8;
-                    if (live) {
-                        pq[(size_t)((t0 + j) >> 2) * B] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
-                        pq[(size_t)((t0 + j + 4) >> 2) * B] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
-                    }
-                    j += 8;
-                    continue;
-                }
+            for (int k = 0; k < 8; k++) {
+                const uint32_t e = (ew[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+                const uint32_t db = (dw[k >> 2] >> (8 * (k & 3))) & 0x3u;
+                rec[k] = pos | (db << 8) | hi;
+                pos = mtl[e * 256u + pos];
+                pk[k] = pos;
+                ev |= (unsigned)(pos == g) << k;
             }
-            uint32_t r0 = 0u, r1 = 0u, r2 = 0u, r3 = 0u;
-            const int kn = (tn - j) < 4 ? (tn - j) : 4;
-#pragma unroll 1
-            for (int k = 0; k < kn; k++) {
-                const uint32_t v = step(t0 + j + k, ac[(j + k) * LPW]);
-                r0 = k == 0 ? v : r0;
-                r1 = k == 1 ? v : r1;
-                r2 = k == 2 ? v : r2;
-                r3 = k == 3 ? v : r3;
+            ev &= (1u << n) - 1u;
+            const unsigned kl = ev ? (unsigned)(__ffs(ev) - 1) : 8u;
+            const unsigned km = __reduce_min_sync(0xFFFFFFFFu, kl);
+            const int cnt = km < (unsigned)n ? (int)km + 1 : n;
+            const bool dn = kl == km && km < (unsigned)n;
+            const bool reached = dn && pk[km] == g;
+            if (lane < LPW) {
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    if (k < cnt)
+                        S.rec[me][j + k] = rec[k] | (dn && k == (int)km ? ((uint32_t)reached << 10) | (1u << 11) : 0u);
             }
-            if (live) pq[(size_t)((t0 + j) >> 2) * B] = make_uint4(r0, r1, r2, r3);
-            j += 4;
+            const uint32_t pe = pk[cnt - 1];
+            const uint32_t de = cnt == 8 ? d : ((dw[cnt >> 2] >> (8 * (cnt & 3))) & 3u);
+            ps = pe | (de << 8) | hi;
+            time += cnt;
+            j += cnt;
+            if (km < (unsigned)n) {
+                const int t = t0 + j - 1;
+                if (reached && live) reward[(int64_t)t * B + l] = use_lut ? s_rew[time] : goal_reward(time, G.tep);
+                episode_end(t, dn);
+            }
         }
+        // the chunk's records: quads of lane L at pq[(t0 / 4 + q) * B]
+        __syncwarp();
+        for (int x = lane; x < nv * (ACH / 4); x += 32) {
+            const int qq = x / (ACH / 4), cq = x - qq * (ACH / 4);
+            if (4 * cq < tn)
+                reinterpret_cast<uint4 *>(poses)[(size_t)((t0 >> 2) + cq) * B + lane0 + qq] =
+                    *reinterpret_cast<const uint4 *>(&S.rec[qq][4 * cq]);
+        }
+        __syncwarp();
     }
     DYN_MARK(2);
     L.s.r = (int)(ps & 15u);
