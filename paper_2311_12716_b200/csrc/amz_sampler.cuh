@@ -64,7 +64,7 @@ __device__ __forceinline__ void warp_stage_stream(uint64_t k0, uint64_t k1, uint
 struct WarpSampler {
     uint32_t sw[kWNW];   // staged stream words
     uint32_t L[128][4];  // L[q]: bit set of the steps i with j_i == q (128-bit)
-    uint8_t J[128];      // j_i of Fisher-Yates step i (J[0] = 0)
+    __align__(16) uint8_t J[128];  // j_i of Fisher-Yates step i (J[0] = 0)
     uint8_t T[128];      // terminal of the succ chain from i (pointer jumping)
 };
 
@@ -95,6 +95,15 @@ __device__ __forceinline__ int set_next(const WarpSampler &X, int q, int after) 
 //      step after k that drew the same j as k (or to j_k itself if there is none), then
 //      along succ(q) = first step after q that drew q.  The succ chains are collapsed by
 //      pointer jumping.
+#ifdef AMZ_SAMP_PROF
+__device__ long long g_samp_prof[8];
+#define SAMP_T(k_) \
+    do { if ((threadIdx.x & 31) == 0) g_samp_prof[k_] += clock64(); } while (0)
+#else
+#define SAMP_T(k_) \
+    do {           \
+    } while (0)
+#endif
 template <bool kTrack = false>
 __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, const Geo &G, WarpSampler &X, Mask &mask,
                                                   int &ar, int &ac, int &ad, int &gr, int &gc) {
@@ -102,10 +111,13 @@ __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, cons
     const int ni = G.ni;
     if (!kTrack)
         for (int x = lane; x < 128; x += 32) reinterpret_cast<uint4 *>(&X.L[0][0])[x] = make_uint4(0u, 0u, 0u, 0u);
+    SAMP_T(0);
     warp_stage_stream(k0, k1, X.sw);
+    SAMP_T(1);
     const WarpStream S{X.sw, k0, k1};
     uint32_t p = 0;
     const uint32_t nw = S.below(p, (uint32_t)G.budget + 1u);
+    SAMP_T(2);
     // ---- 1. j_i ----
     const unsigned lt = (1u << lane) - 1u;
     int i = ni - 1;
@@ -133,6 +145,7 @@ __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, cons
     }
     if (lane == 0) X.J[0] = 0;
     __syncwarp();
+    SAMP_T(3);
     if (kTrack) {
         // ---- 2. final positions of this lane's elements ----
         int q0 = lane, q1 = lane + 32, q2 = lane + 64, q3 = lane + 96;
@@ -144,6 +157,7 @@ __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, cons
             q2 = q2 == i ? j : (q2 == j ? i : q2);
             q3 = q3 == i ? j : (q3 == j ? i : q3);
         }
+        SAMP_T(4);
         mask.w[0] = __ballot_sync(0xFFFFFFFFu, lane < ni && q0 < (int)nw);
         mask.w[1] = __ballot_sync(0xFFFFFFFFu, lane + 32 < ni && q1 < (int)nw);
         mask.w[2] = __ballot_sync(0xFFFFFFFFu, lane + 64 < ni && q2 < (int)nw);
@@ -167,6 +181,7 @@ __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, cons
         gc = goal % G.iw + 1;
         ar = agent / G.iw + 1;
         ac = agent % G.iw + 1;
+        SAMP_T(5);
     } else {
         // ---- 2. final positions ----
         for (int k = lane; k < ni; k += 32) atomicOr(&X.L[X.J[k]][k >> 5], 1u << (k & 31));
