@@ -182,35 +182,6 @@ __device__ __forceinline__ int load_action(const void *a, int dtype, int64_t i) 
     return (v < 0 || v > 2) ? 3 : (int)v;
 }
 
-// Fresh episode for a finished lane: RESAMPLE draws key wrap ++ [step, global lane];
-// HOME restarts the lane's own level (env/wrappers.py:64-71).
-__device__ __forceinline__ void lane_autoreset(const Geo &G, int mode, const amz_seed_t &wrap, uint32_t step,
-                                               uint32_t glane, LaneRec &L, Mask &m, uint8_t *perm, int pstride,
-                                               uint32_t *board, int bstride, bool &new_level) {
-    new_level = false;
-    if (mode == AMZ_RESET_RESAMPLE) {
-        amz_seed_t s = wrap;
-        seed_absorb(s, step);
-        seed_absorb(s, glane);
-        Stream g;
-        g.init(s);
-        int ar, ac, ad, gr, gc;
-        sample_level_dev(g, G, perm, pstride, m, ar, ac, ad, gr, gc);
-        build_board(m, G, board, bstride);
-        L.hr = ar;
-        L.hc = ac;
-        L.hd = ad;
-        L.gr = gr;
-        L.gc = gc;
-        new_level = true;
-    }
-    L.s.r = L.hr;
-    L.s.c = L.hc;
-    L.s.d = L.hd;
-    L.s.time = 0;
-    L.term = false;
-}
-
 template <int V>
 __global__ void __launch_bounds__(128) k_env_step(Geo G, EnvDev E, const void *__restrict__ actions, int adtype,
                                                   int mode, amz_seed_t wrap, uint32_t step_base,

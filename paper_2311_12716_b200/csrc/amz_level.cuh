@@ -81,32 +81,6 @@ __device__ __forceinline__ int mask_select(const Mask &m, uint32_t k) {
     return -1;
 }
 
-// sample_random_level (amaze/generator.py:36-52).  `perm` is this thread's ni-byte
-// scratch with element stride `stride` (a shared-memory column).
-__device__ __forceinline__ void sample_level_dev(Stream &g, const Geo &G, uint8_t *perm, int stride,
-                                                 Mask &mask, int &ar, int &ac, int &ad, int &gr, int &gc) {
-    const uint32_t nw = g.below((uint32_t)G.budget + 1u);
-    for (int i = 0; i < G.ni; i++) perm[i * stride] = (uint8_t)i;
-    for (int i = G.ni - 1; i >= 1; i--) {
-        uint32_t j = g.interval((uint32_t)i);
-        uint8_t a = perm[i * stride], b = perm[j * stride];
-        perm[i * stride] = b;
-        perm[j * stride] = a;
-    }
-    mask.w[0] = mask.w[1] = mask.w[2] = mask.w[3] = 0u;
-    for (uint32_t k = 0; k < nw; k++) mask_set(mask, perm[k * stride], 1u);
-    const uint32_t nfree = (uint32_t)G.ni - nw;
-    const uint32_t gk = g.below(nfree);
-    const int goal = perm[(nw + gk) * stride];
-    const uint32_t ak = g.below(nfree - 1u);
-    const int agent = perm[(nw + (ak < gk ? ak : ak + 1u)) * stride];
-    ad = (int)g.below(4u);
-    gr = goal / G.iw + 1;
-    gc = goal % G.iw + 1;
-    ar = agent / G.iw + 1;
-    ac = agent % G.iw + 1;
-}
-
 // mutate_level (amaze/generator.py:55-84): goal relocation w.p. 0.05 to the k-th
 // row-major non-wall non-agent interior cell, else toggle the k-th row-major interior
 // cell other than agent and goal.

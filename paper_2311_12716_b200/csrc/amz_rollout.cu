@@ -142,24 +142,6 @@ __device__ __forceinline__ void init_spread(uint64_t *spread) {
     }
 }
 
-// rows vr = k, k+G, ... of one lane's observation (G threads per lane); see-through only
-template <int V, int G, int BS>
-__device__ __forceinline__ void render_rows_see(int r, int c, int d, int gr, int gc, int H, int W,
-                                                const uint32_t *board, const uint64_t *spread, int k, uint8_t *out) {
-    constexpr int h = V / 2;
-    const int fr = dir_dr(d), fc = dir_dc(d);
-    const int dr = gr - r, dcol = gc - c;
-    const int g_ahead = dr * fr + dcol * fc;
-    const int g_side = dr * fc - dcol * fr;
-    const bool g_vis = g_ahead >= 0 && g_ahead < V && g_side >= -h && g_side <= h;
-    const int g_vr = V - 1 - g_ahead, g_vc = g_side + h;
-    for (int vr = k; vr < V; vr += G) {
-        uint32_t wall, inb;
-        row_bits<V, BS>(r, c, d, H, W, board, vr, wall, inb);
-        emit_row<V>(wall, inb, g_vis && g_vr == vr, g_vc, spread, out + vr * V);
-    }
-}
-
 // observe_batch + apply_occlusion (amaze/env.py:111-137, 352-364) for one lane
 template <int V, bool SEE, int BS = 32>
 __device__ __forceinline__ void render_lane(int r, int c, int d, int gr, int gc, int H, int W, const uint32_t *board,
@@ -305,7 +287,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                                                   const uint32_t *__restrict__ spec_step, int avec, int use_lut) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    static_assert(LPW % 4 == 0 && LPW <= 32, "lane-major action gather needs LPW a multiple of 4");
+    static_assert((LPW % 4 == 0 || LPW == 2) && LPW <= 32, "lane-major action gather: LPW 2 or a multiple of 4");
     DynSmem<LPW> &S = reinterpret_cast<DynSmem<LPW> *>(smem)[warp];
     // goal rewards R[time] = 1 - 0.9*time/T_ep (numpy's op order), tabulated per CTA
     double *s_rew = reinterpret_cast<double *>(smem + WPC * sizeof(DynSmem<LPW>));
@@ -432,11 +414,19 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             const uint32_t *row = reinterpret_cast<const uint32_t *>(&S.act[(t0 / ACH) & 1][0][0]) + (me >> 2);
             const uint32_t sel = (uint32_t)(me & 3) | ((uint32_t)(4 + (me & 3)) << 4);
             if (lane < LPW) {
+                if (LPW % 4 == 0) {
 #pragma unroll
-                for (int q = 0; q < ACH / 4; q++) {
-                    const uint32_t lo = __byte_perm(row[(4 * q) * (LPW / 4)], row[(4 * q + 1) * (LPW / 4)], sel);
-                    const uint32_t hi = __byte_perm(row[(4 * q + 2) * (LPW / 4)], row[(4 * q + 3) * (LPW / 4)], sel);
-                    S.aw[me][q] = __byte_perm(lo, hi, 0x5410);
+                    for (int q = 0; q < ACH / 4; q++) {
+                        const uint32_t lo = __byte_perm(row[(4 * q) * (LPW / 4)], row[(4 * q + 1) * (LPW / 4)], sel);
+                        const uint32_t hi = __byte_perm(row[(4 * q + 2) * (LPW / 4)], row[(4 * q + 3) * (LPW / 4)], sel);
+                        S.aw[me][q] = __byte_perm(lo, hi, 0x5410);
+                    }
+                } else {
+                    const uint8_t *ab = &S.act[(t0 / ACH) & 1][0][me];
+#pragma unroll
+                    for (int q = 0; q < ACH / 4; q++)
+                        S.aw[me][q] = (uint32_t)ab[(4 * q) * LPW] | ((uint32_t)ab[(4 * q + 1) * LPW] << 8) |
+                                      ((uint32_t)ab[(4 * q + 2) * LPW] << 16) | ((uint32_t)ab[(4 * q + 3) * LPW] << 24);
                 }
                 S.aw[me][ACH / 4] = S.aw[me][ACH / 4 + 1] = 0u;
             }
@@ -698,7 +688,9 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
     // every resample of any of its lanes, so small warps finish sooner.  AMZ_DYN_LPW
     // (4, 8, 16) overrides the choice for tuning runs (tools/dyn_lpw.sh).
     static const int forced = getenv("AMZ_DYN_LPW") ? atoi(getenv("AMZ_DYN_LPW")) : 0;
-    if (forced == 8)
+    if (forced == 2)
+        launch_dyn<2, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+    else if (forced == 8)
         launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
     else if (forced == 16)
         launch_dyn<16, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);

@@ -9,7 +9,6 @@
 //   * the Fisher-Yates of permutation(ni) (masked rejection per step) is resolved 32
 //     stream words at a time, and the permuted array is read off the transpositions
 //     without replaying them (see warp_sample_level).
-// A staged SIMT variant (one level per lane, sequential Fisher-Yates) follows.
 #pragma once
 #include <stdint.h>
 
@@ -259,130 +258,6 @@ __device__ __forceinline__ void warp_sample_each(unsigned need, uint64_t k0, uin
             gc = h0;
         }
     }
-}
-
-}  // namespace amz
-
-namespace amz {
-
-// ---------------------------------------------------------------------------------
-// Staged SIMT sampler: every lane whose bit is set in `need` samples its OWN level.
-// The whole warp first computes the Philox blocks of all requesting lanes round-robin
-// (block b of requesting lane L is one work item) into per-lane word columns of `sw`
-// ([kSNW][LPW], word q of lane L at q*LPW + L); then each requesting lane runs the
-// sequential Fisher-Yates over its staged words, continuing with inline blocks in the
-// rare case the level needs more than kSNB blocks.  Cost per batch of W levels:
-// ceil(28W/32) Philox blocks per thread + one Fisher-Yates (SIMT over the W lanes).
-// ---------------------------------------------------------------------------------
-constexpr int kSNB = 24;
-constexpr int kSNW = kSNB * 8;
-
-struct LaneStream {
-    const uint32_t *w;
-    int stride;
-    uint32_t p;
-    uint64_t k0, k1;
-    uint64_t cb;
-    uint64_t c0, c1, c2, c3;
-
-    __device__ __forceinline__ uint32_t next32() {
-        if (p < (uint32_t)kSNW) return w[(p++) * stride];
-        const uint64_t blk = p >> 3;
-        if (cb != blk + 1) {
-            philox_block(blk + 1, k0, k1, c0, c1, c2, c3);
-            cb = blk + 1;
-        }
-        const uint32_t j = (p & 7u) >> 1;
-        const uint64_t v = j == 0 ? c0 : j == 1 ? c1 : j == 2 ? c2 : c3;
-        const bool hi = p & 1u;
-        p++;
-        return hi ? (uint32_t)(v >> 32) : (uint32_t)v;
-    }
-    __device__ __forceinline__ uint32_t below(uint32_t n) {
-        if (n <= 1u) return 0u;
-        uint64_t m = (uint64_t)next32() * n;
-        uint32_t left = (uint32_t)m;
-        if (left < n) {
-            const uint32_t thresh = (0u - n) % n;
-            while (left < thresh) {
-                m = (uint64_t)next32() * n;
-                left = (uint32_t)m;
-            }
-        }
-        return (uint32_t)(m >> 32);
-    }
-    __device__ __forceinline__ uint32_t interval(uint32_t max) {
-        const uint32_t mk = 0xFFFFFFFFu >> __clz(max);
-        uint32_t v;
-        do {
-            v = next32() & mk;
-        } while (v > max);
-        return v;
-    }
-};
-
-// sample_random_level over any 32-bit draw source (amaze/generator.py:36-52);
-// `perm` is this lane's ni-byte column (stride `ps`).
-template <class Src>
-__device__ __forceinline__ void sample_level_seq(Src &g, const Geo &G, uint8_t *perm, int ps, Mask &mask, int &ar,
-                                                 int &ac, int &ad, int &gr, int &gc) {
-    const uint32_t nw = g.below((uint32_t)G.budget + 1u);
-    for (int i = 0; i < G.ni; i++) perm[i * ps] = (uint8_t)i;
-    for (int i = G.ni - 1; i >= 1; i--) {
-        const uint32_t j = g.interval((uint32_t)i);
-        const uint8_t a = perm[i * ps], b = perm[j * ps];
-        perm[i * ps] = b;
-        perm[j * ps] = a;
-    }
-    mask.w[0] = mask.w[1] = mask.w[2] = mask.w[3] = 0u;
-    for (uint32_t k = 0; k < nw; k++) mask_set(mask, perm[k * ps], 1u);
-    const uint32_t nfree = (uint32_t)G.ni - nw;
-    const uint32_t gk = g.below(nfree);
-    const int goal = perm[(nw + gk) * ps];
-    const uint32_t ak = g.below(nfree - 1u);
-    const int agent = perm[(nw + (ak < gk ? ak : ak + 1u)) * ps];
-    ad = (int)g.below(4u);
-    gr = goal / G.iw + 1;
-    gc = goal % G.iw + 1;
-    ar = agent / G.iw + 1;
-    ac = agent % G.iw + 1;
-}
-
-// All 32 lanes of the warp call this (uniform `need`); lanes with their bit set get a
-// level for their own key (k0, k1).  skey: [LPW] x 2 u64 scratch.
-template <int LPW>
-__device__ __forceinline__ void warp_sample_batch(unsigned need, uint64_t k0, uint64_t k1, const Geo &G,
-                                                  uint32_t *sw, uint8_t *perm, uint64_t *skey, Mask &mask, int &ar,
-                                                  int &ac, int &ad, int &gr, int &gc) {
-    const int lane = threadIdx.x & 31;
-    const bool mine = (need >> lane) & 1u;
-    if (mine) {
-        skey[2 * lane] = k0;
-        skey[2 * lane + 1] = k1;
-    }
-    __syncwarp();
-    const int cnt = __popc(need);
-    for (int x = lane; x < cnt * kSNB; x += 32) {
-        const int idx = x / kSNB, b = x - idx * kSNB;
-        const int L = (int)__fns(need, 0, idx + 1);
-        uint64_t o0, o1, o2, o3;
-        philox_block((uint64_t)b + 1ull, skey[2 * L], skey[2 * L + 1], o0, o1, o2, o3);
-        uint32_t *d = sw + (8 * b) * LPW + L;
-        d[0 * LPW] = (uint32_t)o0;
-        d[1 * LPW] = (uint32_t)(o0 >> 32);
-        d[2 * LPW] = (uint32_t)o1;
-        d[3 * LPW] = (uint32_t)(o1 >> 32);
-        d[4 * LPW] = (uint32_t)o2;
-        d[5 * LPW] = (uint32_t)(o2 >> 32);
-        d[6 * LPW] = (uint32_t)o3;
-        d[7 * LPW] = (uint32_t)(o3 >> 32);
-    }
-    __syncwarp();
-    if (mine) {
-        LaneStream s{sw + lane, LPW, 0u, k0, k1, 0ull, 0ull, 0ull, 0ull, 0ull};
-        sample_level_seq(s, G, perm + lane, LPW, mask, ar, ac, ad, gr, gc);
-    }
-    __syncwarp();
 }
 
 }  // namespace amz
