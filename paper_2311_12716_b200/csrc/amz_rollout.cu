@@ -49,6 +49,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -236,6 +239,7 @@ struct DynSmem {
     uint32_t aw[LPW][ACH / 4 + 2];  // this chunk's actions per lane, 4 steps per word (+2 zero pad)
     uint32_t rec[LPW][ACH];         // this chunk's step records per lane
     WarpSampler samp;
+    __align__(16) amz_level_t spec[LPW];  // the lanes' prepared timeout levels
 };
 
 // Move table of lane L (whole warp): mt[e][pos], pos = r | c << 4, is the position after
@@ -323,7 +327,13 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             rec[w] = v[w];
         }
         rec[16] = (uint32_t)L.gr | ((uint32_t)L.gc << 8);
-        if (mode == AMZ_RESET_RESAMPLE) my_spec = spec_step[l];
+        if (mode == AMZ_RESET_RESAMPLE) {
+            my_spec = spec_step[l];
+            if (my_spec != 0xFFFFFFFFu) {  // in flight with the first action chunk
+                cp_async16(&S.spec[lane], spec + l);
+                cp_async16(reinterpret_cast<uint8_t *>(&S.spec[lane]) + 16, reinterpret_cast<const uint8_t *>(spec + l) + 16);
+            }
+        }
     }
     __syncwarp();
     for (int q = 0; q < nv; q++) build_move_table<LPW>(&S.board[0][0], q, &S.mt[q][0][0]);
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                     if (lane == 0) g_dyn_prof[(int64_t)blockIdx.x * WPC + warp][7] += __popc(need);
 #endif
                 }
-                if (hit) load_level(spec + l, m, ar, acol, ad, gr, gc);
+                if (hit) load_level(&S.spec[lane], m, ar, acol, ad, gr, gc);
                 if (dn) {
                     build_board(m, G, bd, LPW);
                     L.hr = ar;
