@@ -510,9 +510,14 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
     PairwisePlan P;
     if (make_pairwise_plan(T, P)) return AMZ_ECONFIG;
     const double gl = gamma * lam;  // Python evaluates gamma * lam first (agents/gae.py:35)
-    const bool g3 = do_gae && T <= kG4MaxT && B % 16 == 0 && ((uintptr_t)r & 15u) == 0 &&
+    // measured on B200 (T = 256): the whole-column kernel wins up to ~12k lanes (latency),
+    // the two-warp streaming kernel up to ~128k, the one-thread-per-lane kernel beyond
+    const bool g3 = do_gae && T <= kG4MaxT && B <= 12288 && B % 16 == 0 && ((uintptr_t)r & 15u) == 0 &&
                     ((uintptr_t)v & 15u) == 0 && ((uintptr_t)d & 15u) == 0;
     static const int lw = getenv("AMZ_GAE_LW") ? atoi(getenv("AMZ_GAE_LW")) : 8;
+    static const int gsel = getenv("AMZ_GAE_KERNEL") ? atoi(getenv("AMZ_GAE_KERNEL")) : 0;  // tuning runs
+    if (gsel == 2) goto k2;
+    if (gsel == 1) goto k1;
     if (g3 && lw == 16) {
         const size_t sm = sizeof(G4Smem<16>);
         cudaFuncSetAttribute(k_gae_score4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -531,13 +536,15 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
             stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
         return 0;
     }
-    if (B <= 148 * 32 * 8) {
+k2:
+    if (gsel == 2 || B <= 131072) {
         k_gae_score2<<<(unsigned)((B + 31) / 32), 64, 0, s>>>(
             T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
             stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
             stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, do_gae, P);
         return 0;
     }
+k1:
     const int threads = B >= 148 * 64 ? 64 : 32;
     k_gae_score<<<(unsigned)((B + threads - 1) / threads), threads, 0, s>>>(
         T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
