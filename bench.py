@@ -4,8 +4,8 @@
 
 One "step" = one pass of the hot path over one batch of synthetic input (config 2,
 "AMaze 13x13 DR with PPO rollout batch 4096 envs x 256 steps and GAE on 1xB200"):
-  1. DR level generation for every lane (keys (seed, (0, lane))),
-  2. reset_to_levels of every lane,
+  1.+2. DR level generation for every lane (keys (seed, (0, lane))) fused with the reset
+     of every lane (VectorBatchEnv.reset),
   3. 256 fused env steps with RESAMPLE auto-reset driven by a uint8 [T, B] action
      stream resident in HBM (the policy is out of scope; its values are a resident
      float64 [T, B] tensor),
@@ -213,17 +213,16 @@ class Workload:
                     "final_view": torch.empty((B, v, v), dtype=torch.uint8, device=device),
                     "final_dir": torch.empty((B,), dtype=torch.uint8, device=device)}
         self.root = amz.RngStream.from_seed(seed)
-        # our kernels per step: k_sample_levels_w, k_env_reset, k_spec_levels, k_dyn, k_render, k_gae_score3
-        self.launches_per_step = 6
+        # our kernels per step: k_env_reset_dr, k_dyn, k_render, k_gae_score4
+        self.launches_per_step = 4
         self.ev_roll = None
 
     def step(self, it, actions=None, values=None, last=None, timing=None):
         amz, torch = self.amz, self.torch
         rng = self.root.fold_in(it)
-        rng_env, rng_wrap = rng.split(2)
-        levels = amz.sample_levels(rng_env, self.B, self.p, lane0=self.lane_offset, device=self.dev)
-        res = self.benv.reset_to_levels(None, levels, self.p)
-        res = self.env._attach(res, rng_wrap)
+        # DR level generation + reset in one launch; it also prepares the timeout levels of
+        # the rollout's first auto-resets (keys rng_wrap ++ [tep - 1, lane])
+        res = self.env.reset(rng, self.p)
         if timing is not None:
             timing[0].record()
         traj, cur = amz.rollout_actions(self.env, res, self.actions if actions is None else actions, self.p,
@@ -356,7 +355,8 @@ def run_ours(args, rank, world, local_rank):
                      "peak_source": src,
                      "algorithmic_bytes": f"{ENV_BYTES_PER_STEP} B/env-step x {B * T} env-steps per launch",
                      "kernel_ms": roll,
-                     "note": "k_env_rollout = k_spec_levels + k_dyn + k_render; at 4096 lanes the per-lane "
+                     "note": "k_env_rollout = k_dyn + k_render (the timeout levels of the first auto-resets "
+                             "come prepared from the fused reset launch, so no k_spec_levels); at 4096 lanes the per-lane "
                              "256-step dynamics chain (latency) bounds it, not HBM; the HBM point is "
                              "large_batch (65536 lanes)"},
         "kernels": {"k_env_rollout_ms": roll, "k_gae_score_ms": gae, "k_gae_score_GBs": gae_gbs,

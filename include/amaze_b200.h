@@ -169,6 +169,12 @@ int amz_env_set_lane_offset(amz_env_t *env, uint32_t offset);
  * lanes_dev == NULL: all n_lanes lanes, levels_dev[n_lanes];
  * otherwise lanes_dev[n] lane ids with levels_dev[n].  view_dev [n][V][V] u8,
  * dir_dev [n] int64 (either may be NULL). */
+/* VectorBatchEnv.reset fused with DR level generation: lane l plays the level of key
+ * prefix ++ [lane_offset + l] (amaze/generator.py:36-52).  With `wrap` (the auto-reset
+ * wrapper's key) the lanes' timeout levels for the first RESAMPLE rollout (step0 = 0,
+ * same key) are prepared in the same launch.  view/dir may be NULL. */
+int amz_env_reset_dr(amz_env_t *env, const amz_seed_t *prefix, const amz_seed_t *wrap, uint8_t *view_dev,
+                     int64_t *dir_dev, void *stream);
 int amz_env_reset_to_levels(amz_env_t *env, const amz_level_t *levels_dev, const int64_t *lanes_dev,
                             int64_t n, uint8_t *view_dev, int64_t *dir_dev, void *stream);
 

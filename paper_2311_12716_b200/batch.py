@@ -177,10 +177,23 @@ class VectorBatchEnv:
                           self._reshape(zb), info)
 
     # -- reference API ---------------------------------------------------------
-    def reset(self, rng, params) -> StepResult:
+    def reset(self, rng, params, _prepare_wrap: RngStream | None = None) -> StepResult:
+        """Level generation and reset in one launch (lane l plays the level of key
+        rng.key + (lane_offset + l,), as sample_levels + reset_to_levels would).
+        ``_prepare_wrap`` (AutoResetWrapper, RESAMPLE) also prepares the lanes'
+        timeout levels for the first rollout under that wrapper key."""
+        torch = _torch()
         p = as_params(params).validate()
-        levels = sample_levels(as_stream(rng), self.n_lanes, p, lane0=self.lane_offset, device=self.device)
-        return self.reset_to_levels(rng, levels, p)
+        lanes = self._ensure(p)
+        v = p.agent_view_size
+        view = torch.empty((self.n_lanes, v, v), dtype=torch.uint8, device=self.device)
+        dirs = torch.empty((self.n_lanes,), dtype=torch.int64, device=self.device)
+        seed = as_stream(rng).seed_prefix()
+        wseed = _prepare_wrap.seed_prefix() if _prepare_wrap is not None else None
+        _lib.call("amz_env_reset_dr", lanes.handle, ctypes.byref(seed),
+                  ctypes.byref(wseed) if wseed is not None else None, _lib.ptr(view), _lib.ptr(dirs),
+                  lanes.stream())
+        return self._zeros_result({"view": view, "dir": dirs}, lanes)
 
     def reset_to_levels(self, rng, levels, params) -> StepResult:
         torch = _torch()
@@ -276,7 +289,9 @@ class AutoResetWrapper:
 
     def reset(self, rng, params) -> StepResult:
         rng_env, rng_wrap = as_stream(rng).split(2)
-        return self._attach(self.benv.reset(rng_env, params), rng_wrap)
+        prep = rng_wrap if self.mode == RESAMPLE and isinstance(self.benv, VectorBatchEnv) else None
+        res = self.benv.reset(rng_env, params, prep) if prep is not None else self.benv.reset(rng_env, params)
+        return self._attach(res, rng_wrap)
 
     def reset_to_levels(self, rng, levels, params) -> StepResult:
         rng_env, rng_wrap = as_stream(rng).split(2)

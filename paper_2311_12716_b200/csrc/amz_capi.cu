@@ -45,6 +45,10 @@ struct amz_env {
     amz_level_t *spec = nullptr;   // speculative timeout levels [B]
     uint32_t *spec_step = nullptr; // [B]
     int64_t rollout_T = 0;
+    // timeout levels prepared by a fused DR reset for the next RESAMPLE rollout with this
+    // wrapper key starting at step 0 (consumed by that rollout, dropped by anything else)
+    bool spec_ready = false;
+    amz_seed_t spec_wrap{};
 };
 
 struct amz_plr {
@@ -324,12 +328,26 @@ int64_t amz_env_lanes(const amz_env_t *e) { return e ? e->E.B : -1; }
 int amz_env_set_lane_offset(amz_env_t *e, uint32_t offset) {
     if (!e) return fail(AMZ_ECONFIG, "null env");
     e->E.lane_offset = offset;
+    e->spec_ready = false;
     return 0;
+}
+
+int amz_env_reset_dr(amz_env_t *e, const amz_seed_t *prefix, const amz_seed_t *wrap, uint8_t *view, int64_t *dirs,
+                     void *stream) {
+    if (!e || !prefix) return fail(AMZ_ECONFIG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = launch_env_reset_dr(e->G, e->E, *prefix, wrap, e->spec, e->spec_step, view, dirs, s);
+    if (rc) return fail(rc, "reset: unsupported agent_view_size");
+    cudaMemsetAsync(e->term, 0, 2 * sizeof(int), s);
+    e->spec_ready = wrap != nullptr;
+    if (wrap) e->spec_wrap = *wrap;
+    return cuda_status("env_reset_dr");
 }
 
 int amz_env_reset_to_levels(amz_env_t *e, const amz_level_t *lv, const int64_t *lanes, int64_t n, uint8_t *view,
                             int64_t *dirs, void *stream) {
     if (!e || !lv) return fail(AMZ_ECONFIG, "null argument");
+    e->spec_ready = false;
     if (!lanes && n != e->E.B) return fail(AMZ_ESHAPE, "expected %lld levels, got %lld", (long long)e->E.B, (long long)n);
     cudaStream_t s = (cudaStream_t)stream;
     int rc = launch_env_reset(e->G, e->E, lv, lanes, n, view, dirs, s);
@@ -348,6 +366,7 @@ static int env_step_impl(amz_env_t *e, const void *actions, int adtype, int mode
     if (mode == AMZ_RESET_RESAMPLE && !wrap && !wrap_dev) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
     cudaStream_t s = (cudaStream_t)stream;
     amz_seed_t w = wrap ? *wrap : amz_seed_t{};
+    e->spec_ready = false;
     int *tin = e->term + e->parity, *tout = e->term + (e->parity ^ 1);
     if (mode == AMZ_RESET_NONE) {
         cudaMemsetAsync(tout, 0, sizeof(int), s);
@@ -401,8 +420,11 @@ int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const
         }
         e->rollout_T = T;
     }
+    const bool ready = e->spec_ready && mode == AMZ_RESET_RESAMPLE && step0 == 0 &&
+                       memcmp(&e->spec_wrap, &w, sizeof(w)) == 0;
+    e->spec_ready = false;
     int rc = launch_env_rollout(e->G, e->E, T, actions, mode, w, step0, view, dirs, reward, done, fview, fdir,
-                                e->poses, e->epochs, e->final_pose, e->spec, e->spec_step, s);
+                                e->poses, e->epochs, e->final_pose, e->spec, e->spec_step, ready ? 1 : 0, s);
     if (rc) return fail(rc, "rollout: unsupported agent_view_size");
     return cuda_status("env_rollout");
 }
@@ -428,6 +450,7 @@ int amz_env_state(amz_env_t *e, int32_t *out, void *stream) {
 
 int amz_env_set_state(amz_env_t *e, const int32_t *in, void *stream) {
     if (!e || !in) return fail(AMZ_ECONFIG, "null argument");
+    e->spec_ready = false;
     launch_env_set_state(e->E, in, (cudaStream_t)stream);
     return cuda_status("env_set_state");
 }

@@ -113,6 +113,62 @@ __global__ void __launch_bounds__(128) k_env_reset(Geo G, EnvDev E, const amz_le
     }
 }
 
+// Domain-randomised reset fused with level generation (VectorBatchEnv.reset,
+// env/batch.py:86-95 over amaze/generator.py:36-52): one warp per lane samples the
+// level of key prefix ++ [global lane] (warp-cooperative sampler), then writes the lane
+// state, board and observation.  With a wrapper key it also prepares the lane's timeout
+// level for the first RESAMPLE rollout (key wrap ++ [tep - 1, global lane]: a fresh
+// episode times out at step tep - 1), so that rollout needs no k_spec_levels pass.
+template <int V>
+__global__ void __launch_bounds__(128) k_env_reset_dr(Geo G, EnvDev E, amz_seed_t prefix, int prep,
+                                                      amz_seed_t wrap, amz_level_t *__restrict__ spec,
+                                                      uint32_t *__restrict__ spec_step, uint8_t *__restrict__ view,
+                                                      int64_t *__restrict__ dirs) {
+    __shared__ __align__(16) WarpSampler X[4];
+    __shared__ uint8_t stage[4][V * V];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t l = (int64_t)blockIdx.x * 4 + warp;
+    if (l >= E.B) return;
+    const uint32_t gl = E.lane_offset + (uint32_t)l;
+    uint64_t k0, k1;
+    {
+        amz_seed_t sd = prefix;
+        seed_absorb(sd, gl);
+        seed_key(sd, k0, k1);
+    }
+    Mask m;
+    LaneRec L;
+    warp_sample_level(k0, k1, G, X[warp], m, L.s.r, L.s.c, L.s.d, L.gr, L.gc);
+    if (lane == 0) {
+        L.hr = L.s.r;
+        L.hc = L.s.c;
+        L.hd = L.s.d;
+        L.s.time = 0;
+        L.term = false;
+        E.st[l] = pack_st(L);
+        E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+        build_board(m, G, E.board + l, (int)E.B);
+        if (dirs) dirs[l] = L.s.d;
+        if (view) lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, E.board + l, (int)E.B, stage[warp]);
+    }
+    __syncwarp();
+    if (view)
+        for (int j = lane; j < V * V; j += 32) view[l * V * V + j] = stage[warp][j];
+    if (prep) {
+        amz_seed_t sd = wrap;
+        seed_absorb(sd, (uint32_t)(G.tep - 1));
+        seed_absorb(sd, gl);
+        seed_key(sd, k0, k1);
+        Mask ms;
+        int ar, ac, ad, gr, gc;
+        warp_sample_level(k0, k1, G, X[warp], ms, ar, ac, ad, gr, gc);
+        if (lane == 0) {
+            store_level(spec + l, ms, ar, ac, ad, gr, gc);
+            spec_step[l] = (uint32_t)(G.tep - 1);
+        }
+    }
+}
+
 template <int V>
 __global__ void __launch_bounds__(128) k_env_observe(Geo G, EnvDev E, uint8_t *__restrict__ view,
                                                      int64_t *__restrict__ dirs) {
@@ -318,6 +374,16 @@ int launch_env_reset(const Geo &G, const EnvDev &E, const amz_level_t *lv, const
                      uint8_t *view, int64_t *dirs, cudaStream_t s) {
     if (n <= 0) return 0;
     AMZ_DISPATCH_V(G.V, (k_env_reset<VT><<<blocks_for(n, 128), 128, 0, s>>>(G, E, lv, lanes, n, view, dirs)));
+    return 0;
+}
+
+int launch_env_reset_dr(const Geo &G, const EnvDev &E, const amz_seed_t &prefix, const amz_seed_t *wrap,
+                        amz_level_t *spec, uint32_t *spec_step, uint8_t *view, int64_t *dirs, cudaStream_t s) {
+    if (E.B <= 0) return 0;
+    const amz_seed_t w = wrap ? *wrap : amz_seed_t{};
+    const int prep = wrap != nullptr;
+    AMZ_DISPATCH_V(G.V, (k_env_reset_dr<VT><<<(unsigned)((E.B + 3) / 4), 128, 0, s>>>(G, E, prefix, prep, w, spec,
+                                                                                         spec_step, view, dirs)));
     return 0;
 }
 

@@ -41,6 +41,8 @@ int launch_teacher_levels(int64_t B, const uint4 *mask, const uint4 *st, amz_lev
 int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
                        const amz_seed_t *prefix_dev, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
                        uint8_t *act8, double *logp, cudaStream_t s);
+int launch_env_reset_dr(const Geo &G, const EnvDev &E, const amz_seed_t &prefix, const amz_seed_t *wrap,
+                        amz_level_t *spec, uint32_t *spec_step, uint8_t *view, int64_t *dirs, cudaStream_t s);
 int launch_level_metrics(const Geo &G, const amz_level_t *lv, int64_t n, int32_t *n_walls, int32_t *spl,
                          uint8_t *solvable, double *passable, cudaStream_t s);
 int launch_check_levels(const Geo &G, const amz_level_t *lv, int64_t n, unsigned long long *first_bad,
@@ -60,7 +62,8 @@ int launch_env_step(const Geo &G, const EnvDev &E, const void *actions, int adty
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
                        const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
                        uint8_t *done, uint8_t *fview, uint8_t *fdir, uint32_t *poses, uint32_t *epochs,
-                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s);
+                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, int spec_ready,
+                       cudaStream_t s);
 int launch_gae_score(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *last,
                      double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
                      double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,

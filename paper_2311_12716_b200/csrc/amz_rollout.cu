@@ -664,12 +664,12 @@ __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, con
 template <int LPW, int WPC>
 static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode, const amz_seed_t &wrap,
                        uint32_t step0, double *reward, uint8_t *done, uint32_t *poses, uint32_t *epochs,
-                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s) {
+                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, int spec_ready, cudaStream_t s) {
     const int use_lut = G.tep <= 4096;
     const size_t sm = (size_t)WPC * sizeof(DynSmem<LPW>) + (use_lut ? ((size_t)G.tep + 1) * 8 : 0);
     cudaFuncSetAttribute(k_dyn<LPW, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int avec = (E.B % 4 == 0) && ((((uintptr_t)actions) & 3u) == 0);
-    if (mode == AMZ_RESET_RESAMPLE)
+    if (mode == AMZ_RESET_RESAMPLE && !spec_ready)
         k_spec_levels<<<(unsigned)((E.B + 4 * kSpecLPW - 1) / (4 * kSpecLPW)), 128, 0, s>>>(G, E, T, wrap, step0, spec,
                                                                                            spec_step);
     const int64_t warps = (E.B + LPW - 1) / LPW;
@@ -692,24 +692,25 @@ static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *po
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,
                        const amz_seed_t &wrap, uint32_t step0, uint8_t *view, uint8_t *dirs, double *reward,
                        uint8_t *done, uint8_t *fview, uint8_t *fdir, uint32_t *poses, uint32_t *epochs,
-                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, cudaStream_t s) {
+                       uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, int spec_ready,
+                       cudaStream_t s) {
     if (E.B <= 0) return 0;
     // few lanes per warp: the per-lane chain is latency-bound, and a warp stalls for
     // every resample of any of its lanes, so small warps finish sooner.  AMZ_DYN_LPW
     // (4, 8, 16) overrides the choice for tuning runs (tools/dyn_lpw.sh).
     static const int forced = getenv("AMZ_DYN_LPW") ? atoi(getenv("AMZ_DYN_LPW")) : 0;
     if (forced == 2)
-        launch_dyn<2, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+        launch_dyn<2, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, spec_ready, s);
     else if (forced == 8)
-        launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+        launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, spec_ready, s);
     else if (forced == 16)
-        launch_dyn<16, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, s);
+        launch_dyn<16, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, spec_ready, s);
     else if (E.B <= 148 * 8 * 16)
-        launch_dyn<4, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step,
+        launch_dyn<4, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, spec_ready,
                          s);
     else
         launch_dyn<8, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec,
-                         spec_step, s);
+                         spec_step, spec_ready, s);
     const int64_t n = (int64_t)T * E.B;
 #define AMZ_RR(VV_)                                                                                         \
     case VV_:                                                                                               \
