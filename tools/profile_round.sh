@@ -6,7 +6,7 @@ python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${R}_bench_re
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${R}_launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_dyn|k_render|k_gae_score|k_spec|k_sample_levels_w|k_env_reset" \
-    --launch-skip 6 -c 6 -o gpurun_out/${R}_full python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extra > /dev/null 2>&1
+    --launch-skip 8 -c 4 -o gpurun_out/${R}_full python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extra > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_plr_update|k_plr_sample" -c 4 \
     -o gpurun_out/${R}_plr_full python tools/plr_update_micro.py > /dev/null 2>&1
 echo done
