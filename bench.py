@@ -60,6 +60,8 @@ def _peaks():
 # CPU reference (oracle port), lane-sharded over processes
 # ------------------------------------------------------------------------------------
 def _cpu_shard(args):
+    """One lane shard of the config-2 step with the numpy oracle port; returns the wall
+    seconds of each phase (reset, rollout, gae, scores) and the total."""
     lane0, n, T, seed, act_seed, gamma, lam = args
     import numpy as np
 
@@ -67,19 +69,24 @@ def _cpu_shard(args):
 
     p = onp.Params()
     env = onp.AutoReset(n, p, "resample", lane_offset=lane0)
-    t0 = time.perf_counter()
-    obs = env.reset(seed)
     rng = np.random.default_rng(act_seed + lane0)
     acts = rng.integers(0, 3, (T, n)).astype(np.uint8)
     values = rng.uniform(0, 1, (T, n))
+    t0 = time.perf_counter()
+    obs = env.reset(seed)
+    t1 = time.perf_counter()
     view, dirs, rew, dn, fobs = onp.rollout(env, obs, acts)
+    t2 = time.perf_counter()
     adv, ret = onp.gae(rew, values, dn, values[-1], gamma, lam)
+    t3 = time.perf_counter()
     sc, mx, _ = onp.lane_scores(values, adv, rew, dn, np.zeros(n))
-    return time.perf_counter() - t0
+    t4 = time.perf_counter()
+    return {"reset": t1 - t0, "rollout": t2 - t1, "gae": t3 - t2, "scores": t4 - t3, "total": t4 - t0}
 
 
-def cpu_reference_step(B, T, seed, workers, pool):
-    """One full step of the workload on the host: returns wall seconds."""
+def cpu_reference_step(B, T, seed, workers, pool, phases=None):
+    """One full step of the workload on the host: returns wall seconds.  ``phases``
+    (a list) receives the per-phase seconds of the slowest shard."""
     shards = []
     per = (B + workers - 1) // workers
     for w in range(workers):
@@ -89,10 +96,38 @@ def cpu_reference_step(B, T, seed, workers, pool):
             shards.append((lo, n, T, seed, 17, 0.995, 0.95))
     t0 = time.perf_counter()
     if pool is None:
-        for s in shards:
-            _cpu_shard(s)
+        res = [_cpu_shard(s) for s in shards]
     else:
-        pool.map(_cpu_shard, shards)
+        res = pool.map(_cpu_shard, shards)
+    wall = time.perf_counter() - t0
+    if phases is not None:
+        phases.append(max(res, key=lambda r: r["total"]))
+    return wall
+
+
+def _oracle_levels(p, n, seed):
+    from oracle import amaze_np as onp
+
+    return onp.pack_levels([onp.sample_level(seed, (0, i), p) for i in range(n)], p)
+
+
+def cpu_buffer_update_seconds(n_new=4096, K=4000, it=1):
+    """Oracle PLR⊥ buffer update (runners SPEC.md:360-377): n_new DR candidates into a
+    full K-entry buffer, single process (the update is sequential by definition)."""
+    import numpy as np
+
+    from oracle import amaze_np as onp
+    from oracle import plr_np
+
+    p = onp.Params()
+    buf = plr_np.LevelBuffer(K)
+    rs = np.random.default_rng(5)
+    fill = _oracle_levels(p, K, 5)
+    buf.update(fill, rs.uniform(0, 1, K), rs.uniform(0, 1, K), 0)
+    cand = _oracle_levels(p, n_new, 6)
+    sc, mr = rs.uniform(0, 1, n_new), rs.uniform(0, 1, n_new)
+    t0 = time.perf_counter()
+    buf.update(cand, sc, mr, it)
     return time.perf_counter() - t0
 
 
@@ -527,9 +562,15 @@ def run_reference(args, rank, world):
     with ctx.Pool(cores) as pool:
         for _ in range(args.warmup):
             cpu_reference_step(B, T, args.seed, cores, pool)
-        secs = [cpu_reference_step(B, T, args.seed, cores, pool) for _ in range(args.steps)]
+        phases = []
+        secs = [cpu_reference_step(B, T, args.seed, cores, pool, phases) for _ in range(args.steps)]
     s = statistics.mean(secs)
     val = B * T / s
+    # the phases separately (slowest shard, mean over the timed steps), one
+    # single-process step (no sharding), and the oracle buffer update (sequential)
+    phase_ms = {k: 1e3 * statistics.mean(ph[k] for ph in phases) for k in ("reset", "rollout", "gae", "scores")}
+    one = cpu_reference_step(B, T, args.seed, 1, None)
+    buf_s = cpu_buffer_update_seconds(4096, 4000)
     return {
         "impl": "reference",
         "metric": "AMaze env steps/sec (DR reset + 256-step RESAMPLE rollout + GAE/MaxMC)",
@@ -542,6 +583,9 @@ def run_reference(args, rank, world):
                          "sample": f"full config-2 step per timed step, numpy oracle port of the reference, "
                                    f"lanes sharded over {cores} processes; host: {_cpu_model()}"},
         "e2e": {"value": val, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases_ms_per_step": phase_ms,
+        "single_process": {"env_steps_per_s": B * T / one, "ms_per_step": one * 1e3, "cores": 1},
+        "buffer_update_ms_4096_new_levels": buf_s * 1e3,
     }
 
 
