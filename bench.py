@@ -278,7 +278,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     B, T = args.lanes, args.T
     wl = Workload(B, T, args.seed, rank * B, dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    # 256 MB (> 126 MB L2) written as int64 words: the 8-byte fill runs near HBM write speed
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.int64, device=dev)
 
     def barrier():
         if world > 1:
@@ -338,11 +339,66 @@ def run_ours(args, rank, world, local_rank):
         h_mx.copy_(o["max_returns"], non_blocking=True)
         e2e_ev[i][1].record()
     torch.cuda.synchronize()
-    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    seq_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+
+    # pipelined: step i+1's host->device copies run on a copy stream (double-buffered
+    # device inputs) while step i computes; one timed region around all K steps, every
+    # step's copies, L2 flush, step and result read inside it
+    # two copy streams: the box's H2D path reaches ~45 GB/s only with two DMA engines busy
+    css = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    main = torch.cuda.current_stream(dev)
+    bufs = [(torch.empty_like(wl.actions), torch.empty_like(wl.values), torch.empty_like(wl.last)) for _ in range(2)]
+    outs = [(torch.empty((B,), dtype=torch.float64, pin_memory=True),
+             torch.empty((B,), dtype=torch.float64, pin_memory=True)) for _ in range(2)]
+    copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
+    freed = [torch.cuda.Event() for _ in range(2)]
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    half = T // 2
+
+    def h2d(k):
+        a, v, l_ = bufs[k]
+        for c, cs in enumerate(css):
+            cs.wait_event(freed[k])
+            with torch.cuda.stream(cs):
+                if c == 0:
+                    v[:half].copy_(h_val[:half], non_blocking=True)
+                    a.copy_(h_act, non_blocking=True)
+                else:
+                    v[half:].copy_(h_val[half:], non_blocking=True)
+                    l_.copy_(h_last, non_blocking=True)
+                copied[k][c].record(cs)
+
+    torch.cuda.synchronize()
+    barrier()
+    for k in range(2):
+        freed[k].record(main)
+    clocks.active = True
+    p0.record(main)
+    host0 = time.perf_counter()
+    for cs in css:
+        cs.wait_event(p0)
+    h2d(0)
+    for i in range(args.steps):
+        k = i & 1
+        if i + 1 < args.steps:
+            h2d(k ^ 1)
+        main.wait_event(copied[k][0])
+        main.wait_event(copied[k][1])
+        flush.fill_(i & 0xFF)
+        a, v, l_ = bufs[k]
+        o = wl.step(20_000 + i, actions=a, values=v, last=l_)
+        outs[k][0].copy_(o["scores"], non_blocking=True)
+        outs[k][1].copy_(o["max_returns"], non_blocking=True)
+        freed[k].record(main)
+    p1.record(main)
+    host_ms = (time.perf_counter() - host0) * 1e3 / args.steps
+    torch.cuda.synchronize()
+    clocks.active = False
+    e2e_ms = p0.elapsed_time(p1)
+    te = torch.tensor([e2e_ms, seq_ms], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+    e2e_ms, seq_ms = float(te[0].item()), float(te[1].item())
     peaks, src = _peaks()
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     extra = {}
@@ -381,7 +437,12 @@ def run_ours(args, rank, world, local_rank):
                    "lanes_per_gpu": B, "T": T, "gamma": 0.995, "lambda": 0.95, "l2": "flushed (256 MB write) "
                    "before every timed step", "parallelism": f"lane-sharded x{world}"},
         "e2e": {"value": units / (e2e_ms * 1e-3 / args.steps), "unit": "env-steps/s",
-                "h2d_bytes_per_step": T * B * (1 + 8) + B * 8, "d2h_bytes_per_step": 2 * B * 8},
+                "h2d_bytes_per_step": T * B * (1 + 8) + B * 8, "d2h_bytes_per_step": 2 * B * 8,
+                "ms_per_step": e2e_ms / args.steps, "host_enqueue_ms_per_step": host_ms,
+                "mode": "pipelined: step i+1's pinned H2D copies (two copy streams, double-buffered) overlap step i; "
+                        "one timed region over all K steps including every copy, the L2 flush and the result read",
+                "sequential": {"value": units / (seq_ms * 1e-3 / args.steps), "ms_per_step": seq_ms / args.steps,
+                               "mode": "copies, step and read back to back per step (flush outside the timing)"}},
         "gpu_launches": wl.launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
                      "frac": roll_gbs / peak,
