@@ -314,14 +314,15 @@ def run_ours(args, rank, world, local_rank):
     total_ms = float(t.item())
 
     # ---- e2e through the public API: pinned host inputs in, scores out ----
-    h_act = torch.empty((T, B), dtype=torch.uint8, pin_memory=True)
+    from paper_2311_12716_b200 import pinned_empty as amz_pinned_empty
+    h_act = amz_pinned_empty((T, B), torch.uint8)
     h_act.copy_(wl.actions.cpu())
-    h_val = torch.empty((T, B), dtype=torch.float64, pin_memory=True)
+    h_val = amz_pinned_empty((T, B), torch.float64)
     h_val.copy_(wl.values.cpu())
-    h_last = torch.empty((B,), dtype=torch.float64, pin_memory=True)
+    h_last = amz_pinned_empty((B,), torch.float64)
     h_last.copy_(wl.last.cpu())
-    h_sc = torch.empty((B,), dtype=torch.float64, pin_memory=True)
-    h_mx = torch.empty((B,), dtype=torch.float64, pin_memory=True)
+    h_sc = amz_pinned_empty((B,), torch.float64)
+    h_mx = amz_pinned_empty((B,), torch.float64)
     d_act = torch.empty_like(wl.actions)
     d_val = torch.empty_like(wl.values)
     d_last = torch.empty_like(wl.last)
@@ -350,15 +351,14 @@ def run_ours(args, rank, world, local_rank):
     # one pinned staging buffer per step's inputs (values | last values | actions), two
     # copies per step (one per copy stream) instead of one per tensor
     nv, nl, na = T * B * 8, B * 8, T * B
-    h_in = torch.empty(nv + nl + na, dtype=torch.uint8, pin_memory=True)
+    h_in = amz_pinned_empty(nv + nl + na, torch.uint8)
     h_in[:nv].view(torch.float64).copy_(h_val.reshape(-1))
     h_in[nv:nv + nl].view(torch.float64).copy_(h_last)
     h_in[nv + nl:].copy_(h_act.reshape(-1))
     d_in = [torch.empty_like(h_in, device=dev) for _ in range(2)]
     bufs = [(d[nv + nl:].view(T, B), d[:nv].view(torch.float64).view(T, B), d[nv:nv + nl].view(torch.float64))
             for d in d_in]
-    outs = [(torch.empty((B,), dtype=torch.float64, pin_memory=True),
-             torch.empty((B,), dtype=torch.float64, pin_memory=True)) for _ in range(2)]
+    outs = [(amz_pinned_empty(B, torch.float64), amz_pinned_empty(B, torch.float64)) for _ in range(2)]
     copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
     freed = [torch.cuda.Event() for _ in range(2)]
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

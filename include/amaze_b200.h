@@ -101,6 +101,13 @@ int amz_abi_version(void);
 const char *amz_last_error(void);
 int amz_validate_params(const amz_params_t *p);
 
+/* Pinned host staging memory (cudaHostAlloc, portable) for the trajectory feed: the
+ * host->device copies of actions/values run at full PCIe rate from it (the reference
+ * keeps these arrays in numpy memory, agents/rollout.py:19-70).  Free with
+ * amz_host_free.  bytes = 0 gives NULL. */
+int amz_host_alloc(size_t bytes, void **out);
+int amz_host_free(void *p);
+
 /* Host-side key setup.  run = SeedSequence run entropy as u32 words (numpy's
  * _int_to_uint32_array), key = RngStream key prefix words.  The full spawn key is
  * prefix ++ suffix with a non-empty suffix, so the run entropy is zero-padded to 4. */

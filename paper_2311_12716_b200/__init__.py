@@ -14,6 +14,7 @@ from .core import BatchShape, StaticParams, StepResult
 from .errors import (AutocurriculaError, ConfigError, ContractViolation, LevelError, LevelParseError, RunnerFault,
                      ShapeError)
 from .gae import compute_gae, gae_and_scores, per_lane_episode_stats
+from .host import pinned_empty
 from .level import MazeLevel, decode_level, encode_level, pack_levels, unpack_levels
 from .rng import RngStream
 from .policy import GraphRollout, TorchPolicyActor, policy_head, rollout, sample_actions

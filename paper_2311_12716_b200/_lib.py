@@ -55,6 +55,8 @@ _SIGS = {
     "amz_teacher_levels": ([P, P, VP], I32),
     "amz_policy_head_dev": ([P, I32, I64, I32, P, P, I32, I64, P, P, P, VP], I32),
     "amz_env_step_dev": ([P, P, I32, I32, P, P, P, P, P, P, P, P, VP], I32),
+    "amz_host_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], I32),
+    "amz_host_free": ([P], I32),
     "amz_env_reset_dr": ([P, ctypes.POINTER(AmzSeed), ctypes.POINTER(AmzSeed), P, P, VP], I32),
     "amz_env_create": ([ctypes.POINTER(AmzParams), I64, ctypes.POINTER(ctypes.c_void_p)], I32),
     "amz_env_destroy": ([P], I32),

@@ -107,6 +107,26 @@ int amz_validate_params(const amz_params_t *p) {
     return 0;
 }
 
+int amz_host_alloc(size_t bytes, void **out) {
+    if (!out) return fail(AMZ_ECONFIG, "null argument");
+    *out = nullptr;
+    if (bytes == 0) return 0;
+    if (cudaHostAlloc(out, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return fail(AMZ_ECUDA, "cudaHostAlloc of %zu bytes failed", bytes);
+    }
+    return 0;
+}
+
+int amz_host_free(void *p) {
+    if (p && cudaFreeHost(p) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(AMZ_ECUDA, "cudaFreeHost failed");
+    }
+    return 0;
+}
+
 int amz_seed_prefix(const uint32_t *run, int n_run, const uint32_t *key, int n_key, amz_seed_t *out) {
     if (!out || n_run < 1 || (n_key > 0 && !key) || !run) return fail(AMZ_ECONFIG, "bad seed prefix arguments");
     seed_prefix_host(run, n_run, key, n_key, *out);

@@ -135,7 +135,8 @@ __device__ __forceinline__ void build_board(const Mask &m, const Geo &G, uint32_
 #pragma unroll
     for (int r = 0; r < 16; r++) t[r] = a[r];
 #pragma unroll
-    for (int s = 8; s >= 1; s >>= 1) {
+    for (int k = 3; k >= 0; k--) {  // s = 8, 4, 2, 1 (a linear counter, so it fully unrolls)
+        const int s = 1 << k;
         const uint32_t msk = s == 8 ? 0x00FFu : s == 4 ? 0x0F0Fu : s == 2 ? 0x3333u : 0x5555u;
 #pragma unroll
         for (int i = 0; i < 16; i++) {

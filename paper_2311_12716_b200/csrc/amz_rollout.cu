@@ -203,6 +203,12 @@ constexpr int kRec = 20;  // u32 words per epoch record: board[16], goal, pad
 // ---------------------------------------------------------------------------------
 #ifdef AMZ_DYN_PROF
 __device__ unsigned long long g_dyn_prof[65536][8];
+__device__ unsigned long long g_dyn_prof2[65536][8];
+#define DYN_ACC2(k_, v_)                                                                                        \
+    do {                                                                                                        \
+        const int64_t wi_ = (int64_t)blockIdx.x * WPC + (threadIdx.x >> 5);                                     \
+        if ((threadIdx.x & 31) == 0 && wi_ < 65536) g_dyn_prof2[wi_][k_] += (unsigned long long)(clock64() - v_); \
+    } while (0)
 __device__ __forceinline__ unsigned smid_() {
     unsigned r;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -228,6 +234,9 @@ __device__ __forceinline__ unsigned smid_() {
     } while (0)
 #define DYN_MARK(k_) \
     do {             \
+    } while (0)
+#define DYN_ACC2(k_, v_) \
+    do {                 \
     } while (0)
 #endif
 
@@ -361,7 +370,9 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                 const bool hit = dn && my_spec == gstep;
                 const unsigned need = __ballot_sync(0xFFFFFFFFu, dn && !hit);
                 int ar = 0, acol = 0, ad = 0, gr = 0, gc = 0;
+                DYN_ACC2(0, c_evt);
                 if (need) {
+                    DYN_T0(c_key);
                     uint64_t k0 = 0, k1 = 0;
                     if (dn && !hit) {
                         amz_seed_t sd = wrap;
@@ -369,6 +380,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                         seed_absorb(sd, E.lane_offset + (uint32_t)l);
                         seed_key(sd, k0, k1);
                     }
+                    DYN_ACC2(1, c_key);
                     DYN_T0(c_smp);
                     warp_sample_each<true>(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
                     DYN_ACC(5, c_smp);
@@ -376,6 +388,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                     if (lane == 0) g_dyn_prof[(int64_t)blockIdx.x * WPC + warp][7] += __popc(need);
 #endif
                 }
+                DYN_T0(c_bb);
                 if (hit) load_level(&S.spec[lane], m, ar, acol, ad, gr, gc);
                 if (dn) {
                     build_board(m, G, bd, LPW);
@@ -391,6 +404,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                     for (int w = 0; w < 16; w++) rec[w] = bd[w * LPW];
                     rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
                 }
+                DYN_ACC2(2, c_bb);
             }
             if (mode == AMZ_RESET_RESAMPLE) {
                 __syncwarp();
@@ -409,6 +423,9 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                 time = 0;
             }
             DYN_ACC(4, c_evt);
+#ifdef AMZ_DYN_PROF
+            if (lane == 0) g_dyn_prof[(int64_t)blockIdx.x * WPC + warp][7] += (1ull << 32) + ((unsigned long long)__popc(fin) << 48);
+#endif
         }
     };
 
@@ -468,7 +485,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                 ew[h] = (da & fwd) | (0x04040404u & ~fwd);
                 d = da >> 24;
             }
-            uint32_t rec[8], pk[8];
+            uint32_t rec[8], pkw[2] = {0u, 0u};  // positions after each step, one byte each
             unsigned ev = (time + n >= tep) ? (1u << (tep - time - 1)) : 0u;  // timeout step, if inside
 #pragma unroll
             for (int k = 0; k < 8; k++) {
@@ -476,7 +493,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                 const uint32_t db = (dw[k >> 2] >> (8 * (k & 3))) & 0x3u;
                 rec[k] = pos | (db << 8) | hi;
                 pos = mtl[e * 256u + pos];
-                pk[k] = pos;
+                pkw[k >> 2] |= pos << (8 * (k & 3));
                 ev |= (unsigned)(pos == g) << k;
             }
             ev &= (1u << n) - 1u;
@@ -484,15 +501,17 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             const unsigned km = __reduce_min_sync(0xFFFFFFFFu, kl);
             const int cnt = km < (unsigned)n ? (int)km + 1 : n;
             const bool dn = kl == km && km < (unsigned)n;
-            const bool reached = dn && pk[km] == g;
+            // position after step cnt - 1 (byte-packed: an array indexed at run time would
+            // live in local memory)
+            const uint32_t pe = ((((cnt - 1) >> 2) ? pkw[1] : pkw[0]) >> (8 * ((cnt - 1) & 3))) & 0xFFu;
+            const bool reached = dn && pe == g;  // km = cnt - 1 whenever dn
             if (lane < LPW) {
 #pragma unroll
                 for (int k = 0; k < 8; k++)
                     if (k < cnt)
                         S.rec[me][j + k] = rec[k] | (dn && k == (int)km ? ((uint32_t)reached << 10) | (1u << 11) : 0u);
             }
-            const uint32_t pe = pk[cnt - 1];
-            const uint32_t de = cnt == 8 ? d : ((dw[cnt >> 2] >> (8 * (cnt & 3))) & 3u);
+            const uint32_t de = cnt == 8 ? d : ((((cnt >> 2) ? dw[1] : dw[0]) >> (8 * (cnt & 3))) & 3u);
             ps = pe | (de << 8) | hi;
             time += cnt;
             j += cnt;
@@ -531,10 +550,14 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
 }
 
 #ifdef AMZ_DYN_PROF
+extern "C" int amz_debug_dyn_prof2(void *host) {
+    return (int)cudaMemcpyFromSymbol(host, g_dyn_prof2, sizeof(g_dyn_prof2));
+}
 extern "C" int amz_debug_dyn_prof(void *out) {
     return (int)cudaMemcpyFromSymbol(out, g_dyn_prof, sizeof(g_dyn_prof));
 }
 extern "C" int amz_debug_dyn_prof_reset(const void *zero) {
+    cudaMemcpyToSymbol(g_dyn_prof2, zero, sizeof(g_dyn_prof2));
     return (int)cudaMemcpyToSymbol(g_dyn_prof, zero, sizeof(g_dyn_prof));
 }
 #endif

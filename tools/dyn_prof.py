@@ -41,5 +41,13 @@ for mode in (amz.HOME, amz.RESAMPLE):
     ev, smp, tbl, q = [b[:, k].astype(np.int64) for k in (4, 5, 6, 7)]
     w = int(np.argmax(loop))
     print("   event cyc med/max", int(np.median(ev)), int(ev.max()), "sampler med/max", int(np.median(smp)), int(smp.max()),
-          "table med/max", int(np.median(tbl)), int(tbl.max()), "sampled levels med/max/sum", int(np.median(q)), int(q.max()), int(q.sum()))
-    print("   slowest warp: loop", int(loop[w]), "events", int(ev[w]), "sampler", int(smp[w]), "table", int(tbl[w]), "quads", int(q[w]))
+          "table med/max", int(np.median(tbl)), int(tbl.max()), "sampled levels med/max", int(np.median(q & 0xFFFFFFFF)), int((q & 0xFFFFFFFF).max()))
+    nsmp, nev, nfin = q & 0xFFFFFFFF, (q >> 32) & 0xFFFF, q >> 48
+    b2 = np.zeros((65536, 8), dtype=np.uint64)
+    if hasattr(_l.lib(), "amz_debug_dyn_prof2"):
+        _l.lib().amz_debug_dyn_prof2(ctypes.c_void_p(b2.ctypes.data))
+    b2 = b2[:nw].astype(np.int64)
+    print("   slowest warp sub-phases: pre-sample", int(b2[w, 0]), "key", int(b2[w, 1]), "board+record", int(b2[w, 2]))
+    print("   slowest warp: loop", int(loop[w]), "events", int(ev[w]), "sampler", int(smp[w]), "table", int(tbl[w]),
+          "sampled", int(nsmp[w]), "event steps", int(nev[w]), "lane ends", int(nfin[w]))
+    print("   event steps med/max", int(np.median(nev)), int(nev.max()), "lane ends med/max", int(np.median(nfin)), int(nfin.max()))
