@@ -261,32 +261,45 @@ struct DynSmem {
 template <int LPW>
 __device__ __forceinline__ void build_move_table(const uint32_t *board, int L, uint8_t *mt) {
     const int lane = threadIdx.x & 31;
+    // table word w = lane + 32 k (k = 0..9): heading e = k >> 1, column c = lane / 4 +
+    // 8 (k & 1), rows r0..r0+3 with r0 = 4 (lane & 3).  A lane only ever needs columns
+    // c0 - 1 .. c0 + 1 and c0 + 7 .. c0 + 9 (c0 = lane / 4): six loads up front, then
+    // ten independent words.
     auto col = [&](int x) -> uint32_t { return (x >= 0 && x < 16) ? (board[x * LPW + L] >> 16) : 0xFFFFu; };
-    for (int w = lane; w < 5 * 64; w += 32) {
-        const int e = w >> 6, c = (w & 63) >> 2, r0 = (w & 3) << 2;
+    const int c0 = lane >> 2, r0 = (lane & 3) << 2;
+    uint32_t cm[2], cc[2], cp[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        cm[h] = col(c0 + 8 * h - 1);
+        cc[h] = col(c0 + 8 * h);
+        cp[h] = col(c0 + 8 * h + 1);
+    }
+#pragma unroll
+    for (int k = 0; k < 10; k++) {
+        const int e = k >> 1, h = k & 1, c = c0 + 8 * h;
         const uint32_t base4 = (uint32_t)(r0 | (c << 4)) * 0x01010101u + 0x03020100u;
         uint32_t out = base4;
         if (e < 4) {
             uint32_t m;
             int off;
             if (e == 0) {  // N
-                m = ((col(c) << 1) | 1u) >> r0;
+                m = ((cc[h] << 1) | 1u) >> r0;
                 off = -1;
             } else if (e == 2) {  // S
-                m = (col(c) | 0x10000u) >> (r0 + 1);
+                m = (cc[h] | 0x10000u) >> (r0 + 1);
                 off = 1;
             } else if (e == 1) {  // E
-                m = col(c + 1) >> r0;
+                m = cp[h] >> r0;
                 off = 16;
             } else {  // W
-                m = col(c - 1) >> r0;
+                m = cm[h] >> r0;
                 off = -16;
             }
             const uint32_t open = ~m & 0xFu;
             const uint32_t spread = (open * 0x00204081u) & 0x01010101u;
             out = base4 + spread * (uint32_t)off;
         }
-        reinterpret_cast<uint32_t *>(mt)[w] = out;
+        reinterpret_cast<uint32_t *>(mt)[lane + 32 * k] = out;
     }
     __syncwarp();
 }
