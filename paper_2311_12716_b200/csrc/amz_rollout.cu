@@ -117,7 +117,9 @@ __device__ __forceinline__ void emit_row(uint32_t wall, uint32_t inb, bool goal_
                                          const uint64_t *spread, uint8_t *o) {
     constexpr uint32_t vm = (1u << V) - 1u;
     if (V <= 5) {
-        uint64_t bytes = spread[wall & inb] | (spread[~inb & vm] * 3ull);
+        // bit j -> byte j by one multiply (partial products at bits 7j never overlap)
+        auto spr = [](uint32_t x) { return ((uint64_t)x * 0x10204081ull) & 0x0101010101ull; };
+        uint64_t bytes = spr(wall & inb) | (spr(~inb & vm) * 3ull);
         if (goal_here) bytes = (bytes & ~(0xFFull << (8 * g_vc))) | (2ull << (8 * g_vc));
         const uint32_t lo = (uint32_t)bytes, hi = (uint32_t)(bytes >> 32);
         o[0] = (uint8_t)lo;
