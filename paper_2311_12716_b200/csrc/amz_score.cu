@@ -443,23 +443,48 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
         }
         // warps 1-3 only: pass 1 keeps running in warp 0 meanwhile
         asm volatile("bar.sync 1, 96;\n" ::: "memory");
-        // ---- pass 2 (warp 1): the reverse scan; A and R = A + V stored as it goes ----
+        // ---- pass 2 (warp 1): the reverse scan, A_t over delta_t in shared memory.  The
+        // operands of step t - 2 are loaded before step t's store (volatile asm keeps that
+        // order; plain code would wait for each load behind the previous store) ----
         if (warp == 1 && lane < kG4LW) {
             const double gl0 = gl * 0.0;
             double run = 0.0;
-            double *pa = adv + (int64_t)(T - 1) * B + l0 + lane, *pr = ret + (int64_t)(T - 1) * B + l0 + lane;
+            auto ld = [&](int t, double &x, uint32_t &dd) {
+                asm volatile("ld.shared.f64 %0, [%1];"
+                             : "=d"(x)
+                             : "r"((uint32_t)__cvta_generic_to_shared(&S.a[t][lane])));
+                asm volatile("ld.shared.u8 %0, [%1];"
+                             : "=r"(dd)
+                             : "r"((uint32_t)__cvta_generic_to_shared(&S.d[t][lane])));
+            };
+            double x0 = 0.0, x1 = 0.0;
+            uint32_t d0 = 0u, d1 = 0u;
+            ld(T - 1, x0, d0);
+            if (T >= 2) ld(T - 2, x1, d1);
             for (int t = T - 1; t >= 0; t--) {
-                const double glk = S.d[t][lane] ? gl0 : gl;
-                run = S.a[t][lane] + glk * run;  // delta_t, overwritten by A_t
-                S.a[t][lane] = run;
-                *pa = run;
-                *pr = run + S.v[t][lane];
-                pa -= B;
-                pr -= B;
+                double x2 = 0.0;
+                uint32_t d2 = 0u;
+                if (t >= 2) ld(t - 2, x2, d2);
+                run = x0 + (d0 ? gl0 : gl) * run;  // A_t = delta_t + glk * A_{t+1}
+                asm volatile("st.shared.f64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&S.a[t][lane])),
+                             "d"(run)
+                             : "memory");
+                x0 = x1;
+                d0 = d1;
+                x1 = x2;
+                d1 = d2;
             }
         }
     }
     __syncthreads();
+    // A and R = A + V written out by the whole CTA (row segments of kG4LW doubles)
+    for (int x = tid; x < T * kG4LW; x += 128) {
+        const int t = x / kG4LW, c = x - t * kG4LW;
+        const double a = S.a[t][c];
+        const int64_t o = (int64_t)t * B + l0 + c;
+        adv[o] = a;
+        ret[o] = a + S.v[t][c];
+    }
     if (!scores) return;
     // ---- pass 3: pairwise leaves from shared memory, 8 lanes x leaves over the warps ----
     for (int x = tid; x < P.n_leaves * kG4LW; x += 128) {
