@@ -248,7 +248,7 @@ struct DynSmem {
     uint8_t mt[LPW][5][256];  // move table: position after a step, [heading or 4 = no move][pos]
     uint8_t act[2][ACH][LPW];
     uint32_t aw[LPW][ACH / 4 + 2];  // this chunk's actions per lane, 4 steps per word (+2 zero pad)
-    uint32_t rec[LPW][ACH];         // this chunk's step records per lane
+    uint32_t rec[LPW][ACH + 8];     // this chunk's step records per lane (+8: a batch stores all 8)
     WarpSampler samp;
     __align__(16) amz_level_t spec[LPW];  // the lanes' prepared timeout levels
 };
@@ -521,10 +521,11 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
             const uint32_t pe = ((((cnt - 1) >> 2) ? pkw[1] : pkw[0]) >> (8 * ((cnt - 1) & 3))) & 0xFFu;
             const bool reached = dn && pe == g;  // km = cnt - 1 whenever dn
             if (lane < LPW) {
+                // all 8 records unconditionally (those past cnt are rewritten by the next
+                // batch, which starts at j + cnt), then the episode-end flags
 #pragma unroll
-                for (int k = 0; k < 8; k++)
-                    if (k < cnt)
-                        S.rec[me][j + k] = rec[k] | (dn && k == (int)km ? ((uint32_t)reached << 10) | (1u << 11) : 0u);
+                for (int k = 0; k < 8; k++) S.rec[me][j + k] = rec[k];
+                if (dn) S.rec[me][j + km] |= ((uint32_t)reached << 10) | (1u << 11);
             }
             const uint32_t de = cnt == 8 ? d : ((((cnt >> 2) ? dw[1] : dw[0]) >> (8 * (cnt & 3))) & 3u);
             ps = pe | (de << 8) | hi;
