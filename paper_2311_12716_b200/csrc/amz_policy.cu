@@ -35,21 +35,27 @@ __device__ __forceinline__ double np_row_sum(const double *e, int n) {
     return res;
 }
 
-template <typename TL>
-__global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logits, int64_t B, int A, uint64_t k0,
+// KA > 0: the action count fixed at compile time (AMaze's 3), so x/z/e live in registers;
+// KA = 0: any A <= kMaxActions (the arrays then sit in local memory)
+template <typename TL, int KA>
+__global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logits, int64_t B, int A_, uint64_t k0,
                                                      uint64_t k1, const amz_seed_t *__restrict__ prefix_dev,
                                                      const uint32_t *__restrict__ step_dev, int greedy,
                                                      int64_t lane0, int64_t *__restrict__ act64,
                                                      uint8_t *__restrict__ act8, double *__restrict__ logp) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B) return;
-    double x[kMaxActions], z[kMaxActions], e[kMaxActions];
+    const int A = KA > 0 ? KA : A_;
+    constexpr int NA = KA > 0 ? KA : kMaxActions;
+    double x[NA], z[NA], e[NA];
     const TL *row = logits + i * A;
     double mx = (double)row[0];
+#pragma unroll
     for (int a = 0; a < A; a++) {
         x[a] = (double)row[a];
         if (!isnan(mx) && (isnan(x[a]) || x[a] > mx)) mx = x[a];
     }
+#pragma unroll
     for (int a = 0; a < A; a++) {
         z[a] = __dsub_rn(x[a], mx);
         e[a] = exp(z[a]);
@@ -59,9 +65,13 @@ __global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logi
     if (greedy) {
         // np.argmax: first maximum, a NaN wins at its first occurrence
         act = 0;
+        double xa = x[0];
+#pragma unroll
         for (int a = 1; a < A; a++) {
-            if (isnan(x[act])) break;
-            if (isnan(x[a]) || x[a] > x[act]) act = a;
+            if (!isnan(xa) && (isnan(x[a]) || x[a] > xa)) {
+                act = a;
+                xa = x[a];
+            }
         }
     } else {
         if (prefix_dev) {  // graph replay: the key prefix and the step word come from device memory
@@ -77,6 +87,7 @@ __global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logi
         const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
         int cnt = 0;
         double cum = 0.0;
+#pragma unroll
         for (int a = 0; a < A; a++) {
             const double p = __ddiv_rn(e[a], s);
             cum = a == 0 ? p : __dadd_rn(cum, p);
@@ -86,7 +97,13 @@ __global__ void __launch_bounds__(128) k_policy_head(const TL *__restrict__ logi
     }
     if (act64) act64[i] = act;
     if (act8) act8[i] = (uint8_t)act;
-    if (logp) logp[i] = __dsub_rn(z[act], log(s));
+    if (logp) {
+        double za = z[0];
+#pragma unroll
+        for (int a = 1; a < A; a++)
+            if (a == act) za = z[a];
+        logp[i] = __dsub_rn(za, log(s));
+    }
 }
 
 int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
@@ -95,12 +112,18 @@ int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t
     if (B <= 0) return 0;
     if (A < 1 || A > kMaxActions) return AMZ_ESHAPE;
     const unsigned g = (unsigned)((B + 127) / 128);
-    if (dtype == 0)
-        k_policy_head<float><<<g, 128, 0, s>>>((const float *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy, lane0,
-                                               act64, act8, logp);
+    if (dtype == 0 && A == 3)
+        k_policy_head<float, 3><<<g, 128, 0, s>>>((const float *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy,
+                                                  lane0, act64, act8, logp);
+    else if (dtype == 0)
+        k_policy_head<float, 0><<<g, 128, 0, s>>>((const float *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy,
+                                                  lane0, act64, act8, logp);
+    else if (A == 3)
+        k_policy_head<double, 3><<<g, 128, 0, s>>>((const double *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy,
+                                                   lane0, act64, act8, logp);
     else
-        k_policy_head<double><<<g, 128, 0, s>>>((const double *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy, lane0,
-                                                act64, act8, logp);
+        k_policy_head<double, 0><<<g, 128, 0, s>>>((const double *)logits, B, A, k0, k1, prefix_dev, step_dev, greedy,
+                                                   lane0, act64, act8, logp);
     return 0;
 }
 
