@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(128) k_env_reset_dr(Geo G, EnvDev E, amz_seed_
                                                       int64_t *__restrict__ dirs) {
     __shared__ __align__(16) WarpSampler X[4];
     __shared__ uint8_t stage[4][V * V];
+    __shared__ uint32_t sboard[4][16];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t l = (int64_t)blockIdx.x * 4 + warp;
     if (l >= E.B) return;
@@ -147,10 +148,17 @@ __global__ void __launch_bounds__(128) k_env_reset_dr(Geo G, EnvDev E, amz_seed_
         L.term = false;
         E.st[l] = pack_st(L);
         E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
-        build_board(m, G, E.board + l, (int)E.B);
         if (dirs) dirs[l] = L.s.d;
-        if (view) lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, E.board + l, (int)E.B, stage[warp]);
     }
+    {
+        const uint32_t bw = warp_board_word(m, G);  // the sampler's mask is warp-uniform
+        if (lane < 16) {
+            E.board[lane * E.B + l] = bw;
+            sboard[warp][lane] = bw;
+        }
+    }
+    __syncwarp();
+    if (lane == 0 && view) lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, sboard[warp], 1, stage[warp]);
     __syncwarp();
     if (view)
         for (int j = lane; j < V * V; j += 32) view[l * V * V + j] = stage[warp][j];

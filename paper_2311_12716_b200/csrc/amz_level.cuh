@@ -151,6 +151,24 @@ __device__ __forceinline__ void build_board(const Mask &m, const Geo &G, uint32_
     for (int k = 0; k < 16; k++) board[k * stride] = a[k] | (t[k] << 16);
 }
 
+// build_board by a whole warp for one level (m warp-uniform): lane r < 16 forms row word
+// r, and the 16 column words are 16 ballots of one bit of every row (the transpose).
+__device__ __forceinline__ uint32_t warp_board_word(const Mask &m, const Geo &G) {
+    const int lane = threadIdx.x & 31;
+    uint32_t v = 0u;
+    if (lane == 0 || lane == G.H - 1)
+        v = (1u << G.W) - 1u;
+    else if (lane < G.H - 1)
+        v = 1u | (mask_bits(m, (lane - 1) * G.iw, G.iw) << 1) | (1u << (G.W - 1));
+    uint32_t col = 0u;
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+        const uint32_t b = __ballot_sync(0xFFFFFFFFu, (v >> c) & 1u) & 0xFFFFu;
+        col = lane == c ? b : col;
+    }
+    return v | (col << 16);  // board word `lane` (meaningful for lanes < 16)
+}
+
 // amz_level_t <-> registers
 __device__ __forceinline__ void load_level(const amz_level_t *lv, Mask &m, int &ar, int &ac, int &ad, int &gr,
                                            int &gc) {

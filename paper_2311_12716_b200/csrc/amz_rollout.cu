@@ -406,7 +406,6 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                 DYN_T0(c_bb);
                 if (hit) load_level(&S.spec[lane], m, ar, acol, ad, gr, gc);
                 if (dn) {
-                    build_board(m, G, bd, LPW);
                     L.hr = ar;
                     L.hc = acol;
                     L.hd = ad;
@@ -414,20 +413,32 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
                     L.gc = gc;
                     lvl_changed = true;
                     epoch++;
-                    uint32_t *rec = epochs + ((size_t)epoch * B + l) * kRec;
-#pragma unroll
-                    for (int w = 0; w < 16; w++) rec[w] = bd[w * LPW];
-                    rec[16] = (uint32_t)gr | ((uint32_t)gc << 8);
                 }
                 DYN_ACC2(2, c_bb);
             }
             if (mode == AMZ_RESET_RESAMPLE) {
+                // per finishing lane q, the whole warp: board words (ballot transpose), the
+                // epoch record, the move table
                 __syncwarp();
                 DYN_T0(c_tbl);
                 unsigned chg = fin & ((LPW >= 32) ? 0xFFFFFFFFu : ((1u << LPW) - 1u));
                 while (chg) {
                     const int q = __ffs(chg) - 1;
                     chg &= chg - 1;
+                    Mask mq;
+#pragma unroll
+                    for (int i = 0; i < 4; i++) mq.w[i] = __shfl_sync(0xFFFFFFFFu, m.w[i], q);
+                    const uint32_t eq = __shfl_sync(0xFFFFFFFFu, epoch, q);
+                    const uint32_t gq = __shfl_sync(0xFFFFFFFFu, (uint32_t)L.gr | ((uint32_t)L.gc << 8), q);
+                    const uint32_t bw = warp_board_word(mq, G);
+                    uint32_t *rec = epochs + ((size_t)eq * B + lane0 + q) * kRec;
+                    if (lane < 16) {
+                        S.board[lane][q] = bw;
+                        rec[lane] = bw;
+                    } else if (lane == 16) {
+                        rec[16] = gq;
+                    }
+                    __syncwarp();
                     build_move_table<LPW>(&S.board[0][0], q, &S.mt[q][0][0]);
                 }
                 DYN_ACC(6, c_tbl);
