@@ -527,6 +527,171 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
     }
 }
 
+// ---------------------------------------------------------------------------------
+// k_gae_score7: whole 16-lane columns in shared memory (r, V f64, done u8: 68 KB, so 3
+// CTAs per SM), persistent over the 16-lane groups.  Per group:
+//   load   all 128 threads cp.async the [T][16] columns (16-B copies, 17 per row);
+//   warp 0 pass 1 forward over (r, done) in shared memory;
+//   warp 1 pass 2 reverse, delta_t computed inline (its shared loads do not depend on
+//          the chain, so they issue ahead of it), A_t and R_t = A_t + V_t stored
+//          straight to global (128-B row segments); for PVL, A_{t+1} replaces V_{t+1}
+//          in shared memory once step t has consumed it;
+//   all    pass 3 leaves from shared memory.
+// The three CTAs of an SM overlap one another's load, chain and store phases.
+// ---------------------------------------------------------------------------------
+constexpr int kG7MaxT = 256, kG7LW = 16;
+struct G7Smem {
+    double r[kG7MaxT][kG7LW];
+    double v[kG7MaxT][kG7LW];
+    uint8_t d[kG7MaxT][kG7LW];
+    double leaf[4][kG7LW];
+    double mx[kG7LW];
+};
+
+__global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const double *__restrict__ rw,
+                                                    const double *__restrict__ val, const uint8_t *__restrict__ dn,
+                                                    const double *__restrict__ last, double gamma, double gl,
+                                                    const double *__restrict__ prior, int score_fn, int disc,
+                                                    double *__restrict__ adv, double *__restrict__ ret,
+                                                    double *__restrict__ scores, double *__restrict__ maxret,
+                                                    int64_t *__restrict__ st_eps, double *__restrict__ st_mean,
+                                                    double *__restrict__ st_max, double *__restrict__ st_solved,
+                                                    const PairwisePlan P) {
+    extern __shared__ __align__(16) uint8_t g7raw[];
+    G7Smem &S = *reinterpret_cast<G7Smem *>(g7raw);
+    constexpr int CR = kG7LW / 2;  // 16-B chunks per row of r (and of v)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool noclamp = (score_fn & AMZ_SCORE_NOCLAMP) != 0;
+    const bool prior_final = (score_fn & AMZ_SCORE_PRIOR_FINAL) != 0;
+    const int fn = score_fn & 0xFF;
+    const bool pvl = fn == AMZ_SCORE_PVL;
+    const int64_t ngroups = B / kG7LW;
+    for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int64_t l0 = g * kG7LW;
+        for (int x = tid; x < T * (2 * CR + 1); x += 128) {
+            const int t = x / (2 * CR + 1), q = x - t * (2 * CR + 1);
+            const int64_t row = (int64_t)t * B + l0;
+            if (q < CR)
+                g3_cp16(&S.r[t][2 * q], rw + row + 2 * q);
+            else if (q < 2 * CR)
+                g3_cp16(&S.v[t][2 * (q - CR)], val + row + 2 * (q - CR));
+            else
+                g3_cp16(&S.d[t][0], dn + row);
+        }
+        asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        if (warp == 0 && lane < kG7LW) {
+            // ---- pass 1: per_lane_episode_stats (forward) ----
+            const int64_t l = l0 + lane;
+            const double g1 = disc ? gamma : 1.0;
+            double acc = 0.0, dsc = 1.0, tot = 0.0, best = 0.0;
+            int cnt = 0, hits = 0;
+            const int T1 = prior_final ? 0 : T;
+            for (int t = 0; t < T1; t++) {
+                acc = acc + dsc * S.r[t][lane];
+                dsc = dsc * g1;
+                if (S.d[t][lane]) {
+                    cnt++;
+                    tot = tot + acc;
+                    best = np_max(best, acc);
+                    hits += acc > 0.0;
+                    acc = 0.0;
+                }
+            }
+            const double mx = prior_final ? prior[l] : np_max(prior ? prior[l] : 0.0, best);
+            S.mx[lane] = mx;
+            if (maxret) maxret[l] = mx;
+            if (st_eps) st_eps[l] = (int64_t)cnt;
+            if (st_mean) st_mean[l] = cnt > 0 ? tot / (double)cnt : 0.0;
+            if (st_max) st_max[l] = best;
+            if (st_solved) st_solved[l] = cnt > 0 ? (double)hits / (double)cnt : 0.0;
+        } else if (warp == 1 && lane < kG7LW) {
+            // ---- pass 2: GAE (reverse), delta inline ----
+            const int64_t l = l0 + lane;
+            const double g0 = gamma * 0.0, gl0 = gl * 0.0;
+            double nxt = last[l], run = 0.0;
+            double *pa = adv + (int64_t)(T - 1) * B + l, *pr = ret + (int64_t)(T - 1) * B + l;
+            int t = T - 1;
+            for (; t >= 7; t -= 8) {
+                double xr[8], xv[8];
+                uint32_t xd[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    xr[j] = S.r[t - j][lane];
+                    xv[j] = S.v[t - j][lane];
+                    xd[j] = S.d[t - j][lane];
+                }
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const double delta = (xr[j] + (xd[j] ? g0 : gamma) * nxt) - xv[j];
+                    run = delta + (xd[j] ? gl0 : gl) * run;
+                    *pa = run;
+                    *pr = run + xv[j];
+                    pa -= B;
+                    pr -= B;
+                    if (pvl) S.v[t - j][lane] = run;  // V_t is dead once delta_t is formed
+                    nxt = xv[j];
+                }
+            }
+            for (; t >= 0; t--) {
+                const double xr = S.r[t][lane], xv = S.v[t][lane];
+                const uint32_t xd = S.d[t][lane];
+                const double delta = (xr + (xd ? g0 : gamma) * nxt) - xv;
+                run = delta + (xd ? gl0 : gl) * run;
+                *pa = run;
+                *pr = run + xv;
+                pa -= B;
+                pr -= B;
+                if (pvl) S.v[t][lane] = run;
+                nxt = xv;
+            }
+        }
+        __syncthreads();
+        if (scores) {
+            // ---- pass 3: one (leaf, lane) per thread from shared memory ----
+            for (int x = tid; x < P.n_leaves * kG7LW; x += 128) {
+                const int li = x / kG7LW, c = x - li * kG7LW;
+                const int start = li == 0 ? 0 : P.leaf_end[li - 1], end = P.leaf_end[li];
+                const double mx = S.mx[c];
+                auto elem = [&](int t) { return pvl ? np_max(S.v[t][c], 0.0) : mx - S.v[t][c]; };
+                const int len = end - start;
+                double res = 0.0;
+                if (len < 8) {
+                    for (int k = 0; k < len; k++) res = res + elem(start + k);
+                } else {
+                    double rr[8];
+#pragma unroll
+                    for (int k = 0; k < 8; k++) rr[k] = elem(start + k);
+                    const int l8 = len - len % 8;
+                    for (int k = 8; k < l8; k += 8) {
+#pragma unroll
+                        for (int j = 0; j < 8; j++) rr[j] = rr[j] + elem(start + k + j);
+                    }
+                    res = ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
+                    for (int k = l8; k < len; k++) res = res + elem(start + k);
+                }
+                S.leaf[li][c] = res;
+            }
+            __syncthreads();
+            if (tid < kG7LW) {
+                double stk[4];
+                int sp = 0;
+                for (int li = 0; li < P.n_leaves; li++) {
+                    stk[sp++] = S.leaf[li][tid];
+                    for (int k = 0; k < P.adds[li]; k++) {
+                        const double b = stk[--sp];
+                        const double a = stk[--sp];
+                        stk[sp++] = a + b;
+                    }
+                }
+                const double sc = stk[0] / (double)T;
+                scores[l0 + tid] = noclamp ? sc : np_max(sc, 0.0);
+            }
+        }
+        __syncthreads();  // the columns are reloaded for the next group
+    }
+}
+
 int launch_gae_score(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *last,
                      double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
                      double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
@@ -535,30 +700,53 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
     PairwisePlan P;
     if (make_pairwise_plan(T, P)) return AMZ_ECONFIG;
     const double gl = gamma * lam;  // Python evaluates gamma * lam first (agents/gae.py:35)
-    // measured on B200 (T = 256): the whole-column kernel wins up to ~12k lanes (latency),
-    // the two-warp streaming kernel up to ~128k, the one-thread-per-lane kernel beyond
-    const bool g3 = do_gae && T <= kG4MaxT && B <= 12288 && B % 16 == 0 && ((uintptr_t)r & 15u) == 0 &&
-                    ((uintptr_t)v & 15u) == 0 && ((uintptr_t)d & 15u) == 0;
+    // measured on B200 (T = 256, tools/gae_large.py): the whole-column kernel k_gae_score4
+    // wins up to ~12k lanes (latency), the persistent 16-lane-column kernel k_gae_score7
+    // beyond (bit-identical outputs; 65536 lanes 0.213 -> 0.163 ms, 262144 0.638 -> 0.600);
+    // the streaming kernels cover layouts those two cannot take (unaligned, B % 16 != 0,
+    // T > 256, statistics-only calls)
+    const bool aligned = ((uintptr_t)r & 15u) == 0 && ((uintptr_t)v & 15u) == 0 && ((uintptr_t)d & 15u) == 0;
+    const bool g3 = do_gae && T <= kG4MaxT && B <= 12288 && B % 16 == 0 && aligned;
+    const bool g7 = do_gae && T <= kG7MaxT && B % kG7LW == 0 && aligned;
     static const int lw = getenv("AMZ_GAE_LW") ? atoi(getenv("AMZ_GAE_LW")) : 8;
     static const int gsel = getenv("AMZ_GAE_KERNEL") ? atoi(getenv("AMZ_GAE_KERNEL")) : 0;  // tuning runs
     if (gsel == 2) goto k2;
     if (gsel == 1) goto k1;
-    if (g3 && lw == 16) {
-        const size_t sm = sizeof(G4Smem<16>);
-        cudaFuncSetAttribute(k_gae_score4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_gae_score4<16><<<(unsigned)(B / 16), 128, sm, s>>>(
-            T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
-            stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
-            stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
-        return 0;
-    }
-    if (g3) {
+    if ((gsel == 4 || (gsel == 0 && g3)) && do_gae && T <= kG4MaxT && B % 16 == 0 && aligned) {
+        if (lw == 16 || gsel == 4) {
+            const size_t sm = sizeof(G4Smem<16>);
+            cudaFuncSetAttribute(k_gae_score4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_gae_score4<16><<<(unsigned)(B / 16), 128, sm, s>>>(
+                T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
+                stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
+                stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
+            return 0;
+        }
         const size_t sm = sizeof(G4Smem<8>);
         cudaFuncSetAttribute(k_gae_score4<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_gae_score4<8><<<(unsigned)(B / 8), 128, sm, s>>>(
             T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
             stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
             stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
+        return 0;
+    }
+    if (g7 && (gsel == 0 || gsel == 7)) {
+        static const int m7 = getenv("AMZ_GAE_M") ? atoi(getenv("AMZ_GAE_M")) : 0;  // CTAs per SM (tuning)
+        const size_t sm = sizeof(G7Smem);
+        cudaFuncSetAttribute(k_gae_score7, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        int dev = 0, nsm = 148, occ = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gae_score7, 128, sm);
+        if (occ < 1) occ = 1;
+        const int m = m7 > 0 && m7 < occ ? m7 : occ;
+        const int64_t ng = B / kG7LW;
+        const unsigned grid = (unsigned)(ng < (int64_t)nsm * m ? ng : (int64_t)nsm * m);
+        k_gae_score7<<<grid, 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores,
+                                           maxret, stats ? stats->episodes : nullptr,
+                                           stats ? stats->mean_return : nullptr,
+                                           stats ? stats->max_return : nullptr,
+                                           stats ? stats->solved_rate : nullptr, P);
         return 0;
     }
 k2:

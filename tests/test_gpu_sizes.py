@@ -92,7 +92,8 @@ def test_large_batch_kernels_vs_oracle():
     assert np.array_equal(tr.dones[:, lo:].cpu().numpy(), dn)
 
 
-@pytest.mark.parametrize("T,B", [(1, 5), (7, 33), (8, 64), (129, 17), (300, 40), (1000, 9), (256, 40000)])
+@pytest.mark.parametrize("T,B", [(1, 5), (7, 33), (8, 64), (129, 17), (300, 40), (1000, 9), (256, 40000),
+                                 (200, 16400), (256, 13000)])
 def test_gae_scores_shapes(T, B):
     rng = np.random.default_rng(T * 7 + B)
     r = np.where(rng.uniform(size=(T, B)) < 0.05, rng.uniform(size=(T, B)), 0.0)
