@@ -348,63 +348,72 @@ def run_ours(args, rank, world, local_rank):
     # two copy streams: the box's H2D path reaches ~45 GB/s only with two DMA engines busy
     css = [torch.cuda.Stream(device=dev) for _ in range(2)]
     main = torch.cuda.current_stream(dev)
-    # one pinned staging buffer per step's inputs (values | last values | actions), two
-    # copies per step (one per copy stream) instead of one per tensor
-    nv, nl, na = T * B * 8, B * 8, T * B
-    h_in = amz_pinned_empty(nv + nl + na, torch.uint8)
-    h_in[:nv].view(torch.float64).copy_(h_val.reshape(-1))
-    h_in[nv:nv + nl].view(torch.float64).copy_(h_last)
-    h_in[nv + nl:].copy_(h_act.reshape(-1))
-    d_in = [torch.empty_like(h_in, device=dev) for _ in range(2)]
-    bufs = [(d[nv + nl:].view(T, B), d[:nv].view(torch.float64).view(T, B), d[nv:nv + nl].view(torch.float64))
-            for d in d_in]
-    outs = [(amz_pinned_empty(B, torch.float64), amz_pinned_empty(B, torch.float64)) for _ in range(2)]
-    copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
-    freed = [torch.cuda.Event() for _ in range(2)]
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    half = (h_in.numel() // 2) & ~15
 
-    def h2d(k):
-        for c, cs in enumerate(css):
-            cs.wait_event(freed[k])
-            with torch.cuda.stream(cs):
-                if c == 0:
-                    d_in[k][:half].copy_(h_in[:half], non_blocking=True)
-                else:
-                    d_in[k][half:].copy_(h_in[half:], non_blocking=True)
-                copied[k][c].record(cs)
+    def pipelined(vdt, step0):
+        """One timed region over K pipelined steps; values (and last values) staged as vdt."""
+        # one pinned staging buffer per step's inputs (values | last values | actions), two
+        # copies per step (one per copy stream) instead of one per tensor
+        es = torch.empty((), dtype=vdt).element_size()
+        nv, nl, na = T * B * es, B * es, T * B
+        h_in = amz_pinned_empty(nv + nl + na, torch.uint8)
+        h_in[:nv].view(vdt).copy_(wl.values.to(vdt).cpu().reshape(-1))
+        h_in[nv:nv + nl].view(vdt).copy_(wl.last.to(vdt).cpu())
+        h_in[nv + nl:].copy_(h_act.reshape(-1))
+        d_in = [torch.empty_like(h_in, device=dev) for _ in range(2)]
+        bufs = [(d[nv + nl:].view(T, B), d[:nv].view(vdt).view(T, B), d[nv:nv + nl].view(vdt)) for d in d_in]
+        outs = [(amz_pinned_empty(B, torch.float64), amz_pinned_empty(B, torch.float64)) for _ in range(2)]
+        copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
+        freed = [torch.cuda.Event() for _ in range(2)]
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        half = (h_in.numel() // 2) & ~15
 
-    torch.cuda.synchronize()
-    barrier()
-    for k in range(2):
-        freed[k].record(main)
-    clocks.active = True
-    p0.record(main)
-    host0 = time.perf_counter()
-    for cs in css:
-        cs.wait_event(p0)
-    h2d(0)
-    for i in range(args.steps):
-        k = i & 1
-        if i + 1 < args.steps:
-            h2d(k ^ 1)
-        main.wait_event(copied[k][0])
-        main.wait_event(copied[k][1])
-        flush.fill_(i & 0xFF)
-        a, v, l_ = bufs[k]
-        o = wl.step(20_000 + i, actions=a, values=v, last=l_)
-        outs[k][0].copy_(o["scores"], non_blocking=True)
-        outs[k][1].copy_(o["max_returns"], non_blocking=True)
-        freed[k].record(main)
-    p1.record(main)
-    host_ms = (time.perf_counter() - host0) * 1e3 / args.steps
-    torch.cuda.synchronize()
-    clocks.active = False
-    e2e_ms = p0.elapsed_time(p1)
-    te = torch.tensor([e2e_ms, seq_ms], dtype=torch.float64, device=dev)
+        def h2d(k):
+            for c, cs in enumerate(css):
+                cs.wait_event(freed[k])
+                with torch.cuda.stream(cs):
+                    if c == 0:
+                        d_in[k][:half].copy_(h_in[:half], non_blocking=True)
+                    else:
+                        d_in[k][half:].copy_(h_in[half:], non_blocking=True)
+                    copied[k][c].record(cs)
+
+        torch.cuda.synchronize()
+        barrier()
+        for k in range(2):
+            freed[k].record(main)
+        clocks.active = True
+        p0.record(main)
+        host0 = time.perf_counter()
+        for cs in css:
+            cs.wait_event(p0)
+        h2d(0)
+        for i in range(args.steps):
+            k = i & 1
+            if i + 1 < args.steps:
+                h2d(k ^ 1)
+            main.wait_event(copied[k][0])
+            main.wait_event(copied[k][1])
+            flush.fill_(i & 0xFF)
+            a, v, l_ = bufs[k]
+            o = wl.step(step0 + i, actions=a, values=v, last=l_)
+            outs[k][0].copy_(o["scores"], non_blocking=True)
+            outs[k][1].copy_(o["max_returns"], non_blocking=True)
+            freed[k].record(main)
+        p1.record(main)
+        host_ms = (time.perf_counter() - host0) * 1e3 / args.steps
+        torch.cuda.synchronize()
+        clocks.active = False
+        return p0.elapsed_time(p1), host_ms, nv + nl + na
+
+    e2e_ms, host_ms, _ = pipelined(torch.float64, 20_000)
+    # the same pipeline with the values as the policy's float32 (the reference's actor
+    # returns value.double() of a float32 output, agents/ppo.py:96); the kernel widens
+    # them, so a float32-valued stream scores identically with half the value bytes
+    e32_ms, _, h2d32 = pipelined(torch.float32, 30_000)
+    te = torch.tensor([e2e_ms, seq_ms, e32_ms], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_ms, seq_ms = float(te[0].item()), float(te[1].item())
+    e2e_ms, seq_ms, e32_ms = float(te[0].item()), float(te[1].item()), float(te[2].item())
     peaks, src = _peaks()
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     extra = {}
@@ -448,7 +457,11 @@ def run_ours(args, rank, world, local_rank):
                 "mode": "pipelined: step i+1's pinned H2D copies (two copy streams, double-buffered) overlap step i; "
                         "one timed region over all K steps including every copy, the L2 flush and the result read",
                 "sequential": {"value": units / (seq_ms * 1e-3 / args.steps), "ms_per_step": seq_ms / args.steps,
-                               "mode": "copies, step and read back to back per step (flush outside the timing)"}},
+                               "mode": "copies, step and read back to back per step (flush outside the timing)"},
+                "values_f32": {"value": units / (e32_ms * 1e-3 / args.steps), "ms_per_step": e32_ms / args.steps,
+                               "h2d_bytes_per_step": h2d32,
+                               "mode": "pipelined as above with values / last values staged as float32 (the "
+                                       "policy's output dtype; gae_and_scores widens them in-kernel)"}},
         "gpu_launches": wl.launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
                      "frac": roll_gbs / peak,

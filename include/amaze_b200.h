@@ -22,7 +22,7 @@
  *                            env/batch.py:78-115 (VectorBatchEnv),
  *                            env/wrappers.py:20-78 (AutoResetWrapper)
  *   amz_env_rollout          the env side of agents/rollout.py:120-179 with an action stream
- *   amz_gae_score            agents/gae.py:8-37, agents/rollout.py:155-189,
+ *   amz_gae_score(_v32)      agents/gae.py:8-37, agents/rollout.py:155-189,
  *                            runners/scoring.py:18-63
  *   amz_plr_*                the PLR level buffer runners/buffer.py imported at
  *                            runners/scoring.py:14 but absent from the reference;
@@ -236,6 +236,15 @@ int amz_gae_score(int T, int64_t B, const double *rewards_dev, const double *val
                   const double *prior_max_dev, int score_fn, int maxmc_discounted, double *adv_dev,
                   double *ret_dev, double *scores_dev, double *max_ret_dev,
                   const amz_episode_stats_t *stats, void *stream);
+
+/* amz_gae_score with values and last values as float32: the reference's values are the
+ * policy's float32 outputs widened by `value.double()` (agents/ppo.py:96), so passing them
+ * unwidened gives bit-identical results and halves the value bytes read (and copied). */
+int amz_gae_score_v32(int T, int64_t B, const double *rewards_dev, const float *values_dev,
+                      const uint8_t *dones_dev, const float *last_value_dev, double gamma, double lam,
+                      const double *prior_max_dev, int score_fn, int maxmc_discounted, double *adv_dev,
+                      double *ret_dev, double *scores_dev, double *max_ret_dev,
+                      const amz_episode_stats_t *stats, void *stream);
 
 /* lane_scores with caller-supplied advantages (runners/scoring.py:34-63): episode
  * stats + running max + MaxMC/PVL means, no GAE pass.  adv_dev needed for PVL only. */

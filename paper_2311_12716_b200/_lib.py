@@ -72,6 +72,8 @@ _SIGS = {
     "amz_env_check": ([P, VP], I32),
     "amz_gae_score": ([I32, I64, P, P, P, P, D, D, P, I32, I32, P, P, P, P,
                        ctypes.POINTER(AmzEpisodeStats), VP], I32),
+    "amz_gae_score_v32": ([I32, I64, P, P, P, P, D, D, P, I32, I32, P, P, P, P,
+                           ctypes.POINTER(AmzEpisodeStats), VP], I32),
     "amz_plr_create": ([I64, ctypes.POINTER(ctypes.c_void_p)], I32),
     "amz_plr_destroy": ([P], I32),
     "amz_plr_update": ([P, P, P, P, I64, I64, VP], I32),

@@ -504,6 +504,21 @@ int amz_gae_score(int T, int64_t B, const double *r, const double *v, const uint
     return cuda_status("gae_score");
 }
 
+int amz_gae_score_v32(int T, int64_t B, const double *r, const float *v, const uint8_t *d, const float *last,
+                      double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
+                      double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats, void *stream) {
+    if (T < 1) return fail(AMZ_ECONTRACT, "cannot score an empty trajectory slice");
+    if (B < 0) return fail(AMZ_ESHAPE, "negative lane count");
+    if (!r || !v || !d || !last || !adv || !ret) return fail(AMZ_ECONFIG, "null argument");
+    if ((score_fn & 0xFF) != AMZ_SCORE_MAXMC && (score_fn & 0xFF) != AMZ_SCORE_PVL)
+        return fail(AMZ_ECONFIG, "unknown score_fn %d", score_fn);
+    if ((score_fn & AMZ_SCORE_PRIOR_FINAL) && !prior) return fail(AMZ_ECONFIG, "PRIOR_FINAL needs prior_max");
+    int rc = launch_gae_score_v32(T, B, r, v, d, last, gamma, lam, prior, score_fn, disc, adv, ret, scores, maxret,
+                                  stats, (cudaStream_t)stream);
+    if (rc) return fail(rc, "gae_score: T=%d too long for the pairwise schedule", T);
+    return cuda_status("gae_score_v32");
+}
+
 int amz_lane_scores(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *adv,
                     double gamma, const double *prior, int score_fn, int disc, double *scores, double *maxret,
                     const amz_episode_stats_t *stats, void *stream) {

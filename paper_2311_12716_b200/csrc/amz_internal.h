@@ -68,6 +68,11 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
                      double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
                      double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
                      cudaStream_t s, int do_gae = 1);
+// values (and last values) as the policy's float32, widened exactly in the kernel
+int launch_gae_score_v32(int T, int64_t B, const double *r, const float *v, const uint8_t *d, const float *last,
+                         double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
+                         double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
+                         cudaStream_t s);
 
 // PLR buffer (amz_plr.cu)
 struct PlrDev {

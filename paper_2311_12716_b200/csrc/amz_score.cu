@@ -94,9 +94,10 @@ struct PairwiseSum {
     __device__ __forceinline__ double total() const { return stk[0]; }
 };
 
+template <typename VT>
 __global__ void __launch_bounds__(64) k_gae_score(int T, int64_t B, const double *__restrict__ rw,
-                                                  const double *__restrict__ val, const uint8_t *__restrict__ dn,
-                                                  const double *__restrict__ last, double gamma, double gl,
+                                                  const VT *__restrict__ val, const uint8_t *__restrict__ dn,
+                                                  const VT *__restrict__ last, double gamma, double gl,
                                                   const double *__restrict__ prior, int score_fn, int disc,
                                                   double *__restrict__ adv, double *__restrict__ ret,
                                                   double *__restrict__ scores, double *__restrict__ maxret,
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(64) k_gae_score(int T, int64_t B, const double
     if (st_solved) st_solved[l] = cnt > 0 ? (double)hits / (double)cnt : 0.0;
 
     // ---- pass 2: GAE (reverse) ----
-    double nxt = do_gae ? last[l] : 0.0, run = 0.0;
+    double nxt = do_gae ? (double)last[l] : 0.0, run = 0.0;
     for (int t1 = do_gae ? T : 0; t1 > 0; t1 -= 8) {
         double xr[8], xv[8];
         uint8_t xd[8];
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(64) k_gae_score(int T, int64_t B, const double
         for (int j = 0; j < 8; j++) {
             const int t = t1 - 1 - j;
             xr[j] = t >= 0 ? rw[(int64_t)t * B + l] : 0.0;
-            xv[j] = t >= 0 ? val[(int64_t)t * B + l] : 0.0;
+            xv[j] = t >= 0 ? (double)val[(int64_t)t * B + l] : 0.0;
             xd[j] = t >= 0 ? dn[(int64_t)t * B + l] : 0;
         }
 #pragma unroll
@@ -173,13 +174,13 @@ __global__ void __launch_bounds__(64) k_gae_score(int T, int64_t B, const double
     if (scores) {
         PairwiseSum S;
         S.begin(P);
-        const double *src = score_fn == AMZ_SCORE_PVL ? adv : val;
+        const bool pv = score_fn == AMZ_SCORE_PVL;
         for (int t0 = 0; t0 < T; t0 += 8) {
             double x[8];
 #pragma unroll
             for (int j = 0; j < 8; j++) {
                 const int t = t0 + j;
-                x[j] = t < T ? src[(int64_t)t * B + l] : 0.0;
+                x[j] = t < T ? (pv ? adv[(int64_t)t * B + l] : (double)val[(int64_t)t * B + l]) : 0.0;
             }
 #pragma unroll
             for (int j = 0; j < 8; j++) {
@@ -199,10 +200,11 @@ __global__ void __launch_bounds__(64) k_gae_score(int T, int64_t B, const double
 // pass 2 (reverse GAE) -- the passes are independent -- then the pairwise leaves of
 // pass 3 are split between the two warps and warp 0 combines them in numpy's order.
 // This halves the per-lane sequential chain, which is what bounds small batches.
-__device__ __forceinline__ double leaf_sum(const double *__restrict__ src, int64_t B, int64_t l, int s, int len,
+template <typename ST>
+__device__ __forceinline__ double leaf_sum(const ST *__restrict__ src, int64_t B, int64_t l, int s, int len,
                                            int fn, double mx) {
     auto elem = [&](int t) {
-        const double x = src[(int64_t)t * B + l];
+        const double x = (double)src[(int64_t)t * B + l];
         return fn == AMZ_SCORE_PVL ? np_max(x, 0.0) : mx - x;
     };
     if (len < 8) {
@@ -226,9 +228,10 @@ __device__ __forceinline__ double leaf_sum(const double *__restrict__ src, int64
     return res;
 }
 
+template <typename VT>
 __global__ void __launch_bounds__(64) k_gae_score2(int T, int64_t B, const double *__restrict__ rw,
-                                                   const double *__restrict__ val, const uint8_t *__restrict__ dn,
-                                                   const double *__restrict__ last, double gamma, double gl,
+                                                   const VT *__restrict__ val, const uint8_t *__restrict__ dn,
+                                                   const VT *__restrict__ last, double gamma, double gl,
                                                    const double *__restrict__ prior, int score_fn, int disc,
                                                    double *adv, double *__restrict__ ret,
                                                    double *__restrict__ scores, double *__restrict__ maxret,
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(64) k_gae_score2(int T, int64_t B, const doubl
     }
     if (warp == 1 && live && do_gae) {
         // ---- pass 2: GAE (reverse) ----
-        double nxt = last[l], run = 0.0;
+        double nxt = (double)last[l], run = 0.0;
         for (int t1 = T; t1 > 0; t1 -= 8) {
             double xr[8], xv[8];
             uint8_t xd[8];
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(64) k_gae_score2(int T, int64_t B, const doubl
             for (int j = 0; j < 8; j++) {
                 const int t = t1 - 1 - j;
                 xr[j] = t >= 0 ? rw[(int64_t)t * B + l] : 0.0;
-                xv[j] = t >= 0 ? val[(int64_t)t * B + l] : 0.0;
+                xv[j] = t >= 0 ? (double)val[(int64_t)t * B + l] : 0.0;
                 xd[j] = t >= 0 ? dn[(int64_t)t * B + l] : 0;
             }
 #pragma unroll
@@ -311,13 +314,14 @@ __global__ void __launch_bounds__(64) k_gae_score2(int T, int64_t B, const doubl
     if (!scores) return;
     __syncthreads();
     // ---- pass 3: pairwise leaves split across the two warps ----
-    const double *src = fn == AMZ_SCORE_PVL ? adv : val;
     const double mx = s_mx[lane];
     if (live) {
         int start = 0;
         for (int li = 0; li < P.n_leaves; li++) {
             const int end = P.leaf_end[li];
-            if ((li & 1) == warp) s_leaf[li][lane] = leaf_sum(src, B, l, start, end - start, fn, mx);
+            if ((li & 1) == warp)
+                s_leaf[li][lane] = fn == AMZ_SCORE_PVL ? leaf_sum(adv, B, l, start, end - start, fn, mx)
+                                                       : leaf_sum(val, B, l, start, end - start, fn, mx);
             start = end;
         }
     }
@@ -358,10 +362,10 @@ __device__ __forceinline__ void g3_cp16(void *sdst, const void *gsrc) {
 // Same float64 operations in the same order as the reference (bit-exact).
 // ---------------------------------------------------------------------------------
 constexpr int kG4MaxT = 256;
-template <int kG4LW>
+template <int kG4LW, typename VT>
 struct G4Smem {
     double r[kG4MaxT][kG4LW];    // rewards
-    double v[kG4MaxT][kG4LW];    // values
+    VT v[kG4MaxT][kG4LW];        // values (f64, or the policy's f32)
     double a[kG4MaxT][kG4LW];    // delta, then advantages (in place)
     uint8_t d[kG4MaxT][kG4LW];   // dones
     double leaf[kMaxLeaves][kG4LW];
@@ -374,10 +378,10 @@ __device__ __forceinline__ void g4_cp8(void *sdst, const void *gsrc) {
                  : "memory");
 }
 
-template <int kG4LW>
+template <int kG4LW, typename VT>
 __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const double *__restrict__ rw,
-                                                    const double *__restrict__ val, const uint8_t *__restrict__ dn,
-                                                    const double *__restrict__ last, double gamma, double gl,
+                                                    const VT *__restrict__ val, const uint8_t *__restrict__ dn,
+                                                    const VT *__restrict__ last, double gamma, double gl,
                                                     const double *__restrict__ prior, int score_fn, int disc,
                                                     double *__restrict__ adv, double *__restrict__ ret,
                                                     double *__restrict__ scores, double *__restrict__ maxret,
@@ -385,22 +389,24 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
                                                     double *__restrict__ st_max, double *__restrict__ st_solved,
                                                     const PairwisePlan P) {
     extern __shared__ __align__(16) uint8_t g4raw[];
-    G4Smem<kG4LW> &S = *reinterpret_cast<G4Smem<kG4LW> *>(g4raw);
-    constexpr int CR = kG4LW / 2;  // 16-B chunks per row of r (and of v)
+    G4Smem<kG4LW, VT> &S = *reinterpret_cast<G4Smem<kG4LW, VT> *>(g4raw);
+    constexpr int CR = kG4LW / 2;                            // 16-B chunks per row of r
+    constexpr int CV = kG4LW * (int)sizeof(VT) / 16;         // ... and of v
+    constexpr int EV = 16 / (int)sizeof(VT);                 // values per chunk
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t l0 = (int64_t)blockIdx.x * kG4LW;
     const bool noclamp = (score_fn & AMZ_SCORE_NOCLAMP) != 0;
     const bool prior_final = (score_fn & AMZ_SCORE_PRIOR_FINAL) != 0;
     const int fn = score_fn & 0xFF;
     const bool pvl = fn == AMZ_SCORE_PVL;
-    // ---- load: CR + CR 16-B chunks of r and v per row, one chunk of dones ----
-    for (int x = tid; x < T * (2 * CR + 1); x += 128) {
-        const int t = x / (2 * CR + 1), q = x - t * (2 * CR + 1);
+    // ---- load: CR + CV 16-B chunks of r and v per row, one chunk of dones ----
+    for (int x = tid; x < T * (CR + CV + 1); x += 128) {
+        const int t = x / (CR + CV + 1), q = x - t * (CR + CV + 1);
         const int64_t row = (int64_t)t * B + l0;
         if (q < CR)
             g3_cp16(&S.r[t][2 * q], rw + row + 2 * q);
-        else if (q < 2 * CR)
-            g3_cp16(&S.v[t][2 * (q - CR)], val + row + 2 * (q - CR));
+        else if (q < CR + CV)
+            g3_cp16(&S.v[t][EV * (q - CR)], val + row + EV * (q - CR));
         else if (kG4LW == 16)
             g3_cp16(&S.d[t][0], dn + row);
         else
@@ -437,9 +443,9 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
         const double g0 = gamma * 0.0;
         for (int x = tid - 32; x < T * kG4LW; x += 96) {
             const int t = x / kG4LW, c = x - t * kG4LW;
-            const double nxt = t + 1 < T ? S.v[t + 1][c] : last[l0 + c];
+            const double nxt = t + 1 < T ? (double)S.v[t + 1][c] : (double)last[l0 + c];
             const double gk = S.d[t][c] ? g0 : gamma;
-            S.a[t][c] = (S.r[t][c] + gk * nxt) - S.v[t][c];
+            S.a[t][c] = (S.r[t][c] + gk * nxt) - (double)S.v[t][c];
         }
         // warps 1-3 only: pass 1 keeps running in warp 0 meanwhile
         asm volatile("bar.sync 1, 96;\n" ::: "memory");
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
         const double a = S.a[t][c];
         const int64_t o = (int64_t)t * B + l0 + c;
         adv[o] = a;
-        ret[o] = a + S.v[t][c];
+        ret[o] = a + (double)S.v[t][c];
     }
     if (!scores) return;
     // ---- pass 3: pairwise leaves from shared memory, 8 lanes x leaves over the warps ----
@@ -491,7 +497,7 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
         const int li = x / kG4LW, c = x - li * kG4LW;
         const int start = li == 0 ? 0 : P.leaf_end[li - 1], end = P.leaf_end[li];
         const double mx = S.mx[c];
-        auto elem = [&](int t) { return pvl ? np_max(S.a[t][c], 0.0) : mx - S.v[t][c]; };
+        auto elem = [&](int t) { return pvl ? np_max(S.a[t][c], 0.0) : mx - (double)S.v[t][c]; };
         const int len = end - start;
         double res = 0.0;
         if (len < 8) {
@@ -540,17 +546,22 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
 // The three CTAs of an SM overlap one another's load, chain and store phases.
 // ---------------------------------------------------------------------------------
 constexpr int kG7MaxT = 256, kG7LW = 16;
+// kA: PVL's advantages get their own column (f32 values cannot hold them); with f64
+// values they replace V in place
+template <typename VT, bool kA>
 struct G7Smem {
     double r[kG7MaxT][kG7LW];
-    double v[kG7MaxT][kG7LW];
+    VT v[kG7MaxT][kG7LW];
+    double a[kA ? kG7MaxT : 1][kG7LW];
     uint8_t d[kG7MaxT][kG7LW];
     double leaf[4][kG7LW];
     double mx[kG7LW];
 };
 
+template <typename VT, bool kA>
 __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const double *__restrict__ rw,
-                                                    const double *__restrict__ val, const uint8_t *__restrict__ dn,
-                                                    const double *__restrict__ last, double gamma, double gl,
+                                                    const VT *__restrict__ val, const uint8_t *__restrict__ dn,
+                                                    const VT *__restrict__ last, double gamma, double gl,
                                                     const double *__restrict__ prior, int score_fn, int disc,
                                                     double *__restrict__ adv, double *__restrict__ ret,
                                                     double *__restrict__ scores, double *__restrict__ maxret,
@@ -558,8 +569,10 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
                                                     double *__restrict__ st_max, double *__restrict__ st_solved,
                                                     const PairwisePlan P) {
     extern __shared__ __align__(16) uint8_t g7raw[];
-    G7Smem &S = *reinterpret_cast<G7Smem *>(g7raw);
-    constexpr int CR = kG7LW / 2;  // 16-B chunks per row of r (and of v)
+    G7Smem<VT, kA> &S = *reinterpret_cast<G7Smem<VT, kA> *>(g7raw);
+    constexpr int CR = kG7LW / 2;                     // 16-B chunks per row of r
+    constexpr int CV = kG7LW * (int)sizeof(VT) / 16;  // ... and of v
+    constexpr int EV = 16 / (int)sizeof(VT);          // values per chunk
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool noclamp = (score_fn & AMZ_SCORE_NOCLAMP) != 0;
     const bool prior_final = (score_fn & AMZ_SCORE_PRIOR_FINAL) != 0;
@@ -568,13 +581,13 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
     const int64_t ngroups = B / kG7LW;
     for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
         const int64_t l0 = g * kG7LW;
-        for (int x = tid; x < T * (2 * CR + 1); x += 128) {
-            const int t = x / (2 * CR + 1), q = x - t * (2 * CR + 1);
+        for (int x = tid; x < T * (CR + CV + 1); x += 128) {
+            const int t = x / (CR + CV + 1), q = x - t * (CR + CV + 1);
             const int64_t row = (int64_t)t * B + l0;
             if (q < CR)
                 g3_cp16(&S.r[t][2 * q], rw + row + 2 * q);
-            else if (q < 2 * CR)
-                g3_cp16(&S.v[t][2 * (q - CR)], val + row + 2 * (q - CR));
+            else if (q < CR + CV)
+                g3_cp16(&S.v[t][EV * (q - CR)], val + row + EV * (q - CR));
             else
                 g3_cp16(&S.d[t][0], dn + row);
         }
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
             // ---- pass 2: GAE (reverse), delta inline ----
             const int64_t l = l0 + lane;
             const double g0 = gamma * 0.0, gl0 = gl * 0.0;
-            double nxt = last[l], run = 0.0;
+            double nxt = (double)last[l], run = 0.0;
             double *pa = adv + (int64_t)(T - 1) * B + l, *pr = ret + (int64_t)(T - 1) * B + l;
             int t = T - 1;
             for (; t >= 7; t -= 8) {
@@ -618,7 +631,7 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
 #pragma unroll
                 for (int j = 0; j < 8; j++) {
                     xr[j] = S.r[t - j][lane];
-                    xv[j] = S.v[t - j][lane];
+                    xv[j] = (double)S.v[t - j][lane];
                     xd[j] = S.d[t - j][lane];
                 }
 #pragma unroll
@@ -629,12 +642,15 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
                     *pr = run + xv[j];
                     pa -= B;
                     pr -= B;
-                    if (pvl) S.v[t - j][lane] = run;  // V_t is dead once delta_t is formed
+                    if (kA)
+                        S.a[t - j][lane] = run;
+                    else if (pvl)
+                        S.v[t - j][lane] = (VT)run;  // (f64 values) V_t is dead once delta_t is formed
                     nxt = xv[j];
                 }
             }
             for (; t >= 0; t--) {
-                const double xr = S.r[t][lane], xv = S.v[t][lane];
+                const double xr = S.r[t][lane], xv = (double)S.v[t][lane];
                 const uint32_t xd = S.d[t][lane];
                 const double delta = (xr + (xd ? g0 : gamma) * nxt) - xv;
                 run = delta + (xd ? gl0 : gl) * run;
@@ -642,7 +658,10 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
                 *pr = run + xv;
                 pa -= B;
                 pr -= B;
-                if (pvl) S.v[t][lane] = run;
+                if (kA)
+                    S.a[t][lane] = run;
+                else if (pvl)
+                    S.v[t][lane] = (VT)run;
                 nxt = xv;
             }
         }
@@ -653,7 +672,9 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
                 const int li = x / kG7LW, c = x - li * kG7LW;
                 const int start = li == 0 ? 0 : P.leaf_end[li - 1], end = P.leaf_end[li];
                 const double mx = S.mx[c];
-                auto elem = [&](int t) { return pvl ? np_max(S.v[t][c], 0.0) : mx - S.v[t][c]; };
+                auto elem = [&](int t) {
+                    return pvl ? np_max(kA ? S.a[t][c] : (double)S.v[t][c], 0.0) : mx - (double)S.v[t][c];
+                };
                 const int len = end - start;
                 double res = 0.0;
                 if (len < 8) {
@@ -692,10 +713,11 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
     }
 }
 
-int launch_gae_score(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *last,
-                     double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
-                     double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
-                     cudaStream_t s, int do_gae) {
+template <typename VT>
+static int launch_gae_score_t(int T, int64_t B, const double *r, const VT *v, const uint8_t *d, const VT *last,
+                              double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
+                              double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
+                              cudaStream_t s, int do_gae) {
     if (B <= 0 || T <= 0) return 0;
     PairwisePlan P;
     if (make_pairwise_plan(T, P)) return AMZ_ECONFIG;
@@ -710,60 +732,82 @@ int launch_gae_score(int T, int64_t B, const double *r, const double *v, const u
     const bool g7 = do_gae && T <= kG7MaxT && B % kG7LW == 0 && aligned;
     static const int lw = getenv("AMZ_GAE_LW") ? atoi(getenv("AMZ_GAE_LW")) : 8;
     static const int gsel = getenv("AMZ_GAE_KERNEL") ? atoi(getenv("AMZ_GAE_KERNEL")) : 0;  // tuning runs
+    auto st = [&](int k) -> void * {
+        if (!stats) return nullptr;
+        return k == 0 ? (void *)stats->episodes
+                      : k == 1 ? (void *)stats->mean_return : k == 2 ? (void *)stats->max_return : (void *)stats->solved_rate;
+    };
+    int64_t *s_eps = (int64_t *)st(0);
+    double *s_mean = (double *)st(1), *s_max = (double *)st(2), *s_sol = (double *)st(3);
     if (gsel == 2) goto k2;
     if (gsel == 1) goto k1;
     if ((gsel == 4 || (gsel == 0 && g3)) && do_gae && T <= kG4MaxT && B % 16 == 0 && aligned) {
         if (lw == 16 || gsel == 4) {
-            const size_t sm = sizeof(G4Smem<16>);
-            cudaFuncSetAttribute(k_gae_score4<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_gae_score4<16><<<(unsigned)(B / 16), 128, sm, s>>>(
-                T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
-                stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
-                stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
+            const size_t sm = sizeof(G4Smem<16, VT>);
+            cudaFuncSetAttribute(k_gae_score4<16, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_gae_score4<16, VT><<<(unsigned)(B / 16), 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn,
+                                                                     disc, adv, ret, scores, maxret, s_eps, s_mean,
+                                                                     s_max, s_sol, P);
             return 0;
         }
-        const size_t sm = sizeof(G4Smem<8>);
-        cudaFuncSetAttribute(k_gae_score4<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_gae_score4<8><<<(unsigned)(B / 8), 128, sm, s>>>(
-            T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
-            stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
-            stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, P);
+        const size_t sm = sizeof(G4Smem<8, VT>);
+        cudaFuncSetAttribute(k_gae_score4<8, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_gae_score4<8, VT><<<(unsigned)(B / 8), 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc,
+                                                               adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol,
+                                                               P);
         return 0;
     }
     if (g7 && (gsel == 0 || gsel == 7)) {
         static const int m7 = getenv("AMZ_GAE_M") ? atoi(getenv("AMZ_GAE_M")) : 0;  // CTAs per SM (tuning)
-        const size_t sm = sizeof(G7Smem);
-        cudaFuncSetAttribute(k_gae_score7, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        int dev = 0, nsm = 148, occ = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gae_score7, 128, sm);
-        if (occ < 1) occ = 1;
-        const int m = m7 > 0 && m7 < occ ? m7 : occ;
-        const int64_t ng = B / kG7LW;
-        const unsigned grid = (unsigned)(ng < (int64_t)nsm * m ? ng : (int64_t)nsm * m);
-        k_gae_score7<<<grid, 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores,
-                                           maxret, stats ? stats->episodes : nullptr,
-                                           stats ? stats->mean_return : nullptr,
-                                           stats ? stats->max_return : nullptr,
-                                           stats ? stats->solved_rate : nullptr, P);
+        auto go = [&](auto kern, size_t sm) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int dev = 0, nsm = 148, occ = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, sm);
+            if (occ < 1) occ = 1;
+            const int m = m7 > 0 && m7 < occ ? m7 : occ;
+            const int64_t ng = B / kG7LW;
+            const unsigned grid = (unsigned)(ng < (int64_t)nsm * m ? ng : (int64_t)nsm * m);
+            kern<<<grid, 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
+                                       s_eps, s_mean, s_max, s_sol, P);
+        };
+        // f64 values: PVL's advantages overwrite V in place; f32 values: a separate column
+        if (sizeof(VT) == 8 || (score_fn & 0xFF) != AMZ_SCORE_PVL)
+            go(k_gae_score7<VT, false>, sizeof(G7Smem<VT, false>));
+        else
+            go(k_gae_score7<VT, true>, sizeof(G7Smem<VT, true>));
         return 0;
     }
 k2:
     if (gsel == 2 || B <= 131072) {
-        k_gae_score2<<<(unsigned)((B + 31) / 32), 64, 0, s>>>(
-            T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
-            stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
-            stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, do_gae, P);
+        k_gae_score2<VT><<<(unsigned)((B + 31) / 32), 64, 0, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc,
+                                                                 adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol,
+                                                                 do_gae, P);
         return 0;
     }
 k1:
     const int threads = B >= 148 * 64 ? 64 : 32;
-    k_gae_score<<<(unsigned)((B + threads - 1) / threads), threads, 0, s>>>(
-        T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
-        stats ? stats->episodes : nullptr, stats ? stats->mean_return : nullptr,
-        stats ? stats->max_return : nullptr, stats ? stats->solved_rate : nullptr, do_gae, P);
+    k_gae_score<VT><<<(unsigned)((B + threads - 1) / threads), threads, 0, s>>>(
+        T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol,
+        do_gae, P);
     return 0;
+}
+
+int launch_gae_score(int T, int64_t B, const double *r, const double *v, const uint8_t *d, const double *last,
+                     double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
+                     double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
+                     cudaStream_t s, int do_gae) {
+    return launch_gae_score_t<double>(T, B, r, v, d, last, gamma, lam, prior, score_fn, disc, adv, ret, scores,
+                                      maxret, stats, s, do_gae);
+}
+
+int launch_gae_score_v32(int T, int64_t B, const double *r, const float *v, const uint8_t *d, const float *last,
+                         double gamma, double lam, const double *prior, int score_fn, int disc, double *adv,
+                         double *ret, double *scores, double *maxret, const amz_episode_stats_t *stats,
+                         cudaStream_t s) {
+    return launch_gae_score_t<float>(T, B, r, v, d, last, gamma, lam, prior, score_fn, disc, adv, ret, scores,
+                                     maxret, stats, s, 1);
 }
 
 }  // namespace amz

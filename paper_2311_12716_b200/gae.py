@@ -51,16 +51,21 @@ def gae_and_scores(rewards, values, dones, last_value, gamma: float, lam: float,
                    score_fn: str = "maxmc", maxmc_discounted: bool = False, with_stats: bool = False):
     """One launch: advantages, returns, per-lane scores, running max returns (+ stats).
 
-    Equals ``compute_gae`` followed by ``lane_scores(traj, adv, prior, cfg, gamma)``."""
+    Equals ``compute_gae`` followed by ``lane_scores(traj, adv, prior, cfg, gamma)``.
+    ``values`` and ``last_value`` may both be float32 tensors -- the policy's own output
+    dtype, which the reference widens with ``value.double()`` (agents/ppo.py:96) -- and are
+    then widened inside the kernel (bit-identical results, half the value bytes)."""
     torch = _torch()
     dev = _device_of(rewards, values, dones, last_value)
     r = _dev(rewards, torch.float64, dev)
-    v = _dev(values, torch.float64, dev)
+    v32 = (torch.is_tensor(values) and values.dtype == torch.float32 and torch.is_tensor(last_value)
+           and last_value.dtype == torch.float32)
+    v = _dev(values, torch.float32 if v32 else torch.float64, dev)
     if r.dim() != 2 or v.shape != r.shape:
         raise ShapeError(f"rewards {tuple(r.shape)} / values {tuple(v.shape)} must be equal [T, B]")
     T, B = r.shape
     d = _dev(dones, torch.bool, dev).view(torch.uint8)
-    last = _dev(last_value, torch.float64, dev).reshape(-1)
+    last = _dev(last_value, torch.float32 if v32 else torch.float64, dev).reshape(-1)
     if d.shape != r.shape or last.numel() != B:
         raise ShapeError("dones must be [T, B] and last_value [B]")
     prior = None if prior_max_returns is None else _dev(prior_max_returns, torch.float64, dev).reshape(-1)
@@ -71,7 +76,7 @@ def gae_and_scores(rewards, values, dones, last_value, gamma: float, lam: float,
     stats, cst = _stats_struct(B, dev) if with_stats else (None, None)
     fn = {"maxmc": _lib.AMZ_SCORE_MAXMC, "pvl": _lib.AMZ_SCORE_PVL}[score_fn]
     with torch.cuda.device(dev):
-        _lib.call("amz_gae_score", T, B, _lib.ptr(r), _lib.ptr(v), _lib.ptr(d), _lib.ptr(last), float(gamma),
+        _lib.call("amz_gae_score_v32" if v32 else "amz_gae_score", T, B, _lib.ptr(r), _lib.ptr(v), _lib.ptr(d), _lib.ptr(last), float(gamma),
                   float(lam), _lib.ptr(prior), fn, int(bool(maxmc_discounted)), _lib.ptr(adv), _lib.ptr(ret),
                   _lib.ptr(scores), _lib.ptr(maxret), ctypes.byref(cst) if cst is not None else None,
                   _lib.stream_handle(dev))

@@ -120,3 +120,33 @@ def test_dr_levels_valid_and_distributed():
     host = amz.amaze.to_host_levels(lv, p)
     walls = np.array([h.n_interior_walls() for h in host])
     assert walls.min() == 0 and walls.max() == 60 and abs(walls.mean() - 30) < 1.5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T,B", [(256, 4096), (256, 12288), (200, 16400), (256, 40000), (256, 13000), (129, 17),
+                                 (300, 40)])
+def test_gae_scores_f32_values(T, B):
+    """Values as the policy's float32 (agents/ppo.py:96 widens them with .double()): the
+    f32 entry equals the f64 path on the widened values, bit for bit, on every kernel."""
+    rng = np.random.default_rng(T * 11 + B)
+    r = np.where(rng.uniform(size=(T, B)) < 0.05, rng.uniform(size=(T, B)), 0.0)
+    v32 = rng.uniform(-1, 1, (T, B)).astype(np.float32)
+    d = rng.uniform(size=(T, B)) < 0.05
+    last32 = rng.uniform(size=B).astype(np.float32)
+    prior = rng.uniform(size=B) * (rng.uniform(size=B) < 0.3)
+    v, last = v32.astype(np.float64), last32.astype(np.float64)
+    adv, ret = onp.gae(r, v, d, last, 0.99, 0.9)
+    for fn in ("maxmc", "pvl"):
+        o = amz.gae_and_scores(torch.from_numpy(r).cuda(), torch.from_numpy(v32).cuda(), torch.from_numpy(d).cuda(),
+                               torch.from_numpy(last32).cuda(), 0.99, 0.9, torch.from_numpy(prior).cuda(), fn,
+                               with_stats=True)
+        sc, mx, _ = onp.lane_scores(v, adv, r, d, prior, fn)
+        assert np.array_equal(o["advantages"].cpu().numpy(), adv)
+        assert np.array_equal(o["returns"].cpu().numpy(), ret)
+        assert np.array_equal(o["scores"].cpu().numpy(), sc)
+        assert np.array_equal(o["max_returns"].cpu().numpy(), mx)
+        o64 = amz.gae_and_scores(torch.from_numpy(r).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(d).cuda(),
+                                 torch.from_numpy(last).cuda(), 0.99, 0.9, torch.from_numpy(prior).cuda(), fn,
+                                 with_stats=True)
+        for k in ("episodes", "mean_return", "max_return", "solved_rate"):
+            assert torch.equal(o["stats"][k], o64["stats"][k]), k

@@ -28,8 +28,10 @@ for B in [int(b) for b in (sys.argv[1:] or ["16384", "65536", "262144"])]:
     g.manual_seed(B)
     r = (torch.rand((T, B), generator=g, device="cuda", dtype=torch.float64) < 0.01).double()
     v = torch.rand((T, B), generator=g, device="cuda", dtype=torch.float64)
+    if os.environ.get("GAE_V32"):  # the policy's float32 values (gae_and_scores' f32 entry)
+        v = v.float()
     d = torch.rand((T, B), generator=g, device="cuda") < 0.01
-    last = torch.rand((B,), generator=g, device="cuda", dtype=torch.float64)
+    last = torch.rand((B,), generator=g, device="cuda", dtype=torch.float64).to(v.dtype)
     res = {}
     for fn in ("maxmc", "pvl"):
         ts = []
@@ -43,8 +45,8 @@ for B in [int(b) for b in (sys.argv[1:] or ["16384", "65536", "262144"])]:
             if it >= 2:
                 ts.append(e0.elapsed_time(e1))
         ms = sum(ts) / len(ts)
-        gbs = 33 * B * T / (ms * 1e-3) / 1e9
+        gbs = (29 if v.dtype == torch.float32 else 33) * B * T / (ms * 1e-3) / 1e9
         res[fn] = {"ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / peak, 3),
                    "digest": digest(*[x for x in o.values() if torch.is_tensor(x)])}
     print(json.dumps({"B": B, "kernel": os.environ.get("AMZ_GAE_KERNEL", "0"), "m": os.environ.get("AMZ_GAE_M"),
-                      "u": os.environ.get("AMZ_GAE_U"), **res}), flush=True)
+                      "v32": bool(os.environ.get("GAE_V32")), **res}), flush=True)
