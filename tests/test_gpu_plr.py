@@ -54,6 +54,36 @@ def test_update_tie_heavy_matches_oracle(K, n, pool):
         _assert_same(gpu, ref)
 
 
+@pytest.mark.parametrize("K", [64, 500, 4000])
+def test_update_inplace_runs_then_inserts(K):
+    """Long runs of in-place updates (the PLR/ACCEL replay lanes) followed by inserts and
+    evictions: the deferred heap repair must leave the same buffer as the sequential oracle."""
+    rng = np.random.default_rng(K + 1)
+    pool = 3 * K + 400
+    recs = _pool(pool, seed=K + 1)
+    gpu = LevelBuffer(PlrConfig(buffer_size=K))
+    ref = plr_np.LevelBuffer(K)
+    vals = [0.0, 0.0, -0.0, 0.05, 0.1, 0.1, 0.3, 0.7]
+    keys = {r.tobytes(): i for i, r in enumerate(records_to_rows(recs))}
+    for it in range(5):
+        if it == 0:
+            idx = rng.permutation(pool)[:K]
+        else:
+            lv, *_ = ref.snapshot()
+            present = np.array([keys[r.tobytes()] for r in records_to_rows(lv)])
+            runs = [rng.choice(present, K // 2 + 40),                 # in-place run (with twins)
+                    rng.integers(0, pool, K // 4 + 33),               # new / mixed
+                    rng.choice(present, 64),                          # another run
+                    rng.integers(0, pool, 50)]
+            idx = np.concatenate(runs)
+        n = len(idx)
+        sc = rng.choice(vals, n) + (it % 2) * rng.choice([0.0, 1e-3], n)
+        mx = rng.uniform(0, 1, n)
+        gpu.update(records_to_tensor(recs[idx]), torch.from_numpy(sc), torch.from_numpy(mx), it)
+        ref.update(recs[idx], sc, mx, it)
+        _assert_same(gpu, ref)
+
+
 def test_spec_update_example():
     recs = _pool(3)
     gpu = LevelBuffer(PlrConfig(buffer_size=2))
