@@ -150,6 +150,7 @@ struct SampleSmem {
     double leaf[64];
     int leafinfo[3 * 64 + 4];
     unsigned long long st_total;
+    unsigned long long seq_min, seq_max;
     int rank_slot[kPlrMaxK];
 };
 
@@ -167,16 +168,40 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         return;
     }
     // ---- 1. ranks: sort by seq asc, then stable by score desc ----
+    // seq values are distinct and span a narrow range: the first sort only runs over the
+    // bits of (seq - min seq), with the padding keys (all ones) above every valid key
     using Sort = cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int>;
     unsigned long long keys[4];
     int vals[4];
+    if (tid == 0) {
+        S.seq_min = ~0ull;
+        S.seq_max = 0ull;
+    }
+    __syncthreads();
+    {
+        unsigned long long mn = ~0ull, mx = 0ull;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int i = tid * 4 + k;
+            keys[k] = i < size ? (unsigned long long)D.seq[i] : 0ull;
+            if (i < size) {
+                mn = keys[k] < mn ? keys[k] : mn;
+                mx = keys[k] > mx ? keys[k] : mx;
+            }
+        }
+        atomicMin(&S.seq_min, mn);
+        atomicMax(&S.seq_max, mx);
+    }
+    __syncthreads();
+    const unsigned long long smin = S.seq_min;
+    const int seq_bits = 64 - __clzll((long long)(S.seq_max - smin + 1ull));
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         const int i = tid * 4 + k;
-        keys[k] = i < size ? (unsigned long long)D.seq[i] : ~0ull;
+        keys[k] = i < size ? keys[k] - smin : ~0ull;
         vals[k] = i;
     }
-    Sort(S.sort).Sort(keys, vals);
+    Sort(S.sort).Sort(keys, vals, 0, seq_bits < 1 ? 1 : seq_bits);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -227,10 +252,25 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     }
     __syncthreads();
     if (tid == 0) {
-        double acc = 0.0;
-        for (int i = 0; i < size; i++) {
-            acc = acc + S.p[i];
-            S.p[i] = acc;
+        // numpy's sequential cumsum; the next 16 loads are issued ahead of this block's
+        // stores so only the add chain is serial
+        constexpr int CB = 16;
+        double acc = 0.0, cur[CB], nxt[CB];
+#pragma unroll
+        for (int j = 0; j < CB; j++) cur[j] = j < size ? S.p[j] : 0.0;
+        for (int b = 0; b < size; b += CB) {
+#pragma unroll
+            for (int j = 0; j < CB; j++) nxt[j] = b + CB + j < size ? S.p[b + CB + j] : 0.0;
+#pragma unroll
+            for (int j = 0; j < CB; j++) {
+                acc = acc + cur[j];
+                cur[j] = acc;
+            }
+#pragma unroll
+            for (int j = 0; j < CB; j++)
+                if (b + j < size) S.p[b + j] = cur[j];
+#pragma unroll
+            for (int j = 0; j < CB; j++) cur[j] = nxt[j];
         }
     }
     __syncthreads();
