@@ -248,6 +248,12 @@ class Workload:
                     "final_view": torch.empty((B, v, v), dtype=torch.uint8, device=device),
                     "final_dir": torch.empty((B,), dtype=torch.uint8, device=device)}
         self.root = amz.RngStream.from_seed(seed)
+        # GAE/score results reused every step; scores and max returns share one [2, B]
+        # tensor so the end-to-end result read is a single device->host copy
+        self.res = torch.empty((2, B), dtype=torch.float64, device=device)
+        self.gout = {"advantages": torch.empty((T, B), dtype=torch.float64, device=device),
+                     "returns": torch.empty((T, B), dtype=torch.float64, device=device),
+                     "scores": self.res[0], "max_returns": self.res[1]}
         # our kernels per step: k_env_reset_dr, k_dyn, k_render, k_gae_score4
         self.launches_per_step = 4
         self.ev_roll = None
@@ -265,7 +271,7 @@ class Workload:
         if timing is not None:
             timing[1].record()
         o = amz.gae_and_scores(traj.rewards, self.values if values is None else values, traj.dones,
-                               self.last if last is None else last, 0.995, 0.95)
+                               self.last if last is None else last, 0.995, 0.95, out=self.gout)
         if timing is not None:
             timing[2].record()
         return o
@@ -321,8 +327,7 @@ def run_ours(args, rank, world, local_rank):
     h_val.copy_(wl.values.cpu())
     h_last = amz_pinned_empty((B,), torch.float64)
     h_last.copy_(wl.last.cpu())
-    h_sc = amz_pinned_empty((B,), torch.float64)
-    h_mx = amz_pinned_empty((B,), torch.float64)
+    h_res = amz_pinned_empty((2, B), torch.float64)
     d_act = torch.empty_like(wl.actions)
     d_val = torch.empty_like(wl.values)
     d_last = torch.empty_like(wl.last)
@@ -335,9 +340,8 @@ def run_ours(args, rank, world, local_rank):
         d_act.copy_(h_act, non_blocking=True)
         d_val.copy_(h_val, non_blocking=True)
         d_last.copy_(h_last, non_blocking=True)
-        o = wl.step(10_000 + i, actions=d_act, values=d_val, last=d_last)
-        h_sc.copy_(o["scores"], non_blocking=True)
-        h_mx.copy_(o["max_returns"], non_blocking=True)
+        wl.step(10_000 + i, actions=d_act, values=d_val, last=d_last)
+        h_res.copy_(wl.res, non_blocking=True)  # scores | max returns
         e2e_ev[i][1].record()
     torch.cuda.synchronize()
     seq_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
@@ -361,7 +365,7 @@ def run_ours(args, rank, world, local_rank):
         h_in[nv + nl:].copy_(h_act.reshape(-1))
         d_in = [torch.empty_like(h_in, device=dev) for _ in range(2)]
         bufs = [(d[nv + nl:].view(T, B), d[:nv].view(vdt).view(T, B), d[nv:nv + nl].view(vdt)) for d in d_in]
-        outs = [(amz_pinned_empty(B, torch.float64), amz_pinned_empty(B, torch.float64)) for _ in range(2)]
+        outs = [amz_pinned_empty((2, B), torch.float64) for _ in range(2)]
         copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
         freed = [torch.cuda.Event() for _ in range(2)]
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -395,9 +399,8 @@ def run_ours(args, rank, world, local_rank):
             main.wait_event(copied[k][1])
             flush.fill_(i & 0xFF)
             a, v, l_ = bufs[k]
-            o = wl.step(step0 + i, actions=a, values=v, last=l_)
-            outs[k][0].copy_(o["scores"], non_blocking=True)
-            outs[k][1].copy_(o["max_returns"], non_blocking=True)
+            wl.step(step0 + i, actions=a, values=v, last=l_)
+            outs[k].copy_(wl.res, non_blocking=True)  # scores | max returns
             freed[k].record(main)
         p1.record(main)
         host_ms = (time.perf_counter() - host0) * 1e3 / args.steps

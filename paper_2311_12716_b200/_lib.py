@@ -120,6 +120,14 @@ def ptr(t) -> int | None:
 
 
 def stream_handle(device=None) -> int:
+    """Raw cudaStream_t of torch's current stream on ``device`` (per call: the caller may
+    have switched streams).  torch's raw-stream query skips the Stream object."""
     import torch
 
-    return torch.cuda.current_stream(device).cuda_stream
+    if device is None:
+        idx = torch.cuda.current_device()
+    elif isinstance(device, int):
+        idx = device
+    else:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(idx)

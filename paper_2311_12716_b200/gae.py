@@ -48,13 +48,16 @@ def _stats_struct(B, device):
 
 
 def gae_and_scores(rewards, values, dones, last_value, gamma: float, lam: float, prior_max_returns=None,
-                   score_fn: str = "maxmc", maxmc_discounted: bool = False, with_stats: bool = False):
+                   score_fn: str = "maxmc", maxmc_discounted: bool = False, with_stats: bool = False,
+                   out: dict | None = None):
     """One launch: advantages, returns, per-lane scores, running max returns (+ stats).
 
     Equals ``compute_gae`` followed by ``lane_scores(traj, adv, prior, cfg, gamma)``.
     ``values`` and ``last_value`` may both be float32 tensors -- the policy's own output
     dtype, which the reference widens with ``value.double()`` (agents/ppo.py:96) -- and are
-    then widened inside the kernel (bit-identical results, half the value bytes)."""
+    then widened inside the kernel (bit-identical results, half the value bytes).
+    ``out`` may supply the result tensors (keys advantages, returns [T, B] and scores,
+    max_returns [B], float64, contiguous, on the device) to keep a loop allocation-free."""
     torch = _torch()
     dev = _device_of(rewards, values, dones, last_value)
     r = _dev(rewards, torch.float64, dev)
@@ -69,10 +72,20 @@ def gae_and_scores(rewards, values, dones, last_value, gamma: float, lam: float,
     if d.shape != r.shape or last.numel() != B:
         raise ShapeError("dones must be [T, B] and last_value [B]")
     prior = None if prior_max_returns is None else _dev(prior_max_returns, torch.float64, dev).reshape(-1)
-    adv = torch.empty_like(r)
-    ret = torch.empty_like(r)
-    scores = torch.empty(B, dtype=torch.float64, device=dev)
-    maxret = torch.empty(B, dtype=torch.float64, device=dev)
+    o = out or {}
+
+    def _out(k, shape):
+        t = o.get(k)
+        if t is None:
+            return torch.empty(shape, dtype=torch.float64, device=dev)
+        if tuple(t.shape) != shape or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ShapeError(f"out[{k!r}] must be a contiguous float64 {shape} tensor on {dev}")
+        return t
+
+    adv = _out("advantages", (T, B))
+    ret = _out("returns", (T, B))
+    scores = _out("scores", (B,))
+    maxret = _out("max_returns", (B,))
     stats, cst = _stats_struct(B, dev) if with_stats else (None, None)
     fn = {"maxmc": _lib.AMZ_SCORE_MAXMC, "pvl": _lib.AMZ_SCORE_PVL}[score_fn]
     with torch.cuda.device(dev):

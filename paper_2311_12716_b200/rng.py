@@ -33,11 +33,12 @@ def _u32_words(x: int) -> list[int]:
 class RngStream:
     """Immutable key (entropy, key) naming one numpy-compatible random stream."""
 
-    __slots__ = ("_entropy", "_key")
+    __slots__ = ("_entropy", "_key", "_prefix")
 
     def __init__(self, entropy, key: tuple = ()):
         self._entropy = entropy
         self._key = tuple(int(k) for k in key)
+        self._prefix = None
 
     @classmethod
     def from_seed(cls, seed: int) -> "RngStream":
@@ -60,7 +61,11 @@ class RngStream:
         return RngStream(self._entropy, self._key + (int(data),))
 
     def seed_prefix(self) -> _lib.AmzSeed:
-        """SeedSequence state after this stream's key; device lanes append suffix words."""
+        """SeedSequence state after this stream's key; device lanes append suffix words.
+        Streams are immutable values, so the prefix is computed once per stream (a reset
+        and the rollout that follows it both absorb the same wrapper key)."""
+        if self._prefix is not None:
+            return self._prefix
         run = _u32_words(self._entropy)
         key = [w for k in self._key for w in _u32_words(k)]
         ra = (ctypes.c_uint32 * len(run))(*run)
@@ -68,10 +73,14 @@ class RngStream:
         out = _lib.AmzSeed()
         _lib.call("amz_seed_prefix", ctypes.cast(ra, ctypes.c_void_p), len(run),
                   ctypes.cast(ka, ctypes.c_void_p), len(key), ctypes.byref(out))
+        self._prefix = out
         return out
 
     def __repr__(self) -> str:
         return f"RngStream(entropy={self._entropy}, key={self._key})"
+
+    def __reduce__(self):
+        return (RngStream, (self._entropy, self._key))  # the cached prefix is not part of the value
 
     def __eq__(self, other) -> bool:
         return isinstance(other, RngStream) and (self._entropy, self._key) == (other._entropy, other._key)
