@@ -27,3 +27,22 @@ for i in range(200):
 pr.disable()
 torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+
+# per-call host cost (no profiler): reset, rollout_actions, gae_and_scores
+amz = wl.amz
+res = wl.env.reset(wl.root.fold_in(0), wl.p)
+traj, _ = amz.rollout_actions(wl.env, res, wl.actions, wl.p, out=wl.out)
+torch.cuda.synchronize()
+N = 200
+t0 = time.perf_counter()
+for i in range(N):
+    res = wl.env.reset(wl.root.fold_in(i), wl.p)
+t1 = time.perf_counter()
+for i in range(N):
+    amz.rollout_actions(wl.env, res, wl.actions, wl.p, out=wl.out)
+t2 = time.perf_counter()
+for i in range(N):
+    amz.gae_and_scores(traj.rewards, wl.values, traj.dones, wl.last, 0.995, 0.95, out=wl.gout)
+t3 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"reset {(t1 - t0) / N * 1e6:.1f} us  rollout {(t2 - t1) / N * 1e6:.1f} us  gae {(t3 - t2) / N * 1e6:.1f} us")
