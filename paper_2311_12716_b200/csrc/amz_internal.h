@@ -2,11 +2,40 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/amaze_b200.h"
 #include "amz_level.cuh"
 
 namespace amz {
+
+// Programmatic dependent launch along the rollout chain (k_env_reset_dr -> k_dyn ->
+// k_render -> GAE): a dependent kernel is launched with launch_pdl, runs its
+// shared-memory-only prologue, then pdl_wait() -- which returns once the preceding grid
+// has completed and its writes are visible -- before touching global memory the
+// preceding kernels write.  No kernel triggers early (pdl_trigger): measured on B200,
+// dependents launched at the start of k_dyn parked their CTAs on the SMs and slowed it
+// (step 0.152 -> 0.156 ms), while the implicit trigger at completion gains ~1-3%
+// (launch processing and the dependents' prologues overlap the tail).  Both are no-ops
+// for ordinary launches; AMZ_NO_PDL=1 launches without the attribute (A/B runs).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool off = getenv("AMZ_NO_PDL") != nullptr;  // A/B runs
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // device view of an amz_env_t
 struct EnvDev {

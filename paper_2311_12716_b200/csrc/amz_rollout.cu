@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
     if (use_lut)
         for (int tt = threadIdx.x; tt <= G.tep; tt += blockDim.x) s_rew[tt] = goal_reward(tt, G.tep);
     __syncthreads();
+    pdl_wait();  // lane state from the reset
     const int64_t B = E.B;
     DYN_MARK(0);
     const int64_t lane0 = ((int64_t)blockIdx.x * WPC + warp) * LPW;
@@ -649,6 +650,7 @@ __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, con
     __shared__ uint64_t s_spread[32];
     __shared__ int64_t s_t0;
     init_spread(s_spread);
+    pdl_wait();  // poses / epochs from k_dyn
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
         const int buf = it & 1;
@@ -723,8 +725,9 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
         k_spec_levels<<<(unsigned)((E.B + 4 * kSpecLPW - 1) / (4 * kSpecLPW)), 128, 0, s>>>(G, E, T, wrap, step0, spec,
                                                                                            spec_step);
     const int64_t warps = (E.B + LPW - 1) / LPW;
-    k_dyn<LPW, WPC><<<(unsigned)((warps + WPC - 1) / WPC), 32 * WPC, sm, s>>>(
-        G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, avec, use_lut);
+    launch_pdl(k_dyn<LPW, WPC>, dim3((unsigned)((warps + WPC - 1) / WPC)), dim3(32 * WPC), sm, s, G, E, T, actions,
+               mode, wrap, step0, reward, done, poses, epochs, final_pose, (const amz_level_t *)spec,
+               (const uint32_t *)spec_step, avec, use_lut);
 }
 
 template <int V, bool SEE>
@@ -735,8 +738,8 @@ static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *po
     const int bulk = al16(view) && al16(dirs) && al16(done) && al16(fview) && al16(fdir);
     const int64_t g1 = (n + 127) / 128, g2 = fview ? (B + 127) / 128 : 0, nt = g1 + g2;
     const int64_t grid = nt < 148 * 12 ? nt : 148 * 12;
-    k_render<V, SEE><<<(unsigned)grid, 128, 0, s>>>(G, B, n, poses, final_pose, epochs, view, dirs, reward, done, fview,
-                                                    fdir, bulk, g1, nt);
+    launch_pdl(k_render<V, SEE>, dim3((unsigned)grid), dim3(128), 0, s, G, B, n, poses, final_pose, epochs, view, dirs,
+               reward, done, fview, fdir, bulk, g1, nt);
 }
 
 int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode,

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(64) k_gae_score(int T, int64_t B, const double
                                                   int64_t *__restrict__ st_eps, double *__restrict__ st_mean,
                                                   double *__restrict__ st_max, double *__restrict__ st_solved,
                                                   const int do_gae, const PairwisePlan P) {
+    pdl_wait();  // rewards / dones from the rollout (launch_pdl)
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= B) return;
     const bool noclamp = (score_fn & AMZ_SCORE_NOCLAMP) != 0;
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(64) k_gae_score2(int T, int64_t B, const doubl
                                                    const int do_gae, const PairwisePlan P) {
     __shared__ double s_mx[32];
     __shared__ double s_leaf[kMaxLeaves][32];
+    pdl_wait();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t l = (int64_t)blockIdx.x * 32 + lane;
     const bool live = l < B;
@@ -390,6 +392,7 @@ __global__ void __launch_bounds__(128) k_gae_score4(int T, int64_t B, const doub
                                                     const PairwisePlan P) {
     extern __shared__ __align__(16) uint8_t g4raw[];
     G4Smem<kG4LW, VT> &S = *reinterpret_cast<G4Smem<kG4LW, VT> *>(g4raw);
+    pdl_wait();
     constexpr int CR = kG4LW / 2;                            // 16-B chunks per row of r
     constexpr int CV = kG4LW * (int)sizeof(VT) / 16;         // ... and of v
     constexpr int EV = 16 / (int)sizeof(VT);                 // values per chunk
@@ -570,6 +573,7 @@ __global__ void __launch_bounds__(128) k_gae_score7(int T, int64_t B, const doub
                                                     const PairwisePlan P) {
     extern __shared__ __align__(16) uint8_t g7raw[];
     G7Smem<VT, kA> &S = *reinterpret_cast<G7Smem<VT, kA> *>(g7raw);
+    pdl_wait();
     constexpr int CR = kG7LW / 2;                     // 16-B chunks per row of r
     constexpr int CV = kG7LW * (int)sizeof(VT) / 16;  // ... and of v
     constexpr int EV = 16 / (int)sizeof(VT);          // values per chunk
@@ -745,16 +749,14 @@ static int launch_gae_score_t(int T, int64_t B, const double *r, const VT *v, co
         if (lw == 16 || gsel == 4) {
             const size_t sm = sizeof(G4Smem<16, VT>);
             cudaFuncSetAttribute(k_gae_score4<16, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_gae_score4<16, VT><<<(unsigned)(B / 16), 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn,
-                                                                     disc, adv, ret, scores, maxret, s_eps, s_mean,
-                                                                     s_max, s_sol, P);
+            launch_pdl(k_gae_score4<16, VT>, dim3((unsigned)(B / 16)), dim3(128), sm, s, T, B, r, v, d, last, gamma, gl,
+                       prior, score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol, P);
             return 0;
         }
         const size_t sm = sizeof(G4Smem<8, VT>);
         cudaFuncSetAttribute(k_gae_score4<8, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_gae_score4<8, VT><<<(unsigned)(B / 8), 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc,
-                                                               adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol,
-                                                               P);
+        launch_pdl(k_gae_score4<8, VT>, dim3((unsigned)(B / 8)), dim3(128), sm, s, T, B, r, v, d, last, gamma, gl, prior,
+                   score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol, P);
         return 0;
     }
     if (g7 && (gsel == 0 || gsel == 7)) {
@@ -769,8 +771,8 @@ static int launch_gae_score_t(int T, int64_t B, const double *r, const VT *v, co
             const int m = m7 > 0 && m7 < occ ? m7 : occ;
             const int64_t ng = B / kG7LW;
             const unsigned grid = (unsigned)(ng < (int64_t)nsm * m ? ng : (int64_t)nsm * m);
-            kern<<<grid, 128, sm, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret,
-                                       s_eps, s_mean, s_max, s_sol, P);
+            launch_pdl(kern, dim3(grid), dim3(128), sm, s, T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret,
+                       scores, maxret, s_eps, s_mean, s_max, s_sol, P);
         };
         // f64 values: PVL's advantages overwrite V in place; f32 values: a separate column
         if (sizeof(VT) == 8 || (score_fn & 0xFF) != AMZ_SCORE_PVL)
@@ -781,16 +783,14 @@ static int launch_gae_score_t(int T, int64_t B, const double *r, const VT *v, co
     }
 k2:
     if (gsel == 2 || B <= 131072) {
-        k_gae_score2<VT><<<(unsigned)((B + 31) / 32), 64, 0, s>>>(T, B, r, v, d, last, gamma, gl, prior, score_fn, disc,
-                                                                 adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol,
-                                                                 do_gae, P);
+        launch_pdl(k_gae_score2<VT>, dim3((unsigned)((B + 31) / 32)), dim3(64), 0, s, T, B, r, v, d, last, gamma, gl,
+                   prior, score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol, do_gae, P);
         return 0;
     }
 k1:
     const int threads = B >= 148 * 64 ? 64 : 32;
-    k_gae_score<VT><<<(unsigned)((B + threads - 1) / threads), threads, 0, s>>>(
-        T, B, r, v, d, last, gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol,
-        do_gae, P);
+    launch_pdl(k_gae_score<VT>, dim3((unsigned)((B + threads - 1) / threads)), dim3(threads), 0, s, T, B, r, v, d, last,
+               gamma, gl, prior, score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol, do_gae, P);
     return 0;
 }
 
