@@ -42,7 +42,7 @@ GAE_BYTES_PER_ELEM = 33  # r f64 + V f64 + done u8 in, A f64 + R f64 out
 def _traffic():
     """Per-launch DRAM bytes of the roofline kernels from the committed ncu capture."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1i_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1m_traffic.json")) as f:
             return json.load(f)
     except (OSError, ValueError):
         return {}
@@ -469,7 +469,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
                      "frac": roll_gbs / peak,
                      "traffic": _traffic().get("k_env_rollout", {}).get("dram_bytes"),
-                     "traffic_source": "profiles/r1i_traffic.json (ncu --set full, per launch)",
+                     "traffic_source": "profiles/r1m_traffic.json (ncu --set full, per launch)",
                      "peak_source": src,
                      "algorithmic_bytes": f"{ENV_BYTES_PER_STEP} B/env-step x {B * T} env-steps per launch",
                      "kernel_ms": roll,
