@@ -528,9 +528,9 @@ def measure_plr(dev, n_per_gpu, T, accel, iters, flush, world):
     # with 4096 replays of buffered levels (in-place updates)
     new_lv = amz.sample_levels(amz.RngStream(99, (0,)), 4096, amz.StaticParams(), device=dev)
     sc = torch.rand(4096, device=dev, dtype=torch.float64)
-    old_lv = plr.buffer.export()["levels"][:4000]
     sc2 = torch.rand(4000, device=dev, dtype=torch.float64)
     t_upd = _timed(lambda i: plr.buffer.update(new_lv, sc, sc, 1000 + i), iters, flush, torch)
+    old_lv = plr.buffer.export()["levels"][:4000]  # exported after t_upd: every level is buffered
     t_rep = _timed(lambda i: plr.buffer.update(old_lv, sc2, sc2, 1000 + i), iters, flush, torch)
     t_smp = _timed(lambda i: plr.buffer.sample(amz.RngStream(5, (i,)), n_per_gpu * world, 2000 + i), iters, flush,
                    torch)

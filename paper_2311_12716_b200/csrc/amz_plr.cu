@@ -350,6 +350,8 @@ struct UpdSmem {
     int n_rel;
     int full;
     int size;
+    int rcur;     // next chunk position for warp 0
+    int bulk_hi;  // end of the in-place run to apply in bulk (-1 = none)
 };
 static_assert(sizeof(CandChunk) <= sizeof(uint32_t) * kHash, "chunk must fit in the hash table space");
 
@@ -440,6 +442,26 @@ __device__ __forceinline__ void heap_down_t(UpdSmem &S, int h, int n) {
     }
     heap_put(S, h, xk, xt, xs);
 }
+
+// the buffer slot candidate r of the staged chunk updates in place, or -1
+__device__ __forceinline__ int cand_present(const UpdSmem &S, const UpdScratch &W, int r) {
+    const int im = S.u.chunk.im[r];
+    if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) return im;
+    const int f = S.u.chunk.tf[r];
+    return f != S.u.chunk.cid[r] ? W.keyslot[f] : -1;
+}
+// length of the run of consecutive in-place candidates starting at r (whole warp)
+__device__ __forceinline__ int inplace_run(const UpdSmem &S, const UpdScratch &W, int r, int cn, int lane) {
+    int L = 0;
+    while (true) {
+        const int i = r + L + lane;
+        const bool pr = i < cn && cand_present(S, W, i) >= 0;
+        const unsigned fail = ~__ballot_sync(0xFFFFFFFFu, pr);
+        if (fail) return L + __ffs(fail) - 1;
+        L += 32;
+    }
+}
+constexpr int kBulkRun = 64;  // shorter in-place runs stay on the sequential warp path
 
 __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
                                 int64_t hsize) {
@@ -585,10 +607,18 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     // A skipped first occurrence is never inserted (score <= mlow), so its later twins,
     // which are always relevant, correctly find no entry for the key (keyslot = -1).
 
-    // ---- C: ordered replay by one thread ----
+    // ---- C: ordered replay (warp 0); long in-place runs applied by the whole CTA ----
+    // In-place updates never change which later candidates find their key (only fills and
+    // evictions do), so warp 0 scans ahead for the run of consecutive in-place candidates
+    // starting at r.  A run of >= kBulkRun is applied in bulk: the last candidate per slot
+    // wins (atomicMax on the candidate index, which is increasing along the order), and the
+    // heap is rebuilt level-parallel.  (score, last_sampled, seq) is a total order (seq is
+    // unique), so the heap's shape never affects which entry is the minimum.
     const int nrel = S.n_rel;
-    int size = size0;
-    int64_t next_seq = D.meta[1];
+    if (tid == 0) {
+        S.size = size0;
+        S.next_seq = D.meta[1];
+    }
     for (int base = 0; base < nrel; base += kChunk) {
         const int cn = (nrel - base) < kChunk ? (nrel - base) : kChunk;
         __syncthreads();
@@ -599,62 +629,92 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             S.u.chunk.tf[i] = W.twin_first[c];
             S.u.chunk.im[i] = W.init_match[c];
         }
+        if (tid == 0) S.rcur = 0;
         __syncthreads();
-        if (tid >= 32) continue;
-        for (int r = 0; r < cn; r++) {
-            const int c = S.u.chunk.cid[r];
-            const double sc = S.u.chunk.sc[r];
-            const int f = S.u.chunk.tf[r];
-            const int im = S.u.chunk.im[r];
-            int present = -1;
-            if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
-            if (present < 0 && f != c) present = W.keyslot[f];
-            const uint64_t sk = score_key(sc);
-            if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
-                const int h = S.pos[present];
-                const uint64_t ok = S.hk[h], ot = S.ht[h];
+        while (true) {
+            if (tid < 32) {
+                int size = S.size;
+                int64_t next_seq = S.next_seq;
+                int r = S.rcur, scan_end = r, bulk_hi = -1;
+                for (; r < cn; r++) {
+                    if (r >= scan_end) {
+                        const int L = inplace_run(S, W, r, cn, lane);
+                        if (L >= kBulkRun) {
+                            bulk_hi = r + L;
+                            break;
+                        }
+                        scan_end = r + L + 1;
+                    }
+                    const int c = S.u.chunk.cid[r];
+                    const double sc = S.u.chunk.sc[r];
+                    const int f = S.u.chunk.tf[r];
+                    const int present = cand_present(S, W, r);
+                    const uint64_t sk = score_key(sc);
+                    if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
+                        const int h = S.pos[present];
+                        const uint64_t ok = S.hk[h], ot = S.ht[h];
+                        __syncwarp();
+                        if (lane == 0) S.mr_src[present] = c;
+                        if (sk < ok)
+                            sift_up_w(S, h, sk, ot, present, lane);
+                        else if (sk > ok)
+                            sift_down_w(S, h, size, sk, ot, present, lane);
+                        __syncwarp();
+                        continue;
+                    }
+                    const uint64_t tbn = ((uint64_t)iter << 32) | (uint32_t)next_seq;
+                    int slot;
+                    if (size < K) {  // fill
+                        slot = size;
+                        const int h = size++;
+                        __syncwarp();
+                        sift_up_w(S, h, sk, tbn, slot, lane);
+                    } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
+                        if (!(sk > S.hk[0])) continue;
+                        slot = S.hslot[0];
+                        const int ow = S.owner[slot];
+                        __syncwarp();
+                        if (lane == 0 && ow >= 0) W.keyslot[ow] = -1;
+                        sift_down_w(S, 0, size, sk, tbn, slot, lane);
+                    }
+                    if (lane == 0) {
+                        S.owner[slot] = f;
+                        S.replaced[slot >> 5] |= 1u << (slot & 31);
+                        S.src[slot] = c;
+                        S.mr_src[slot] = c;
+                        W.keyslot[f] = slot;
+                    }
+                    __syncwarp();
+                    next_seq++;
+                }
                 __syncwarp();
-                if (lane == 0) S.mr_src[present] = c;
-                if (sk < ok)
-                    sift_up_w(S, h, sk, ot, present, lane);
-                else if (sk > ok)
-                    sift_down_w(S, h, size, sk, ot, present, lane);
-                __syncwarp();
-                continue;
+                if (lane == 0) {
+                    S.size = size;
+                    S.next_seq = next_seq;
+                    S.rcur = r;
+                    S.bulk_hi = bulk_hi;
+                }
             }
-            const uint64_t tbn = ((uint64_t)iter << 32) | (uint32_t)next_seq;
-            int slot;
-            if (size < K) {  // fill
-                slot = size;
-                const int h = size++;
-                __syncwarp();
-                sift_up_w(S, h, sk, tbn, slot, lane);
-            } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
-                if (!(sk > S.hk[0])) continue;
-                slot = S.hslot[0];
-                const int ow = S.owner[slot];
-                __syncwarp();
-                if (lane == 0 && ow >= 0) W.keyslot[ow] = -1;
-                sift_down_w(S, 0, size, sk, tbn, slot, lane);
+            __syncthreads();
+            const int lo = S.rcur, hi = S.bulk_hi;
+            if (hi < 0) break;
+            for (int i = lo + tid; i < hi; i += blockDim.x) atomicMax(&S.mr_src[cand_present(S, W, i)], S.u.chunk.cid[i]);
+            __syncthreads();
+            for (int i = lo + tid; i < hi; i += blockDim.x) {
+                const int p = cand_present(S, W, i);
+                if (S.mr_src[p] == S.u.chunk.cid[i]) S.hk[S.pos[p]] = score_key(S.u.chunk.sc[i]);
             }
-            if (lane == 0) {
-                S.owner[slot] = f;
-                S.replaced[slot >> 5] |= 1u << (slot & 31);
-                S.src[slot] = c;
-                S.mr_src[slot] = c;
-                W.keyslot[f] = slot;
+            const int hs = S.size;
+            const int starts[4] = {0, 1, 33, 1057};
+            for (int lv = 2; lv >= 0; lv--) {
+                __syncthreads();
+                const int l0 = starts[lv], l1 = min(starts[lv + 1], hs);
+                for (int h = l0 + tid; h < l1; h += blockDim.x) heap_down_t(S, h, hs);
             }
-            __syncwarp();
-            next_seq++;
+            __syncthreads();
+            if (tid == 0) S.rcur = hi;
+            __syncthreads();
         }
-        if (lane == 0) {
-            S.size = size;
-            S.next_seq = next_seq;
-        }
-    }
-    if (tid == 0 && nrel == 0) {
-        S.size = size;
-        S.next_seq = next_seq;
     }
     __syncthreads();
     // ---- epilogue: scatter the heap back to slots, deferred level / max_return copies ----

@@ -84,6 +84,36 @@ def test_update_inplace_runs_then_inserts(K):
         _assert_same(gpu, ref)
 
 
+@pytest.mark.parametrize("K", [300, 4000])
+def test_update_bulk_run_boundaries(K):
+    """In-place runs of lengths around the bulk threshold (63/64/65 ...) separated by single
+    inserts, with in-place scores that often drop below the minimum so the next insert
+    evicts an entry the run just rewrote (bulk heap rebuild vs sequential sifts)."""
+    rng = np.random.default_rng(K + 7)
+    pool = 3 * K + 400
+    recs = _pool(pool, seed=K + 7)
+    gpu = LevelBuffer(PlrConfig(buffer_size=K))
+    ref = plr_np.LevelBuffer(K)
+    keys = {r.tobytes(): i for i, r in enumerate(records_to_rows(recs))}
+    for it in range(4):
+        if it == 0:
+            idx = rng.permutation(pool)[:K]
+        else:
+            lv, *_ = ref.snapshot()
+            present = np.array([keys[r.tobytes()] for r in records_to_rows(lv)])
+            parts = []
+            for L in [63, 64, 65, 1, 0, 128, 31, 64, 900, 2, 64, 1100]:
+                parts.append(rng.choice(present, L))
+                parts.append(rng.integers(0, pool, 1 + (L % 3)))
+            idx = np.concatenate(parts)
+        n = len(idx)
+        sc = rng.choice([0.0, 0.01, 0.2, 0.5, 0.9], n) + rng.choice([0.0, 1e-3], n)
+        mx = rng.uniform(0, 1, n)
+        gpu.update(records_to_tensor(recs[idx]), torch.from_numpy(sc), torch.from_numpy(mx), it)
+        ref.update(recs[idx], sc, mx, it)
+        _assert_same(gpu, ref)
+
+
 def test_spec_update_example():
     recs = _pool(3)
     gpu = LevelBuffer(PlrConfig(buffer_size=2))
