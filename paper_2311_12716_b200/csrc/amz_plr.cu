@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 //                     drops below m_low), so it is skipped; everything else is
 //                     "relevant" and compacted in order.
 //   C  (one warp)     replays the relevant candidates in order against an indexed
-//                     32-ary min-heap of (score, tb) in shared memory, tb = last_sampled
+//                     64-ary min-heap of (score, tb) in shared memory, tb = last_sampled
 //                     << 32 | seq (the stale-first eviction order): an in-place update is
 //                     one sift, an eviction is replace-top + sift-down, candidate data are
 //                     prefetched into shared memory by the whole CTA chunk by chunk, and
@@ -378,20 +378,30 @@ __device__ __forceinline__ unsigned warp_argmin_word(unsigned eq, uint32_t v, in
     const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, in ? v : 0xFFFFFFFFu);
     return __ballot_sync(0xFFFFFFFFu, in && v == m);
 }
-// 32-ary min-heap (children of h are 32h+1 .. 32h+32; 4096 entries -> 3 levels below the
-// root).  The entry x = (xk, xt, xs) is sifted from the hole h: each level is one coalesced
-// load of the 32 children by the warp, a ballot of "child < x" and a redux arg-min; the
-// winning lane moves its child into the hole.  Whole warp, uniform control flow.
+// 64-ary min-heap (children of h are 64h+1 .. 64h+64; up to 4160 entries -> 2 levels below
+// the root).  The entry x = (xk, xt, xs) is sifted from the hole h: at each level lane l
+// loads children 64h+1+2l and 64h+2+2l and keeps the smaller, then a ballot of "child < x"
+// and a redux arg-min over the lanes; the winning lane moves its child into the hole.
+// Whole warp, uniform control flow.
 __device__ __forceinline__ void sift_down_w(UpdSmem &S, int h, int n, uint64_t xk, uint64_t xt, int xs, int lane) {
     while (true) {
-        const int c = 32 * h + 1 + lane;
-        const bool valid = c < n;
+        const int c0 = 64 * h + 1 + 2 * lane;
         uint64_t ck = ~0ull, ct = ~0ull;
-        int cs = 0;
+        int cs = 0, cc = c0;
+        const bool valid = c0 < n;
         if (valid) {
-            ck = S.hk[c];
-            ct = S.ht[c];
-            cs = S.hslot[c];
+            ck = S.hk[c0];
+            ct = S.ht[c0];
+            cs = S.hslot[c0];
+            if (c0 + 1 < n) {
+                const uint64_t k1 = S.hk[c0 + 1], t1 = S.ht[c0 + 1];
+                if (ukey_lt(k1, t1, ck, ct)) {
+                    ck = k1;
+                    ct = t1;
+                    cs = S.hslot[c0 + 1];
+                    cc = c0 + 1;
+                }
+            }
         }
         unsigned eq = __ballot_sync(0xFFFFFFFFu, valid && ukey_lt(ck, ct, xk, xt));
         if (eq == 0u) break;
@@ -401,14 +411,14 @@ __device__ __forceinline__ void sift_down_w(UpdSmem &S, int h, int n, uint64_t x
         if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)ct, lane);
         const int win = __ffs(eq) - 1;
         if (lane == win) heap_put(S, h, ck, ct, cs);
-        h = 32 * h + 1 + win;
+        h = __shfl_sync(0xFFFFFFFFu, cc, win);
     }
     if (lane == 0) heap_put(S, h, xk, xt, xs);
     __syncwarp();
 }
 __device__ __forceinline__ void sift_up_w(UpdSmem &S, int h, uint64_t xk, uint64_t xt, int xs, int lane) {
     while (h > 0) {
-        const int p = (h - 1) >> 5;
+        const int p = (h - 1) >> 6;
         const uint64_t pk = S.hk[p], pt = S.ht[p];
         if (!ukey_lt(xk, xt, pk, pt)) break;
         const int ps = S.hslot[p];
@@ -423,9 +433,9 @@ __device__ __forceinline__ void heap_down_t(UpdSmem &S, int h, int n) {
     const uint64_t xk = S.hk[h], xt = S.ht[h];
     const int xs = S.hslot[h];
     while (true) {
-        const int c0 = 32 * h + 1;
+        const int c0 = 64 * h + 1;
         if (c0 >= n) break;
-        const int ce = c0 + 32 < n ? c0 + 32 : n;
+        const int ce = c0 + 64 < n ? c0 + 64 : n;
         int m = c0;
         uint64_t mk = S.hk[c0], mt = S.ht[c0];
         for (int c = c0 + 1; c < ce; c++) {
@@ -569,9 +579,9 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         S.mlow = m;
     }
     // ---- heapify, level-parallel (all sift-downs of one level touch disjoint subtrees) ----
-    // level starts of the 32-ary heap: 0, 1, 33, 1057
+    // level starts of the 64-ary heap: 0, 1, 65, 4161
     {
-        const int starts[4] = {0, 1, 33, 1057};
+        const int starts[4] = {0, 1, 65, 4161};
         for (int lv = 2; lv >= 0; lv--) {
             __syncthreads();
             const int lo = starts[lv], hi = min(starts[lv + 1], size0);
@@ -636,19 +646,37 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 int size = S.size;
                 int64_t next_seq = S.next_seq;
                 int r = S.rcur, scan_end = r, bulk_hi = -1;
+                // candidate fields are prefetched one ahead (the replaced bit and the twin's
+                // keyslot are read after the previous candidate is applied)
+                int c_n = 0, f_n = 0, im_n = -1;
+                double sc_n = 0.0;
+                if (r < cn) {
+                    c_n = S.u.chunk.cid[r];
+                    sc_n = S.u.chunk.sc[r];
+                    f_n = S.u.chunk.tf[r];
+                    im_n = S.u.chunk.im[r];
+                }
                 for (; r < cn; r++) {
-                    if (r >= scan_end) {
+                    const int c = c_n, f = f_n, im = im_n;
+                    const double sc = sc_n;
+                    if (r + 1 < cn) {
+                        c_n = S.u.chunk.cid[r + 1];
+                        sc_n = S.u.chunk.sc[r + 1];
+                        f_n = S.u.chunk.tf[r + 1];
+                        im_n = S.u.chunk.im[r + 1];
+                    }
+                    int present = -1;
+                    if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
+                    if (present < 0 && f != c) present = W.keyslot[f];
+                    // only an in-place candidate can open a run worth applying in bulk
+                    if (present >= 0 && r >= scan_end) {
                         const int L = inplace_run(S, W, r, cn, lane);
                         if (L >= kBulkRun) {
                             bulk_hi = r + L;
                             break;
                         }
-                        scan_end = r + L + 1;
+                        scan_end = r + L;
                     }
-                    const int c = S.u.chunk.cid[r];
-                    const double sc = S.u.chunk.sc[r];
-                    const int f = S.u.chunk.tf[r];
-                    const int present = cand_present(S, W, r);
                     const uint64_t sk = score_key(sc);
                     if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
                         const int h = S.pos[present];
@@ -705,7 +733,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 if (S.mr_src[p] == S.u.chunk.cid[i]) S.hk[S.pos[p]] = score_key(S.u.chunk.sc[i]);
             }
             const int hs = S.size;
-            const int starts[4] = {0, 1, 33, 1057};
+            const int starts[4] = {0, 1, 65, 4161};
             for (int lv = 2; lv >= 0; lv--) {
                 __syncthreads();
                 const int l0 = starts[lv], l1 = min(starts[lv + 1], hs);
