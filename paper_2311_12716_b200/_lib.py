@@ -129,5 +129,6 @@ def stream_handle(device=None) -> int:
     elif isinstance(device, int):
         idx = device
     else:
+        device = torch.device(device)  # accepts "cuda:0" strings as well as torch.device
         idx = device.index if device.index is not None else torch.cuda.current_device()
     return torch._C._cuda_getCurrentRawStream(idx)

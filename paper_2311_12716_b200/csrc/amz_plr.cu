@@ -144,8 +144,12 @@ __device__ double block_pairwise_sum(const double *x, int n, double *leafbuf /* 
 // ---------------------------------------------------------------------------------
 // sampling
 // ---------------------------------------------------------------------------------
+#ifndef AMZ_SORT_BITS
+#define AMZ_SORT_BITS 4
+#endif
+using SampleSort = cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int, AMZ_SORT_BITS>;
 struct SampleSmem {
-    typename cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int>::TempStorage sort;
+    typename SampleSort::TempStorage sort;
     double p[kPlrMaxK];
     double leaf[64];
     int leafinfo[3 * 64 + 4];
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     // ---- 1. ranks: sort by seq asc, then stable by score desc ----
     // seq values are distinct and span a narrow range: the first sort only runs over the
     // bits of (seq - min seq), with the padding keys (all ones) above every valid key
-    using Sort = cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int>;
+    using Sort = SampleSort;
     unsigned long long keys[4];
     int vals[4];
     if (tid == 0) {

@@ -189,3 +189,14 @@ def test_parallel_iterations_match_oracle(accel, score_fn):
         assert np.array_equal(res.scores.cpu().numpy(), sc)
         assert np.array_equal(res.max_returns.cpu().numpy(), mx)
         _assert_same(plr.buffer, ref)
+
+
+def test_string_device_arguments():
+    """device="cuda:0" strings resolve to the right stream (str has an .index method too)."""
+    lv = amz.sample_levels(amz.RngStream(3, (0,)), 64, amz.StaticParams(), device="cuda:0")
+    ref = amz.sample_levels(amz.RngStream(3, (0,)), 64, amz.StaticParams(), device=torch.device("cuda", 0))
+    assert torch.equal(lv, ref)
+    buf = LevelBuffer(PlrConfig(buffer_size=16), device="cuda:0")
+    buf.update(lv, torch.rand(64, dtype=torch.float64), torch.zeros(64, dtype=torch.float64), 1)
+    out = buf.sample(amz.RngStream(5, (0,)), 8, 2)
+    assert out["slots"].shape == (8,) and int(out["slots"].max()) < 16
