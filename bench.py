@@ -9,15 +9,22 @@ One "step" = one pass of the hot path over one batch of synthetic input (config 
   3. 256 fused env steps with RESAMPLE auto-reset driven by a uint8 [T, B] action
      stream resident in HBM (the policy is out of scope; its values are a resident
      float64 [T, B] tensor),
-  4. GAE (gamma 0.995, lambda 0.95) + MaxMC regret scores + running max returns.
+  4. GAE (gamma 0.995, lambda 0.98: the paper's DR column) + MaxMC
+     regret scores + running max returns.
 metric = env-steps/s = lanes * T / step time (whole job, all ranks).
 
-Under torchrun each rank runs its own lane shard (global lane ids rank*B + i, so the
-keys equal a 1-GPU run over N*B lanes): weak scaling, no data-path collective.
+--gpus N > 1 without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks (one per GPU, NCCL); it fails if fewer than N GPUs
+are visible.  Each rank runs its own lane shard of the headline workload (global lane
+ids rank*B + i, so the keys equal a 1-GPU run over N*B lanes): weak scaling, no
+data-path collective.  The ``parallel_plr`` key is configs[4]: 32768 GLOBAL lanes of a
+PLR|| iteration split over the N ranks with the NCCL candidate all-gather (strong).
 
---impl reference times the oracle port of the reference (oracle/amaze_np.py, numpy,
-lane-sharded over all host cores; the reference itself is pure Python and cannot be
-installed on the GPU box) on the same workload, rank 0 only.
+--impl reference times the reference itself (the unmodified autocurricula package
+installed into baseline/_ref, driven through its public API: AutoResetWrapper /
+batch_lift / compute_gae / lane_scores) on the host cores, lane-sharded over worker
+processes, rank 0 only; without baseline/_ref it falls back to the oracle port
+(oracle/amaze_np.py, bit-exact with the reference) and says so (kind "port").
 """
 
 from __future__ import annotations
@@ -35,6 +42,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+GAMMA, LAMBDA = 0.995, 0.98  # PAPER.md:334-335, DR column
 ENV_BYTES_PER_STEP = 36  # action u8 + view 25 u8 + dir u8 + reward f64 + done u8
 GAE_BYTES_PER_ELEM = 33  # r f64 + V f64 + done u8 in, A f64 + R f64 out
 
@@ -84,21 +92,90 @@ def _cpu_shard(args):
     return {"reset": t1 - t0, "rollout": t2 - t1, "gae": t3 - t2, "scores": t4 - t3, "total": t4 - t0}
 
 
-def cpu_reference_step(B, T, seed, workers, pool, phases=None):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _import_reference():
+    """The unmodified reference from baseline/_ref.  runners/scoring.py imports a
+    runners/buffer.py the reference never shipped: a stub module carrying the
+    two fields lane_scores reads (runners/scoring.py:52,59) stands in for it."""
+    import importlib
+    import types
+    from dataclasses import dataclass
+
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    if "autocurricula.runners.buffer" not in sys.modules:
+        stub = types.ModuleType("autocurricula.runners.buffer")
+
+        @dataclass
+        class PlrConfig:
+            score_fn: str = "maxmc"
+            maxmc_discounted: bool = False
+
+        stub.PlrConfig = PlrConfig
+        sys.modules["autocurricula.runners.buffer"] = stub
+    mods = {k: importlib.import_module("autocurricula." + k)
+            for k in ("amaze", "env", "rng", "agents.gae", "agents.rollout", "runners.scoring")}
+    return types.SimpleNamespace(amaze=mods["amaze"], env=mods["env"], rng=mods["rng"], gae=mods["agents.gae"],
+                                 rollout=mods["agents.rollout"], scoring=mods["runners.scoring"],
+                                 PlrConfig=sys.modules["autocurricula.runners.buffer"].PlrConfig)
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "autocurricula"))
+
+
+def _ref_shard(args):
+    """One lane shard of the config-2 step through the REFERENCE's public API: DR reset
+    (AutoResetWrapper(batch_lift(MazeEnv)).reset), T RESAMPLE steps, compute_gae,
+    lane_scores (MaxMC).  Shards use seed + lane0 (the reference has no lane offset);
+    the work per lane is statistically the same.  Returns per-phase wall seconds."""
+    lane0, n, T, seed, act_seed, gamma, lam = args
+    import numpy as np
+
+    R = _import_reference()
+    P = R.env.StaticParams()
+    wrap = R.env.AutoResetWrapper(R.env.batch_lift(R.amaze.MazeEnv(), R.env.BatchShape(1, 1, n)), "resample")
+    rng = np.random.default_rng(act_seed + lane0)
+    acts = rng.integers(0, 3, (T, 1, n))
+    values = rng.uniform(0, 1, (T, n))
+    t0 = time.perf_counter()
+    res = wrap.reset(R.rng.RngStream.from_seed(seed + lane0), P)
+    t1 = time.perf_counter()
+    state, extras = res.state, res.extras
+    rews, dones = np.empty((T, n)), np.empty((T, n), dtype=bool)
+    for t in range(T):
+        r = wrap.step(None, state, acts[t], P, extras)
+        rews[t], dones[t] = r.reward.reshape(-1), r.done.reshape(-1)
+        state, extras = r.state, r.extras
+    t2 = time.perf_counter()
+    adv, _ = R.gae.compute_gae(rews, values, dones, values[-1], gamma, lam)
+    t3 = time.perf_counter()
+    tb = R.rollout.TrajectoryBatch({}, np.zeros((T, n), np.int64), np.zeros((T, n)), values, rews, dones,
+                                   np.zeros((T, n, 1)))
+    R.scoring.lane_scores(tb, adv, np.zeros(n), R.PlrConfig(score_fn="maxmc"))
+    t4 = time.perf_counter()
+    return {"reset": t1 - t0, "rollout": t2 - t1, "gae": t3 - t2, "scores": t4 - t3, "total": t4 - t0}
+
+
+def cpu_reference_step(B, T, seed, workers, pool, phases=None, kind="port"):
     """One full step of the workload on the host: returns wall seconds.  ``phases``
-    (a list) receives the per-phase seconds of the slowest shard."""
+    (a list) receives the per-phase seconds of the slowest shard.  kind "reference" runs
+    the reference package (baseline/_ref), "port" the numpy oracle port."""
     shards = []
     per = (B + workers - 1) // workers
     for w in range(workers):
         lo = w * per
         n = min(per, B - lo)
         if n > 0:
-            shards.append((lo, n, T, seed, 17, 0.995, 0.95))
+            shards.append((lo, n, T, seed, 17, GAMMA, LAMBDA))
+    fn = _ref_shard if kind == "reference" else _cpu_shard
     t0 = time.perf_counter()
     if pool is None:
-        res = [_cpu_shard(s) for s in shards]
+        res = [fn(s) for s in shards]
     else:
-        res = pool.map(_cpu_shard, shards)
+        res = pool.map(fn, shards)
     wall = time.perf_counter() - t0
     if phases is not None:
         phases.append(max(res, key=lambda r: r["total"]))
@@ -129,6 +206,17 @@ def cpu_buffer_update_seconds(n_new=4096, K=4000, it=1):
     t0 = time.perf_counter()
     buf.update(cand, sc, mr, it)
     return time.perf_counter() - t0
+
+
+METRIC = "AMaze env steps/sec (DR reset + 256-step RESAMPLE rollout + GAE/MaxMC)"
+
+
+def workload_config(args, world):
+    """The `config` dict both arms print (identical keys and values)."""
+    return {"workload": "configs[1]: AMaze 13x13 DR, 4096 envs x 256 steps, RESAMPLE auto-reset, GAE+MaxMC",
+            "lanes_per_gpu": args.lanes, "T": args.T, "gamma": GAMMA, "lambda": LAMBDA,
+            "l2": "flushed (256 MB write) before every timed step (GPU arm)",
+            "parallelism": f"lane-sharded x{world}"}
 
 
 def _cores():
@@ -271,7 +359,7 @@ class Workload:
         if timing is not None:
             timing[1].record()
         o = amz.gae_and_scores(traj.rewards, self.values if values is None else values, traj.dones,
-                               self.last if last is None else last, 0.995, 0.95, out=self.gout)
+                               self.last if last is None else last, GAMMA, LAMBDA, out=self.gout)
         if timing is not None:
             timing[2].record()
         return o
@@ -421,9 +509,21 @@ def run_ours(args, rank, world, local_rank):
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     extra = {}
     if not args.no_extra:
-        extra["plr"] = measure_plr(dev, 2048, T, False, max(3, min(args.steps, 10)), flush, world)
-        extra["accel"] = measure_plr(dev, 2048, T, True, max(3, min(args.steps, 10)), flush, world)
+        its = max(3, min(args.steps, 10))
+        # configs[4]: 32768 GLOBAL lanes of PLR|| split over the ranks, NCCL all-gather (strong scaling)
+        extra["parallel_plr"] = measure_plr_parallel(dev, 16384, T, False, its, flush, world, "plr_parallel",
+                                                     "configs[4] Parallel PLR multi-device: 32768 global lanes "
+                                                     "(16384 new | 16384 replay), K=4000")
+        extra["parallel_plr"]["scaling"] = "strong"
         if world == 1:
+            extra["plr_perp"] = measure_plr_perp(dev, 4096, T, False, 2 * its, flush, "plr_perp",
+                                                 "configs[2] PLR-perp: 4096 lanes, K=4000, MaxMC, rank replay")
+            extra["accel_perp"] = measure_plr_perp(dev, 4096, T, True, 2 * its, flush, "accel_perp",
+                                                   "configs[3] ACCEL: PLR-perp + 4 mutants x 20 edits per replay")
+            extra["plr_parallel"] = measure_plr_parallel(dev, 2048, T, False, its, flush, 1, "plr_parallel",
+                                                         "PLR|| (paper variant of configs[2]): 2048 new | 2048 replay")
+            extra["accel_parallel"] = measure_plr_parallel(dev, 2048, T, True, its, flush, 1, "accel_parallel",
+                                                           "ACCEL|| (paper variant of configs[3]): 2048 x 3 lanes")
             extra["large_batch"] = measure_large_batch(dev, 65536, T, 3, flush, peak)
             extra["level_metrics"] = measure_level_metrics(dev, 65536, 5, flush)
             extra["policy_rollout"] = measure_policy_rollout(dev, 4096, 64)
@@ -439,7 +539,7 @@ def run_ours(args, rank, world, local_rank):
     gae_gbs = GAE_BYTES_PER_ELEM * B * T / (gae * 1e-3) / 1e9
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     line = {
-        "metric": "AMaze env steps/sec (DR reset + 256-step RESAMPLE rollout + GAE/MaxMC)",
+        "metric": METRIC,
         "value": units / (total_ms * 1e-3 / args.steps),
         "unit": "env-steps/s",
         "n_gpus": world,
@@ -451,9 +551,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "u8/int32 env, f64 GAE",
         "data": "synthetic: DR levels from (seed, lane) keys, uniform random actions and values resident in HBM",
-        "config": {"workload": "configs[1]: AMaze 13x13 DR, 4096 envs x 256 steps, RESAMPLE auto-reset, GAE+MaxMC",
-                   "lanes_per_gpu": B, "T": T, "gamma": 0.995, "lambda": 0.95, "l2": "flushed (256 MB write) "
-                   "before every timed step", "parallelism": f"lane-sharded x{world}"},
+        "config": workload_config(args, world),
         "e2e": {"value": units / (e2e_ms * 1e-3 / args.steps), "unit": "env-steps/s",
                 "h2d_bytes_per_step": T * B * (1 + 8) + B * 8, "d2h_bytes_per_step": 2 * B * 8,
                 "ms_per_step": e2e_ms / args.steps, "host_enqueue_ms_per_step": host_ms,
@@ -499,52 +597,120 @@ def _timed(fn, iters, flush, torch):
     return [a.elapsed_time(b) for a, b in evs]
 
 
-def measure_plr(dev, n_per_gpu, T, accel, iters, flush, world):
-    """Parallel PLR (configs[2]) / ACCEL (configs[3]) iteration, env side: compose lanes
-    (DR + rank-prioritised replay [+ 20-edit mutants]), HOME rollout, GAE + MaxMC,
-    NCCL candidate all-gather (N > 1), buffer update.  Buffer K = 4000."""
-    import torch
+# paper Table 4: (gamma, lambda, staleness rho, replay rate p)
+HP = {"plr_perp": (0.999, 0.98, 0.3, 0.5), "plr_parallel": (0.999, 0.95, 0.5, 0.5),
+      "accel_perp": (0.999, 0.98, 0.5, 0.8), "accel_parallel": (0.999, 0.98, 0.5, 0.8)}
 
-    import paper_2311_12716_b200 as amz
-    from paper_2311_12716_b200.buffer import AccelConfig, PlrConfig
-    from paper_2311_12716_b200.plr import ParallelPLR
 
-    cfg = PlrConfig(buffer_size=4000, score_fn="maxmc", temperature=0.3,
-                    staleness_coef=0.5 if accel else 0.3, replay_rate=0.8 if accel else 0.5)
-    plr = ParallelPLR(n_per_gpu * world, amz.StaticParams(), cfg, amz.RngStream.from_seed(7),
-                      AccelConfig(20, 4) if accel else None, device=dev)
-    L = plr.hi - plr.lo
+def _plr_cfg(name):
+    from paper_2311_12716_b200.buffer import PlrConfig
+
+    g, lam, rho, p = HP[name]
+    return PlrConfig(buffer_size=4000, score_fn="maxmc", temperature=0.3, staleness_coef=rho, replay_rate=p), g, lam
+
+
+def _policy_inputs(dev, T, L, seed, torch):
     g = torch.Generator(device=dev)
-    g.manual_seed(99 + plr.rank)
+    g.manual_seed(seed)
     acts = torch.randint(0, 3, (T, L), generator=g, device=dev, dtype=torch.uint8)
     vals = torch.rand((T, L), generator=g, device=dev, dtype=torch.float64) * 0.2
     last = torch.rand((L,), generator=g, device=dev, dtype=torch.float64) * 0.2
-    for it in range(3):  # fills the 4000-level buffer (first iteration inserts 4000 of the new levels)
-        plr.iteration(it, acts, vals, last)
-    torch.cuda.synchronize()
-    ms = _timed(lambda i: plr.iteration(3 + i, acts, vals, last), iters, flush, torch)
-    # the two buffer kernels on their own (latency-bound single-CTA kernels): an update
-    # with 4096 distinct new levels (scores U(0,1): most evict -- the worst case) and one
-    # with 4096 replays of buffered levels (in-place updates)
-    new_lv = amz.sample_levels(amz.RngStream(99, (0,)), 4096, amz.StaticParams(), device=dev)
-    sc = torch.rand(4096, device=dev, dtype=torch.float64)
-    sc2 = torch.rand(4000, device=dev, dtype=torch.float64)
-    t_upd = _timed(lambda i: plr.buffer.update(new_lv, sc, sc, 1000 + i), iters, flush, torch)
-    old_lv = plr.buffer.export()["levels"][:4000]  # exported after t_upd: every level is buffered
-    t_rep = _timed(lambda i: plr.buffer.update(old_lv, sc2, sc2, 1000 + i), iters, flush, torch)
-    t_smp = _timed(lambda i: plr.buffer.sample(amz.RngStream(5, (i,)), n_per_gpu * world, 2000 + i), iters, flush,
-                   torch)
-    t = torch.tensor([statistics.mean(ms)], dtype=torch.float64, device=dev)
+    return acts, vals, last
+
+
+def _max_over_ranks(ms, dev, world, torch):
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    it_ms = float(t.item())
-    lanes = plr.L
-    return {"config": "configs[3] ACCEL-parallel" if accel else "configs[2] PLR-parallel",
-            "lanes_global": lanes, "T": T, "buffer_size": 4000, "iteration_ms": it_ms,
-            "levels_scored_per_s": lanes / (it_ms * 1e-3), "env_steps_per_s": lanes * T / (it_ms * 1e-3),
-            "buffer_update_us_4096_new_levels": 1e3 * statistics.mean(t_upd),
-            "buffer_update_us_4000_replays": 1e3 * statistics.mean(t_rep),
-            "buffer_sample_us": 1e3 * statistics.mean(t_smp)}
+    return float(t.item())
+
+
+def measure_plr_parallel(dev, n, T, accel, iters, flush, world, name, config_label):
+    """PLR|| / ACCEL|| iteration, env side: compose lanes (DR + rank-
+    prioritised replay [+ 20-edit mutants]), HOME rollout, GAE + MaxMC, NCCL candidate
+    all-gather (N > 1), replicated buffer update.  n new lanes, L = 2n / 3n GLOBAL lanes
+    split over the ranks; K = 4000.  Iteration time = max over ranks."""
+    import torch
+
+    import paper_2311_12716_b200 as amz
+    from paper_2311_12716_b200.buffer import AccelConfig
+    from paper_2311_12716_b200.plr import ParallelPLR
+
+    cfg, gamma, lam = _plr_cfg(name)
+    plr = ParallelPLR(n, amz.StaticParams(), cfg, amz.RngStream.from_seed(7), AccelConfig(20, 4) if accel else None,
+                      gamma=gamma, lam=lam, device=dev, check_every=0)
+    acts, vals, last = _policy_inputs(dev, T, plr.hi - plr.lo, 99 + plr.rank, torch)
+    for it in range(3):  # fills the 4000-level buffer (the first iteration inserts its new levels)
+        plr.iteration(it, acts, vals, last)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = _timed(lambda i: plr.iteration(3 + i, acts, vals, last), iters, flush, torch)
+    it_ms = _max_over_ranks(statistics.mean(ms), dev, world, torch)
+    plr.check_replicas()  # the drift check once per measurement (digest on device + all-reduce)
+    out = {"config": config_label, "lanes_global": plr.L, "lanes_per_rank": plr.hi - plr.lo, "T": T,
+           "buffer_size": 4000, "gamma": gamma, "lambda": lam, "staleness_coef": cfg.staleness_coef,
+           "replay_rate": cfg.replay_rate, "iteration_ms": it_ms,
+           "levels_scored_per_s": plr.L / (it_ms * 1e-3), "env_steps_per_s": plr.L * T / (it_ms * 1e-3),
+           "collective": "NCCL all_gather_into_tensor of 48-byte candidate records" if world > 1 else "none (1 rank)"}
+    if world == 1 and n <= 4096:
+        # the two buffer kernels on their own: an update with 4096 distinct new levels
+        # (scores U(0,1): most evict -- the worst case) and one with 4000 replays of
+        # buffered levels (in-place updates); the replay draw
+        new_lv = amz.sample_levels(amz.RngStream(99, (0,)), 4096, amz.StaticParams(), device=dev)
+        sc = torch.rand(4096, device=dev, dtype=torch.float64)
+        sc2 = torch.rand(4000, device=dev, dtype=torch.float64)
+        t_upd = _timed(lambda i: plr.buffer.update(new_lv, sc, sc, 1000 + i), iters, flush, torch)
+        old_lv = plr.buffer.export()["levels"][:4000]  # exported after t_upd: every level is buffered
+        t_rep = _timed(lambda i: plr.buffer.update(old_lv, sc2, sc2, 1000 + i), iters, flush, torch)
+        t_smp = _timed(lambda i: plr.buffer.sample(amz.RngStream(5, (i,)), n, 2000 + i), iters, flush, torch)
+        out.update({"buffer_update_us_4096_new_levels": 1e3 * statistics.mean(t_upd),
+                    "buffer_update_us_4000_replays": 1e3 * statistics.mean(t_rep),
+                    "buffer_sample_us": 1e3 * statistics.mean(t_smp)})
+    return out
+
+
+def measure_plr_perp(dev, n, T, accel, iters, flush, name, config_label):
+    """PLR-perp / ACCEL-perp iteration: decision; NEW = n fresh DR
+    levels, HOME rollout, score, update; REPLAY = n draws, rollout, in-place re-score
+    [+ q=4 mutants, 20 edits, rolled out and inserted].  K = 4000, one GPU."""
+    import torch
+
+    import paper_2311_12716_b200 as amz
+    from paper_2311_12716_b200.buffer import AccelConfig
+    from paper_2311_12716_b200.plr import SequentialPLR
+
+    cfg, gamma, lam = _plr_cfg(name)
+    plr = SequentialPLR(n, amz.StaticParams(), cfg, amz.RngStream.from_seed(11), AccelConfig(20, 4) if accel else None,
+                        gamma=gamma, lam=lam, device=dev)
+    acts, vals, last = _policy_inputs(dev, T, n, 123, torch)
+    it = 0
+    while plr.buffer.size() < 4000 and it < 8:  # NEW iterations fill the buffer
+        plr.iteration(it, acts, vals, last)
+        it += 1
+    torch.cuda.synchronize()
+    branch = {"new": [], "replay": []}
+    evs = []
+    for i in range(iters):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = plr.iteration(it + i, acts, vals, last)
+        b.record()
+        evs.append((r.branch, a, b))
+    torch.cuda.synchronize()
+    for br, a, b in evs:
+        branch[br].append(a.elapsed_time(b))
+    allms = [x for v in branch.values() for x in v]
+    it_ms = statistics.mean(allms)
+    out = {"config": config_label, "lanes": n, "T": T, "buffer_size": 4000, "gamma": gamma, "lambda": lam,
+           "staleness_coef": cfg.staleness_coef, "replay_rate": cfg.replay_rate, "iterations": len(allms),
+           "iteration_ms": it_ms, "levels_scored_per_s": n / (it_ms * 1e-3), "env_steps_per_s": n * T / (it_ms * 1e-3)}
+    for br, v in branch.items():
+        if v:
+            out[f"{br}_iterations"] = len(v)
+            out[f"{br}_iteration_ms"] = statistics.mean(v)
+    return out
 
 
 def measure_large_batch(dev, B, T, iters, flush, peak):
@@ -621,17 +787,24 @@ def measure_policy_rollout(dev, B, T):
 
 
 def measure_cpu_baseline(args, steps=1):
+    """One config-2 step on the host cores, bounded (~10-30 s): the reference package
+    when baseline/_ref is present, else the oracle port."""
     import multiprocessing as mp
 
     cores = _cores()
     B, T = args.lanes, args.T
+    kind = "reference" if reference_available() else "port"
+    if kind == "reference":
+        _import_reference()  # once in the parent: the forked workers inherit the modules
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        secs = [cpu_reference_step(B, T, args.seed, cores, pool) for _ in range(steps)]
+        secs = [cpu_reference_step(B, T, args.seed, cores, pool, kind=kind) for _ in range(steps)]
     s = statistics.mean(secs)
-    return {"value": B * T / s, "unit": "env-steps/s", "cores": cores, "kind": "port",
-            "sample": f"one full step ({B} lanes x {T} steps DR reset + rollout + GAE/MaxMC) with the numpy oracle "
-                      f"port, lanes sharded over {cores} processes; host: {_cpu_model()}"}
+    what = ("the reference package (baseline/_ref, unmodified) through its public API" if kind == "reference"
+            else "the numpy oracle port of the reference")
+    return {"value": B * T / s, "unit": "env-steps/s", "cores": cores, "kind": kind,
+            "sample": f"one full step ({B} lanes x {T} steps DR reset + RESAMPLE rollout + GAE/MaxMC) with {what}, "
+                      f"lanes sharded over {cores} processes; host: {_cpu_model()}"}
 
 
 def run_reference(args, rank, world):
@@ -641,35 +814,80 @@ def run_reference(args, rank, world):
 
     cores = _cores()
     B, T = args.lanes, args.T
+    kind = "reference" if reference_available() else "port"
+    if kind == "reference":
+        _import_reference()  # once in the parent: the forked workers inherit the modules
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         for _ in range(args.warmup):
-            cpu_reference_step(B, T, args.seed, cores, pool)
+            cpu_reference_step(B, T, args.seed, cores, pool, kind=kind)
         phases = []
-        secs = [cpu_reference_step(B, T, args.seed, cores, pool, phases) for _ in range(args.steps)]
+        secs = [cpu_reference_step(B, T, args.seed, cores, pool, phases, kind=kind) for _ in range(args.steps)]
     s = statistics.mean(secs)
     val = B * T / s
     # the phases separately (slowest shard, mean over the timed steps), one
-    # single-process step (no sharding), and the oracle buffer update (sequential)
+    # single-process step (no sharding), and the oracle buffer update (sequential; the
+    # reference never shipped its buffer)
     phase_ms = {k: 1e3 * statistics.mean(ph[k] for ph in phases) for k in ("reset", "rollout", "gae", "scores")}
-    one = cpu_reference_step(B, T, args.seed, 1, None)
+    one = cpu_reference_step(B, T, args.seed, 1, None, kind=kind)
     buf_s = cpu_buffer_update_seconds(4096, 4000)
+    what = ("the unmodified reference package (baseline/_ref) through its public API (AutoResetWrapper/batch_lift, "
+            "compute_gae, lane_scores)" if kind == "reference" else
+            "the numpy oracle port of the reference (baseline/_ref absent)")
     return {
         "impl": "reference",
-        "metric": "AMaze env steps/sec (DR reset + 256-step RESAMPLE rollout + GAE/MaxMC)",
+        "metric": METRIC,
         "value": val, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "int64 env, f64 GAE", "data": "synthetic (same workload, numpy random actions/values)",
-        "config": {"workload": "configs[1]: AMaze 13x13 DR, 4096 envs x 256 steps, RESAMPLE auto-reset, GAE+MaxMC",
-                   "lanes": B, "T": T},
-        "cpu_baseline": {"value": val, "unit": "env-steps/s", "cores": cores, "kind": "port",
-                         "sample": f"full config-2 step per timed step, numpy oracle port of the reference, "
-                                   f"lanes sharded over {cores} processes; host: {_cpu_model()}"},
+        "dtype": "int64 env, f64 GAE", "data": "synthetic (same workload shape, numpy random actions/values)",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": val, "unit": "env-steps/s", "cores": cores, "kind": kind,
+                         "sample": f"one full config-2 step per timed step with {what}, lanes sharded over {cores} "
+                                   f"processes (shard seeds seed+lane0); host: {_cpu_model()}"},
         "e2e": {"value": val, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phases_ms_per_step": phase_ms,
         "single_process": {"env_steps_per_s": B * T / one, "ms_per_step": one * 1e3, "cores": 1},
         "buffer_update_ms_4096_new_levels": buf_s * 1e3,
+        "buffer_update_impl": "oracle/plr_np.py (SPEC.md:373-377 transcription; the reference has no buffer)",
     }
+
+
+def _relaunch(args):
+    """--gpus N > 1 outside torchrun: re-exec this script under torch.distributed.run with
+    N ranks on this node (127.0.0.1 rendezvous).  NCCL's INIT lines go to stderr so the
+    communicator size (comm nranks) is on record without touching the JSON line."""
+    import socket
+
+    if not args.launcher_check:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def launcher_check(rank, world):
+    """--launcher-check: the rank world only (gloo, no GPU work) -- lets a CPU test see
+    that --gpus N really starts N ranks."""
+    import torch
+
+    torch.distributed.init_process_group("gloo")
+    t = torch.ones(1)
+    torch.distributed.all_reduce(t)
+    torch.distributed.destroy_process_group()
+    if rank == 0:
+        return {"launcher_check": True, "world": world, "ranks_seen": int(t.item())}
+    return None
 
 
 def main():
@@ -683,25 +901,30 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the PLR/ACCEL and large-batch measurements")
+    ap.add_argument("--launcher-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
+    if args.launcher_check:
+        line = launcher_check(rank, world)
+    elif args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
         import torch
 
         if world > 1:
             torch.cuda.set_device(local_rank)
-            torch.distributed.init_process_group("nccl")
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         line = run_ours(args, rank, world, local_rank)
         if world > 1:
             torch.distributed.destroy_process_group()
     if line is not None:
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -282,6 +282,11 @@ int amz_plr_top_q(const double *scores_dev, int64_t n, int q, int32_t *out_dev, 
 /* Synchronous: current size; reports a deferred empty-buffer sampling error. */
 int amz_plr_size(amz_plr_t *plr, int64_t *size_host, void *stream);
 
+/* Replica drift check (the analogue of the shard-sync check at agents/ppo.py:322-328):
+ * a 64-bit digest of the valid slots and meta written to out_dev[0] (device int64),
+ * asynchronously on `stream`; equal buffers give equal digests. */
+int amz_plr_digest(amz_plr_t *plr, int64_t *out_dev, void *stream);
+
 /* Device-to-device copy of the whole buffer state (checkpoint / drift checks):
  * levels [K], score [K], max_return [K], last_sampled [K] i64, seq [K] i64,
  * meta [2] i64 = (size, next_seq).  Any output may be NULL for export. */

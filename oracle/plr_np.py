@@ -31,7 +31,13 @@ Choices SPEC leaves open, pinned here (and in DESIGN.md) so GPU and oracle agree
     ties to the lower lane index; mutant lane j uses parent j % q;
   * iteration keys: it = root.fold_in(iter); new-level lane keys it.fold_in(1)+(lane,),
     replay draw it.fold_in(2), mutation keys it.fold_in(3)+(j,), PLR-perp decision
-    it.fold_in(0).
+    it.fold_in(0), HOME rollout reset it.fold_in(4) (PLR-perp mutant rollout: it.fold_in(5));
+  * PLR-perp: NEW = n fresh levels, roll out, score, update; REPLAY =
+    n draws, roll out from the entries' max returns, re-score the drawn entries in place
+    (an update with the drawn levels); ACCEL-perp adds q mutants after a replay (parents
+    = the q highest buffer scores among the drawn entries at sampling time, mutant j
+    from parent j, keys it.fold_in(3)+(j,)), rolled out and scored from max return 0,
+    then one update with them.
 """
 
 from __future__ import annotations
@@ -174,3 +180,38 @@ def compose_lanes(buf: LevelBuffer, entropy: int, root_key: tuple, it: int, n: i
         parts.append(onp.pack_levels(muts, p))
         prior.append(np.zeros(n))
     return np.concatenate(parts), np.concatenate(prior), n, slots
+
+
+def plr_perp_iteration(buf: LevelBuffer, entropy: int, root_key: tuple, it: int, n: int, p: onp.Params,
+                       cfg: PlrConfig, rollout_score, accel=None):
+    """One PLR-perp (or ACCEL-perp) iteration against this buffer.
+
+    ``rollout_score(levels, prior, reset_key, which)`` rolls the packed levels out (HOME
+    auto-reset from ``reset_key``) and returns (scores, max_returns); ``which`` is
+    "main" or "mutants" so a harness can feed each rollout its own action stream.
+    Returns dict(branch, levels, scores, max_returns, slots, mutants...)."""
+    itk = tuple(root_key) + (it,)
+    replay = buf.decision(entropy, itk + (0,), cfg.replay_rate)
+    out = {"branch": "replay" if replay else "new"}
+    if not replay:
+        levels = onp.pack_levels([onp.sample_level(entropy, itk + (1, i), p) for i in range(n)], p)
+        sc, mx = rollout_score(levels, np.zeros(n), itk + (4,), "main")
+        buf.update(levels, sc, mx, it)
+        out.update(levels=levels, scores=sc, max_returns=mx)
+        return out
+    slots = buf.sample(entropy, itk + (2,), n, cfg, it)
+    levels = buf.levels[slots].copy()
+    before = buf.score[slots].copy()
+    sc, mx = rollout_score(levels, buf.max_return[slots].copy(), itk + (4,), "main")
+    buf.update(levels, sc, mx, it)
+    out.update(levels=levels, scores=sc, max_returns=mx, slots=slots)
+    if accel is not None:
+        q, n_edits = accel
+        parents = top_q(before, q)
+        par_levels = onp.unpack_levels(levels[parents], p)
+        muts = onp.pack_levels([onp.mutate_level(entropy, itk + (3, j), par_levels[j], n_edits, p)
+                                for j in range(q)], p)
+        msc, mmx = rollout_score(muts, np.zeros(q), itk + (5,), "mutants")
+        buf.update(muts, msc, mmx, it)
+        out.update(mutants=muts, mutant_scores=msc, mutant_max_returns=mmx)
+    return out

@@ -80,6 +80,7 @@ _SIGS = {
     "amz_plr_sample": ([P, ctypes.POINTER(AmzSeed), I64, D, P, I64, P, P, P, P, VP], I32),
     "amz_plr_top_q": ([P, I64, I32, P, VP], I32),
     "amz_plr_size": ([P, ctypes.POINTER(ctypes.c_int64), VP], I32),
+    "amz_plr_digest": ([P, P, VP], I32),
     "amz_plr_export": ([P, P, P, P, P, P, P, VP], I32),
     "amz_plr_import": ([P, P, P, P, P, P, P, VP], I32),
     "amz_lane_scores": ([I32, I64, P, P, P, P, D, P, I32, I32, P, P, ctypes.POINTER(AmzEpisodeStats), VP], I32),

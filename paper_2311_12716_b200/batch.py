@@ -257,7 +257,7 @@ class VectorBatchEnv:
         torch = _torch()
         p = as_params(params)
         dl = state if isinstance(state, DeviceLanes) else self.lanes
-        idx = torch.as_tensor(lanes, device=self.device).to(torch.int64).contiguous()
+        idx = _lane_indices(lanes, dl.n).to(self.device)
         lv = to_device_levels(levels, p, self.device)
         if lv.shape[0] != idx.numel():
             raise ShapeError(f"{idx.numel()} lanes vs {lv.shape[0]} levels")
@@ -267,6 +267,26 @@ class VectorBatchEnv:
         _lib.call("amz_env_reset_to_levels", dl.handle, _lib.ptr(lv), _lib.ptr(idx), idx.numel(), _lib.ptr(view),
                   _lib.ptr(dirs), dl.stream())
         return dl, {"view": view, "dir": dirs}
+
+
+def _lane_indices(lanes, n: int):
+    """numpy's indexing rules for ``state.replace_lanes(lanes, ...)`` (amaze/env.py:308-313):
+    a bool mask of length n selects its True lanes, negative indices wrap once, anything
+    outside [-n, n) raises IndexError.  Checked on the host (this path is not the fused
+    hot path; a device tensor is read back) so the kernel never sees an invalid lane."""
+    torch = _torch()
+    t = torch.as_tensor(lanes).detach().cpu()
+    if t.dtype == torch.bool:
+        if t.dim() != 1 or t.numel() != n:
+            raise IndexError(f"boolean lane mask of shape {tuple(t.shape)} does not match {n} lanes")
+        return t.nonzero().reshape(-1).to(torch.int64).contiguous()
+    if t.is_floating_point() or t.is_complex():
+        raise IndexError("lane indices must be integers or a boolean mask")
+    t = t.to(torch.int64).reshape(-1)
+    if t.numel() and (int(t.min()) < -n or int(t.max()) >= n):
+        bad = int(t.min()) if int(t.min()) < -n else int(t.max())
+        raise IndexError(f"lane index {bad} is out of bounds for {n} lanes")
+    return torch.where(t < 0, t + n, t).contiguous()
 
 
 class AutoResetWrapper:

@@ -137,6 +137,14 @@ class LevelBuffer:
         _lib.call("amz_plr_size", self.handle, ctypes.byref(v), self._stream())
         return int(v.value)
 
+    def digest(self, out=None):
+        """Device int64 [1] digest of the buffer state (amz_plr_digest): the replica drift
+        check's input, computed without a host round trip."""
+        torch = _torch()
+        out = torch.empty(1, dtype=torch.int64, device=self.device) if out is None else out
+        _lib.call("amz_plr_digest", self.handle, _lib.ptr(out), self._stream())
+        return out
+
     def export(self) -> dict:
         torch = _torch()
         K, dev = self.K, self.device
@@ -152,8 +160,28 @@ class LevelBuffer:
         return st
 
     def load(self, st: dict) -> None:
+        """Import a state exported by ``export`` (checkpoint resume).  The state is checked
+        first: 0 <= size <= K, next_seq >= 0, and the valid slots' seq values distinct and
+        below next_seq (the update relies on new entries sorting after every stored one)."""
         torch = _torch()
-        t = {k: v.to(self.device).contiguous() for k, v in st.items()}
+        dtypes = {"levels": torch.int32, "score": torch.float64, "max_return": torch.float64,
+                  "last_sampled": torch.int64, "seq": torch.int64, "meta": torch.int64}
+        t = {}
+        for k, dt in dtypes.items():
+            if k not in st:
+                raise ContractViolation(f"buffer state is missing {k!r}")
+            v = torch.as_tensor(st[k])
+            want = (self.K, 8) if k == "levels" else (2,) if k == "meta" else (self.K,)
+            if tuple(v.shape) != want:
+                raise ContractViolation(f"buffer state {k!r} has shape {tuple(v.shape)}, expected {want}")
+            t[k] = v.to(self.device).to(dt).contiguous()
+        size, next_seq = (int(x) for x in t["meta"].cpu())
+        if not 0 <= size <= self.K:
+            raise ContractViolation(f"buffer state size {size} outside [0, {self.K}]")
+        seq = t["seq"][:size].cpu()
+        if next_seq < 0 or (size and (int(seq.min()) < 0 or int(seq.max()) >= next_seq
+                                      or seq.unique().numel() != size)):
+            raise ContractViolation("buffer state seq values must be distinct and in [0, next_seq)")
         _lib.call("amz_plr_import", self.handle, *(_lib.ptr(t[k]) for k in
                                                    ("levels", "score", "max_return", "last_sampled", "seq", "meta")),
                   self._stream())

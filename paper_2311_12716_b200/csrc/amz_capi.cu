@@ -32,7 +32,29 @@ static int cuda_status(const char *what) {
         if (e_ != cudaSuccess) return fail(AMZ_ECUDA, "%s: %s", what, cudaGetErrorString(e_)); \
     } while (0)
 
+// Every handle remembers the device it was created on; an entry point that takes a
+// handle makes that device current for the call (and restores the caller's), so a handle
+// keeps working when another device is current.
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev && dev >= 0)
+            cudaSetDevice(dev);
+        else
+            prev = -1;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+static int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
 struct amz_env {
+    int device;
     amz_params_t p;
     Geo G;
     EnvDev E;
@@ -52,6 +74,7 @@ struct amz_env {
 };
 
 struct amz_plr {
+    int device;
     PlrDev D;
     UpdScratch W;
     int *err;
@@ -172,6 +195,7 @@ int amz_check_levels(const amz_params_t *p, const amz_level_t *lv, int64_t n, in
 
 // ---- PAIRED level designer (amaze/teacher.py) ----
 struct amz_teacher {
+    int device;
     amz_params_t p;
     Geo G;
     int64_t B;
@@ -186,6 +210,7 @@ int amz_teacher_create(const amz_params_t *p, int64_t n_lanes, amz_teacher_t **o
     if (!out || n_lanes < 1) return fail(AMZ_ESHAPE, "n_lanes must be >= 1, got %lld", (long long)n_lanes);
     amz_teacher *t = new (std::nothrow) amz_teacher();
     if (!t) return fail(AMZ_EFAULT, "out of host memory");
+    t->device = current_device();
     t->p = *p;
     t->G = make_geo(*p);
     t->B = n_lanes;
@@ -206,6 +231,7 @@ int amz_teacher_create(const amz_params_t *p, int64_t n_lanes, amz_teacher_t **o
 
 int amz_teacher_destroy(amz_teacher_t *t) {
     if (!t) return 0;
+    DevGuard guard_(t->device);
     cudaFree(t->mask);
     cudaFree(t->st);
     cudaFree(t->err);
@@ -215,6 +241,7 @@ int amz_teacher_destroy(amz_teacher_t *t) {
 
 int amz_teacher_reset(amz_teacher_t *t, uint8_t *grid, float *phase, int64_t *n_placed, void *stream) {
     if (!t || !grid) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(t->device);
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(t->err, 0, sizeof(int), s);
     launch_teacher_reset(t->G, t->B, t->mask, t->st, grid, phase, n_placed, s);
@@ -224,12 +251,14 @@ int amz_teacher_reset(amz_teacher_t *t, uint8_t *grid, float *phase, int64_t *n_
 int amz_teacher_step(amz_teacher_t *t, const int64_t *actions, uint8_t *grid, float *phase, int64_t *n_placed,
                      uint8_t *done, int64_t *times, void *stream) {
     if (!t || !actions || !grid) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(t->device);
     launch_teacher_step(t->G, t->B, t->mask, t->st, actions, grid, phase, n_placed, done, times, t->err,
                         (cudaStream_t)stream);
     return cuda_status("teacher_step");
 }
 
 static int teacher_err(amz_teacher_t *t, cudaStream_t s) {
+    DevGuard guard_(t->device);
     int h = 0;
     cudaMemcpyAsync(&h, t->err, sizeof(int), cudaMemcpyDeviceToHost, s);
     AMZ_CHECK_CUDA(cudaStreamSynchronize(s), "teacher check");
@@ -243,11 +272,13 @@ static int teacher_err(amz_teacher_t *t, cudaStream_t s) {
 
 int amz_teacher_check(amz_teacher_t *t, void *stream) {
     if (!t) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(t->device);
     return teacher_err(t, (cudaStream_t)stream);
 }
 
 int amz_teacher_levels(amz_teacher_t *t, amz_level_t *out, void *stream) {
     if (!t || !out) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(t->device);
     cudaStream_t s = (cudaStream_t)stream;
     launch_teacher_levels(t->B, t->mask, t->st, out, t->err, s);
     return teacher_err(t, s);
@@ -301,6 +332,7 @@ int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
     if (!out || n_lanes < 1) return fail(AMZ_ESHAPE, "n_lanes must be >= 1, got %lld", (long long)n_lanes);
     amz_env *e = new (std::nothrow) amz_env();
     if (!e) return fail(AMZ_EFAULT, "out of host memory");
+    e->device = current_device();
     e->p = *p;
     e->G = make_geo(*p);
     e->E.B = n_lanes;
@@ -329,6 +361,7 @@ int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
 
 int amz_env_destroy(amz_env_t *e) {
     if (!e) return 0;
+    DevGuard guard_(e->device);
     cudaFree(e->E.st);
     cudaFree(e->E.mask);
     cudaFree(e->E.board);
@@ -347,6 +380,7 @@ int64_t amz_env_lanes(const amz_env_t *e) { return e ? e->E.B : -1; }
 
 int amz_env_set_lane_offset(amz_env_t *e, uint32_t offset) {
     if (!e) return fail(AMZ_ECONFIG, "null env");
+    DevGuard guard_(e->device);
     e->E.lane_offset = offset;
     e->spec_ready = false;
     return 0;
@@ -355,6 +389,7 @@ int amz_env_set_lane_offset(amz_env_t *e, uint32_t offset) {
 int amz_env_reset_dr(amz_env_t *e, const amz_seed_t *prefix, const amz_seed_t *wrap, uint8_t *view, int64_t *dirs,
                      void *stream) {
     if (!e || !prefix) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
     cudaStream_t s = (cudaStream_t)stream;
     int rc = launch_env_reset_dr(e->G, e->E, *prefix, wrap, e->spec, e->spec_step, view, dirs, s);
     if (rc) return fail(rc, "reset: unsupported agent_view_size");
@@ -367,6 +402,7 @@ int amz_env_reset_dr(amz_env_t *e, const amz_seed_t *prefix, const amz_seed_t *w
 int amz_env_reset_to_levels(amz_env_t *e, const amz_level_t *lv, const int64_t *lanes, int64_t n, uint8_t *view,
                             int64_t *dirs, void *stream) {
     if (!e || !lv) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
     e->spec_ready = false;
     if (!lanes && n != e->E.B) return fail(AMZ_ESHAPE, "expected %lld levels, got %lld", (long long)e->E.B, (long long)n);
     cudaStream_t s = (cudaStream_t)stream;
@@ -381,6 +417,7 @@ static int env_step_impl(amz_env_t *e, const void *actions, int adtype, int mode
                          int64_t *dirs, double *reward, uint8_t *done, double *solved, int64_t *times,
                          void *stream) {
     if (!e || !actions) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
     if (adtype < 0 || adtype > 2) return fail(AMZ_ECONTRACT, "bad action dtype code %d", adtype);
     if (mode < AMZ_RESET_NONE || mode > AMZ_RESET_HOME) return fail(AMZ_ECONTRACT, "unknown auto-reset mode %d", mode);
     if (mode == AMZ_RESET_RESAMPLE && !wrap && !wrap_dev) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
@@ -402,6 +439,7 @@ static int env_step_impl(amz_env_t *e, const void *actions, int adtype, int mode
 int amz_env_step(amz_env_t *e, const void *actions, int adtype, int mode, const amz_seed_t *wrap, uint32_t step_idx,
                  uint8_t *view, int64_t *dirs, double *reward, uint8_t *done, double *solved, int64_t *times,
                  void *stream) {
+    DevGuard guard_(e->device);
     return env_step_impl(e, actions, adtype, mode, wrap, step_idx, nullptr, nullptr, view, dirs, reward, done, solved,
                          times, stream);
 }
@@ -409,6 +447,7 @@ int amz_env_step(amz_env_t *e, const void *actions, int adtype, int mode, const 
 int amz_env_step_dev(amz_env_t *e, const void *actions, int adtype, int mode, const amz_seed_t *wrap_dev,
                      const uint32_t *step_dev, uint8_t *view, int64_t *dirs, double *reward, uint8_t *done,
                      double *solved, int64_t *times, void *stream) {
+    DevGuard guard_(e->device);
     if (!step_dev) return fail(AMZ_ECONFIG, "null step counter");
     if (mode == AMZ_RESET_NONE) return fail(AMZ_ECONTRACT, "the device-counter step needs an auto-reset mode");
     if (mode == AMZ_RESET_RESAMPLE && !wrap_dev) return fail(AMZ_ECONFIG, "RESAMPLE needs a wrapper key");
@@ -420,6 +459,7 @@ int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const
                     uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done, uint8_t *fview, uint8_t *fdir,
                     void *stream) {
     if (!e || !actions || !view || !dirs || !reward || !done) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
     if (T < 1) return fail(AMZ_ECONTRACT, "rollout length must be >= 1, got %d", T);
     if (mode != AMZ_RESET_RESAMPLE && mode != AMZ_RESET_HOME)
         return fail(AMZ_ECONTRACT, "rollout needs an auto-resetting env (mode %d)", mode);
@@ -451,6 +491,7 @@ int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const
 
 int amz_env_observe(amz_env_t *e, uint8_t *view, int64_t *dirs, void *stream) {
     if (!e) return fail(AMZ_ECONFIG, "null env");
+    DevGuard guard_(e->device);
     int rc = launch_env_observe(e->G, e->E, view, dirs, (cudaStream_t)stream);
     if (rc) return fail(rc, "observe: unsupported agent_view_size");
     return cuda_status("env_observe");
@@ -458,18 +499,21 @@ int amz_env_observe(amz_env_t *e, uint8_t *view, int64_t *dirs, void *stream) {
 
 int amz_env_levels(amz_env_t *e, amz_level_t *out, void *stream) {
     if (!e || !out) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
     launch_env_levels(e->E, out, (cudaStream_t)stream);
     return cuda_status("env_levels");
 }
 
 int amz_env_state(amz_env_t *e, int32_t *out, void *stream) {
     if (!e || !out) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
     launch_env_state(e->E, out, (cudaStream_t)stream);
     return cuda_status("env_state");
 }
 
 int amz_env_set_state(amz_env_t *e, const int32_t *in, void *stream) {
     if (!e || !in) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
     e->spec_ready = false;
     launch_env_set_state(e->E, in, (cudaStream_t)stream);
     return cuda_status("env_set_state");
@@ -477,6 +521,7 @@ int amz_env_set_state(amz_env_t *e, const int32_t *in, void *stream) {
 
 int amz_env_check(amz_env_t *e, void *stream) {
     if (!e) return fail(AMZ_ECONFIG, "null env");
+    DevGuard guard_(e->device);
     cudaStream_t s = (cudaStream_t)stream;
     int h = 0;
     AMZ_CHECK_CUDA(cudaMemcpyAsync(&h, e->E.err, sizeof(int), cudaMemcpyDeviceToHost, s), "env_check");
@@ -484,6 +529,7 @@ int amz_env_check(amz_env_t *e, void *stream) {
     if (h) {
         cudaMemsetAsync(e->E.err, 0, sizeof(int), s);
         cudaStreamSynchronize(s);
+        if (h & 2) return fail(AMZ_ECONTRACT, "reset_to_levels: lane index out of range");
         return fail(AMZ_ECONTRACT, "step_batch called with terminal lanes");
     }
     return 0;
@@ -541,6 +587,7 @@ int amz_plr_create(int64_t capacity, amz_plr_t **out) {
                                                      (long long)capacity);
     amz_plr *b = new (std::nothrow) amz_plr();
     if (!b) return fail(AMZ_EFAULT, "out of host memory");
+    b->device = current_device();
     b->D.K = capacity;
     size_t K = (size_t)capacity;
     cudaError_t e = cudaMalloc((void **)&b->D.levels, K * sizeof(amz_level_t));
@@ -564,6 +611,7 @@ int amz_plr_create(int64_t capacity, amz_plr_t **out) {
 
 int amz_plr_destroy(amz_plr_t *b) {
     if (!b) return 0;
+    DevGuard guard_(b->device);
     cudaDeviceSynchronize();
     cudaFree(b->D.levels);
     cudaFree(b->D.score);
@@ -584,18 +632,20 @@ int amz_plr_destroy(amz_plr_t *b) {
 int amz_plr_update(amz_plr_t *b, const amz_level_t *levels, const double *scores, const double *max_ret, int64_t n,
                    int64_t iter, void *stream) {
     if (!b || (n > 0 && (!levels || !scores || !max_ret))) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
     if (n < 0) return fail(AMZ_ESHAPE, "negative candidate count");
     if (n > ((int64_t)1 << 30)) return fail(AMZ_ESHAPE, "too many candidates");
     cudaStream_t s = (cudaStream_t)stream;
     int rc = plr_scratch(b, n, s);
     if (rc) return rc;
-    launch_plr_update(b->D, levels, scores, max_ret, n, iter, b->W, s);
+    launch_plr_update(b->D, levels, scores, max_ret, n, iter, b->W, b->err, s);
     return cuda_status("plr_update");
 }
 
 int amz_plr_sample(amz_plr_t *b, const amz_seed_t *key, int64_t n, double rho, const double *lut, int64_t iter,
                    int32_t *slots, amz_level_t *levels, double *max_ret, double *score, void *stream) {
     if (!b || !key || !lut || (n > 0 && !slots)) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
     if (rho < 0.0 || rho > 1.0) return fail(AMZ_ECONFIG, "staleness_coef must be in [0, 1], got %g", rho);
     if (n <= 0) return 0;
     launch_plr_sample(b->D, *key, n, 1.0 - rho, rho, lut, iter, slots, levels, max_ret, score, b->err,
@@ -613,6 +663,7 @@ int amz_plr_top_q(const double *scores, int64_t n, int q, int32_t *out, void *st
 
 int amz_plr_size(amz_plr_t *b, int64_t *size, void *stream) {
     if (!b || !size) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
     cudaStream_t s = (cudaStream_t)stream;
     int64_t meta[2];
     int err = 0;
@@ -623,14 +674,24 @@ int amz_plr_size(amz_plr_t *b, int64_t *size, void *stream) {
     if (err) {
         cudaMemsetAsync(b->err, 0, sizeof(int), s);
         cudaStreamSynchronize(s);
+        if (err & 4)
+            return fail(AMZ_ECONTRACT, "buffer_update refused: last_sampled / seq spans exceed a 64-bit tie key");
         return fail(AMZ_ECONTRACT, "sampled from an empty level buffer");
     }
     return 0;
 }
 
+int amz_plr_digest(amz_plr_t *b, int64_t *out_dev, void *stream) {
+    if (!b || !out_dev) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
+    launch_plr_digest(b->D, out_dev, (cudaStream_t)stream);
+    return cuda_status("plr_digest");
+}
+
 int amz_plr_export(amz_plr_t *b, amz_level_t *levels, double *score, double *max_ret, int64_t *last, int64_t *seq,
                    int64_t *meta, void *stream) {
     if (!b) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t K = (size_t)b->D.K;
     if (levels) cudaMemcpyAsync(levels, b->D.levels, K * sizeof(amz_level_t), cudaMemcpyDeviceToDevice, s);
@@ -645,6 +706,7 @@ int amz_plr_export(amz_plr_t *b, amz_level_t *levels, double *score, double *max
 int amz_plr_import(amz_plr_t *b, const amz_level_t *levels, const double *score, const double *max_ret,
                    const int64_t *last, const int64_t *seq, const int64_t *meta, void *stream) {
     if (!b || !levels || !score || !max_ret || !last || !seq || !meta) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t K = (size_t)b->D.K;
     cudaMemcpyAsync(b->D.levels, levels, K * sizeof(amz_level_t), cudaMemcpyDeviceToDevice, s);

@@ -88,8 +88,16 @@ __global__ void __launch_bounds__(128) k_env_reset(Geo G, EnvDev E, const amz_le
     const int lane = threadIdx.x & 31;
     const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     uint8_t *my = stage + threadIdx.x * V * V;
-    if (i < n) {
-        const int64_t l = lanes ? lanes[i] : i;
+    bool ok = i < n;
+    int64_t l = i;
+    if (ok && lanes) {
+        l = lanes[i];
+        if (l < 0 || l >= E.B) {  // never write outside the lane arrays: flag it instead
+            atomicOr(E.err, 2);
+            ok = false;
+        }
+    }
+    if (ok) {
         Mask m;
         LaneRec L;
         load_level(levels + i, m, L.s.r, L.s.c, L.s.d, L.gr, L.gc);

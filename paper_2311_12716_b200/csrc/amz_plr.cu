@@ -28,6 +28,7 @@ namespace amz {
 constexpr int kPlrThreads = 1024;
 constexpr int kPlrMaxK = 4096;
 constexpr int kHash = 8192;  // smem hash table entries (>= 2 * K)
+constexpr int kMaxDevices = 64;
 
 __device__ __forceinline__ uint32_t level_hash(const uint4 &w, uint32_t pose) {
     uint32_t h = 0x9E3779B9u;
@@ -313,51 +314,96 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 // ---------------------------------------------------------------------------------
 // update
 //
-// Exact sequential semantics, cheap in practice:
+// Exact sequential semantics of SPEC.md:373-377 (oracle/plr_np.py LevelBuffer.update),
+// parallel wherever the order provably cannot matter:
 //   A  (all threads)  smem hash of the current buffer keys; each candidate looks up
 //                     its initial slot (init_match) and its first in-batch twin
-//                     (twin_first, via a global hash with atomicMin)
+//                     (twin_first, via a global hash with atomicMin).  Tie keys are
+//                     made relative: tb = (last - lmin) << bq | (seq - qmin), exact
+//                     for any int64 last_sampled / seq whose spans fit 64 bits together
+//                     (else the update is refused: error bit 4, ContractViolation)
 //   B  (all threads)  m_low = min(current min score, scores of candidates that can
 //                     update in place).  If the buffer starts full, a candidate with
 //                     no key match and score <= m_low can never enter (the minimum never
 //                     drops below m_low), so it is skipped; everything else is
 //                     "relevant" and compacted in order.
 //   C  (one warp)     replays the relevant candidates in order against an indexed
-//                     64-ary min-heap of (score, tb) in shared memory, tb = last_sampled
-//                     << 32 | seq (the stale-first eviction order): an in-place update is
-//                     one sift, an eviction is replace-top + sift-down, candidate data are
-//                     prefetched into shared memory by the whole CTA chunk by chunk, and
-//                     level / max_return copies are deferred to a parallel epilogue.
+//                     64-ary min-heap of (score, tb) in shared memory (the stale-first
+//                     eviction order): an in-place update is one sift, an eviction is
+//                     replace-top + sift-down; level / max_return copies are deferred
+//                     to a parallel epilogue.  Two kinds of stretch leave warp 0 for
+//                     the whole CTA:
+//     bulk in-place run (>= kBulkRun consecutive candidates whose level is present):
+//                     last writer per slot by atomicMax, heap rebuilt level-parallel;
+//     insert run (>= kRunMin consecutive candidates that are certainly new: no key
+//                     match at kernel start, first of their key in the batch):
+//                     a streaming top-K in parallel (k_plr_update comment below,
+//                     tools/plr_insert_runs_proto.py is the host prototype).
 // ---------------------------------------------------------------------------------
 constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses the hash table's space)
+constexpr int kRunMax = 1024; // insert-run candidates per parallel pass (one per thread)
+constexpr int kRunMin = 32;   // shorter insert runs stay on the sequential warp path
+constexpr int kBulkRun = 64;  // shorter in-place runs stay on the sequential warp path
+constexpr int kSeqAfterFlag = 64;  // candidates kept sequential after a run stopped early on a tie
 struct CandChunk {
     double sc[kChunk];
     int32_t cid[kChunk];
     int32_t tf[kChunk];
     int32_t im[kChunk];
 };
+// insert-run scratch (aliases the chunk: the chunk is restaged after a run)
+struct RunArr {
+    uint64_t rsk[kRunMax];   // run candidates' score keys, arrival order
+    uint64_t ask[kRunMax];   // accepted candidates' score keys, sorted by (score, arrival)
+    int32_t aarr[kRunMax];   // arrival index of ask[k]
+    int32_t vlist[kRunMax];  // evictions in order: >= 0 existing sorted position, < 0 -(acceptance + 1)
+    int32_t aslot[kRunMax];  // acceptance index -> slot
+    int32_t acand[kRunMax];  // acceptance index -> arrival index
+};
+using RunSort = cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int, 4>;
+struct SortedEntries {
+    uint64_t ekey[kPlrMaxK];  // score keys of the buffer (virtual free slots = 0), eviction order
+    int32_t eslot[kPlrMaxK];
+};
 struct UpdSmem {
     uint64_t hk[kPlrMaxK];  // heap: order-preserving score key (score_key)
-    uint64_t ht[kPlrMaxK];  // heap: tie-break key (last_sampled << 32) | seq
+    uint64_t ht[kPlrMaxK];  // heap: relative tie key (last - lmin) << bq | (seq - qmin)
     int hslot[kPlrMaxK];    // heap entry -> buffer slot
     int pos[kPlrMaxK];      // buffer slot -> heap entry
     union {
         uint32_t hash[kHash];
         CandChunk chunk;
+        RunArr run;
     } u;
     int owner[kPlrMaxK];   // first-candidate index of the key now in the slot, -1 = initial entry
     int src[kPlrMaxK];     // candidate whose level the slot now holds (-1 = unchanged)
     int mr_src[kPlrMaxK];  // candidate whose score / max_return the slot now holds (-1 = unchanged)
     uint32_t replaced[kPlrMaxK / 32];
+    union {
+        typename RunSort::TempStorage sort;
+        SortedEntries e;
+    } r1;
+    uint32_t evicted[kRunMax / 32];  // insert run: acceptances evicted again inside the run
     double mlow;
     int64_t next_seq;
+    int64_t lmin, qmin, lmax, qmax, last_max0;
+    unsigned long long tie_max;
+    int bq;
     int n_rel;
     int full;
     int size;
-    int rcur;     // next chunk position for warp 0
-    int bulk_hi;  // end of the in-place run to apply in bulk (-1 = none)
+    int rcur;      // next chunk position for warp 0
+    int action;    // 0 = chunk done, 1 = bulk in-place run [rcur, arg), 2 = insert run [rcur, rcur + arg)
+    int arg;
+    int force_seq_until;  // absolute relevant index: candidates before it take the sequential path
+    int run_ok;
+    int flag_first;
+    int run_p;
+    int n_virtual;
 };
 static_assert(sizeof(CandChunk) <= sizeof(uint32_t) * kHash, "chunk must fit in the hash table space");
+static_assert(sizeof(RunArr) <= sizeof(uint32_t) * kHash, "run scratch must fit in the hash table space");
+static_assert(sizeof(UpdSmem) + 1024 <= 227 * 1024, "update shared memory over the 227 KB opt-in limit");
 
 // Scores enter the heap as order-preserving unsigned keys (-0.0 folded onto +0.0, as the
 // float compare of the reference sees them), so every comparison is integer and a warp
@@ -369,6 +415,10 @@ __device__ __forceinline__ uint64_t score_key(double s) {
 }
 __device__ __forceinline__ bool ukey_lt(uint64_t ka, uint64_t ta, uint64_t kb, uint64_t tb) {
     return ka < kb || (ka == kb && ta < tb);
+}
+__device__ __forceinline__ uint64_t tie_pack(const UpdSmem &S, int64_t last, int64_t seq) {
+    const uint64_t q = (uint64_t)seq - (uint64_t)S.qmin;
+    return S.bq >= 64 ? q : ((((uint64_t)last - (uint64_t)S.lmin) << S.bq) | q);
 }
 __device__ __forceinline__ void heap_put(UpdSmem &S, int h, uint64_t k, uint64_t t, int slot) {
     S.hk[h] = k;
@@ -456,6 +506,16 @@ __device__ __forceinline__ void heap_down_t(UpdSmem &S, int h, int n) {
     }
     heap_put(S, h, xk, xt, xs);
 }
+// whole CTA: rebuild the heap property over entries [0, n) (level starts 0, 1, 65, 4161)
+__device__ __forceinline__ void heapify_cta(UpdSmem &S, int n) {
+    const int starts[4] = {0, 1, 65, 4161};
+    for (int lv = 2; lv >= 0; lv--) {
+        __syncthreads();
+        const int l0 = starts[lv], l1 = min(starts[lv + 1], n);
+        for (int h = l0 + (int)threadIdx.x; h < l1; h += blockDim.x) heap_down_t(S, h, n);
+    }
+    __syncthreads();
+}
 
 // the buffer slot candidate r of the staged chunk updates in place, or -1
 __device__ __forceinline__ int cand_present(const UpdSmem &S, const UpdScratch &W, int r) {
@@ -463,6 +523,10 @@ __device__ __forceinline__ int cand_present(const UpdSmem &S, const UpdScratch &
     if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) return im;
     const int f = S.u.chunk.tf[r];
     return f != S.u.chunk.cid[r] ? W.keyslot[f] : -1;
+}
+// certainly new at any point of the batch: no key match at kernel start, first of its key
+__device__ __forceinline__ bool cand_pure(const UpdSmem &S, int r) {
+    return S.u.chunk.im[r] < 0 && S.u.chunk.tf[r] == S.u.chunk.cid[r];
 }
 // length of the run of consecutive in-place candidates starting at r (whole warp)
 __device__ __forceinline__ int inplace_run(const UpdSmem &S, const UpdScratch &W, int r, int cn, int lane) {
@@ -475,7 +539,267 @@ __device__ __forceinline__ int inplace_run(const UpdSmem &S, const UpdScratch &W
         L += 32;
     }
 }
-constexpr int kBulkRun = 64;  // shorter in-place runs stay on the sequential warp path
+// length of the run of consecutive certainly-new candidates starting at r (whole warp)
+__device__ __forceinline__ int pure_run(const UpdSmem &S, int r, int cn, int lane) {
+    int L = 0;
+    while (L < kRunMax) {
+        const int i = r + L + lane;
+        const bool pr = i < cn && cand_pure(S, i);
+        const unsigned fail = ~__ballot_sync(0xFFFFFFFFu, pr);
+        if (fail) return min(L + __ffs(fail) - 1, kRunMax);
+        L += 32;
+    }
+    return kRunMax;
+}
+
+__device__ __forceinline__ int upper_bound_u64(const uint64_t *a, int n, uint64_t x) {  // # a[i] <= x
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ int lower_bound_u64(const uint64_t *a, int n, uint64_t x) {  // # a[i] < x
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// block-wide exclusive prefix count of `flag` (kPlrThreads threads); returns the total
+__device__ __forceinline__ int block_excl_count(bool flag, int &excl, int *wscan) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, flag);
+    if (lane == 0) wscan[w] = __popc(b);
+    __syncthreads();
+    if (w == 0) {
+        const int v = lane < (int)(blockDim.x >> 5) ? wscan[lane] : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        wscan[lane] = x - v;  // exclusive
+        if (lane == 31) wscan[32] = x;
+    }
+    __syncthreads();
+    excl = wscan[w] + __popc(b & ((1u << lane) - 1u));
+    const int tot = wscan[32];
+    __syncthreads();
+    return tot;
+}
+
+// Insert run (whole CTA): candidates rel[r0 .. r0 + m) are certainly new.  With free slots
+// as virtual entries of score -inf (evicted in slot order) the sequential rule is a
+// streaming top-K of the buffer under x < y <=> (score_x < score_y) or (equal score and
+// x entered first); every stored entry entered before every run candidate because
+// tb(stored) < tb(new) (checked: last_sampled <= iter).
+//   accept_i <=> #{j < i : s_j > s_i} < #{x : s_x <= s_i}
+//   the p acceptances evict the p smallest of (buffer U accepted) in order; the k-th
+//   acceptance takes the slot of the k-th eviction (chains through re-evicted ones).
+// The order differs from the rule only where a candidate's score equals the score of the
+// minimum present at its arrival (the rule rejects): a candidate is flagged when the
+// smallest member of its equal-score group in the merged order is among the first p+1
+// and was present before it.  The prefix before the first flagged candidate is committed
+// (the prefix of the streaming process is the same process); returns the number of
+// candidates consumed (the flagged one goes to the sequential path).
+__device__ int insert_run(UpdSmem &S, const UpdScratch &W, const double *__restrict__ cscore, int64_t iter, int r0,
+                          int m, int E, int *wscan) {
+    // E = buffer capacity K: sort items [0, E) are the buffer (stored + virtual free
+    // slots), items [E, kPlrMaxK) padding that sorts last
+    const int tid = threadIdx.x;
+    const int size0 = S.size;
+    // ---- sorted buffer: tie order (stable), then score order ----
+    unsigned long long keys[4];
+    int vals[4];
+    {
+        unsigned long long tmax = 0ull;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int i = tid * 4 + k;  // heap position for i < size0, free slot i otherwise
+            if (i < size0) {
+                keys[k] = S.ht[i];
+                vals[k] = S.hslot[i];
+            } else {
+                keys[k] = (unsigned long long)i;  // virtual entries: slot order (padding: any)
+                vals[k] = i;
+            }
+            tmax = keys[k] > tmax ? keys[k] : tmax;
+        }
+        if (tid == 0) S.tie_max = 0ull;
+        __syncthreads();
+        atomicMax(&S.tie_max, tmax);
+        __syncthreads();
+    }
+    const int tbits = 64 - __clzll((long long)(S.tie_max | 1ull));
+    RunSort(S.r1.sort).Sort(keys, vals, 0, tbits);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int slot = vals[k];
+        // virtual (free) slots: score key 0 (below every real score); padding: all ones
+        keys[k] = slot < size0 ? S.hk[S.pos[slot]] : (slot < E ? 0ull : ~0ull);
+    }
+    RunSort(S.r1.sort).Sort(keys, vals);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        S.r1.e.ekey[tid * 4 + k] = keys[k];
+        S.r1.e.eslot[tid * 4 + k] = vals[k];
+    }
+    if (tid == 0) {
+        S.flag_first = m;
+        S.n_virtual = 0;
+    }
+    __syncthreads();
+    // ---- acceptance ----
+    uint64_t si = 0ull;
+    int cidx = -1;
+    if (tid < m) {
+        cidx = W.rel[r0 + tid];
+        si = score_key(cscore[cidx]);
+        S.u.run.rsk[tid] = si;
+    }
+    __syncthreads();
+    int below = 0;
+    bool acc = false;
+    if (tid < m) {
+        below = upper_bound_u64(S.r1.e.ekey, E, si);
+        int greater = 0;
+        for (int j = 0; j < tid; j++) greater += S.u.run.rsk[j] > si;
+        acc = greater < below;
+    }
+    int q = 0;
+    const int p = block_excl_count(acc, q, wscan);
+    if (acc) S.u.run.acand[q] = tid;
+    __syncthreads();
+    // rank of each acceptance in (score, arrival) order; merged position = rank + below
+    if (acc) {
+        int ra = 0;
+        for (int k = 0; k < p; k++) {
+            const int j = S.u.run.acand[k];
+            const uint64_t sj = S.u.run.rsk[j];
+            ra += sj < si || (sj == si && j < tid);
+        }
+        S.u.run.ask[ra] = si;
+        S.u.run.aarr[ra] = tid;
+        const int mi = ra + below;
+        if (mi < p) S.u.run.vlist[mi] = -(q + 1);
+    }
+    __syncthreads();
+    for (int k = tid; k < p && k < E; k += blockDim.x) {  // existing entries among the first p merged
+        const int mi = k + lower_bound_u64(S.u.run.ask, p, S.r1.e.ekey[k]);
+        if (mi < p) S.u.run.vlist[mi] = k;
+    }
+    // ---- tie flags ----
+    if (tid < m) {
+        const int ke = lower_bound_u64(S.r1.e.ekey, E, si);
+        int mi = 0x7FFFFFFF;
+        bool before = false;
+        if (ke < E && S.r1.e.ekey[ke] == si) {
+            mi = ke + lower_bound_u64(S.u.run.ask, p, si);
+            before = true;
+        } else {
+            const int ka = lower_bound_u64(S.u.run.ask, p, si);
+            if (ka < p && S.u.run.ask[ka] == si) {
+                mi = ka + ke;
+                before = S.u.run.aarr[ka] < tid;
+            }
+        }
+        if (before && mi <= p) atomicMin(&S.flag_first, tid);
+    }
+    __syncthreads();
+    const int f = S.flag_first;
+    // acceptances before the first flagged arrival
+    int pc = 0;
+    {
+        int lo = 0, hi = p;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (S.u.run.acand[mid] < f)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        pc = lo;
+    }
+    for (int k = tid; k < kRunMax / 32; k += blockDim.x) S.evicted[k] = 0u;
+    __syncthreads();
+    // ---- slots: the j-th acceptance takes the slot of the j-th eviction ----
+    for (int j = tid; j < pc; j += blockDim.x) {
+        const int v = S.u.run.vlist[j];
+        if (v >= 0) {
+            const int slot = S.r1.e.eslot[v];
+            S.u.run.aslot[j] = slot;
+            if (slot >= size0) atomicAdd(&S.n_virtual, 1);
+            // an entry inserted earlier in this update loses its key
+            if (slot < size0 && S.owner[slot] >= 0) W.keyslot[S.owner[slot]] = -1;
+        } else {
+            S.u.run.aslot[j] = -1;
+            const int qq = -v - 1;
+            atomicOr(&S.evicted[qq >> 5], 1u << (qq & 31));
+        }
+    }
+    __syncthreads();
+    // pointer jumping along chains of re-evicted acceptances (vlist[j] < 0 -> parent)
+    while (true) {
+        int ns = -1, nv = 0;
+        const int j = tid;
+        bool pend = false;
+        if (j < pc && S.u.run.aslot[j] < 0) {
+            const int par = -S.u.run.vlist[j] - 1;
+            const int ps = S.u.run.aslot[par];
+            pend = true;
+            if (ps >= 0)
+                ns = ps;
+            else
+                nv = S.u.run.vlist[par];
+        }
+        __syncthreads();
+        if (pend) {
+            if (ns >= 0)
+                S.u.run.aslot[j] = ns;
+            else
+                S.u.run.vlist[j] = nv;
+        }
+        if (!__syncthreads_or(pend)) break;
+    }
+    // ---- apply: final occupants only ----
+    const int64_t seq0 = S.next_seq;
+    for (int j = tid; j < pc; j += blockDim.x) {
+        const int a = S.u.run.acand[j];
+        const int c = W.rel[r0 + a];
+        if ((S.evicted[j >> 5] >> (j & 31)) & 1u) {
+            W.keyslot[c] = -1;  // inserted and evicted again inside the run
+            continue;
+        }
+        const int slot = S.u.run.aslot[j];
+        const int h = slot < size0 ? S.pos[slot] : slot;  // free slots fill heap positions in order
+        heap_put(S, h, score_key(cscore[c]), tie_pack(S, iter, seq0 + j), slot);
+        S.owner[slot] = c;
+        S.src[slot] = c;
+        S.mr_src[slot] = c;
+        atomicOr(&S.replaced[slot >> 5], 1u << (slot & 31));
+        W.keyslot[c] = slot;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        S.size = size0 + S.n_virtual;
+        S.next_seq = seq0 + pc;
+    }
+    __syncthreads();
+    heapify_cta(S, S.size);
+    return f;
+}
 
 __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
                                 int64_t hsize) {
@@ -519,32 +843,71 @@ __global__ void k_plr_cand_twin(const amz_level_t *__restrict__ cand, int64_t n,
     }
 }
 
+__device__ __forceinline__ int bits_for(uint64_t span) { return span ? 64 - __clzll((long long)span) : 0; }
+
 __global__ void __launch_bounds__(kPlrThreads, 1)
     k_plr_update(PlrDev D, const amz_level_t *__restrict__ cand, const double *__restrict__ cscore,
-                 const double *__restrict__ cmax, int64_t n, int64_t iter, UpdScratch W) {
+                 const double *__restrict__ cmax, int64_t n, int64_t iter, UpdScratch W, int *err) {
     extern __shared__ __align__(16) uint8_t smraw[];
     UpdSmem &S = *reinterpret_cast<UpdSmem *>(smraw);
+    __shared__ int wscan[33];
     const int tid = threadIdx.x, lane = tid & 31;
     const int K = (int)D.K;
     const int size0 = (int)D.meta[0];
-    // ---- A: load the buffer into the heap arrays + key hash ----
+    // ---- A: tie-key frame, buffer into the heap arrays + key hash ----
     for (int i = tid; i < kHash; i += blockDim.x) S.u.hash[i] = 0u;
     for (int i = tid; i < kPlrMaxK / 32; i += blockDim.x) S.replaced[i] = 0u;
+    for (int i = tid; i < kPlrMaxK; i += blockDim.x) {
+        S.owner[i] = -1;
+        S.src[i] = -1;
+        S.mr_src[i] = -1;
+    }
     if (tid == 0) {
         S.n_rel = 0;
         S.full = size0 >= K;
+        S.next_seq = D.meta[1];
+        S.lmin = iter;
+        S.lmax = iter;
+        S.last_max0 = INT64_MIN;
+        S.qmin = D.meta[1];
+        S.qmax = D.meta[1] + n;
+        S.force_seq_until = 0;
     }
     __syncthreads();
+    {
+        long long lmn = iter, lmx = iter, qmn = S.qmin, lm0 = INT64_MIN;
+        for (int i = tid; i < size0; i += blockDim.x) {
+            const long long l = D.last[i], q = D.seq[i];
+            lmn = l < lmn ? l : lmn;
+            lmx = l > lmx ? l : lmx;
+            lm0 = l > lm0 ? l : lm0;
+            qmn = q < qmn ? q : qmn;
+        }
+        atomicMin((long long *)&S.lmin, lmn);
+        atomicMax((long long *)&S.lmax, lmx);
+        atomicMax((long long *)&S.last_max0, lm0);
+        atomicMin((long long *)&S.qmin, qmn);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int bl = bits_for((uint64_t)S.lmax - (uint64_t)S.lmin);
+        const int bq = bits_for((uint64_t)S.qmax - (uint64_t)S.qmin);
+        S.bq = bq;
+        S.run_ok = (bl + bq <= 64) ? 1 : -1;
+        if (S.run_ok > 0) S.run_ok = S.last_max0 <= iter ? 1 : 0;  // stored ties below every new one
+    }
+    __syncthreads();
+    if (S.run_ok < 0) {  // (last, seq) spans do not fit one 64-bit tie key: refuse, unchanged
+        if (tid == 0) atomicOr(err, 4);
+        return;
+    }
     double my_min = __longlong_as_double(0x7FF0000000000000ll);  // +inf
     for (int i = tid; i < size0; i += blockDim.x) {
         const double sc = D.score[i];
         S.hk[i] = score_key(sc);
-        S.ht[i] = ((uint64_t)D.last[i] << 32) | (uint32_t)D.seq[i];
+        S.ht[i] = tie_pack(S, D.last[i], D.seq[i]);
         S.hslot[i] = i;
         S.pos[i] = i;
-        S.owner[i] = -1;
-        S.src[i] = -1;
-        S.mr_src[i] = -1;
         my_min = fmin(my_min, sc);
         uint4 w;
         uint32_t p0, p1;
@@ -583,18 +946,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         S.mlow = m;
     }
     // ---- heapify, level-parallel (all sift-downs of one level touch disjoint subtrees) ----
-    // level starts of the 64-ary heap: 0, 1, 65, 4161
-    {
-        const int starts[4] = {0, 1, 65, 4161};
-        for (int lv = 2; lv >= 0; lv--) {
-            __syncthreads();
-            const int lo = starts[lv], hi = min(starts[lv + 1], size0);
-            for (int h = lo + tid; h < hi; h += blockDim.x) heap_down_t(S, h, size0);
-        }
-    }
-    __syncthreads();
+    heapify_cta(S, size0);
     // ---- B: relevant candidates, compacted in order (block-wide, chunk by chunk) ----
-    __shared__ int wcount[32];
     for (int64_t base = 0; base < n; base += blockDim.x) {
         const int64_t c = base + tid;
         bool rel = false;
@@ -602,38 +955,27 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             const bool later_twin = W.twin_first[c] != (int32_t)c;
             rel = !S.full || W.init_match[c] >= 0 || later_twin || !(cscore[c] <= S.mlow);
         }
-        unsigned b = __ballot_sync(0xFFFFFFFFu, rel);
-        if (lane == 0) wcount[tid >> 5] = __popc(b);
+        int excl = 0;
+        const int tot = block_excl_count(rel, excl, wscan);
+        if (rel) W.rel[S.n_rel + excl] = (int32_t)c;
         __syncthreads();
-        if (tid == 0) {
-            int acc = S.n_rel;
-            for (int k = 0; k < (int)(blockDim.x >> 5); k++) {
-                int v = wcount[k];
-                wcount[k] = acc;
-                acc += v;
-            }
-            S.n_rel = acc;
-        }
-        __syncthreads();
-        if (rel) W.rel[wcount[tid >> 5] + __popc(b & ((1u << lane) - 1u))] = (int32_t)c;
+        if (tid == 0) S.n_rel += tot;
         __syncthreads();
     }
     // A skipped first occurrence is never inserted (score <= mlow), so its later twins,
     // which are always relevant, correctly find no entry for the key (keyslot = -1).
 
-    // ---- C: ordered replay (warp 0); long in-place runs applied by the whole CTA ----
+    // ---- C: ordered replay (warp 0); bulk in-place runs and insert runs by the CTA ----
     // In-place updates never change which later candidates find their key (only fills and
     // evictions do), so warp 0 scans ahead for the run of consecutive in-place candidates
     // starting at r.  A run of >= kBulkRun is applied in bulk: the last candidate per slot
     // wins (atomicMax on the candidate index, which is increasing along the order), and the
-    // heap is rebuilt level-parallel.  (score, last_sampled, seq) is a total order (seq is
-    // unique), so the heap's shape never affects which entry is the minimum.
+    // heap is rebuilt level-parallel.  (score, tb) is a total order (seq is unique), so the
+    // heap's shape never affects which entry is the minimum.
     const int nrel = S.n_rel;
-    if (tid == 0) {
-        S.size = size0;
-        S.next_seq = D.meta[1];
-    }
-    for (int base = 0; base < nrel; base += kChunk) {
+    if (tid == 0) S.size = size0;
+    int base = 0;
+    while (base < nrel) {
         const int cn = (nrel - base) < kChunk ? (nrel - base) : kChunk;
         __syncthreads();
         for (int i = tid; i < cn; i += blockDim.x) {
@@ -643,119 +985,137 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             S.u.chunk.tf[i] = W.twin_first[c];
             S.u.chunk.im[i] = W.init_match[c];
         }
-        if (tid == 0) S.rcur = 0;
         __syncthreads();
-        while (true) {
-            if (tid < 32) {
-                int size = S.size;
-                int64_t next_seq = S.next_seq;
-                int r = S.rcur, scan_end = r, bulk_hi = -1;
-                // candidate fields are prefetched one ahead (the replaced bit and the twin's
-                // keyslot are read after the previous candidate is applied)
-                int c_n = 0, f_n = 0, im_n = -1;
-                double sc_n = 0.0;
-                if (r < cn) {
-                    c_n = S.u.chunk.cid[r];
-                    sc_n = S.u.chunk.sc[r];
-                    f_n = S.u.chunk.tf[r];
-                    im_n = S.u.chunk.im[r];
+        if (tid < 32) {
+            int size = S.size;
+            int64_t next_seq = S.next_seq;
+            const bool run_ok = S.run_ok > 0;
+            const int seq_until = S.force_seq_until - base;  // chunk-relative
+            int r = 0, scan_end = 0, pscan_end = 0, action = 0, arg = 0;
+            // candidate fields are prefetched one ahead (the replaced bit and the twin's
+            // keyslot are read after the previous candidate is applied)
+            int c_n = 0, f_n = 0, im_n = -1;
+            double sc_n = 0.0;
+            if (r < cn) {
+                c_n = S.u.chunk.cid[r];
+                sc_n = S.u.chunk.sc[r];
+                f_n = S.u.chunk.tf[r];
+                im_n = S.u.chunk.im[r];
+            }
+            for (; r < cn; r++) {
+                const int c = c_n, f = f_n, im = im_n;
+                const double sc = sc_n;
+                if (r + 1 < cn) {
+                    c_n = S.u.chunk.cid[r + 1];
+                    sc_n = S.u.chunk.sc[r + 1];
+                    f_n = S.u.chunk.tf[r + 1];
+                    im_n = S.u.chunk.im[r + 1];
                 }
-                for (; r < cn; r++) {
-                    const int c = c_n, f = f_n, im = im_n;
-                    const double sc = sc_n;
-                    if (r + 1 < cn) {
-                        c_n = S.u.chunk.cid[r + 1];
-                        sc_n = S.u.chunk.sc[r + 1];
-                        f_n = S.u.chunk.tf[r + 1];
-                        im_n = S.u.chunk.im[r + 1];
+                // a stretch of certainly-new candidates worth a parallel insert run
+                if (run_ok && im < 0 && f == c && r >= pscan_end && r >= seq_until) {
+                    const int L = pure_run(S, r, cn, lane);
+                    if (L >= kRunMin) {
+                        action = 2;
+                        arg = L;
+                        break;
                     }
-                    int present = -1;
-                    if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
-                    if (present < 0 && f != c) present = W.keyslot[f];
-                    // only an in-place candidate can open a run worth applying in bulk
-                    if (present >= 0 && r >= scan_end) {
-                        const int L = inplace_run(S, W, r, cn, lane);
-                        if (L >= kBulkRun) {
-                            bulk_hi = r + L;
-                            break;
-                        }
-                        scan_end = r + L;
+                    pscan_end = r + L;
+                }
+                int present = -1;
+                if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
+                if (present < 0 && f != c) present = W.keyslot[f];
+                // only an in-place candidate can open a run worth applying in bulk
+                if (present >= 0 && r >= scan_end) {
+                    const int L = inplace_run(S, W, r, cn, lane);
+                    if (L >= kBulkRun) {
+                        action = 1;
+                        arg = r + L;
+                        break;
                     }
-                    const uint64_t sk = score_key(sc);
-                    if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
-                        const int h = S.pos[present];
-                        const uint64_t ok = S.hk[h], ot = S.ht[h];
-                        __syncwarp();
-                        if (lane == 0) S.mr_src[present] = c;
-                        if (sk < ok)
-                            sift_up_w(S, h, sk, ot, present, lane);
-                        else if (sk > ok)
-                            sift_down_w(S, h, size, sk, ot, present, lane);
-                        __syncwarp();
-                        continue;
-                    }
-                    const uint64_t tbn = ((uint64_t)iter << 32) | (uint32_t)next_seq;
-                    int slot;
-                    if (size < K) {  // fill
-                        slot = size;
-                        const int h = size++;
-                        __syncwarp();
-                        sift_up_w(S, h, sk, tbn, slot, lane);
-                    } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
-                        if (!(sk > S.hk[0])) continue;
-                        slot = S.hslot[0];
-                        const int ow = S.owner[slot];
-                        __syncwarp();
-                        if (lane == 0 && ow >= 0) W.keyslot[ow] = -1;
-                        sift_down_w(S, 0, size, sk, tbn, slot, lane);
-                    }
-                    if (lane == 0) {
-                        S.owner[slot] = f;
-                        S.replaced[slot >> 5] |= 1u << (slot & 31);
-                        S.src[slot] = c;
-                        S.mr_src[slot] = c;
-                        W.keyslot[f] = slot;
-                    }
+                    scan_end = r + L;
+                }
+                const uint64_t sk = score_key(sc);
+                if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
+                    const int h = S.pos[present];
+                    const uint64_t ok = S.hk[h], ot = S.ht[h];
                     __syncwarp();
-                    next_seq++;
+                    if (lane == 0) S.mr_src[present] = c;
+                    if (sk < ok)
+                        sift_up_w(S, h, sk, ot, present, lane);
+                    else if (sk > ok)
+                        sift_down_w(S, h, size, sk, ot, present, lane);
+                    __syncwarp();
+                    continue;
+                }
+                const uint64_t tbn = tie_pack(S, iter, next_seq);
+                int slot;
+                if (size < K) {  // fill
+                    slot = size;
+                    const int h = size++;
+                    __syncwarp();
+                    sift_up_w(S, h, sk, tbn, slot, lane);
+                } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
+                    if (!(sk > S.hk[0])) continue;
+                    slot = S.hslot[0];
+                    const int ow = S.owner[slot];
+                    __syncwarp();
+                    if (lane == 0 && ow >= 0) W.keyslot[ow] = -1;
+                    sift_down_w(S, 0, size, sk, tbn, slot, lane);
+                }
+                if (lane == 0) {
+                    S.owner[slot] = f;
+                    S.replaced[slot >> 5] |= 1u << (slot & 31);
+                    S.src[slot] = c;
+                    S.mr_src[slot] = c;
+                    W.keyslot[f] = slot;
                 }
                 __syncwarp();
-                if (lane == 0) {
-                    S.size = size;
-                    S.next_seq = next_seq;
-                    S.rcur = r;
-                    S.bulk_hi = bulk_hi;
-                }
+                next_seq++;
             }
-            __syncthreads();
-            const int lo = S.rcur, hi = S.bulk_hi;
-            if (hi < 0) break;
-            for (int i = lo + tid; i < hi; i += blockDim.x) atomicMax(&S.mr_src[cand_present(S, W, i)], S.u.chunk.cid[i]);
+            __syncwarp();
+            if (lane == 0) {
+                S.size = size;
+                S.next_seq = next_seq;
+                S.rcur = r;
+                S.action = action;
+                S.arg = arg;
+            }
+        }
+        __syncthreads();
+        const int lo = S.rcur, action = S.action, arg = S.arg;
+        if (action == 0) {
+            base += cn;
+            continue;
+        }
+        if (action == 1) {  // bulk in-place run [lo, arg)
+            const int hi = arg;
+            for (int i = lo + tid; i < hi; i += blockDim.x)
+                atomicMax(&S.mr_src[cand_present(S, W, i)], S.u.chunk.cid[i]);
             __syncthreads();
             for (int i = lo + tid; i < hi; i += blockDim.x) {
                 const int p = cand_present(S, W, i);
                 if (S.mr_src[p] == S.u.chunk.cid[i]) S.hk[S.pos[p]] = score_key(S.u.chunk.sc[i]);
             }
-            const int hs = S.size;
-            const int starts[4] = {0, 1, 65, 4161};
-            for (int lv = 2; lv >= 0; lv--) {
-                __syncthreads();
-                const int l0 = starts[lv], l1 = min(starts[lv + 1], hs);
-                for (int h = l0 + tid; h < l1; h += blockDim.x) heap_down_t(S, h, hs);
-            }
-            __syncthreads();
-            if (tid == 0) S.rcur = hi;
-            __syncthreads();
+            heapify_cta(S, S.size);
+            base += hi;
+            continue;
         }
+        // insert run [base + lo, base + lo + arg)
+        const int used = insert_run(S, W, cscore, iter, base + lo, arg, K, wscan);
+        if (used < arg) {  // stopped on a tie: the flagged candidate (and a few after) go sequential
+            if (tid == 0) S.force_seq_until = base + lo + used + (used < kRunMin ? kSeqAfterFlag : 1);
+        }
+        base += lo + used;
     }
     __syncthreads();
     // ---- epilogue: scatter the heap back to slots, deferred level / max_return copies ----
     const int fsize = S.size;
+    const uint64_t qmask = S.bq >= 64 ? ~0ull : ((1ull << S.bq) - 1ull);
     for (int h = tid; h < fsize; h += blockDim.x) {
         const int slot = S.hslot[h];
         const uint64_t tb = S.ht[h];
-        D.last[slot] = (int64_t)(tb >> 32);
-        D.seq[slot] = (int64_t)(uint32_t)tb;
+        D.last[slot] = (int64_t)((S.bq >= 64 ? 0ull : (tb >> S.bq)) + (uint64_t)S.lmin);
+        D.seq[slot] = (int64_t)((tb & qmask) + (uint64_t)S.qmin);
         if (S.src[slot] >= 0) D.levels[slot] = cand[S.src[slot]];
         const int mr = S.mr_src[slot];
         if (mr >= 0) {
@@ -816,16 +1176,60 @@ __global__ void k_top_q(const double *__restrict__ scores, int64_t n, int q, int
     }
 }
 
+// 64-bit digest of the buffer state (valid slots + meta) for the replica drift check:
+// a wrapping sum of per-slot mixes (slot index, level words, score / max_return bits,
+// last_sampled, seq), so it is order-free across threads and equal iff (up to hash
+// collisions) the replicas hold the same entries in the same slots.
+__device__ __forceinline__ uint64_t mix64(uint64_t h, uint64_t v) {
+    h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 29;
+    return h;
+}
+__global__ void __launch_bounds__(256) k_plr_digest(PlrDev D, int64_t *__restrict__ out) {
+    __shared__ unsigned long long acc;
+    if (threadIdx.x == 0) acc = 0ull;
+    __syncthreads();
+    const int64_t size = D.meta[0];
+    unsigned long long mine = 0ull;
+    for (int64_t i = threadIdx.x; i < size && i < D.K; i += blockDim.x) {
+        const uint4 *lw = reinterpret_cast<const uint4 *>(D.levels + i);
+        const uint4 a = lw[0], b = lw[1];
+        uint64_t h = mix64(0x243F6A8885A308D3ull, (uint64_t)i);
+        h = mix64(h, ((uint64_t)a.y << 32) | a.x);
+        h = mix64(h, ((uint64_t)a.w << 32) | a.z);
+        h = mix64(h, ((uint64_t)b.y << 32) | b.x);
+        h = mix64(h, ((uint64_t)b.w << 32) | b.z);
+        h = mix64(h, (uint64_t)__double_as_longlong(D.score[i]));
+        h = mix64(h, (uint64_t)__double_as_longlong(D.maxret[i]));
+        h = mix64(h, (uint64_t)D.last[i]);
+        h = mix64(h, (uint64_t)D.seq[i]);
+        mine += h;
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&acc, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) out[0] = (int64_t)mix64(mix64(acc, (uint64_t)size), (uint64_t)D.meta[1]);
+}
+
+int launch_plr_digest(const PlrDev &D, int64_t *out, cudaStream_t s) {
+    k_plr_digest<<<1, 256, 0, s>>>(D, out);
+    return 0;
+}
+
 size_t plr_sample_smem() { return sizeof(SampleSmem); }
 size_t plr_update_smem() { return sizeof(UpdSmem); }
 
 int launch_plr_sample(const PlrDev &D, const amz_seed_t &key, int64_t n, double omr, double rho, const double *lut,
                       int64_t iter, int32_t *slots, amz_level_t *levels, double *maxret, double *score, int *err,
                       cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[kMaxDevices] = {};  // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= kMaxDevices || !attr[dev]) {
         cudaFuncSetAttribute(k_plr_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SampleSmem));
-        attr = true;
+        if (dev < kMaxDevices) attr[dev] = true;
     }
     k_plr_sample<<<1, kPlrThreads, sizeof(SampleSmem), s>>>(D, key, n, omr, rho, lut, iter, slots, levels, maxret,
                                                              score, err);
@@ -833,11 +1237,13 @@ int launch_plr_sample(const PlrDev &D, const amz_seed_t &key, int64_t n, double 
 }
 
 int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs, const double *cm, int64_t n,
-                      int64_t iter, const UpdScratch &W, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+                      int64_t iter, const UpdScratch &W, int *err, cudaStream_t s) {
+    static bool attr[kMaxDevices] = {};  // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= kMaxDevices || !attr[dev]) {
         cudaFuncSetAttribute(k_plr_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
-        attr = true;
+        if (dev < kMaxDevices) attr[dev] = true;
     }
     if (n <= 0) return 0;
     int64_t hsize = 1;
@@ -846,7 +1252,7 @@ int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs
     const int g = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
     k_plr_cand_prep<<<g, 256, 0, s>>>(D, cand, n, W, hsize);
     k_plr_cand_twin<<<g, 256, 0, s>>>(cand, n, W, hsize);
-    k_plr_update<<<1, kPlrThreads, sizeof(UpdSmem), s>>>(D, cand, cs, cm, n, iter, W);
+    k_plr_update<<<1, kPlrThreads, sizeof(UpdSmem), s>>>(D, cand, cs, cm, n, iter, W, err);
     return 0;
 }
 

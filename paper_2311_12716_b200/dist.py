@@ -74,9 +74,12 @@ def all_gather_records(rec):
         out = torch.empty((rec.shape[0] * ws, rec.shape[1]), dtype=rec.dtype, device=rec.device)
         torch.distributed.all_gather_into_tensor(out, rec)
         return out
-    parts = [torch.empty_like(rec) for _ in range(ws)]
-    torch.distributed.all_gather(parts, rec)
-    return torch.cat(parts)
+    # gloo (CPU test worlds, several ranks on one device): gather host copies
+    dev = rec.device
+    host = rec.cpu()
+    parts = [torch.empty_like(host) for _ in range(ws)]
+    torch.distributed.all_gather(parts, host)
+    return torch.cat(parts).to(dev)
 
 
 def gather_candidates(levels, scores, max_returns):
@@ -93,18 +96,29 @@ def buffer_digest(state: dict) -> int:
     return int.from_bytes(h.digest(), "little") & 0x7FFFFFFFFFFFFFFF
 
 
-def check_replicas(digest: int, device=None) -> None:
-    """Raise RunnerFault if the ranks' buffers differ (all-reduce MIN and MAX)."""
+def check_replicas(digest, device=None) -> None:
+    """Raise RunnerFault if the ranks' buffers differ: one all-reduce of [d, -d] with MAX
+    gives max and -min of the digests in one collective.  ``digest`` is an int or a
+    device int64 tensor (``LevelBuffer.digest()``, computed on the GPU; with NCCL it
+    never leaves the device until the final comparison)."""
     torch = _torch()
     rank, ws = world()
     if ws == 1:
         return
-    dev = device if device is not None and torch.distributed.get_backend() == "nccl" else "cpu"
-    lo = torch.tensor([digest], dtype=torch.int64, device=dev)
-    hi = lo.clone()
-    torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
-    torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
-    if int(lo.item()) != int(hi.item()):
+    nccl = torch.distributed.get_backend() == "nccl"
+    if torch.is_tensor(digest):
+        d = digest.reshape(1).to(torch.int64)
+        dev = d.device if nccl else "cpu"
+        d = d.to(dev)
+    else:
+        dev = device if device is not None and nccl else "cpu"
+        d = torch.tensor([int(digest)], dtype=torch.int64, device=dev)
+    # -d overflows only for INT64_MIN; the digest is masked to 63 bits first
+    d = d & 0x7FFFFFFFFFFFFFFF
+    both = torch.cat([d, -d])
+    torch.distributed.all_reduce(both, op=torch.distributed.ReduceOp.MAX)
+    hi, neg_lo = (int(x) for x in both.cpu())
+    if hi != -neg_lo:
         raise RunnerFault(f"PLR buffer replicas diverged (rank {rank})")
 
 

@@ -11,6 +11,9 @@ Keys (pinned identically in oracle/plr_np.py): it = root.fold_in(iteration); new
 lane keys it.fold_in(1) + (global lane,), replay draw it.fold_in(2), mutation keys
 it.fold_in(3) + (mutant index,).
 
+PLR-perp / ACCEL-perp (SequentialPLR): one branch per iteration
+(NEW or REPLAY, decided by the iteration key's uniform), same keys, buffer and kernels.
+
 Multi-GPU: each rank owns a contiguous slice of the global lane layout (dist.shard),
 composes only its slice (the replay draw and top-q are replicated, not exchanged),
 rolls out and scores its slice, then all-gathers the 48-byte candidate records and
@@ -48,8 +51,13 @@ class IterationResult:
 
 
 class ParallelPLR:
+    """PLR|| / ACCEL|| over n new lanes per iteration (L = 2n or 3n
+    lanes globally, sharded over the torch.distributed world).  ``check_every`` > 0 runs
+    the replica drift check (on-device buffer digest + one all-reduce, RunnerFault on a
+    mismatch) after every ``check_every``-th iteration when world > 1."""
+
     def __init__(self, n: int, params: StaticParams, cfg: PlrConfig, root_rng, accel: AccelConfig | None = None,
-                 gamma: float = 0.995, lam: float = 0.95, device=None):
+                 gamma: float = 0.995, lam: float = 0.95, device=None, check_every: int = 16):
         torch = _torch()
         self.n = n
         self.p = as_params(params).validate()
@@ -66,6 +74,8 @@ class ParallelPLR:
                                    lane_offset=self.lo)
         self.env = AutoResetWrapper(self.benv, HOME)
         self.buffer = LevelBuffer(cfg, self.device)
+        self.check_every = int(check_every)
+        self.iterations = 0
 
     # -- lane composition ---------------------------------------------------------------
     def compose(self, it: int):
@@ -113,4 +123,103 @@ class ParallelPLR:
                            self.cfg.score_fn, self.cfg.maxmc_discounted)
         g_levels, g_scores, g_max = dist.gather_candidates(levels, o["scores"], o["max_returns"])
         self.buffer.update(g_levels, g_scores, g_max, it)
+        self.iterations += 1
+        if self.world > 1 and self.check_every > 0 and self.iterations % self.check_every == 0:
+            self.check_replicas()
         return IterationResult(levels, o["scores"], o["max_returns"], n_replay, traj, o["advantages"])
+
+    def check_replicas(self) -> None:
+        """Drift check now: every rank's buffer digest must agree (RunnerFault if not)."""
+        dist.check_replicas(self.buffer.digest())
+
+
+@dataclass
+class PerpResult:
+    branch: str            # "new" | "replay"
+    levels: object         # [n, 8] levels rolled out (fresh or drawn)
+    scores: object
+    max_returns: object
+    slots: object          # drawn slots (replay) or None
+    trajectory: object
+    advantages: object
+    mutants: object = None             # ACCEL-perp: [q, 8] mutant levels (replay branch)
+    mutant_scores: object = None
+    mutant_max_returns: object = None
+
+
+class SequentialPLR:
+    """PLR-perp / ACCEL-perp (`plr_iteration`): one branch per iteration.
+
+    * decision (buffer_sample_decision, key it.fold_in(0)): replay w.p. p iff non-empty;
+    * NEW: n fresh DR levels (keys it.fold_in(1) + (lane,)), HOME rollout, score from max
+      return 0, buffer_update with the n candidates;
+    * REPLAY: n rank-prioritised draws (key it.fold_in(2)), rollout from the entries' max
+      returns, the drawn entries re-scored in place (buffer_update with the drawn levels);
+      with ACCEL, the q drawn entries with the highest buffer score at sampling time are
+      mutated (mutant j from parent j, keys it.fold_in(3) + (j,)), rolled out (HOME, reset
+      key it.fold_in(5)) and scored from 0, then one buffer_update with the q mutants.
+
+    The caller (the policy side) supplies actions / values for the n main lanes and,
+    optionally, for the q mutant lanes (default: the first q columns of the main
+    streams).  Same keys, buffer and kernels as ParallelPLR; the oracle is
+    oracle/plr_np.plr_perp_iteration."""
+
+    def __init__(self, n: int, params: StaticParams, cfg: PlrConfig, root_rng, accel: AccelConfig | None = None,
+                 gamma: float = 0.995, lam: float = 0.95, device=None):
+        torch = _torch()
+        self.n = n
+        self.p = as_params(params).validate()
+        self.cfg = cfg.validate()
+        self.accel = accel
+        self.root = as_stream(root_rng)
+        self.gamma, self.lam = gamma, lam
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.env = AutoResetWrapper(VectorBatchEnv(MazeEnv(), BatchShape(1, 1, n), device=self.device), HOME)
+        self.menv = None
+        if accel is not None:
+            self.menv = AutoResetWrapper(VectorBatchEnv(MazeEnv(), BatchShape(1, 1, accel.subsample_size),
+                                                        device=self.device), HOME)
+        self.buffer = LevelBuffer(cfg, self.device)
+
+    def decide(self, it: int) -> bool:
+        """True = replay this iteration (host: one uniform of the iteration's key)."""
+        return self.buffer.decision(self.root.fold_in(it).fold_in(0))
+
+    def _roll_score(self, env, key, levels, prior, actions, values, last, out=None):
+        start = env.reset_to_levels(key, levels, self.p)
+        traj, _ = rollout_actions(env, start, actions, self.p, out=out)
+        o = gae_and_scores(traj.rewards, values, traj.dones, last, self.gamma, self.lam, prior,
+                           self.cfg.score_fn, self.cfg.maxmc_discounted)
+        return traj, o
+
+    def iteration(self, it: int, actions, values, last_values, mutant_inputs=None, out=None) -> PerpResult:
+        """actions uint8 [T, n], values f64 [T, n], last_values f64 [n]; ``mutant_inputs``
+        = (actions [T, q], values [T, q], last [q]) for the ACCEL mutant rollout."""
+        torch = _torch()
+        itr = self.root.fold_in(it)
+        n, dev = self.n, self.device
+        if not self.decide(it):
+            ids = torch.arange(0, n, device=dev, dtype=torch.int32)
+            levels = sample_levels(itr.fold_in(1), n, self.p, lane_ids=ids, device=dev)
+            traj, o = self._roll_score(self.env, itr.fold_in(4), levels, torch.zeros(n, dtype=torch.float64, device=dev),
+                                       actions, values, last_values, out)
+            self.buffer.update(levels, o["scores"], o["max_returns"], it)
+            return PerpResult("new", levels, o["scores"], o["max_returns"], None, traj, o["advantages"])
+        rep = self.buffer.sample(itr.fold_in(2), n, it)
+        traj, o = self._roll_score(self.env, itr.fold_in(4), rep["levels"], rep["max_returns"], actions, values,
+                                   last_values, out)
+        self.buffer.update(rep["levels"], o["scores"], o["max_returns"], it)
+        res = PerpResult("replay", rep["levels"], o["scores"], o["max_returns"], rep["slots"], traj, o["advantages"])
+        if self.accel is not None:
+            q = self.accel.subsample_size
+            top = top_q(rep["scores"], q)  # buffer scores at sampling time
+            muts = mutate_levels(itr.fold_in(3), rep["levels"], self.accel.n_mutations, self.p, lane0=0,
+                                 parent_idx=top)
+            if mutant_inputs is None:
+                mutant_inputs = (actions[:, :q], values[:, :q], last_values[:q])
+            ma, mv, ml = (x.contiguous() for x in mutant_inputs)
+            _, mo = self._roll_score(self.menv, itr.fold_in(5), muts, torch.zeros(q, dtype=torch.float64, device=dev),
+                                     ma, mv, ml)
+            self.buffer.update(muts, mo["scores"], mo["max_returns"], it)
+            res.mutants, res.mutant_scores, res.mutant_max_returns = muts, mo["scores"], mo["max_returns"]
+        return res

@@ -145,7 +145,7 @@ def rollout(rng, actor, env, start, length: int, params, hidden=None, greedy: bo
         values[t].copy_(val)
         hidden = hidden * (~dones[t]).to(hidden.dtype).unsqueeze(-1)
         state, extras = res.state, res.extras
-    traj = TrajectoryBatch({"view": view[:length], "dir": dirs[:length]}, actions, rewards, dones, values, log_probs,
+    traj = TrajectoryBatch({"view": view[:length], "dir": dirs[:length]}, actions, log_probs, values, rewards, dones,
                            pre_hidden)
     return traj, RolloutCursor({"view": view[length], "dir": dirs[length]}, state, extras, hidden)
 
@@ -265,8 +265,8 @@ class GraphRollout:
         for _ in range(steps):
             self.graph.replay()
         c = (lambda x: x.clone()) if copy else (lambda x: x)
-        traj = TrajectoryBatch({"view": c(b["view"]), "dir": c(b["dir"])}, c(b["actions"]), c(b["rewards"]),
-                               c(b["dones"]), c(b["values"]), c(b["log_probs"]), c(b["pre_hidden"]))
+        traj = TrajectoryBatch({"view": c(b["view"]), "dir": c(b["dir"])}, c(b["actions"]), c(b["log_probs"]),
+                               c(b["values"]), c(b["rewards"]), c(b["dones"]), c(b["pre_hidden"]))
         ext = dict(extras)
         ext[AutoResetWrapper.EXTRAS_KEY] = {**wrap, "step": wrap["step"] + self.T}
         cur = RolloutCursor({"view": b["cur_view"].clone(), "dir": b["cur_dir"].clone()}, state, ext,

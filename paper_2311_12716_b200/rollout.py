@@ -29,15 +29,20 @@ def _torch():
 
 @dataclass
 class TrajectoryBatch:
-    """Time-major rollout storage on the GPU ([T, B, ...] over flat lanes)."""
+    """Time-major rollout storage on the GPU ([T, B, ...] over flat lanes), field for
+    field the reference's ``agents/rollout.py:19-70`` (same positional order, so code
+    that builds one positionally keeps working).  The fused action-stream rollout has no
+    policy outputs: its ``log_probs``/``values``/``pre_hidden`` are None."""
 
     obs: dict          # view uint8 [T, B, V, V], dir uint8 [T, B] (int64 from the policy rollout)
     actions: object    # uint8 [T, B] (int64 from the policy rollout)
+    log_probs: object  # float64 [T, B] or None
+    values: object     # float64 [T, B] or None
     rewards: object    # float64 [T, B]
     dones: object      # bool [T, B]
-    values: object = None
-    log_probs: object = None
     pre_hidden: object = None  # [T, B, H]: carry fed to the policy at step t
+
+    FIELDS = ("actions", "log_probs", "values", "rewards", "dones", "pre_hidden")
 
     @property
     def length(self) -> int:
@@ -46,6 +51,45 @@ class TrajectoryBatch:
     @property
     def n_lanes(self) -> int:
         return self.actions.shape[1]
+
+    def reset_masks(self):
+        """True where the recurrent carry restarts before step t (agents/rollout.py:44-48)."""
+        torch = _torch()
+        masks = torch.zeros_like(self.dones)
+        masks[1:] = self.dones[:-1]
+        return masks
+
+    def lane_slice(self, lanes) -> "TrajectoryBatch":
+        """Lanes ``lanes`` (index array / tensor / slice) of every field (agents/rollout.py:50-60)."""
+        torch = _torch()
+        if not isinstance(lanes, slice):
+            lanes = torch.as_tensor(lanes, device=self.actions.device)
+            if lanes.dtype != torch.bool:
+                lanes = lanes.to(torch.int64)
+
+        def pick(v):
+            return None if v is None else v[:, lanes]
+
+        return TrajectoryBatch({k: v[:, lanes] for k, v in self.obs.items()},
+                               *(pick(getattr(self, f)) for f in self.FIELDS))
+
+    @staticmethod
+    def concat_lanes(parts: list) -> "TrajectoryBatch":
+        """Concatenate along the lane axis (agents/rollout.py:62-70); a field that is None
+        in every part stays None."""
+        torch = _torch()
+        keys = parts[0].obs.keys()
+
+        def cat(f):
+            vs = [getattr(p, f) for p in parts]
+            if all(v is None for v in vs):
+                return None
+            if any(v is None for v in vs):
+                raise ShapeError(f"field {f!r} is missing in some of the concatenated trajectories")
+            return torch.cat(vs, dim=1)
+
+        return TrajectoryBatch({k: torch.cat([p.obs[k] for p in parts], dim=1) for k in keys},
+                               *(cat(f) for f in TrajectoryBatch.FIELDS))
 
 
 @dataclass
@@ -102,7 +146,7 @@ def rollout_actions(env: AutoResetWrapper, start, actions, params, out: dict | N
     _lib.call("amz_env_rollout", state.handle, T, _lib.ptr(a), mode, ctypes.byref(seed) if seed else None,
               ctypes.c_uint32(int(wrap["step"])), _lib.ptr(view), _lib.ptr(dirs), _lib.ptr(rew), _lib.ptr(done),
               _lib.ptr(fview), _lib.ptr(fdir), state.stream())
-    traj = TrajectoryBatch({"view": view, "dir": dirs}, a, rew, done)
+    traj = TrajectoryBatch({"view": view, "dir": dirs}, a, None, None, rew, done)
     ext = dict(extras)
     ext[AutoResetWrapper.EXTRAS_KEY] = {**wrap, "step": wrap["step"] + T}
     return traj, RolloutCursor({"view": fview, "dir": fdir}, state, ext)

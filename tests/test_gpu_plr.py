@@ -200,3 +200,32 @@ def test_string_device_arguments():
     buf.update(lv, torch.rand(64, dtype=torch.float64), torch.zeros(64, dtype=torch.float64), 1)
     out = buf.sample(amz.RngStream(5, (0,)), 8, 2)
     assert out["slots"].shape == (8,) and int(out["slots"].max()) < 16
+
+
+@pytest.mark.parametrize("K,n,digits", [(64, 200, 1), (500, 1500, 2), (4000, 4096, 3), (4000, 6000, 1), (1000, 3000, 16)])
+def test_update_insert_runs_match_oracle(K, n, digits):
+    """Mostly-new candidates (the parallel insert-run path): fills, evictions, evictions of
+    entries inserted earlier in the same batch, rounded scores so candidates often tie the
+    running minimum (the run stops and the tie goes through the sequential rule), a few
+    twins and replays mixed in, and replay marks (last_sampled = iter) between updates."""
+    rng = np.random.default_rng(K + n + digits)
+    pool = _pool(3 * n + 64, seed=digits)
+    gpu = LevelBuffer(PlrConfig(buffer_size=K))
+    ref = plr_np.LevelBuffer(K)
+    nxt = 0
+    for it in range(5):
+        idx = np.arange(nxt, nxt + n) % len(pool)
+        nxt += n
+        dup = rng.uniform(size=n) < 0.03  # a few twins / buffered levels
+        idx[dup] = rng.integers(0, len(pool), int(dup.sum()))
+        sc = np.round(rng.uniform(0, 1, n), digits)
+        sc[rng.uniform(size=n) < 0.1] = 0.0
+        mx = rng.uniform(0, 1, n)
+        gpu.update(records_to_tensor(pool[idx]), torch.from_numpy(sc), torch.from_numpy(mx), it)
+        ref.update(pool[idx], sc, mx, it)
+        _assert_same(gpu, ref)
+        if ref.size:
+            out = gpu.sample(amz.RngStream(3, (it,)), 64, it)
+            want = ref.sample(3, (it,), 64, plr_np.PlrConfig(buffer_size=K), it)
+            assert np.array_equal(out["slots"].cpu().numpy(), want)
+            _assert_same(gpu, ref)
