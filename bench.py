@@ -365,13 +365,36 @@ class Workload:
         return o
 
 
+def _graph(dev, B, T, seed, lane_offset, vdt, host_io, torch):
+    """The public API's captured DR iteration (paper_2311_12716_b200.graph)."""
+    import paper_2311_12716_b200 as amz
+    from paper_2311_12716_b200.graph import DRIterationGraph
+
+    benv = amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B), device=dev, lane_offset=lane_offset)
+    gr = DRIterationGraph(benv, amz.RngStream.from_seed(seed), T, amz.StaticParams(), GAMMA, LAMBDA,
+                          value_dtype=vdt, host_io=host_io, overlap=True)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + lane_offset)
+    acts = torch.randint(0, 3, (T, B), generator=g, device=dev, dtype=torch.uint8)
+    vals = torch.rand((T, B), generator=g, device=dev, dtype=torch.float64).to(vdt)
+    last = torch.rand((B,), generator=g, device=dev, dtype=torch.float64).to(vdt)
+    if host_io:
+        gr.host_inputs["actions"].copy_(acts.cpu())
+        gr.host_inputs["values"].copy_(vals.cpu())
+        gr.host_inputs["last"].copy_(last.cpu())
+    else:
+        gr.inputs[0]["actions"].copy_(acts)
+        gr.inputs[0]["values"].copy_(vals)
+        gr.inputs[0]["last"].copy_(last)
+    return gr.capture()
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     B, T = args.lanes, args.T
-    wl = Workload(B, T, args.seed, rank * B, dev)
     # 256 MB (> 126 MB L2) written as int64 words: the 8-byte fill runs near HBM write speed
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.int64, device=dev)
 
@@ -379,132 +402,96 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
 
-    for i in range(args.warmup):
-        wl.step(i)
-    torch.cuda.synchronize()
-    barrier()
+    def max_ranks(*vals):
+        t = torch.tensor(list(vals), dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return [float(x) for x in t.tolist()]
+
     clocks = ClockSampler(dev)
     clocks.start()
-    clocks.active = True
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+
+    # ---- headline: one CUDA-graph replay per step (DR reset -> rollout -> GAE/MaxMC),
+    # inputs resident in HBM, L2 flushed before every step, events around each replay ----
+    gr = _graph(dev, B, T, args.seed, rank * B, torch.float64, False, torch)
+    for i in range(args.warmup):
+        gr.step()
     torch.cuda.synchronize()
     barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks.active = True
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         ev[i][0].record()
-        wl.step(args.warmup + i, timing=kev[i])
+        gr.step()
         ev[i][1].record()
     torch.cuda.synchronize()
-    barrier()
     clocks.active = False
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    roll_ms = [k[0].elapsed_time(k[1]) for k in kev]
-    gae_ms = [k[1].elapsed_time(k[2]) for k in kev]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    total_ms = float(t.item())
-
-    # ---- e2e through the public API: pinned host inputs in, scores out ----
-    from paper_2311_12716_b200 import pinned_empty as amz_pinned_empty
-    h_act = amz_pinned_empty((T, B), torch.uint8)
-    h_act.copy_(wl.actions.cpu())
-    h_val = amz_pinned_empty((T, B), torch.float64)
-    h_val.copy_(wl.values.cpu())
-    h_last = amz_pinned_empty((B,), torch.float64)
-    h_last.copy_(wl.last.cpu())
-    h_res = amz_pinned_empty((2, B), torch.float64)
-    d_act = torch.empty_like(wl.actions)
-    d_val = torch.empty_like(wl.values)
-    d_last = torch.empty_like(wl.last)
-    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    torch.cuda.synchronize()
     barrier()
+    (total_ms,) = max_ranks(sum(a.elapsed_time(b) for a, b in ev))
+    del gr
+
+    # ---- the same step through the eager per-call API, kernel by kernel: the GPU is
+    # held by a spin before each step so the host has enqueued the whole step before it
+    # starts (kernel times without host gaps) ----
+    wl = Workload(B, T, args.seed, rank * B, dev)
+    for i in range(args.warmup):
+        wl.step(i)
+    torch.cuda.synchronize()
+    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    host0 = time.perf_counter()
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
-        e2e_ev[i][0].record()
-        d_act.copy_(h_act, non_blocking=True)
-        d_val.copy_(h_val, non_blocking=True)
-        d_last.copy_(h_last, non_blocking=True)
-        wl.step(10_000 + i, actions=d_act, values=d_val, last=d_last)
-        h_res.copy_(wl.res, non_blocking=True)  # scores | max returns
-        e2e_ev[i][1].record()
+        torch.cuda._sleep(400_000)  # ~0.2 ms of GPU spin: the host runs ahead
+        eev[i][0].record()
+        wl.step(args.warmup + i, timing=kev[i])
+        eev[i][1].record()
+    eager_host_ms = (time.perf_counter() - host0) * 1e3 / args.steps
     torch.cuda.synchronize()
-    seq_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    eager_ms = statistics.mean(a.elapsed_time(b) for a, b in eev)
+    roll_ms = [k[0].elapsed_time(k[1]) for k in kev]
+    gae_ms = [k[1].elapsed_time(k[2]) for k in kev]
+    # eager back to back (no spin): what a plain Python loop over the per-call API gets
+    torch.cuda.synchronize()
+    b2b0, b2b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b2b0.record()
+    for i in range(args.steps):
+        wl.step(1000 + i)
+    b2b1.record()
+    torch.cuda.synchronize()
+    eager_b2b_ms = b2b0.elapsed_time(b2b1) / args.steps
+    del wl
 
-    # pipelined: step i+1's host->device copies run on a copy stream (double-buffered
-    # device inputs) while step i computes; one timed region around all K steps, every
-    # step's copies, L2 flush, step and result read inside it
-    # two copy streams: the box's H2D path reaches ~45 GB/s only with two DMA engines busy
-    css = [torch.cuda.Stream(device=dev) for _ in range(2)]
-    main = torch.cuda.current_stream(dev)
-
-    def pipelined(vdt, step0):
-        """One timed region over K pipelined steps; values (and last values) staged as vdt."""
-        # one pinned staging buffer per step's inputs (values | last values | actions), two
-        # copies per step (one per copy stream) instead of one per tensor
-        es = torch.empty((), dtype=vdt).element_size()
-        nv, nl, na = T * B * es, B * es, T * B
-        h_in = amz_pinned_empty(nv + nl + na, torch.uint8)
-        h_in[:nv].view(vdt).copy_(wl.values.to(vdt).cpu().reshape(-1))
-        h_in[nv:nv + nl].view(vdt).copy_(wl.last.to(vdt).cpu())
-        h_in[nv + nl:].copy_(h_act.reshape(-1))
-        d_in = [torch.empty_like(h_in, device=dev) for _ in range(2)]
-        bufs = [(d[nv + nl:].view(T, B), d[:nv].view(vdt).view(T, B), d[nv:nv + nl].view(vdt)) for d in d_in]
-        outs = [amz_pinned_empty((2, B), torch.float64) for _ in range(2)]
-        copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
-        freed = [torch.cuda.Event() for _ in range(2)]
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        half = (h_in.numel() // 2) & ~15
-
-        def h2d(k):
-            for c, cs in enumerate(css):
-                cs.wait_event(freed[k])
-                with torch.cuda.stream(cs):
-                    if c == 0:
-                        d_in[k][:half].copy_(h_in[:half], non_blocking=True)
-                    else:
-                        d_in[k][half:].copy_(h_in[half:], non_blocking=True)
-                    copied[k][c].record(cs)
-
+    # ---- e2e through the public API: pinned host inputs in, scores | max returns out,
+    # one graph replay per step, the next step's H2D overlapped with this step's kernels;
+    # one timed region over all K steps including every copy, L2 flush and result read ----
+    def e2e(vdt):
+        g2 = _graph(dev, B, T, args.seed, rank * B, vdt, True, torch)
+        for _ in range(args.warmup):
+            g2.step()
         torch.cuda.synchronize()
         barrier()
-        for k in range(2):
-            freed[k].record(main)
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks.active = True
-        p0.record(main)
-        host0 = time.perf_counter()
-        for cs in css:
-            cs.wait_event(p0)
-        h2d(0)
+        p0.record()
+        h0 = time.perf_counter()
         for i in range(args.steps):
-            k = i & 1
-            if i + 1 < args.steps:
-                h2d(k ^ 1)
-            main.wait_event(copied[k][0])
-            main.wait_event(copied[k][1])
             flush.fill_(i & 0xFF)
-            a, v, l_ = bufs[k]
-            wl.step(step0 + i, actions=a, values=v, last=l_)
-            outs[k].copy_(wl.res, non_blocking=True)  # scores | max returns
-            freed[k].record(main)
-        p1.record(main)
-        host_ms = (time.perf_counter() - host0) * 1e3 / args.steps
+            g2.step()
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
+        p1.record()
         torch.cuda.synchronize()
         clocks.active = False
-        return p0.elapsed_time(p1), host_ms, nv + nl + na
+        es = torch.empty((), dtype=vdt).element_size()
+        h2d = T * B * (1 + es) + B * es
+        ms = p0.elapsed_time(p1)
+        del g2
+        return ms, host_ms, h2d
 
-    e2e_ms, host_ms, _ = pipelined(torch.float64, 20_000)
-    # the same pipeline with the values as the policy's float32 (the reference's actor
-    # returns value.double() of a float32 output, agents/ppo.py:96); the kernel widens
-    # them, so a float32-valued stream scores identically with half the value bytes
-    e32_ms, _, h2d32 = pipelined(torch.float32, 30_000)
-    te = torch.tensor([e2e_ms, seq_ms, e32_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_ms, seq_ms, e32_ms = float(te[0].item()), float(te[1].item()), float(te[2].item())
+    e32_ms, host32_ms, h2d32 = e2e(torch.float32)
+    e64_ms, host64_ms, h2d64 = e2e(torch.float64)
+    e32_ms, e64_ms = max_ranks(e32_ms, e64_ms)
     peaks, src = _peaks()
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     extra = {}
@@ -552,18 +539,23 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "u8/int32 env, f64 GAE",
         "data": "synthetic: DR levels from (seed, lane) keys, uniform random actions and values resident in HBM",
         "config": workload_config(args, world),
-        "e2e": {"value": units / (e2e_ms * 1e-3 / args.steps), "unit": "env-steps/s",
-                "h2d_bytes_per_step": T * B * (1 + 8) + B * 8, "d2h_bytes_per_step": 2 * B * 8,
-                "ms_per_step": e2e_ms / args.steps, "host_enqueue_ms_per_step": host_ms,
-                "mode": "pipelined: step i+1's pinned H2D copies (two copy streams, double-buffered) overlap step i; "
-                        "one timed region over all K steps including every copy, the L2 flush and the result read",
-                "sequential": {"value": units / (seq_ms * 1e-3 / args.steps), "ms_per_step": seq_ms / args.steps,
-                               "mode": "copies, step and read back to back per step (flush outside the timing)"},
-                "values_f32": {"value": units / (e32_ms * 1e-3 / args.steps), "ms_per_step": e32_ms / args.steps,
-                               "h2d_bytes_per_step": h2d32,
-                               "mode": "pipelined as above with values / last values staged as float32 (the "
-                                       "policy's output dtype; gae_and_scores widens them in-kernel)"}},
-        "gpu_launches": wl.launches_per_step * args.steps,
+        "mode": "one CUDA-graph replay per step (paper_2311_12716_b200.graph.DRIterationGraph: k_env_reset_dr -> "
+                "k_dyn -> k_render -> k_gae_score -> k_iter_advance), device-timed with CUDA events per step",
+        "eager": {"value": units / (eager_b2b_ms * 1e-3), "ms_per_step": eager_b2b_ms,
+                  "kernel_ms_per_step": eager_ms, "host_enqueue_ms_per_step": eager_host_ms,
+                  "mode": "per-call API (VectorBatchEnv/AutoResetWrapper.reset, rollout_actions, gae_and_scores) back "
+                          "to back; kernel_ms_per_step with the host run ahead (GPU spin before each step)"},
+        "e2e": {"value": units / (e32_ms * 1e-3 / args.steps), "unit": "env-steps/s",
+                "h2d_bytes_per_step": h2d32, "d2h_bytes_per_step": 2 * B * 8,
+                "ms_per_step": e32_ms / args.steps, "host_enqueue_ms_per_step": host32_ms,
+                "inputs": "actions u8 [T, B] + values f32 [T, B] + last values f32 [B] (the policy's output dtype, "
+                          "widened to f64 in-kernel like the reference's value.double(), agents/ppo.py:96)",
+                "mode": "DRIterationGraph(host_io=True): one graph replay per step; its H2D of the NEXT step's pinned "
+                        "inputs runs on a side branch concurrent with this step's kernels, the D2H of scores | max "
+                        "returns ends the replay; one timed region over all K steps incl. the L2 flushes",
+                "values_f64": {"value": units / (e64_ms * 1e-3 / args.steps), "ms_per_step": e64_ms / args.steps,
+                               "h2d_bytes_per_step": h2d64, "host_enqueue_ms_per_step": host64_ms}},
+        "gpu_launches": 5 * args.steps,
         "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
                      "frac": roll_gbs / peak,
                      "traffic": _traffic().get("k_env_rollout", {}).get("dram_bytes"),
@@ -572,8 +564,8 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_bytes": f"{ENV_BYTES_PER_STEP} B/env-step x {B * T} env-steps per launch",
                      "kernel_ms": roll,
                      "note": "k_env_rollout = k_dyn + k_render (the timeout levels of the first auto-resets "
-                             "come prepared from the fused reset launch, so no k_spec_levels); at 4096 lanes the per-lane "
-                             "256-step dynamics chain (latency) bounds it, not HBM; the HBM point is "
+                             "come prepared from the fused reset launch, so no k_spec_levels); at 4096 lanes the "
+                             "per-lane 256-step dynamics chain (latency) bounds it, not HBM; the HBM point is "
                              "large_batch (65536 lanes)"},
         "kernels": {"k_env_rollout_ms": roll, "k_gae_score_ms": gae, "k_gae_score_GBs": gae_gbs,
                     "k_gae_score_frac": gae_gbs / peak,
@@ -724,6 +716,7 @@ def measure_large_batch(dev, B, T, iters, flush, peak):
     kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(iters)]
     for i in range(iters):
         flush.fill_(i & 0xFF)
+        torch.cuda._sleep(400_000)  # the host runs ahead: kernel times without host gaps
         wl.step(10 + i, timing=kev[i])
     torch.cuda.synchronize()
     roll = statistics.mean(k[0].elapsed_time(k[1]) for k in kev)

@@ -214,6 +214,21 @@ int amz_env_rollout(amz_env_t *env, int T, const uint8_t *actions_dev, int mode,
                     uint8_t *done_dev, uint8_t *final_view_dev, uint8_t *final_dir_dev, void *stream);
 
 /* Render the current observation of every lane (observe_batch, amaze/env.py:352-364). */
+/* CUDA-graph replay of the DR iteration (reset -> rollout): the key streams come from a
+ * device iteration counter iter_dev (u32) instead of host-computed prefixes, so one
+ * captured graph serves every iteration.  root = the run's root stream prefix;
+ * iteration it = *iter_dev uses lane levels root.fold_in(it).fold_in(0) + (lane,) and
+ * auto-reset keys root.fold_in(it).fold_in(1) + (step, lane) -- the same streams as
+ * amz_env_reset_dr / amz_env_rollout called with the prefixes of
+ * AutoResetWrapper.reset(root.fold_in(it)) (env/wrappers.py:43-56).  The rollout starts
+ * at step 0 in RESAMPLE mode.  amz_iter_advance adds `by` to the counter on the stream. */
+int amz_env_reset_dr_iter(amz_env_t *env, const amz_seed_t *root, const uint32_t *iter_dev, uint8_t *view_dev,
+                          int64_t *dir_dev, void *stream);
+int amz_env_rollout_iter(amz_env_t *env, int T, const uint8_t *actions_dev, const amz_seed_t *root,
+                         const uint32_t *iter_dev, uint8_t *view_dev, uint8_t *dir_dev, double *reward_dev,
+                         uint8_t *done_dev, uint8_t *final_view_dev, uint8_t *final_dir_dev, void *stream);
+int amz_iter_advance(uint32_t *iter_dev, uint32_t by, void *stream);
+
 int amz_env_observe(amz_env_t *env, uint8_t *view_dev, int64_t *dir_dev, void *stream);
 
 /* lane_levels (env/batch.py:104-105): each lane's level (its reset-time pose). */

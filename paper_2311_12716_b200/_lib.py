@@ -65,6 +65,9 @@ _SIGS = {
     "amz_env_reset_to_levels": ([P, P, P, I64, P, P, VP], I32),
     "amz_env_step": ([P, P, I32, I32, ctypes.POINTER(AmzSeed), U32, P, P, P, P, P, P, VP], I32),
     "amz_env_rollout": ([P, I32, P, I32, ctypes.POINTER(AmzSeed), U32, P, P, P, P, P, P, VP], I32),
+    "amz_env_reset_dr_iter": ([P, ctypes.POINTER(AmzSeed), P, P, P, VP], I32),
+    "amz_env_rollout_iter": ([P, I32, P, ctypes.POINTER(AmzSeed), P, P, P, P, P, P, P, VP], I32),
+    "amz_iter_advance": ([P, U32, VP], I32),
     "amz_env_observe": ([P, P, P, VP], I32),
     "amz_env_levels": ([P, P, VP], I32),
     "amz_env_state": ([P, P, VP], I32),

@@ -71,6 +71,7 @@ struct amz_env {
     // wrapper key starting at step 0 (consumed by that rollout, dropped by anything else)
     bool spec_ready = false;
     amz_seed_t spec_wrap{};
+    const uint32_t *spec_iter = nullptr;  // the iteration counter the prepared levels are keyed by
 };
 
 struct amz_plr {
@@ -395,8 +396,31 @@ int amz_env_reset_dr(amz_env_t *e, const amz_seed_t *prefix, const amz_seed_t *w
     if (rc) return fail(rc, "reset: unsupported agent_view_size");
     cudaMemsetAsync(e->term, 0, 2 * sizeof(int), s);
     e->spec_ready = wrap != nullptr;
+    e->spec_iter = nullptr;
     if (wrap) e->spec_wrap = *wrap;
     return cuda_status("env_reset_dr");
+}
+
+int amz_env_reset_dr_iter(amz_env_t *e, const amz_seed_t *root, const uint32_t *iter_dev, uint8_t *view,
+                          int64_t *dirs, void *stream) {
+    if (!e || !root || !iter_dev) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(e->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    EnvDev E = e->E;
+    E.iter = iter_dev;
+    int rc = launch_env_reset_dr(e->G, E, *root, root, e->spec, e->spec_step, view, dirs, s);
+    if (rc) return fail(rc, "reset: unsupported agent_view_size");
+    cudaMemsetAsync(e->term, 0, 2 * sizeof(int), s);
+    e->spec_ready = true;
+    e->spec_iter = iter_dev;
+    e->spec_wrap = *root;
+    return cuda_status("env_reset_dr_iter");
+}
+
+int amz_iter_advance(uint32_t *iter_dev, uint32_t by, void *stream) {
+    if (!iter_dev) return fail(AMZ_ECONFIG, "null argument");
+    launch_iter_advance(iter_dev, by, (cudaStream_t)stream);
+    return cuda_status("iter_advance");
 }
 
 int amz_env_reset_to_levels(amz_env_t *e, const amz_level_t *lv, const int64_t *lanes, int64_t n, uint8_t *view,
@@ -455,9 +479,27 @@ int amz_env_step_dev(amz_env_t *e, const void *actions, int adtype, int mode, co
                          times, stream);
 }
 
+static int env_rollout_impl(amz_env_t *e, int T, const uint8_t *actions, int mode, const amz_seed_t *wrap,
+                            uint32_t step0, const uint32_t *iter_dev, uint8_t *view, uint8_t *dirs, double *reward,
+                            uint8_t *done, uint8_t *fview, uint8_t *fdir, void *stream);
+
 int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const amz_seed_t *wrap, uint32_t step0,
                     uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done, uint8_t *fview, uint8_t *fdir,
                     void *stream) {
+    return env_rollout_impl(e, T, actions, mode, wrap, step0, nullptr, view, dirs, reward, done, fview, fdir, stream);
+}
+
+int amz_env_rollout_iter(amz_env_t *e, int T, const uint8_t *actions, const amz_seed_t *root,
+                         const uint32_t *iter_dev, uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done,
+                         uint8_t *fview, uint8_t *fdir, void *stream) {
+    if (!iter_dev || !root) return fail(AMZ_ECONFIG, "null argument");
+    return env_rollout_impl(e, T, actions, AMZ_RESET_RESAMPLE, root, 0u, iter_dev, view, dirs, reward, done, fview,
+                            fdir, stream);
+}
+
+static int env_rollout_impl(amz_env_t *e, int T, const uint8_t *actions, int mode, const amz_seed_t *wrap,
+                            uint32_t step0, const uint32_t *iter_dev, uint8_t *view, uint8_t *dirs, double *reward,
+                            uint8_t *done, uint8_t *fview, uint8_t *fdir, void *stream) {
     if (!e || !actions || !view || !dirs || !reward || !done) return fail(AMZ_ECONFIG, "null argument");
     DevGuard guard_(e->device);
     if (T < 1) return fail(AMZ_ECONTRACT, "rollout length must be >= 1, got %d", T);
@@ -480,10 +522,12 @@ int amz_env_rollout(amz_env_t *e, int T, const uint8_t *actions, int mode, const
         }
         e->rollout_T = T;
     }
-    const bool ready = e->spec_ready && mode == AMZ_RESET_RESAMPLE && step0 == 0 &&
+    const bool ready = e->spec_ready && mode == AMZ_RESET_RESAMPLE && step0 == 0 && e->spec_iter == iter_dev &&
                        memcmp(&e->spec_wrap, &w, sizeof(w)) == 0;
     e->spec_ready = false;
-    int rc = launch_env_rollout(e->G, e->E, T, actions, mode, w, step0, view, dirs, reward, done, fview, fdir,
+    EnvDev E = e->E;
+    E.iter = iter_dev;
+    int rc = launch_env_rollout(e->G, E, T, actions, mode, w, step0, view, dirs, reward, done, fview, fdir,
                                 e->poses, e->epochs, e->final_pose, e->spec, e->spec_step, ready ? 1 : 0, s);
     if (rc) return fail(rc, "rollout: unsupported agent_view_size");
     return cuda_status("env_rollout");

@@ -139,6 +139,13 @@ __global__ void __launch_bounds__(128) k_env_reset_dr(Geo G, EnvDev E, amz_seed_
     const int64_t l = (int64_t)blockIdx.x * 4 + warp;
     if (l >= E.B) return;
     const uint32_t gl = E.lane_offset + (uint32_t)l;
+    if (E.iter) {  // graph replay: this iteration's streams from the root key
+        const uint32_t it = *E.iter;
+        seed_absorb(prefix, it);
+        seed_absorb(prefix, 0u);
+        seed_absorb(wrap, it);
+        seed_absorb(wrap, 1u);
+    }
     uint64_t k0, k1;
     {
         amz_seed_t sd = prefix;
@@ -390,6 +397,13 @@ int launch_env_reset(const Geo &G, const EnvDev &E, const amz_level_t *lv, const
                      uint8_t *view, int64_t *dirs, cudaStream_t s) {
     if (n <= 0) return 0;
     AMZ_DISPATCH_V(G.V, (k_env_reset<VT><<<blocks_for(n, 128), 128, 0, s>>>(G, E, lv, lanes, n, view, dirs)));
+    return 0;
+}
+
+__global__ void k_iter_advance(uint32_t *iter, uint32_t by) { *iter += by; }
+
+int launch_iter_advance(uint32_t *iter, uint32_t by, cudaStream_t s) {
+    k_iter_advance<<<1, 1, 0, s>>>(iter, by);
     return 0;
 }
 

@@ -45,6 +45,10 @@ struct EnvDev {
     uint4 *mask;
     uint32_t *board;  // [16][B]
     int *err;
+    // device iteration counter (CUDA-graph replay): when set, the reset / rollout key
+    // prefixes passed in are the ROOT stream's, and the kernels derive the iteration's
+    // streams root.fold_in(*iter).fold_in(0) (lane levels) and .fold_in(1) (auto-reset)
+    const uint32_t *iter = nullptr;
 };
 
 // numpy pairwise summation schedule (numpy/_core/src/umath/loops_utils.h.src
@@ -70,6 +74,7 @@ int launch_teacher_levels(int64_t B, const uint4 *mask, const uint4 *st, amz_lev
 int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
                        const amz_seed_t *prefix_dev, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
                        uint8_t *act8, double *logp, cudaStream_t s);
+int launch_iter_advance(uint32_t *iter, uint32_t by, cudaStream_t s);
 int launch_env_reset_dr(const Geo &G, const EnvDev &E, const amz_seed_t &prefix, const amz_seed_t *wrap,
                         amz_level_t *spec, uint32_t *spec_step, uint8_t *view, int64_t *dirs, cudaStream_t s);
 int launch_level_metrics(const Geo &G, const amz_level_t *lv, int64_t n, int32_t *n_walls, int32_t *spl,

@@ -341,24 +341,65 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 //                     tools/plr_insert_runs_proto.py is the host prototype).
 // ---------------------------------------------------------------------------------
 constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses the hash table's space)
-constexpr int kRunMax = 1024; // insert-run candidates per parallel pass (one per thread)
-constexpr int kRunMin = 32;   // shorter insert runs stay on the sequential warp path
+#ifdef AMZ_PLR_STATS
+// [0] sequential candidates (warp 0), [1] of them in place, [2] bulk runs, [3] bulk
+// candidates, [4] insert_runs calls, [5] insert passes, [6] candidates consumed by runs,
+// [7] relevant candidates, [8] calls
+__device__ unsigned long long g_plr_stats[16];
+#define PLR_STAT(k_, v_) atomicAdd(&g_plr_stats[k_], (unsigned long long)(v_))
+extern "C" int amz_debug_plr_stats(void *host, int reset) {
+    int rc = (int)cudaMemcpyFromSymbol(host, g_plr_stats, sizeof(g_plr_stats));
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_plr_stats, z, sizeof(z));
+    }
+    return rc;
+}
+#else
+#define PLR_STAT(k_, v_) \
+    do {                 \
+    } while (0)
+#endif
+constexpr int kRunMin = 96;   // shorter insert runs stay on the sequential warp path
 constexpr int kBulkRun = 64;  // shorter in-place runs stay on the sequential warp path
-constexpr int kSeqAfterFlag = 64;  // candidates kept sequential after a run stopped early on a tie
 struct CandChunk {
     double sc[kChunk];
     int32_t cid[kChunk];
     int32_t tf[kChunk];
     int32_t im[kChunk];
 };
-// insert-run scratch (aliases the chunk: the chunk is restaged after a run)
+// Insert runs (whole CTA): relevant candidates from r0 on that are certainly new (no key
+// match at kernel start, first of their key in the batch), until the first one that is
+// not.  With free slots as virtual entries of score -inf (evicted in slot order) the
+// sequential rule is a streaming top-K of the buffer under the order
+//   x < y  <=>  score_x < score_y, or equal scores and x entered first
+// (every stored entry entered before every run candidate: tb(stored) < tb(new), checked
+// by run_ok).  For the live candidates of a pass, in arrival order,
+//   accept_i <=> #{live j < i : s_j > s_i} < #{buffer x : s_x <= s_i}
+//   the p acceptances evict the p smallest of (buffer U accepted), in order; the k-th
+//   acceptance takes the slot of the k-th eviction (chained through re-evicted ones);
+//   the minimum present when candidate i arrives is merged element q_i (q_i =
+//   acceptances before i): later acceptances all exceed it.
+// The order differs from the rule only when s_i equals that minimum's score (the rule
+// rejects; the order would accept): the first such candidate f is found exactly, the
+// prefix before it is committed (a prefix of the streaming process is the same
+// process), f and every later candidate with score <= s_f are rejected (the minimum
+// never drops), and the next pass runs over the rest.  The sorted buffer is sorted once
+// per call and then kept sorted by merging each pass's commits into it.
+constexpr int kRunM = 256;  // live candidates per pass (4 threads per candidate)
 struct RunArr {
-    uint64_t rsk[kRunMax];   // run candidates' score keys, arrival order
-    uint64_t ask[kRunMax];   // accepted candidates' score keys, sorted by (score, arrival)
-    int32_t aarr[kRunMax];   // arrival index of ask[k]
-    int32_t vlist[kRunMax];  // evictions in order: >= 0 existing sorted position, < 0 -(acceptance + 1)
-    int32_t aslot[kRunMax];  // acceptance index -> slot
-    int32_t acand[kRunMax];  // acceptance index -> arrival index
+    uint64_t lk[kRunM];        // live candidates' score keys, arrival order
+    uint64_t ask[kRunM];       // this pass's acceptances sorted by (score, arrival)
+    uint64_t apk[kRunM];       // the committed acceptances, sorted
+    uint64_t mkey[kRunM + 1];  // score keys of the first p+1 elements of the merged order
+    int32_t lc[kRunM];         // live candidates' ids
+    int32_t lq[kRunM];         // acceptances before each live candidate
+    int32_t acand[kRunM];      // acceptance index -> live index
+    int32_t arank[kRunM];      // acceptance index -> position in ask
+    int32_t abelow[kRunM];     // acceptance index -> #buffer entries <= its score
+    int32_t apos2[kRunM];      // ask position -> position in apk (committed only)
+    int32_t aslot[kRunM];      // acceptance index -> slot
+    int32_t mref[kRunM + 1];   // merged order: >= 0 sorted buffer position, < 0 -(acceptance + 1)
 };
 using RunSort = cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int, 4>;
 struct SortedEntries {
@@ -383,7 +424,7 @@ struct UpdSmem {
         typename RunSort::TempStorage sort;
         SortedEntries e;
     } r1;
-    uint32_t evicted[kRunMax / 32];  // insert run: acceptances evicted again inside the run
+    uint32_t evicted[kRunM / 32];  // insert run: acceptances evicted again inside the pass
     double mlow;
     int64_t next_seq;
     int64_t lmin, qmin, lmax, qmax, last_max0;
@@ -395,10 +436,8 @@ struct UpdSmem {
     int rcur;      // next chunk position for warp 0
     int action;    // 0 = chunk done, 1 = bulk in-place run [rcur, arg), 2 = insert run [rcur, rcur + arg)
     int arg;
-    int force_seq_until;  // absolute relevant index: candidates before it take the sequential path
     int run_ok;
     int flag_first;
-    int run_p;
     int n_virtual;
 };
 static_assert(sizeof(CandChunk) <= sizeof(uint32_t) * kHash, "chunk must fit in the hash table space");
@@ -542,14 +581,14 @@ __device__ __forceinline__ int inplace_run(const UpdSmem &S, const UpdScratch &W
 // length of the run of consecutive certainly-new candidates starting at r (whole warp)
 __device__ __forceinline__ int pure_run(const UpdSmem &S, int r, int cn, int lane) {
     int L = 0;
-    while (L < kRunMax) {
+    while (L < kRunMin) {
         const int i = r + L + lane;
         const bool pr = i < cn && cand_pure(S, i);
         const unsigned fail = ~__ballot_sync(0xFFFFFFFFu, pr);
-        if (fail) return min(L + __ffs(fail) - 1, kRunMax);
+        if (fail) return L + __ffs(fail) - 1;
         L += 32;
     }
-    return kRunMax;
+    return L;
 }
 
 __device__ __forceinline__ int upper_bound_u64(const uint64_t *a, int n, uint64_t x) {  // # a[i] <= x
@@ -598,207 +637,262 @@ __device__ __forceinline__ int block_excl_count(bool flag, int &excl, int *wscan
     return tot;
 }
 
-// Insert run (whole CTA): candidates rel[r0 .. r0 + m) are certainly new.  With free slots
-// as virtual entries of score -inf (evicted in slot order) the sequential rule is a
-// streaming top-K of the buffer under x < y <=> (score_x < score_y) or (equal score and
-// x entered first); every stored entry entered before every run candidate because
-// tb(stored) < tb(new) (checked: last_sampled <= iter).
-//   accept_i <=> #{j < i : s_j > s_i} < #{x : s_x <= s_i}
-//   the p acceptances evict the p smallest of (buffer U accepted) in order; the k-th
-//   acceptance takes the slot of the k-th eviction (chains through re-evicted ones).
-// The order differs from the rule only where a candidate's score equals the score of the
-// minimum present at its arrival (the rule rejects): a candidate is flagged when the
-// smallest member of its equal-score group in the merged order is among the first p+1
-// and was present before it.  The prefix before the first flagged candidate is committed
-// (the prefix of the streaming process is the same process); returns the number of
-// candidates consumed (the flagged one goes to the sequential path).
-__device__ int insert_run(UpdSmem &S, const UpdScratch &W, const double *__restrict__ cscore, int64_t iter, int r0,
-                          int m, int E, int *wscan) {
+__device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__restrict__ cscore, int64_t iter,
+                           int r0, int rend, int E, int *wscan) {
     // E = buffer capacity K: sort items [0, E) are the buffer (stored + virtual free
     // slots), items [E, kPlrMaxK) padding that sorts last
-    const int tid = threadIdx.x;
-    const int size0 = S.size;
-    // ---- sorted buffer: tie order (stable), then score order ----
-    unsigned long long keys[4];
-    int vals[4];
+    const int tid = threadIdx.x, ci = tid >> 2, part = tid & 3;
+    RunArr &R = S.u.run;
+    // ---- the buffer sorted by (score, tie): tie order (stable), then score order ----
     {
+        const int size0 = S.size;
+        unsigned long long keys[4];
+        int vals[4];
         unsigned long long tmax = 0ull;
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const int i = tid * 4 + k;  // heap position for i < size0, free slot i otherwise
-            if (i < size0) {
-                keys[k] = S.ht[i];
-                vals[k] = S.hslot[i];
-            } else {
-                keys[k] = (unsigned long long)i;  // virtual entries: slot order (padding: any)
-                vals[k] = i;
-            }
+            keys[k] = i < size0 ? S.ht[i] : (unsigned long long)i;  // virtual: slot order
+            vals[k] = i < size0 ? S.hslot[i] : i;
             tmax = keys[k] > tmax ? keys[k] : tmax;
         }
         if (tid == 0) S.tie_max = 0ull;
         __syncthreads();
         atomicMax(&S.tie_max, tmax);
         __syncthreads();
-    }
-    const int tbits = 64 - __clzll((long long)(S.tie_max | 1ull));
-    RunSort(S.r1.sort).Sort(keys, vals, 0, tbits);
-    __syncthreads();
+        const int tbits = 64 - __clzll((long long)(S.tie_max | 1ull));
+        RunSort(S.r1.sort).Sort(keys, vals, 0, tbits);
+        __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int slot = vals[k];
-        // virtual (free) slots: score key 0 (below every real score); padding: all ones
-        keys[k] = slot < size0 ? S.hk[S.pos[slot]] : (slot < E ? 0ull : ~0ull);
-    }
-    RunSort(S.r1.sort).Sort(keys, vals);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        S.r1.e.ekey[tid * 4 + k] = keys[k];
-        S.r1.e.eslot[tid * 4 + k] = vals[k];
-    }
-    if (tid == 0) {
-        S.flag_first = m;
-        S.n_virtual = 0;
-    }
-    __syncthreads();
-    // ---- acceptance ----
-    uint64_t si = 0ull;
-    int cidx = -1;
-    if (tid < m) {
-        cidx = W.rel[r0 + tid];
-        si = score_key(cscore[cidx]);
-        S.u.run.rsk[tid] = si;
-    }
-    __syncthreads();
-    int below = 0;
-    bool acc = false;
-    if (tid < m) {
-        below = upper_bound_u64(S.r1.e.ekey, E, si);
-        int greater = 0;
-        for (int j = 0; j < tid; j++) greater += S.u.run.rsk[j] > si;
-        acc = greater < below;
-    }
-    int q = 0;
-    const int p = block_excl_count(acc, q, wscan);
-    if (acc) S.u.run.acand[q] = tid;
-    __syncthreads();
-    // rank of each acceptance in (score, arrival) order; merged position = rank + below
-    if (acc) {
-        int ra = 0;
-        for (int k = 0; k < p; k++) {
-            const int j = S.u.run.acand[k];
-            const uint64_t sj = S.u.run.rsk[j];
-            ra += sj < si || (sj == si && j < tid);
+        for (int k = 0; k < 4; k++) {
+            const int slot = vals[k];
+            keys[k] = slot < size0 ? S.hk[S.pos[slot]] : (slot < E ? 0ull : ~0ull);
         }
-        S.u.run.ask[ra] = si;
-        S.u.run.aarr[ra] = tid;
-        const int mi = ra + below;
-        if (mi < p) S.u.run.vlist[mi] = -(q + 1);
+        RunSort(S.r1.sort).Sort(keys, vals);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            S.r1.e.ekey[tid * 4 + k] = keys[k];
+            S.r1.e.eslot[tid * 4 + k] = vals[k];
+        }
     }
-    __syncthreads();
-    for (int k = tid; k < p && k < E; k += blockDim.x) {  // existing entries among the first p merged
-        const int mi = k + lower_bound_u64(S.u.run.ask, p, S.r1.e.ekey[k]);
-        if (mi < p) S.u.run.vlist[mi] = k;
-    }
-    // ---- tie flags ----
-    if (tid < m) {
-        const int ke = lower_bound_u64(S.r1.e.ekey, E, si);
-        int mi = 0x7FFFFFFF;
-        bool before = false;
-        if (ke < E && S.r1.e.ekey[ke] == si) {
-            mi = ke + lower_bound_u64(S.u.run.ask, p, si);
-            before = true;
-        } else {
-            const int ka = lower_bound_u64(S.u.run.ask, p, si);
-            if (ka < p && S.u.run.ask[ka] == si) {
-                mi = ka + ke;
-                before = S.u.run.aarr[ka] < tid;
+    const uint64_t *ekey = S.r1.e.ekey;
+    int pos = r0;
+    bool more = true;
+    while (more && pos < rend) {
+        // ---- next chunk of certainly-new candidates ----
+        if (tid == 0) S.flag_first = kRunM;
+        __syncthreads();
+        int c = -1;
+        if (tid < kRunM) {
+            const int idx = pos + tid;
+            bool ok = idx < rend;
+            if (ok) {
+                c = W.rel[idx];
+                ok = W.init_match[c] < 0 && W.twin_first[c] == c;
             }
-        }
-        if (before && mi <= p) atomicMin(&S.flag_first, tid);
-    }
-    __syncthreads();
-    const int f = S.flag_first;
-    // acceptances before the first flagged arrival
-    int pc = 0;
-    {
-        int lo = 0, hi = p;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (S.u.run.acand[mid] < f)
-                lo = mid + 1;
-            else
-                hi = mid;
-        }
-        pc = lo;
-    }
-    for (int k = tid; k < kRunMax / 32; k += blockDim.x) S.evicted[k] = 0u;
-    __syncthreads();
-    // ---- slots: the j-th acceptance takes the slot of the j-th eviction ----
-    for (int j = tid; j < pc; j += blockDim.x) {
-        const int v = S.u.run.vlist[j];
-        if (v >= 0) {
-            const int slot = S.r1.e.eslot[v];
-            S.u.run.aslot[j] = slot;
-            if (slot >= size0) atomicAdd(&S.n_virtual, 1);
-            // an entry inserted earlier in this update loses its key
-            if (slot < size0 && S.owner[slot] >= 0) W.keyslot[S.owner[slot]] = -1;
-        } else {
-            S.u.run.aslot[j] = -1;
-            const int qq = -v - 1;
-            atomicOr(&S.evicted[qq >> 5], 1u << (qq & 31));
-        }
-    }
-    __syncthreads();
-    // pointer jumping along chains of re-evicted acceptances (vlist[j] < 0 -> parent)
-    while (true) {
-        int ns = -1, nv = 0;
-        const int j = tid;
-        bool pend = false;
-        if (j < pc && S.u.run.aslot[j] < 0) {
-            const int par = -S.u.run.vlist[j] - 1;
-            const int ps = S.u.run.aslot[par];
-            pend = true;
-            if (ps >= 0)
-                ns = ps;
-            else
-                nv = S.u.run.vlist[par];
+            if (!ok) atomicMin(&S.flag_first, tid);
         }
         __syncthreads();
-        if (pend) {
-            if (ns >= 0)
-                S.u.run.aslot[j] = ns;
-            else
-                S.u.run.vlist[j] = nv;
+        int m = S.flag_first;
+        if (m < kRunM) more = false;
+        if (m == 0) break;
+        if (tid < m) {
+            R.lc[tid] = c;
+            R.lk[tid] = score_key(cscore[c]);
         }
-        if (!__syncthreads_or(pend)) break;
-    }
-    // ---- apply: final occupants only ----
-    const int64_t seq0 = S.next_seq;
-    for (int j = tid; j < pc; j += blockDim.x) {
-        const int a = S.u.run.acand[j];
-        const int c = W.rel[r0 + a];
-        if ((S.evicted[j >> 5] >> (j & 31)) & 1u) {
-            W.keyslot[c] = -1;  // inserted and evicted again inside the run
-            continue;
+        pos += m;
+        // ---- passes over the live candidates ----
+        while (m > 0) {
+            if (tid == 0) PLR_STAT(5, 1);
+            __syncthreads();
+            if (tid == 0) {
+                S.flag_first = m;
+                S.n_virtual = 0;
+            }
+            const int size_cur = S.size;
+            const int64_t seq0 = S.next_seq;
+            const bool live = ci < m;
+            const uint64_t si = live ? R.lk[ci] : 0ull;
+            int below = 0, g = 0;
+            if (live) {
+                below = upper_bound_u64(ekey, E, si);
+                for (int j = part; j < ci; j += 4) g += R.lk[j] > si;
+            }
+            g += __shfl_xor_sync(0xFFFFFFFFu, g, 1);
+            g += __shfl_xor_sync(0xFFFFFFFFu, g, 2);
+            const bool acc = live && g < below;
+            int q = 0;
+            const int p = block_excl_count(part == 0 && acc, q, wscan);
+            q = __shfl_sync(0xFFFFFFFFu, q, (threadIdx.x & 31) & ~3);  // the group's part-0 count
+            if (part == 0 && live) R.lq[ci] = q;
+            if (part == 0 && acc) {
+                R.acand[q] = ci;
+                R.abelow[q] = below;
+            }
+            __syncthreads();
+            // rank among this pass's acceptances (score, then arrival)
+            int rk = 0;
+            if (acc)
+                for (int k = part; k < p; k += 4) {
+                    const int j = R.acand[k];
+                    const uint64_t sj = R.lk[j];
+                    rk += sj < si || (sj == si && j < ci);
+                }
+            rk += __shfl_xor_sync(0xFFFFFFFFu, rk, 1);
+            rk += __shfl_xor_sync(0xFFFFFFFFu, rk, 2);
+            if (part == 0 && acc) {
+                R.ask[rk] = si;
+                R.arank[q] = rk;
+            }
+            __syncthreads();
+            // the first p+1 elements of the merged order (buffer before acceptance at equal score)
+            for (int k = tid; k <= p && k < E; k += blockDim.x) {
+                const int mi = k + lower_bound_u64(R.ask, p, ekey[k]);
+                if (mi <= p) {
+                    R.mkey[mi] = ekey[k];
+                    R.mref[mi] = k;
+                }
+            }
+            if (part == 0 && acc) {
+                const int mi = rk + below;
+                if (mi <= p) {
+                    R.mkey[mi] = si;
+                    R.mref[mi] = -(q + 1);
+                }
+            }
+            __syncthreads();
+            // exact ties: the minimum present at arrival is merged element q_i
+            if (part == 0 && live && R.mkey[R.lq[ci]] == si) atomicMin(&S.flag_first, ci);
+            for (int k = tid; k < kRunM / 32; k += blockDim.x) S.evicted[k] = 0u;
+            __syncthreads();
+            const int f = S.flag_first;
+            const int pc = f < m ? R.lq[f] : p;  // acceptances committed (arrival < f)
+            // ---- slots: the j-th acceptance takes the slot of the j-th eviction ----
+            for (int j = tid; j < pc; j += blockDim.x) {
+                const int v = R.mref[j];
+                if (v >= 0) {
+                    const int slot = S.r1.e.eslot[v];
+                    R.aslot[j] = slot;
+                    if (slot >= size_cur) {
+                        atomicAdd(&S.n_virtual, 1);
+                    } else if (S.owner[slot] >= 0) {
+                        W.keyslot[S.owner[slot]] = -1;  // inserted earlier in this update: evicted
+                    }
+                } else {
+                    R.aslot[j] = -1;
+                    const int qq = -v - 1;
+                    atomicOr(&S.evicted[qq >> 5], 1u << (qq & 31));
+                }
+            }
+            __syncthreads();
+            while (true) {  // pointer jumping along chains of re-evicted acceptances
+                int ns = -1, nv = 0;
+                bool pend = false;
+                if (tid < pc && R.aslot[tid] < 0) {
+                    const int par = -R.mref[tid] - 1;
+                    const int ps = R.aslot[par];
+                    pend = true;
+                    if (ps >= 0)
+                        ns = ps;
+                    else
+                        nv = R.mref[par];
+                }
+                __syncthreads();
+                if (pend) {
+                    if (ns >= 0)
+                        R.aslot[tid] = ns;
+                    else
+                        R.mref[tid] = nv;
+                }
+                if (!__syncthreads_or(pend)) break;
+            }
+            // ---- apply: final occupants ----
+            for (int j = tid; j < pc; j += blockDim.x) {
+                const int li = R.acand[j];
+                const int cj = R.lc[li];
+                if ((S.evicted[j >> 5] >> (j & 31)) & 1u) {
+                    W.keyslot[cj] = -1;  // inserted and evicted again inside the pass
+                    continue;
+                }
+                const int slot = R.aslot[j];
+                const int h = slot < size_cur ? S.pos[slot] : slot;  // free slots fill heap positions in order
+                heap_put(S, h, R.lk[li], tie_pack(S, iter, seq0 + j), slot);
+                S.owner[slot] = cj;
+                S.src[slot] = cj;
+                S.mr_src[slot] = cj;
+                atomicOr(&S.replaced[slot >> 5], 1u << (slot & 31));
+                W.keyslot[cj] = slot;
+            }
+            // the committed acceptances sorted (apk): ask positions whose acceptance index is
+            // < pc, compacted in order; apos2[ask position] = its position in apk
+            __syncthreads();
+            if (tid < p) R.apos2[R.arank[tid]] = tid;  // ask position -> acceptance index
+            __syncthreads();
+            const bool cm = tid < p && R.apos2[tid] < pc;
+            int e2 = 0;
+            block_excl_count(cm, e2, wscan);
+            if (cm) {
+                R.apk[e2] = R.ask[tid];
+                R.apos2[tid] = e2;
+            }
+            __syncthreads();
+            uint64_t nk[4];
+            int ns[4], np[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int e = tid * 4 + k;
+                np[k] = -1;
+                if (e < E && pc > 0) {
+                    nk[k] = ekey[e];
+                    ns[k] = S.r1.e.eslot[e];
+                    np[k] = e + lower_bound_u64(R.apk, pc, nk[k]) - pc;
+                }
+            }
+            uint64_t ak = 0ull;
+            int as = 0, ap = -1;
+            if (tid < pc && !((S.evicted[tid >> 5] >> (tid & 31)) & 1u)) {
+                const int r = R.arank[tid];
+                ak = R.ask[r];
+                as = R.aslot[tid];
+                ap = R.apos2[r] + R.abelow[tid] - pc;
+            }
+            __syncthreads();
+            if (pc > 0) {
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    if (np[k] >= 0) {
+                        S.r1.e.ekey[np[k]] = nk[k];
+                        S.r1.e.eslot[np[k]] = ns[k];
+                    }
+                if (ap >= 0) {
+                    S.r1.e.ekey[ap] = ak;
+                    S.r1.e.eslot[ap] = as;
+                }
+            }
+            if (tid == 0) {
+                S.size = size_cur + S.n_virtual;
+                S.next_seq = seq0 + pc;
+            }
+            // ---- next pass: drop f and every later candidate with score <= s_f ----
+            int nm = 0;
+            if (f < m) {
+                const uint64_t mu = R.lk[f];
+                const bool keepc = part == 0 && live && ci > f && si > mu;
+                const int cc = live ? R.lc[ci] : 0;
+                int e3 = 0;
+                nm = block_excl_count(keepc, e3, wscan);
+                if (keepc) {
+                    R.lk[e3] = si;
+                    R.lc[e3] = cc;
+                }
+            }
+            m = nm;
         }
-        const int slot = S.u.run.aslot[j];
-        const int h = slot < size0 ? S.pos[slot] : slot;  // free slots fill heap positions in order
-        heap_put(S, h, score_key(cscore[c]), tie_pack(S, iter, seq0 + j), slot);
-        S.owner[slot] = c;
-        S.src[slot] = c;
-        S.mr_src[slot] = c;
-        atomicOr(&S.replaced[slot >> 5], 1u << (slot & 31));
-        W.keyslot[c] = slot;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        S.size = size0 + S.n_virtual;
-        S.next_seq = seq0 + pc;
     }
     __syncthreads();
     heapify_cta(S, S.size);
-    return f;
+    return pos - r0;
 }
 
 __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
@@ -871,7 +965,6 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         S.last_max0 = INT64_MIN;
         S.qmin = D.meta[1];
         S.qmax = D.meta[1] + n;
-        S.force_seq_until = 0;
     }
     __syncthreads();
     {
@@ -973,7 +1066,11 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     // heap is rebuilt level-parallel.  (score, tb) is a total order (seq is unique), so the
     // heap's shape never affects which entry is the minimum.
     const int nrel = S.n_rel;
-    if (tid == 0) S.size = size0;
+    if (tid == 0) {
+        S.size = size0;
+        PLR_STAT(7, nrel);
+        PLR_STAT(8, 1);
+    }
     int base = 0;
     while (base < nrel) {
         const int cn = (nrel - base) < kChunk ? (nrel - base) : kChunk;
@@ -990,7 +1087,6 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             int size = S.size;
             int64_t next_seq = S.next_seq;
             const bool run_ok = S.run_ok > 0;
-            const int seq_until = S.force_seq_until - base;  // chunk-relative
             int r = 0, scan_end = 0, pscan_end = 0, action = 0, arg = 0;
             // candidate fields are prefetched one ahead (the replaced bit and the twin's
             // keyslot are read after the previous candidate is applied)
@@ -1012,7 +1108,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     im_n = S.u.chunk.im[r + 1];
                 }
                 // a stretch of certainly-new candidates worth a parallel insert run
-                if (run_ok && im < 0 && f == c && r >= pscan_end && r >= seq_until) {
+                if (run_ok && im < 0 && f == c && r >= pscan_end) {
                     const int L = pure_run(S, r, cn, lane);
                     if (L >= kRunMin) {
                         action = 2;
@@ -1035,7 +1131,9 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     scan_end = r + L;
                 }
                 const uint64_t sk = score_key(sc);
-                if (present >= 0) {  // identical level: score / max_return in place (tb unchanged)
+                if (lane == 0) PLR_STAT(0, 1);
+                if (present >= 0) {
+                    if (lane == 0) PLR_STAT(1, 1);  // identical level: score / max_return in place (tb unchanged)
                     const int h = S.pos[present];
                     const uint64_t ok = S.hk[h], ot = S.ht[h];
                     __syncwarp();
@@ -1088,6 +1186,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             continue;
         }
         if (action == 1) {  // bulk in-place run [lo, arg)
+            if (tid == 0) {
+                PLR_STAT(2, 1);
+                PLR_STAT(3, arg - lo);
+            }
             const int hi = arg;
             for (int i = lo + tid; i < hi; i += blockDim.x)
                 atomicMax(&S.mr_src[cand_present(S, W, i)], S.u.chunk.cid[i]);
@@ -1101,11 +1203,14 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             continue;
         }
         // insert run [base + lo, base + lo + arg)
-        const int used = insert_run(S, W, cscore, iter, base + lo, arg, K, wscan);
-        if (used < arg) {  // stopped on a tie: the flagged candidate (and a few after) go sequential
-            if (tid == 0) S.force_seq_until = base + lo + used + (used < kRunMin ? kSeqAfterFlag : 1);
+        {
+            const int used = insert_runs(S, W, cscore, iter, base + lo, nrel, K, wscan);
+            if (tid == 0) {
+                PLR_STAT(4, 1);
+                PLR_STAT(6, used);
+            }
+            base += lo + used;
         }
-        base += lo + used;
     }
     __syncthreads();
     // ---- epilogue: scatter the heap back to slots, deferred level / max_return copies ----

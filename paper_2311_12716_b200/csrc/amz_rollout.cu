@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     static_assert((LPW % 4 == 0 || LPW == 2) && LPW <= 32, "lane-major action gather: LPW 2 or a multiple of 4");
+
     DynSmem<LPW> &S = reinterpret_cast<DynSmem<LPW> *>(smem)[warp];
     // goal rewards R[time] = 1 - 0.9*time/T_ep (numpy's op order), tabulated per CTA
     double *s_rew = reinterpret_cast<double *>(smem + WPC * sizeof(DynSmem<LPW>));
@@ -323,6 +324,10 @@ __global__ void __launch_bounds__(32 * WPC, 1) k_dyn(Geo G, EnvDev E, int T, con
         for (int tt = threadIdx.x; tt <= G.tep; tt += blockDim.x) s_rew[tt] = goal_reward(tt, G.tep);
     __syncthreads();
     pdl_wait();  // lane state from the reset
+    if (E.iter && mode == AMZ_RESET_RESAMPLE) {  // graph replay: root.fold_in(*iter).fold_in(1)
+        seed_absorb(wrap, *E.iter);
+        seed_absorb(wrap, 1u);
+    }
     const int64_t B = E.B;
     DYN_MARK(0);
     const int64_t lane0 = ((int64_t)blockIdx.x * WPC + warp) * LPW;
@@ -601,6 +606,10 @@ __global__ void __launch_bounds__(128) k_spec_levels(Geo G, EnvDev E, int T, amz
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t l0 = ((int64_t)blockIdx.x * 4 + warp) * LPW;
     if (l0 >= E.B) return;
+    if (E.iter) {
+        seed_absorb(wrap, *E.iter);
+        seed_absorb(wrap, 1u);
+    }
     const int64_t l = l0 + lane;
     bool mine = false;
     uint64_t k0 = 0, k1 = 0;

@@ -1,0 +1,184 @@
+"""The DR iteration (configs[1]) as ONE CUDA-graph replay per step.
+
+One step of the hot path is: DR level generation + reset of every lane
+(``AutoResetWrapper.reset(root.fold_in(it))``, env/wrappers.py:43-56), T fused
+RESAMPLE-auto-reset env steps driven by the policy's action stream (the env side of
+agents/rollout.py:120-152), and GAE + MaxMC/PVL scores (agents/gae.py:8-37,
+runners/scoring.py:34-63).  Eagerly that is 4 kernels plus ~0.1-0.2 ms of Python/ctypes
+enqueue per step -- more than the kernels take at 4096 lanes.  Here the whole step is
+captured once: the iteration's key streams come from a device iteration counter
+(``amz_env_reset_dr_iter`` / ``amz_env_rollout_iter``, advanced by the graph itself), so
+a replay needs no host-side key work, and the host's cost per step is one
+``cudaGraphLaunch``.
+
+``host_io=True`` captures the end-to-end form: the step's inputs (actions u8 [T, B],
+values [T, B] and last values [B] in ``value_dtype``) are copied host->device from
+pinned staging at the start of the graph and scores | max returns (float64 [2, B]) are
+copied device->host at the end.  With ``overlap=True`` two graphs alternate between two
+device input buffers and each copies the NEXT step's inputs on a side stream while it
+computes the current step (the copy engines and the SMs work at the same time).
+
+Results equal the eager calls bit for bit (tests/test_gpu_graph.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from .batch import RESAMPLE, AutoResetWrapper, VectorBatchEnv
+from .core import as_params
+from .errors import ContractViolation
+from .gae import gae_and_scores
+from .host import pinned_empty
+from .rng import as_stream
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class DRIterationGraph:
+    """Captured DR iteration over ``benv`` (a VectorBatchEnv of B lanes) with T steps.
+
+    ``step(it)`` replays iteration ``it`` (keys root.fold_in(it)); iterations normally
+    run in order (the graph advances its device counter), a jump costs one small
+    synchronous copy.  Outputs live in ``self.out`` (trajectory tensors), ``self.gae``
+    (advantages / returns / scores / max_returns) and, with ``host_io``, ``self.host_result``
+    (pinned float64 [2, B]: scores | max returns of the last completed step)."""
+
+    def __init__(self, benv: VectorBatchEnv, root_rng, T: int, params, gamma: float, lam: float,
+                 score_fn: str = "maxmc", value_dtype=None, host_io: bool = False, overlap: bool = True):
+        torch = _torch()
+        if not isinstance(benv, VectorBatchEnv):
+            raise ContractViolation("DRIterationGraph needs a VectorBatchEnv")
+        self.torch = torch
+        self.benv = benv
+        self.env = AutoResetWrapper(benv, RESAMPLE)
+        self.p = as_params(params).validate()
+        self.T, self.B = int(T), benv.n_lanes
+        self.gamma, self.lam, self.score_fn = float(gamma), float(lam), score_fn
+        self.dev = benv.device
+        self.vdt = value_dtype or torch.float64
+        self.root = as_stream(root_rng)
+        self.root_pfx = self.root.seed_prefix()
+        self.host_io = host_io
+        self.overlap = overlap and host_io
+        T, B, dev, v = self.T, self.B, self.dev, self.p.agent_view_size
+        self.it_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.next_it = 0
+        nbuf = 2 if self.overlap else 1
+        self.inputs = [{"actions": torch.zeros((T, B), dtype=torch.uint8, device=dev),
+                        "values": torch.zeros((T, B), dtype=self.vdt, device=dev),
+                        "last": torch.zeros((B,), dtype=self.vdt, device=dev)} for _ in range(nbuf)]
+        self.out = {"view": torch.empty((T, B, v, v), dtype=torch.uint8, device=dev),
+                    "dir": torch.empty((T, B), dtype=torch.uint8, device=dev),
+                    "rewards": torch.empty((T, B), dtype=torch.float64, device=dev),
+                    "dones": torch.empty((T, B), dtype=torch.bool, device=dev),
+                    "final_view": torch.empty((B, v, v), dtype=torch.uint8, device=dev),
+                    "final_dir": torch.empty((B,), dtype=torch.uint8, device=dev),
+                    "reset_view": torch.empty((B, v, v), dtype=torch.uint8, device=dev),
+                    "reset_dir": torch.empty((B,), dtype=torch.int64, device=dev)}
+        self.res = torch.empty((2, B), dtype=torch.float64, device=dev)  # scores | max returns
+        self.gae = {"advantages": torch.empty((T, B), dtype=torch.float64, device=dev),
+                    "returns": torch.empty((T, B), dtype=torch.float64, device=dev),
+                    "scores": self.res[0], "max_returns": self.res[1]}
+        if host_io:
+            self.host_inputs = {"actions": pinned_empty((T, B), torch.uint8),
+                                "values": pinned_empty((T, B), self.vdt),
+                                "last": pinned_empty((B,), self.vdt)}
+            self.host_result = pinned_empty((2, B), torch.float64)
+        self.graphs = []
+        self.launches_per_step = 5  # k_env_reset_dr, k_dyn, k_render, k_gae_score*, k_iter_advance
+        self._step_count = 0
+        self._pending_h2d = False
+
+    # -- one step's kernels on the current stream ------------------------------------
+    def _kernels(self, inp):
+        torch = self.torch
+        lanes = self.benv._ensure(self.p)
+        o = self.out
+        st = lanes.stream()
+        _lib.call("amz_env_reset_dr_iter", lanes.handle, ctypes.byref(self.root_pfx), _lib.ptr(self.it_dev),
+                  _lib.ptr(o["reset_view"]), _lib.ptr(o["reset_dir"]), st)
+        _lib.call("amz_env_rollout_iter", lanes.handle, self.T, _lib.ptr(inp["actions"]), ctypes.byref(self.root_pfx),
+                  _lib.ptr(self.it_dev), _lib.ptr(o["view"]), _lib.ptr(o["dir"]), _lib.ptr(o["rewards"]),
+                  _lib.ptr(o["dones"]), _lib.ptr(o["final_view"]), _lib.ptr(o["final_dir"]), st)
+        gae_and_scores(o["rewards"], inp["values"], o["dones"], inp["last"], self.gamma, self.lam,
+                       score_fn=self.score_fn, out=self.gae)
+        _lib.call("amz_iter_advance", _lib.ptr(self.it_dev), 1, st)
+        del torch
+
+    def _h2d(self, inp):
+        for k in ("actions", "values", "last"):
+            inp[k].copy_(self.host_inputs[k], non_blocking=True)
+
+    def capture(self):
+        """Warm up (allocates the rollout scratch) and capture the graph(s)."""
+        torch = self.torch
+        with torch.cuda.device(self.dev):
+            s = torch.cuda.Stream(device=self.dev)
+            s.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(s):
+                self._kernels(self.inputs[0])  # warm-up: scratch allocation, attributes
+            torch.cuda.current_stream(self.dev).wait_stream(s)
+            torch.cuda.synchronize(self.dev)
+            self.graphs = []
+            for k in range(len(self.inputs)):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    cur = torch.cuda.current_stream(self.dev)
+                    if self.host_io and not self.overlap:
+                        self._h2d(self.inputs[k])
+                    if self.overlap:
+                        # next step's inputs on a side branch, concurrent with this step
+                        side = torch.cuda.Stream(device=self.dev)
+                        side.wait_stream(cur)
+                        with torch.cuda.stream(side):
+                            self._h2d(self.inputs[k ^ 1])
+                    self._kernels(self.inputs[k])
+                    if self.host_io:
+                        self.host_result.copy_(self.res, non_blocking=True)
+                    if self.overlap:
+                        cur.wait_stream(side)
+                self.graphs.append(g)
+            torch.cuda.synchronize(self.dev)
+        self.set_iteration(0)
+        return self
+
+    def set_iteration(self, it: int) -> None:
+        """Point the device counter at iteration ``it`` (synchronous)."""
+        if not 0 <= it < 2 ** 32:
+            raise ContractViolation(f"iteration {it} outside the u32 counter range")
+        torch = self.torch
+        torch.cuda.synchronize(self.dev)
+        self.it_dev.fill_(int(it) if it < 2 ** 31 else int(it) - 2 ** 32)
+        torch.cuda.synchronize(self.dev)
+        self.next_it = int(it)
+        self._pending_h2d = False
+
+    def prefetch(self):
+        """overlap mode: copy the first step's inputs (later steps' copies ride along in
+        the previous replay)."""
+        if self.overlap:
+            with self.torch.cuda.device(self.dev):
+                self._h2d(self.inputs[self._step_count & 1])
+            self._pending_h2d = True
+
+    def step(self, it: int | None = None):
+        """Replay one iteration (``it`` defaults to the next in order)."""
+        if not self.graphs:
+            self.capture()
+        if it is not None and it != self.next_it:
+            self.set_iteration(it)
+        if self.overlap and not self._pending_h2d:
+            self.prefetch()
+        self.graphs[self._step_count % len(self.graphs)].replay()
+        self._step_count += 1
+        self.next_it += 1
+        return self.gae
+
+
+__all__ = ["DRIterationGraph"]

@@ -14,10 +14,11 @@ score -inf in slot order).  With that order:
   the k-th acceptance takes the slot of the k-th eviction (chained through earlier
   acceptances that are evicted again).
 The order differs from the real rule only when a candidate's score EQUALS the score of
-the minimum present at its arrival (the real rule rejects, the order would accept).  A
-candidate is flagged if the smallest member of its equal-score group in the merged
-order is among the first p+1 and was present before it; the prefix before the first
-flagged candidate is committed, the flagged one goes through the sequential path.
+the minimum present at its arrival (the real rule rejects, the order would accept).
+That minimum is exactly element q_i of the merged order (q_i = acceptances before i:
+every later acceptance exceeds it), so the first such candidate f is found exactly; the
+prefix before f is committed, f and every later candidate scoring <= s_f are rejected
+(the minimum never drops), and the next pass runs over the rest.
 """
 import sys
 
@@ -52,76 +53,62 @@ def proto_update(buf: plr_np.LevelBuffer, levels, scores, maxrets, it, stats):
 
 
 def run(buf, levels, scores, maxrets, it, r0, r1, stats):
-    """Apply candidates [r0, r1) (all pure inserts); returns the next index to process."""
-    K, size = buf.K, buf.size
-    s = np.asarray(scores[r0:r1], dtype=np.float64) + 0.0  # -0.0 -> 0.0
-    m = len(s)
-    # buffer entries in eviction order (virtual free slots first, in slot order)
-    ex_score = np.concatenate([np.full(K - size, -np.inf), buf.score[:size] + 0.0])
-    ex_last = np.concatenate([np.zeros(K - size, np.int64), buf.last_sampled[:size]])
-    ex_seq = np.concatenate([np.arange(K - size), buf.seq[:size]])
-    ex_slot = np.concatenate([np.arange(size, K), np.arange(size)])
-    ex_virtual = np.concatenate([np.ones(K - size, bool), np.zeros(size, bool)])
-    order = np.lexsort((ex_seq, ex_last, ~ex_virtual, ex_score))
-    sorted_scores = ex_score[order]
-    below = np.searchsorted(sorted_scores, s, side="right")
-    prefix_greater = np.array([(s[:i] > s[i]).sum() for i in range(m)], dtype=np.int64)
-    acc = prefix_greater < below
-    A = np.nonzero(acc)[0]
-    p = len(A)
-    # merged order of (buffer) U (accepted): key (score, class, tie) -- buffer entries before
-    # newcomers at equal score, newcomers by arrival
-    items = [(ex_score[o], 0, k, ("b", o)) for k, o in enumerate(order)]
-    items += [(s[a], 1, a, ("a", a)) for a in A]
-    items.sort(key=lambda x: (x[0], x[1], x[2]))
-    # tie flags
-    flagged = np.zeros(m, bool)
-    first_of_score = {}
-    for idx, itm in enumerate(items):
-        first_of_score.setdefault(itm[0], (idx, itm))
-    for i in range(m):
-        g = first_of_score.get(s[i])
-        if g is None:
-            continue
-        gidx, gitm = g
-        if gidx <= p and (gitm[3][0] == "b" or gitm[3][1] < i):
-            flagged[i] = True
-    f = int(np.argmax(flagged)) if flagged.any() else m
-    stats["runs"] += 1
-    stats["flagged"] += int(flagged.any())
-    # commit arrivals < f
-    acc_before = [a for a in A if a < f]
-    pp = len(acc_before)
-    evict = [items[k][3] for k in range(pp)]
-    slot_of_new = {}
-    size_new = size
-    for jj, a in enumerate(acc_before):
-        kind, ref = evict[jj]
-        if kind == "b":
-            slot = int(ex_slot[ref])
-            if ex_virtual[ref]:
-                size_new += 1
+    """Apply candidates [r0, r1) (all certainly new) in passes; returns r1."""
+    live = list(range(r0, r1))
+    while live:
+        K, size = buf.K, buf.size
+        s = np.array([scores[c] for c in live], dtype=np.float64) + 0.0  # -0.0 -> 0.0
+        m = len(s)
+        # buffer in eviction order (virtual free slots first, in slot order)
+        ex_score = np.concatenate([np.full(K - size, -np.inf), buf.score[:size] + 0.0])
+        ex_last = np.concatenate([np.zeros(K - size, np.int64), buf.last_sampled[:size]])
+        ex_seq = np.concatenate([np.arange(K - size), buf.seq[:size]])
+        ex_slot = np.concatenate([np.arange(size, K), np.arange(size)])
+        ex_virtual = np.concatenate([np.ones(K - size, bool), np.zeros(size, bool)])
+        order = np.lexsort((ex_seq, ex_last, ~ex_virtual, ex_score))
+        below = np.searchsorted(ex_score[order], s, side="right")
+        greater = np.array([(s[:i] > s[i]).sum() for i in range(m)], dtype=np.int64)
+        acc = greater < below
+        A = np.nonzero(acc)[0]
+        p = len(A)
+        q = np.concatenate([[0], np.cumsum(acc)])[:m]  # acceptances before each arrival
+        items = [(ex_score[o], 0, k, ("b", o)) for k, o in enumerate(order)]
+        items += [(s[a], 1, a, ("a", a)) for a in A]
+        items.sort(key=lambda x: (x[0], x[1], x[2]))
+        # exact ties: the minimum present at arrival i is merged element q_i
+        flags = [i for i in range(m) if items[q[i]][0] == s[i]]
+        f = flags[0] if flags else m
+        stats["runs"] += 1
+        stats["flagged"] += int(bool(flags))
+        acc_before = [a for a in A if a < f]
+        slot_of_new = {}
+        size_new = size
+        for jj, a in enumerate(acc_before):
+            kind, ref = items[jj][3]
+            if kind == "b":
+                slot = int(ex_slot[ref])
+                if ex_virtual[ref]:
+                    size_new += 1
+                else:
+                    del buf._index[buf.key(buf.levels[slot])]
             else:
-                del buf._index[buf.key(buf.levels[slot])]
+                slot = slot_of_new.pop(ref)
+                del buf._index[buf.key(levels[live[ref]])]
+            slot_of_new[a] = slot
+            c = live[a]
+            buf.levels[slot] = levels[c]
+            buf.score[slot] = scores[c]
+            buf.max_return[slot] = maxrets[c]
+            buf.last_sampled[slot] = it
+            buf.seq[slot] = buf.next_seq
+            buf.next_seq += 1
+            buf._index[buf.key(levels[c])] = slot
+        buf.size = size_new
+        stats["par"] += f
+        if f < m:  # f and every later candidate scoring <= s_f are rejected
+            live = [live[i] for i in range(f + 1, m) if s[i] > s[f]]
         else:
-            slot = slot_of_new.pop(ref)
-            del buf._index[buf.key(levels[r0 + ref])]
-        slot_of_new[a] = slot
-        c = r0 + a
-        buf.levels[slot] = levels[c]
-        buf.score[slot] = scores[c]
-        buf.max_return[slot] = maxrets[c]
-        buf.last_sampled[slot] = it
-        buf.seq[slot] = buf.next_seq
-        buf.next_seq += 1
-        buf._index[buf.key(levels[c])] = slot
-    buf.size = size_new
-    stats["par"] += f
-    if f < m:  # the flagged candidate through the sequential rule
-        c = r0 + f
-        buf.update(levels[c:c + 1], scores[c:c + 1], maxrets[c:c + 1], it)
-        stats["seq"] += 1
-        return c + 1
+            live = []
     return r1
 
 
