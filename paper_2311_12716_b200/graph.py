@@ -50,7 +50,8 @@ class DRIterationGraph:
     (pinned float64 [2, B]: scores | max returns of the last completed step)."""
 
     def __init__(self, benv: VectorBatchEnv, root_rng, T: int, params, gamma: float, lam: float,
-                 score_fn: str = "maxmc", value_dtype=None, host_io: bool = False, overlap: bool = True):
+                 score_fn: str = "maxmc", value_dtype=None, host_io: bool = False, overlap: bool = True,
+                 copy_streams: int = 1):
         torch = _torch()
         if not isinstance(benv, VectorBatchEnv):
             raise ContractViolation("DRIterationGraph needs a VectorBatchEnv")
@@ -66,13 +67,18 @@ class DRIterationGraph:
         self.root_pfx = self.root.seed_prefix()
         self.host_io = host_io
         self.overlap = overlap and host_io
+        self.copy_streams = max(1, min(2, int(copy_streams)))
         T, B, dev, v = self.T, self.B, self.dev, self.p.agent_view_size
         self.it_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.next_it = 0
         nbuf = 2 if self.overlap else 1
-        self.inputs = [{"actions": torch.zeros((T, B), dtype=torch.uint8, device=dev),
-                        "values": torch.zeros((T, B), dtype=self.vdt, device=dev),
-                        "last": torch.zeros((B,), dtype=self.vdt, device=dev)} for _ in range(nbuf)]
+        # one contiguous byte buffer per input slot (values | last values | actions), so the
+        # host->device copy is two large copies (one per DMA engine) instead of three
+        es = torch.empty((), dtype=self.vdt).element_size()
+        self._nv, self._nl, self._na = T * B * es, B * es, T * B
+        self._nbytes = self._nv + self._nl + self._na
+        self._raw = [torch.zeros(self._nbytes, dtype=torch.uint8, device=dev) for _ in range(nbuf)]
+        self.inputs = [self._views(r) for r in self._raw]
         self.out = {"view": torch.empty((T, B, v, v), dtype=torch.uint8, device=dev),
                     "dir": torch.empty((T, B), dtype=torch.uint8, device=dev),
                     "rewards": torch.empty((T, B), dtype=torch.float64, device=dev),
@@ -86,9 +92,8 @@ class DRIterationGraph:
                     "returns": torch.empty((T, B), dtype=torch.float64, device=dev),
                     "scores": self.res[0], "max_returns": self.res[1]}
         if host_io:
-            self.host_inputs = {"actions": pinned_empty((T, B), torch.uint8),
-                                "values": pinned_empty((T, B), self.vdt),
-                                "last": pinned_empty((B,), self.vdt)}
+            self._host_raw = pinned_empty((self._nbytes,), torch.uint8)
+            self.host_inputs = self._views(self._host_raw)
             self.host_result = pinned_empty((2, B), torch.float64)
         self.graphs = []
         self.launches_per_step = 5  # k_env_reset_dr, k_dyn, k_render, k_gae_score*, k_iter_advance
@@ -111,9 +116,28 @@ class DRIterationGraph:
         _lib.call("amz_iter_advance", _lib.ptr(self.it_dev), 1, st)
         del torch
 
-    def _h2d(self, inp):
-        for k in ("actions", "values", "last"):
-            inp[k].copy_(self.host_inputs[k], non_blocking=True)
+    def _views(self, raw):
+        T, B, nv, nl = self.T, self.B, self._nv, self._nl
+        return {"values": raw[:nv].view(self.vdt).view(T, B), "last": raw[nv:nv + nl].view(self.vdt),
+                "actions": raw[nv + nl:].view(T, B)}
+
+    def _h2d(self, k, streams=None):
+        """Copy the pinned staging into input slot k: two halves, one per copy stream
+        (two DMA engines) when ``streams`` are given, else on the current stream."""
+        torch = self.torch
+        dst, src = self._raw[k], self._host_raw
+        half = (self._nbytes // 2) & ~15
+        if streams is None or len(streams) == 1:
+            if streams is None:
+                dst.copy_(src, non_blocking=True)
+            else:
+                with torch.cuda.stream(streams[0]):
+                    dst.copy_(src, non_blocking=True)
+            return
+        for i, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                sl = slice(0, half) if i == 0 else slice(half, self._nbytes)
+                dst[sl].copy_(src[sl], non_blocking=True)
 
     def capture(self):
         """Warm up (allocates the rollout scratch) and capture the graph(s)."""
@@ -131,18 +155,20 @@ class DRIterationGraph:
                 with torch.cuda.graph(g, stream=s):
                     cur = torch.cuda.current_stream(self.dev)
                     if self.host_io and not self.overlap:
-                        self._h2d(self.inputs[k])
+                        self._h2d(k)
                     if self.overlap:
-                        # next step's inputs on a side branch, concurrent with this step
-                        side = torch.cuda.Stream(device=self.dev)
-                        side.wait_stream(cur)
-                        with torch.cuda.stream(side):
-                            self._h2d(self.inputs[k ^ 1])
+                        # next step's inputs on two side branches (two DMA engines),
+                        # concurrent with this step's kernels
+                        sides = [torch.cuda.Stream(device=self.dev) for _ in range(self.copy_streams)]
+                        for sd in sides:
+                            sd.wait_stream(cur)
+                        self._h2d(k ^ 1, sides)
                     self._kernels(self.inputs[k])
                     if self.host_io:
                         self.host_result.copy_(self.res, non_blocking=True)
                     if self.overlap:
-                        cur.wait_stream(side)
+                        for sd in sides:
+                            cur.wait_stream(sd)
                 self.graphs.append(g)
             torch.cuda.synchronize(self.dev)
         self.set_iteration(0)
@@ -164,7 +190,7 @@ class DRIterationGraph:
         the previous replay)."""
         if self.overlap:
             with self.torch.cuda.device(self.dev):
-                self._h2d(self.inputs[self._step_count & 1])
+                self._h2d(self._step_count & 1)
             self._pending_h2d = True
 
     def step(self, it: int | None = None):
