@@ -203,10 +203,10 @@ __device__ __forceinline__ void render_lane(int r, int c, int d, int gr, int gc,
 // See-through 5x5 observation (the default view) with word-level arithmetic: a view row
 // is one board word (grid row for N/S headings, grid column for E/W), its 5-cell window
 // and in-grid mask become code bytes (3 off-grid, 1 wall, 0 empty) by two
-// multiply-spreads, the S/W mirror is one byte permute, and the goal byte is stored last
-// (it is never off-grid or a wall).  ~160 instructions per observation instead of ~440.
-__device__ __forceinline__ void render5_see(int r, int c, int d, int gr, int gc, int H, int W, const uint32_t *board,
-                                            uint8_t *out) {
+// multiply-spreads, the S/W mirror is one byte permute, the goal byte is patched into its
+// row (it is never off-grid or a wall).  The 25 bytes come back as 7 little-endian words.
+__device__ __forceinline__ void render5_see_words(int r, int c, int d, int gr, int gc, int H, int W,
+                                                  const uint32_t *board, uint32_t (&w)[7]) {
     const bool ns = (d & 1) == 0;
     const int sgn = (d == 0 || d == 3) ? -1 : 1;
     const int base = ns ? r : c, center = ns ? c : r;
@@ -217,29 +217,61 @@ __device__ __forceinline__ void render5_see(int r, int c, int d, int gr, int gc,
     const uint32_t ibm = ((((1u << llen) - 1u) << 16) >> sx) & 31u;
     const bool rev = d >= 2;
     const uint32_t sel = rev ? 0x1234u : 0x3210u;
+    const int fr = dir_dr(d), fc = dir_dc(d);
+    const int dr = gr - r, dcol = gc - c;
+    const int g_ahead = dr * fr + dcol * fc, g_side = dr * fc - dcol * fr;
+    const int g_vr = (g_ahead >= 0 && g_ahead < 5 && g_side >= -2 && g_side <= 2) ? 4 - g_ahead : -1;
+    const int g_vc = g_side + 2;  // 0..4 when visible
+    const uint32_t glo_clr = g_vc < 4 ? ~(0xFFu << (8 * (g_vc & 3))) : 0xFFFFFFFFu;
+    const uint32_t glo_set = g_vc < 4 ? (2u << (8 * (g_vc & 3))) : 0u;
+    uint32_t lo[5], hi[5];
 #pragma unroll
     for (int vr = 0; vr < 5; vr++) {
         const int L = base + sgn * (4 - vr);
         const bool in = (uint32_t)L < nlines;
-        const uint32_t w = in ? board[L] : 0u;
-        const uint32_t x = ((w << up) >> sx) & 31u;
+        const uint32_t bw = in ? board[L] : 0u;
+        const uint32_t x = ((bw << up) >> sx) & 31u;
         const uint32_t m = in ? ibm : 0u;
         const uint32_t wl = x & m, ob = ~m & 31u;
-        const uint32_t lo = (((wl & 15u) * 0x00204081u) & 0x01010101u) + (((ob & 15u) * 0x00204081u) & 0x01010101u) * 3u;
-        const uint32_t hi = ((wl >> 4) & 1u) + ((ob >> 4) & 1u) * 3u;
-        const uint32_t o0 = __byte_perm(lo, hi, sel);
-        const uint32_t o1 = rev ? (lo & 0xFFu) : hi;
-        uint8_t *o = out + vr * 5;
-        o[0] = (uint8_t)o0;
-        o[1] = (uint8_t)(o0 >> 8);
-        o[2] = (uint8_t)(o0 >> 16);
-        o[3] = (uint8_t)(o0 >> 24);
-        o[4] = (uint8_t)o1;
+        const uint32_t l4 = (((wl & 15u) * 0x00204081u) & 0x01010101u) + (((ob & 15u) * 0x00204081u) & 0x01010101u) * 3u;
+        const uint32_t h1 = ((wl >> 4) & 1u) + ((ob >> 4) & 1u) * 3u;
+        uint32_t o0 = __byte_perm(l4, h1, sel);
+        uint32_t o1 = rev ? (l4 & 0xFFu) : h1;
+        if (vr == g_vr) {
+            o0 = (o0 & glo_clr) | glo_set;
+            o1 = g_vc == 4 ? 2u : o1;
+        }
+        lo[vr] = o0;
+        hi[vr] = o1;
     }
-    const int fr = dir_dr(d), fc = dir_dc(d);
-    const int dr = gr - r, dcol = gc - c;
-    const int g_ahead = dr * fr + dcol * fc, g_side = dr * fc - dcol * fr;
-    if (g_ahead >= 0 && g_ahead < 5 && g_side >= -2 && g_side <= 2) out[(4 - g_ahead) * 5 + g_side + 2] = 2;
+    // rows at bytes 0, 5, 10, 15, 20
+    w[0] = lo[0];
+    w[1] = hi[0] | (lo[1] << 8);
+    w[2] = (lo[1] >> 24) | (hi[1] << 8) | (lo[2] << 16);
+    w[3] = (lo[2] >> 16) | (hi[2] << 16) | (lo[3] << 24);
+    w[4] = (lo[3] >> 8) | (hi[3] << 24);
+    w[5] = lo[4];
+    w[6] = hi[4];
+}
+// Warp-collective store of each lane's 25 bytes (7 words from render5_see_words) at byte
+// offset 25 * idx of a 16-byte-aligned staging row, idx = lane index in the row (the
+// warp's lanes hold consecutive idx, idx % 32 == lane): 6-7 aligned 32-bit stores per
+// lane instead of 25 byte stores; the word a lane shares with its successor is merged
+// by a shuffle.  Every lane of the warp must call it (live = false: nothing stored).
+__device__ __forceinline__ void store_obs25(uint8_t *stage, int idx, bool live, const uint32_t (&w)[7]) {
+    const int o = idx & 3;  // (25 * idx) mod 4
+    const int sh = 8 * o;
+    uint32_t a[7];
+    a[0] = w[0] << sh;
+#pragma unroll
+    for (int k = 1; k < 7; k++) a[k] = __funnelshift_l(w[k - 1], w[k], sh);
+    const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, live ? a[0] : 0u, 1);
+    if (o != 3) a[6] |= nxt;  // this lane's last word is the successor's first
+    if (!live) return;
+    uint32_t *dst = reinterpret_cast<uint32_t *>(stage) + ((25 * idx) >> 2);
+    if (o == 0) dst[0] = a[0];
+#pragma unroll
+    for (int k = 1; k < 7; k++) dst[k] = a[k];
 }
 
 constexpr int kRec = 20;  // u32 words per epoch record: board[16], goal, pad
@@ -746,11 +778,8 @@ __global__ void __launch_bounds__(128) k_render(Geo G, int64_t B, int64_t n, con
             const uint32_t *rec = epochs + ((size_t)(pr >> 12) * B + l) * kRec;
             const uint32_t gw = rec[16];
             const int r = pr & 15, c = (pr >> 4) & 15, d = (pr >> 8) & 3;
-            if constexpr (V == 5 && SEE)
-                render5_see(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, s_view[buf] + threadIdx.x * VV);
-            else
-                render_lane<V, SEE, 1>(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, s_spread,
-                                       s_view[buf] + threadIdx.x * VV);
+            render_lane<V, SEE, 1>(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, s_spread,
+                                   s_view[buf] + threadIdx.x * VV);
             s_dir[buf][threadIdx.x] = (uint8_t)d;
             s_done[buf][threadIdx.x] = (uint8_t)((pr >> 11) & 1u);
             if (!fin && reward && !((pr >> 10) & 1u)) reward[i] = 0.0;
@@ -794,11 +823,115 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
                (const uint32_t *)spec_step, avec, use_lut);
 }
 
+// Quad tiles: a CTA renders 128 consecutive lanes x 4 consecutive steps, one lane per
+// thread.  The lane's 4 step records are one 16-byte load (the uint4 quad k_dyn stores),
+// the epoch record address and goal word are fetched once per epoch (a lane rarely
+// changes level inside 4 steps), and the CTA's 4 output rows -- 128 consecutive
+// observations of one step each -- leave as 4 bulk copies (plus dir / done rows).
+// Tiles [0, nq * ng) are (quad, lane group) pairs, quad-major; tiles past that render
+// the final observations.
+template <int V, bool SEE>
+__device__ __forceinline__ void render_obs(int r, int c, int d, uint32_t gw, const Geo &G, const uint32_t *rec,
+                                           const uint64_t *spread, uint8_t *out) {
+    render_lane<V, SEE, 1>(r, c, d, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W, rec, spread, out);
+}
+
+template <int V, bool SEE>
+__global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const uint32_t *__restrict__ poses,
+                                                  const uint32_t *__restrict__ final_pose,
+                                                  const uint32_t *__restrict__ epochs, uint8_t *__restrict__ view,
+                                                  uint8_t *__restrict__ dirs, double *__restrict__ reward,
+                                                  uint8_t *__restrict__ done, uint8_t *__restrict__ fview,
+                                                  uint8_t *__restrict__ fdir, int bulk_ok, int64_t ng, int64_t nq) {
+    constexpr int VV = V * V;
+    __shared__ __align__(128) uint8_t s_view[4][128 * VV];
+    __shared__ __align__(16) uint8_t s_dir[4][128];
+    __shared__ __align__(16) uint8_t s_done[4][128];
+    __shared__ uint64_t s_spread[32];
+    if (!(V == 5 && SEE)) init_spread(s_spread);
+    const int tid = threadIdx.x;
+    const int64_t tile = blockIdx.x;
+    const bool fin = tile >= nq * ng;
+    const int64_t q = fin ? 0 : tile / ng, g = fin ? tile - nq * ng : tile - (tile / ng) * ng;
+    const int64_t l = g * 128 + tid;
+    const bool live = l < B;
+    const int nvalid = (int)((B - g * 128) < 128 ? (B - g * 128) : 128);
+    const int nsteps = fin ? 1 : ((T - 4 * (int)q) < 4 ? (T - 4 * (int)q) : 4);
+    __syncthreads();
+    pdl_wait();  // poses / epochs from k_dyn
+    uint4 pq = make_uint4(0u, 0u, 0u, 0u);
+    if (live) pq = fin ? make_uint4(final_pose[l], 0u, 0u, 0u) : reinterpret_cast<const uint4 *>(poses)[q * B + l];
+    uint32_t ep = 0xFFFFFFFFu, gw = 0u;
+    const uint32_t *rec = nullptr;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        if (k < nsteps) {  // uniform across the CTA
+            const uint32_t pr = k == 0 ? pq.x : k == 1 ? pq.y : k == 2 ? pq.z : pq.w;
+            if (live) {
+                if ((pr >> 12) != ep) {
+                    ep = pr >> 12;
+                    rec = epochs + ((size_t)ep * B + l) * kRec;
+                    gw = rec[16];
+                }
+                s_dir[k][tid] = (uint8_t)((pr >> 8) & 3);
+                s_done[k][tid] = (uint8_t)((pr >> 11) & 1u);
+                if (!fin && reward && !((pr >> 10) & 1u)) reward[(4 * q + k) * B + l] = 0.0;
+            }
+            if constexpr (V == 5 && SEE) {
+                uint32_t w[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                if (live)
+                    render5_see_words(pr & 15, (pr >> 4) & 15, (pr >> 8) & 3, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W,
+                                      rec, w);
+                store_obs25(s_view[k], tid, live, w);  // warp-collective
+            } else {
+                if (live)
+                    render_obs<V, SEE>(pr & 15, (pr >> 4) & 15, (pr >> 8) & 3, gw, G, rec, s_spread,
+                                       s_view[k] + tid * VV);
+            }
+        }
+    }
+    uint8_t *vout = fin ? fview : view;
+    uint8_t *dout = fin ? fdir : dirs;
+    uint8_t *nout = fin ? nullptr : done;
+    if (bulk_ok && nvalid == 128) {
+        fence_proxy_async();
+        __syncthreads();
+        if (tid < nsteps) {
+            const int64_t row = (fin ? 0 : (4 * q + tid) * B) + g * 128;
+            bulk_store(vout + row * VV, s_view[tid], 128 * VV);
+            if (dout) bulk_store(dout + row, s_dir[tid], 128);
+            if (nout) bulk_store(nout + row, s_done[tid], 128);
+            bulk_commit();
+            bulk_wait_all();
+        }
+    } else {
+        __syncthreads();
+        for (int k = 0; k < nsteps; k++) {
+            const int64_t row = (fin ? 0 : (4 * q + k) * B) + g * 128;
+            for (int x = tid; x < nvalid * VV; x += 128) vout[row * VV + x] = s_view[k][x];
+            if (tid < nvalid) {
+                if (dout) dout[row + tid] = s_dir[k][tid];
+                if (nout) nout[row + tid] = s_done[k][tid];
+            }
+        }
+    }
+}
+
 template <int V, bool SEE>
 static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *poses, const uint32_t *final_pose,
                           const uint32_t *epochs, uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done,
                           uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
     auto al16 = [](const void *p) { return p == nullptr || (((uintptr_t)p) & 15u) == 0; };
+    static const int legacy = getenv("AMZ_RENDER_LEGACY") ? atoi(getenv("AMZ_RENDER_LEGACY")) : 0;
+    if (!legacy) {
+        const int bulk = al16(view) && al16(dirs) && al16(done) && al16(fview) && al16(fdir) && B % 16 == 0;
+        const int T = (int)(n / B);
+        const int64_t ng = (B + 127) / 128, nq = (T + 3) / 4;
+        const int64_t nt = nq * ng + (fview ? ng : 0);
+        launch_pdl(k_render_q<V, SEE>, dim3((unsigned)nt), dim3(128), 0, s, G, B, T, poses, final_pose, epochs, view,
+                   dirs, reward, done, fview, fdir, bulk, ng, nq);
+        return;
+    }
     const int bulk = al16(view) && al16(dirs) && al16(done) && al16(fview) && al16(fdir);
     const int64_t g1 = (n + 127) / 128, g2 = fview ? (B + 127) / 128 : 0, nt = g1 + g2;
     const int64_t grid = nt < 148 * 12 ? nt : 148 * 12;
