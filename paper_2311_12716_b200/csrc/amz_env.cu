@@ -127,8 +127,10 @@ __global__ void __launch_bounds__(128) k_env_reset(Geo G, EnvDev E, const amz_le
 // state, board and observation.  With a wrapper key it also prepares the lane's timeout
 // level for the first RESAMPLE rollout (key wrap ++ [tep - 1, global lane]: a fresh
 // episode times out at step tep - 1), so that rollout needs no k_spec_levels pass.
+// 7 resident CTAs per SM (<= 73 registers): a 4096-lane reset is 1024 CTAs, one wave on
+// 148 SMs; at 78 registers (6 per SM) the last 136 CTAs ran as a second wave (27 -> 38 us)
 template <int V>
-__global__ void __launch_bounds__(128) k_env_reset_dr(Geo G, EnvDev E, amz_seed_t prefix, int prep,
+__global__ void __launch_bounds__(128, 7) k_env_reset_dr(Geo G, EnvDev E, amz_seed_t prefix, int prep,
                                                       amz_seed_t wrap, amz_level_t *__restrict__ spec,
                                                       uint32_t *__restrict__ spec_step, uint8_t *__restrict__ view,
                                                       int64_t *__restrict__ dirs) {
@@ -139,16 +141,13 @@ __global__ void __launch_bounds__(128) k_env_reset_dr(Geo G, EnvDev E, amz_seed_
     const int64_t l = (int64_t)blockIdx.x * 4 + warp;
     if (l >= E.B) return;
     const uint32_t gl = E.lane_offset + (uint32_t)l;
-    if (E.iter) {  // graph replay: this iteration's streams from the root key
-        const uint32_t it = *E.iter;
-        seed_absorb(prefix, it);
-        seed_absorb(prefix, 0u);
-        seed_absorb(wrap, it);
-        seed_absorb(wrap, 1u);
-    }
     uint64_t k0, k1;
     {
         amz_seed_t sd = prefix;
+        if (E.iter) {  // graph replay: this iteration's lane-level stream root.fold_in(it).fold_in(0)
+            seed_absorb(sd, *E.iter);
+            seed_absorb(sd, 0u);
+        }
         seed_absorb(sd, gl);
         seed_key(sd, k0, k1);
     }
@@ -179,6 +178,10 @@ __global__ void __launch_bounds__(128) k_env_reset_dr(Geo G, EnvDev E, amz_seed_
         for (int j = lane; j < V * V; j += 32) view[l * V * V + j] = stage[warp][j];
     if (prep) {
         amz_seed_t sd = wrap;
+        if (E.iter) {  // root.fold_in(it).fold_in(1): the iteration's auto-reset stream
+            seed_absorb(sd, *E.iter);
+            seed_absorb(sd, 1u);
+        }
         seed_absorb(sd, (uint32_t)(G.tep - 1));
         seed_absorb(sd, gl);
         seed_key(sd, k0, k1);

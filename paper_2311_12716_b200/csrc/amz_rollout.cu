@@ -30,6 +30,9 @@
 #ifndef AMZ_DYN8_MINB
 #define AMZ_DYN8_MINB 3
 #endif
+#ifndef AMZ_DYN2_MINB
+#define AMZ_DYN2_MINB 1
+#endif
 
 namespace amz {
 
@@ -388,7 +391,7 @@ __device__ __forceinline__ void build_move_table(const uint32_t *board, int L, u
 // (LPW 8) runs many waves, so it trades registers for a third resident CTA
 template <int LPW>
 struct DynOcc {
-    static constexpr int kMinBlocks = LPW >= 8 ? AMZ_DYN8_MINB : 1;
+    static constexpr int kMinBlocks = LPW >= 8 ? AMZ_DYN8_MINB : (LPW <= 2 ? AMZ_DYN2_MINB : 1);
 };
 template <int LPW, int WPC>
 __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions, int mode,
