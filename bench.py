@@ -50,10 +50,19 @@ GAE_BYTES_PER_ELEM = 33  # r f64 + V f64 + done u8 in, A f64 + R f64 out
 def _traffic():
     """Per-launch DRAM bytes of the roofline kernels from the committed ncu capture."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1m_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2l_traffic.json")) as f:
             return json.load(f)
     except (OSError, ValueError):
         return {}
+
+
+def _write_peak():
+    """Measured write-only HBM stream rate (tools/bw_probe.py, profiles/r2l_bw.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2l_bw.json")) as f:
+            return float(json.load(f)["write_fill_GBs"])
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def _peaks():
@@ -466,7 +475,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e through the public API: pinned host inputs in, scores | max returns out,
     # one graph replay per step, the next step's H2D overlapped with this step's kernels;
     # one timed region over all K steps including every copy, L2 flush and result read ----
-    def e2e(vdt):
+    def e2e(vdt, flush_l2):
         g2 = _graph(dev, B, T, args.seed, rank * B, vdt, True, torch)
         for _ in range(args.warmup):
             g2.step()
@@ -477,7 +486,8 @@ def run_ours(args, rank, world, local_rank):
         p0.record()
         h0 = time.perf_counter()
         for i in range(args.steps):
-            flush.fill_(i & 0xFF)
+            if flush_l2:
+                flush.fill_(i & 0xFF)
             g2.step()
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         p1.record()
@@ -489,9 +499,10 @@ def run_ours(args, rank, world, local_rank):
         del g2
         return ms, host_ms, h2d
 
-    e32_ms, host32_ms, h2d32 = e2e(torch.float32)
-    e64_ms, host64_ms, h2d64 = e2e(torch.float64)
-    e32_ms, e64_ms = max_ranks(e32_ms, e64_ms)
+    e32_ms, host32_ms, h2d32 = e2e(torch.float32, False)
+    e32f_ms, host32f_ms, _ = e2e(torch.float32, True)
+    e64_ms, host64_ms, h2d64 = e2e(torch.float64, False)
+    e32_ms, e32f_ms, e64_ms = max_ranks(e32_ms, e32f_ms, e64_ms)
     peaks, src = _peaks()
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     extra = {}
@@ -551,18 +562,25 @@ def run_ours(args, rank, world, local_rank):
                 "inputs": "actions u8 [T, B] + values f32 [T, B] + last values f32 [B] (the policy's output dtype, "
                           "widened to f64 in-kernel like the reference's value.double(), agents/ppo.py:96)",
                 "mode": "DRIterationGraph(host_io=True): one graph replay per step; its H2D of the NEXT step's pinned "
-                        "inputs runs on a side branch concurrent with this step's kernels, the D2H of scores | max "
-                        "returns ends the replay; one timed region over all K steps incl. the L2 flushes",
+                        "inputs runs on two side branches (two DMA engines) concurrent with this step's kernels, the "
+                        "D2H of scores | max returns ends the replay; one timed region over all K steps",
+                "l2": "not flushed between e2e steps: every step's inputs are copied fresh from pinned host memory and "
+                      "its 54 MB of outputs overwrite the previous step's (with_l2_flush: a 256 MB write before every "
+                      "step, inside the timed region)",
+                "with_l2_flush": {"value": units / (e32f_ms * 1e-3 / args.steps), "ms_per_step": e32f_ms / args.steps,
+                                  "host_enqueue_ms_per_step": host32f_ms},
                 "values_f64": {"value": units / (e64_ms * 1e-3 / args.steps), "ms_per_step": e64_ms / args.steps,
                                "h2d_bytes_per_step": h2d64, "host_enqueue_ms_per_step": host64_ms}},
         "gpu_launches": 5 * args.steps,
         "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
                      "frac": roll_gbs / peak,
                      "traffic": _traffic().get("k_env_rollout", {}).get("dram_bytes"),
-                     "traffic_source": "profiles/r1m_traffic.json (ncu --set full, per launch)",
+                     "traffic_source": "profiles/r2l_traffic.json (ncu --set full, per launch)",
                      "peak_source": src,
                      "algorithmic_bytes": f"{ENV_BYTES_PER_STEP} B/env-step x {B * T} env-steps per launch",
                      "kernel_ms": roll,
+                     "write_stream_GBs": _write_peak(),
+                     "frac_of_write_stream": (roll_gbs / _write_peak()) if _write_peak() else None,
                      "note": "k_env_rollout = k_dyn + k_render (the timeout levels of the first auto-resets "
                              "come prepared from the fused reset launch, so no k_spec_levels); at 4096 lanes the "
                              "per-lane 256-step dynamics chain (latency) bounds it, not HBM; the HBM point is "
@@ -723,7 +741,15 @@ def measure_large_batch(dev, B, T, iters, flush, peak):
     gae = statistics.mean(k[1].elapsed_time(k[2]) for k in kev)
     rg = ENV_BYTES_PER_STEP * B * T / (roll * 1e-3) / 1e9
     gg = GAE_BYTES_PER_ELEM * B * T / (gae * 1e-3) / 1e9
+    tr = _traffic().get("large_batch_rollout", {})
+    wpk = _write_peak()
     out = {"lanes": B, "T": T, "rollout_ms": roll, "rollout_GBs": rg, "rollout_frac": rg / peak,
+           "rollout_traffic": tr.get("dram_bytes"), "traffic_source": "profiles/r2l_traffic.json",
+           "rollout_frac_of_write_stream": (rg / wpk) if wpk else None,
+           "write_stream_note": "the rollout's bytes are 97% writes (view, dir, reward, done out; 1 B of action in); "
+                                "a write-only stream (torch fill_) reaches the write_stream_GBs figure on this B200 "
+                                "(profiles/r2l_bw.json), the copy peak above counts reads and writes",
+           "write_stream_GBs": wpk,
            "rollout_env_steps_per_s": B * T / (roll * 1e-3), "gae_score_ms": gae, "gae_score_GBs": gg,
            "gae_score_frac": gg / peak, "levels_scored_per_s": B / (gae * 1e-3)}
     del wl
