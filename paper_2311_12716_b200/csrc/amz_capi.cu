@@ -77,6 +77,7 @@ struct amz_env {
 struct amz_plr {
     int device;
     PlrDev D;
+    int32_t *rank = nullptr;  // [K] sampler scratch: rank - 1 of every entry
     UpdScratch W;
     int *err;
 };
@@ -641,6 +642,7 @@ int amz_plr_create(int64_t capacity, amz_plr_t **out) {
     if (e == cudaSuccess) e = cudaMalloc((void **)&b->D.seq, K * 8);
     if (e == cudaSuccess) e = cudaMalloc((void **)&b->D.meta, 2 * 8);
     if (e == cudaSuccess) e = cudaMalloc((void **)&b->err, 4 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&b->rank, K * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMemset(b->D.meta, 0, 16);
     if (e == cudaSuccess) e = cudaMemset(b->err, 0, 4 * sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(b->D.levels, 0, K * sizeof(amz_level_t));
@@ -664,6 +666,7 @@ int amz_plr_destroy(amz_plr_t *b) {
     cudaFree(b->D.seq);
     cudaFree(b->D.meta);
     cudaFree(b->err);
+    cudaFree(b->rank);
     cudaFree(b->W.init_match);
     cudaFree(b->W.twin_first);
     cudaFree(b->W.keyslot);
@@ -692,7 +695,7 @@ int amz_plr_sample(amz_plr_t *b, const amz_seed_t *key, int64_t n, double rho, c
     DevGuard guard_(b->device);
     if (rho < 0.0 || rho > 1.0) return fail(AMZ_ECONFIG, "staleness_coef must be in [0, 1], got %g", rho);
     if (n <= 0) return 0;
-    launch_plr_sample(b->D, *key, n, 1.0 - rho, rho, lut, iter, slots, levels, max_ret, score, b->err,
+    launch_plr_sample(b->D, b->rank, *key, n, 1.0 - rho, rho, lut, iter, slots, levels, max_ret, score, b->err,
                       (cudaStream_t)stream);
     return cuda_status("plr_sample");
 }

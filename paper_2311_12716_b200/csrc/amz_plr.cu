@@ -29,6 +29,21 @@ constexpr int kPlrThreads = 1024;
 constexpr int kPlrMaxK = 4096;
 constexpr int kHash = 8192;  // smem hash table entries (>= 2 * K)
 constexpr int kMaxDevices = 64;
+#ifdef AMZ_PLR_STATS
+__device__ long long g_samp_clk[16];
+#define SAMP_CLK(k_)                                       \
+    do {                                                   \
+        __syncthreads();                                   \
+        if (threadIdx.x == 0) g_samp_clk[k_] = clock64();  \
+    } while (0)
+extern "C" int amz_debug_samp_clk(void *host) {
+    return (int)cudaMemcpyFromSymbol(host, g_samp_clk, sizeof(g_samp_clk));
+}
+#else
+#define SAMP_CLK(k_) \
+    do {             \
+    } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t level_hash(const uint4 &w, uint32_t pose) {
     uint32_t h = 0x9E3779B9u;
@@ -63,105 +78,157 @@ __device__ __forceinline__ bool entry_less(double sa, int64_t la, int64_t qa, do
 }
 
 // ---------------------------------------------------------------------------------
-// numpy pairwise sum of x[0..n) evaluated by a whole CTA (leaves in parallel).
-// Returns the sum in thread 0 (valid after the call in all threads via smem).
+// numpy pairwise sum of x[0..n) (numpy/_core/src/umath/loops_utils.h.src pairwise_sum):
+// n < 8 sequential; n <= 128 eight accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+// then the n % 8 tail; beyond, left half n2 = n/2 rounded down to a multiple of 8, and
+// the result is pw(left) + pw(right).  The recursion tree (<= 127 nodes for n <= 4096)
+// is built level by level by warp 0, the leaves are summed in parallel and the internal
+// nodes evaluated bottom-up -- every node is the same single addition of the same two
+// operands as numpy's recursion, so the result is bit-identical.
 // ---------------------------------------------------------------------------------
-__device__ double block_pairwise_sum(const double *x, int n, double *leafbuf /* >= 64 */, int *leafinfo /* >= 3*64+1 */) {
-    // thread 0 walks numpy's recursion (pw(s, n) = n <= 128 ? leaf : pw(left) + pw(right),
-    // left length n/2 rounded down to a multiple of 8) and records, per leaf, its range
-    // and how many pending sums close after it.
-    if (threadIdx.x == 0) {
-        int fs[24], fn[24], st[24];
-        int fp = 1, nl = 0;
-        fs[0] = 0;
-        fn[0] = n;
-        st[0] = 0;
-        while (fp > 0) {
-            const int i = fp - 1;
-            if (st[i] == 0 && fn[i] <= 128) {
-                leafinfo[1 + 3 * nl] = fs[i];
-                leafinfo[2 + 3 * nl] = fn[i];
-                leafinfo[3 + 3 * nl] = 0;
-                nl++;
-                fp--;
-            } else if (st[i] < 2) {
-                int n2 = fn[i] / 2;
-                n2 -= n2 % 8;
-                const int cs = st[i] == 0 ? fs[i] : fs[i] + n2;
-                const int cn = st[i] == 0 ? n2 : fn[i] - n2;
-                st[i]++;
-                fs[fp] = cs;
-                fn[fp] = cn;
-                st[fp] = 0;
-                fp++;
-            } else {
-                leafinfo[3 + 3 * (nl - 1)]++;
-                fp--;
-            }
-        }
-        leafinfo[0] = nl;
-    }
-    __syncthreads();
-    const int nl = leafinfo[0];
-    for (int li = threadIdx.x; li < nl; li += blockDim.x) {
-        const int s = leafinfo[1 + 3 * li], len = leafinfo[2 + 3 * li];
-        double res;
-        if (len < 8) {
-            res = 0.0;
-            for (int k = 0; k < len; k++) res = res + x[s + k];
-        } else {
-            double r[8];
+constexpr int kPwNodes = 128;
+struct PwTree {
+    int start[kPwNodes], len[kPwNodes], left[kPwNodes], depth[kPwNodes];
+    double val[kPwNodes];
+    int n_nodes, max_depth;
+};
+__device__ __forceinline__ double pw_leaf(const double *x, int s, int len) {
+    double res;
+    if (len < 8) {
+        res = 0.0;
+        for (int k = 0; k < len; k++) res = res + x[s + k];
+    } else {
+        double r[8];
 #pragma unroll
-            for (int k = 0; k < 8; k++) r[k] = x[s + k];
-            int k = 8;
-            const int l8 = len - len % 8;
-            for (; k < l8; k += 8) {
+        for (int k = 0; k < 8; k++) r[k] = x[s + k];
+        int k = 8;
+        const int l8 = len - len % 8;
+        for (; k < l8; k += 8) {
 #pragma unroll
-                for (int j = 0; j < 8; j++) r[j] = r[j] + x[s + k + j];
-            }
-            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-            for (; k < len; k++) res = res + x[s + k];
+            for (int j = 0; j < 8; j++) r[j] = r[j] + x[s + k + j];
         }
-        leafbuf[li] = res;
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; k < len; k++) res = res + x[s + k];
+    }
+    return res;
+}
+// whole CTA; returns the sum in every thread
+__device__ double block_pairwise_sum(const double *x, int n, PwTree &P) {
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        // level-by-level expansion: nodes of one level are contiguous, children appended
+        if (tid == 0) {
+            P.start[0] = 0;
+            P.len[0] = n;
+            P.depth[0] = 0;
+            P.left[0] = -1;
+            P.n_nodes = 1;
+            P.max_depth = 0;
+        }
+        __syncwarp();
+        int lo = 0, hi = 1, d = 0;
+        while (lo < hi) {
+            // count splits of this level (in order) and append their children
+            const int cnt = hi - lo;
+            int base = hi;
+            for (int c0 = 0; c0 < cnt; c0 += 32) {
+                const int i = lo + c0 + tid;
+                const bool split = c0 + tid < cnt && P.len[i] > 128;
+                const unsigned b = __ballot_sync(0xFFFFFFFFu, split);
+                if (split) {
+                    const int k = base + 2 * __popc(b & ((1u << tid) - 1u));
+                    int n2 = P.len[i] / 2;
+                    n2 -= n2 % 8;
+                    P.start[k] = P.start[i];
+                    P.len[k] = n2;
+                    P.start[k + 1] = P.start[i] + n2;
+                    P.len[k + 1] = P.len[i] - n2;
+                    P.depth[k] = P.depth[k + 1] = d + 1;
+                    P.left[k] = P.left[k + 1] = -1;
+                    P.left[i] = k;
+                }
+                base += 2 * __popc(b);
+            }
+            __syncwarp();
+            lo = hi;
+            hi = base;
+            if (hi > lo) d++;
+        }
+        if (tid == 0) {
+            P.n_nodes = hi;
+            P.max_depth = d;
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double stk[40];
-        int sp = 0;
-        for (int li = 0; li < nl; li++) {
-            stk[sp++] = leafbuf[li];
-            for (int a = 0; a < leafinfo[3 + 3 * li]; a++) {
-                double b = stk[--sp];
-                double c = stk[--sp];
-                stk[sp++] = c + b;
-            }
-        }
-        leafbuf[0] = stk[0];
-    }
+    const int nn = P.n_nodes;
+    for (int i = tid; i < nn; i += blockDim.x)
+        if (P.left[i] < 0) P.val[i] = pw_leaf(x, P.start[i], P.len[i]);
     __syncthreads();
-    return leafbuf[0];
+    for (int d = P.max_depth - 1; d >= 0; d--) {
+        for (int i = tid; i < nn; i += blockDim.x)
+            if (P.depth[i] == d && P.left[i] >= 0) P.val[i] = P.val[P.left[i]] + P.val[P.left[i] + 1];
+        __syncthreads();
+    }
+    return P.val[0];
 }
 
 // ---------------------------------------------------------------------------------
 // sampling
+//   1. ranks: one bitonic sort (1024 threads, 78 compare-exchange stages over the next
+//      power of two >= size) by (score desc, seq asc) -- the order numpy's lexsort of
+//      (seq, -score) gives (rank ties -> older insertion first)
+//   2. w = LUT[rank - 1] ((1/rank)^(1/beta), numpy's host LUT)
+//   3. sum(w) in numpy's pairwise order
+//   4. P = (1-rho) w/sum(w) + rho st/sum(st); cdf = sequential cumsum (one thread: it is
+//      numpy's order) while the other warps draw the uniforms u_i = i-th random() of the
+//      key's stream (counter-based: block i/4 of Philox); then cdf /= cdf[-1] and
+//      slot_i = searchsorted(cdf, u_i, 'right')
 // ---------------------------------------------------------------------------------
-#ifndef AMZ_SORT_BITS
-#define AMZ_SORT_BITS 4
-#endif
-using SampleSort = cub::BlockRadixSort<unsigned long long, kPlrThreads, 4, int, AMZ_SORT_BITS>;
+constexpr int kSampU = 4096;  // uniforms precomputed during the cumsum
 struct SampleSmem {
-    typename SampleSort::TempStorage sort;
+    double u[kSampU];  // uniforms of the first kSampU draws
     double p[kPlrMaxK];
-    double leaf[64];
-    int leafinfo[3 * 64 + 4];
+    PwTree pw;
     unsigned long long st_total;
-    unsigned long long seq_min, seq_max;
-    int rank_slot[kPlrMaxK];
 };
 
+// rank - 1 of every entry under (score desc, seq asc) -- numpy's lexsort((seq, -score)),
+// rank ties -> older insertion first -- by direct counting over a 2-D grid: CTA (bi, bj)
+// stages entries [bj*RJ, (bj+1)*RJ) in shared memory and thread i adds the number of them
+// before entry i to rank[i] (zeroed first).  4000^2 comparisons over ~128 CTAs take a few
+// microseconds; a single-CTA sort of the same keys (CUB block radix, 64-bit score keys)
+// was ~45 us and a bitonic network ~80 us.
+constexpr int kRankThreads = 256;
+constexpr int kRankJ = 256;
+__device__ __forceinline__ void rank_keys(const PlrDev &D, int j, uint64_t &k, uint64_t &q) {
+    double sc = D.score[j];
+    sc = sc == 0.0 ? 0.0 : sc;  // -0.0 ties with 0.0, as in numpy's sort
+    const uint64_t u = (uint64_t)__double_as_longlong(sc);
+    k = (u >> 63) ? ~u : (u | 0x8000000000000000ull);  // ascending = score asc
+    q = (uint64_t)D.seq[j] ^ 0x8000000000000000ull;     // signed -> unsigned order
+}
+__global__ void __launch_bounds__(kRankThreads) k_plr_rank(PlrDev D, int32_t *__restrict__ rank) {
+    __shared__ uint64_t sk[kRankJ];
+    __shared__ uint64_t sq[kRankJ];
+    const int size = (int)D.meta[0];
+    const int j0 = blockIdx.y * kRankJ;
+    const int nj = min(kRankJ, size - j0);
+    if (nj <= 0) return;
+    for (int j = threadIdx.x; j < nj; j += blockDim.x) rank_keys(D, j0 + j, sk[j], sq[j]);
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= size) return;
+    uint64_t ki, qi;
+    rank_keys(D, i, ki, qi);
+    int r = 0;
+#pragma unroll 8
+    for (int j = 0; j < nj; j++) r += (sk[j] > ki) | ((sk[j] == ki) & (sq[j] < qi));
+    if (r) atomicAdd(&rank[i], r);
+}
+
 __global__ void __launch_bounds__(kPlrThreads, 1)
-    k_plr_sample(PlrDev D, amz_seed_t key, int64_t n, double one_minus_rho, double rho,
-                 const double *__restrict__ lut, int64_t iter, int32_t *__restrict__ slots_out,
+    k_plr_sample(PlrDev D, const int32_t *__restrict__ rank, amz_seed_t key, int64_t n, double one_minus_rho,
+                 double rho, const double *__restrict__ lut, int64_t iter, int32_t *__restrict__ slots_out,
                  amz_level_t *__restrict__ levels_out, double *__restrict__ maxret_out,
                  double *__restrict__ score_out, int *__restrict__ err) {
     extern __shared__ __align__(16) uint8_t smraw[];
@@ -172,80 +239,23 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         if (tid == 0) atomicOr(err, 2);
         return;
     }
-    // ---- 1. ranks: sort by seq asc, then stable by score desc ----
-    // seq values are distinct and span a narrow range: the first sort only runs over the
-    // bits of (seq - min seq), with the padding keys (all ones) above every valid key
-    using Sort = SampleSort;
-    unsigned long long keys[4];
-    int vals[4];
-    if (tid == 0) {
-        S.seq_min = ~0ull;
-        S.seq_max = 0ull;
-    }
-    __syncthreads();
-    {
-        unsigned long long mn = ~0ull, mx = 0ull;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int i = tid * 4 + k;
-            keys[k] = i < size ? (unsigned long long)D.seq[i] : 0ull;
-            if (i < size) {
-                mn = keys[k] < mn ? keys[k] : mn;
-                mx = keys[k] > mx ? keys[k] : mx;
-            }
-        }
-        atomicMin(&S.seq_min, mn);
-        atomicMax(&S.seq_max, mx);
-    }
-    __syncthreads();
-    const unsigned long long smin = S.seq_min;
-    const int seq_bits = 64 - __clzll((long long)(S.seq_max - smin + 1ull));
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int i = tid * 4 + k;
-        keys[k] = i < size ? keys[k] - smin : ~0ull;
-        vals[k] = i;
-    }
-    Sort(S.sort).Sort(keys, vals, 0, seq_bits < 1 ? 1 : seq_bits);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int i = vals[k];
-        // descending score = ascending bitwise-inverted key; non-negative doubles order like their bits
-        unsigned long long b = 0ull;
-        if (i < size) {
-            double s = D.score[i];
-            s = s == 0.0 ? 0.0 : s;  // -0.0 ties with 0.0, as in numpy's sort
-            unsigned long long u = (unsigned long long)__double_as_longlong(s);
-            // total order for all doubles: flip negatives entirely, positives' sign bit
-            u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-            b = ~u;
-        } else {
-            b = ~0ull;
-        }
-        keys[k] = b;
-    }
-    Sort(S.sort).Sort(keys, vals);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int pos = tid * 4 + k;
-        if (vals[k] < size) S.rank_slot[vals[k]] = pos;  // rank - 1
-    }
+    SAMP_CLK(0);
     if (tid == 0) S.st_total = 0ull;
     __syncthreads();
     // ---- 2./3. weights and their pairwise sum (slot order) ----
     unsigned long long my_st = 0ull;
     for (int i = tid; i < size; i += blockDim.x) {
-        S.p[i] = lut[S.rank_slot[i]];
+        S.p[i] = lut[rank[i]];
         my_st += (unsigned long long)(iter - D.last[i]);
     }
-    // staleness total (exact integer sum)
     for (int o = 16; o > 0; o >>= 1) my_st += __shfl_down_sync(0xFFFFFFFFu, my_st, o);
     if ((tid & 31) == 0) atomicAdd(&S.st_total, my_st);
-    const double wsum = block_pairwise_sum(S.p, size, S.leaf, S.leafinfo);
+    __syncthreads();
+    SAMP_CLK(4);
+    const double wsum = block_pairwise_sum(S.p, size, S.pw);
     const long long tot = (long long)S.st_total;
-    // ---- 4. P, cdf ----
+    SAMP_CLK(5);
+    // ---- 4. P ----
     for (int i = tid; i < size; i += blockDim.x) {
         const double ps = S.p[i] / wsum;
         if (tot == 0) {
@@ -256,6 +266,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         }
     }
     __syncthreads();
+    SAMP_CLK(6);
+    uint64_t k0, k1;
+    seed_key(key, k0, k1);
+    const int nu = n < kSampU ? (int)n : kSampU;
     if (tid == 0) {
         // numpy's sequential cumsum; the next 16 loads are issued ahead of this block's
         // stores so only the add chain is serial
@@ -277,20 +291,37 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 #pragma unroll
             for (int j = 0; j < CB; j++) cur[j] = nxt[j];
         }
+    } else if ((tid >> 5) & 3) {
+        // meanwhile: the first nu uniforms, one Philox block per 4 draws, on the warps of
+        // the other three schedulers (warp 0's scheduler stays free for the add chain)
+        const int w = tid >> 5, q0 = (w - 1 - (w >> 2)) * 32 + (tid & 31), nw = 24 * 32;
+        for (int q = q0; q < (nu + 3) / 4; q += nw) {
+            uint64_t o[4];
+            philox_block((uint64_t)q + 1ull, k0, k1, o[0], o[1], o[2], o[3]);
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (4 * q + j < nu) S.u[4 * q + j] = (double)(o[j] >> 11) * (1.0 / 9007199254740992.0);
+        }
     }
     __syncthreads();
+    SAMP_CLK(7);
     const double last_cdf = S.p[size - 1];
     __syncthreads();
     for (int i = tid; i < size; i += blockDim.x) S.p[i] = S.p[i] / last_cdf;
     __syncthreads();
+    SAMP_CLK(8);
     // ---- draws ----
-    uint64_t k0, k1;
-    seed_key(key, k0, k1);
     for (int64_t d = tid; d < n; d += blockDim.x) {
-        uint64_t o[4];
-        philox_block((uint64_t)(d >> 2) + 1ull, k0, k1, o[0], o[1], o[2], o[3]);
-        const uint64_t r = o[d & 3];
-        const double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
+        double u;
+        if (d < nu) {
+            u = S.u[d];
+        } else {
+            uint64_t o0, o1, o2, o3;
+            philox_block((uint64_t)(d >> 2) + 1ull, k0, k1, o0, o1, o2, o3);
+            const int j = (int)(d & 3);
+            const uint64_t r = j == 0 ? o0 : j == 1 ? o1 : j == 2 ? o2 : o3;
+            u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
+        }
         // searchsorted(cdf, u, side='right'): first index with cdf[idx] > u
         int lo = 0, hi = size;
         while (lo < hi) {
@@ -307,8 +338,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         if (score_out) score_out[d] = D.score[slot];
     }
     __syncthreads();
+    SAMP_CLK(9);
     // sampled entries: last_sampled = iter (after every probability used the old values)
     for (int64_t d = tid; d < n; d += blockDim.x) D.last[slots_out[d]] = iter;
+    SAMP_CLK(10);
 }
 
 // ---------------------------------------------------------------------------------
@@ -1326,9 +1359,9 @@ int launch_plr_digest(const PlrDev &D, int64_t *out, cudaStream_t s) {
 size_t plr_sample_smem() { return sizeof(SampleSmem); }
 size_t plr_update_smem() { return sizeof(UpdSmem); }
 
-int launch_plr_sample(const PlrDev &D, const amz_seed_t &key, int64_t n, double omr, double rho, const double *lut,
-                      int64_t iter, int32_t *slots, amz_level_t *levels, double *maxret, double *score, int *err,
-                      cudaStream_t s) {
+int launch_plr_sample(const PlrDev &D, int32_t *rank, const amz_seed_t &key, int64_t n, double omr, double rho,
+                      const double *lut, int64_t iter, int32_t *slots, amz_level_t *levels, double *maxret,
+                      double *score, int *err, cudaStream_t s) {
     static bool attr[kMaxDevices] = {};  // the attribute is per device
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1336,8 +1369,11 @@ int launch_plr_sample(const PlrDev &D, const amz_seed_t &key, int64_t n, double 
         cudaFuncSetAttribute(k_plr_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SampleSmem));
         if (dev < kMaxDevices) attr[dev] = true;
     }
-    k_plr_sample<<<1, kPlrThreads, sizeof(SampleSmem), s>>>(D, key, n, omr, rho, lut, iter, slots, levels, maxret,
-                                                             score, err);
+    cudaMemsetAsync(rank, 0, (size_t)D.K * sizeof(int32_t), s);
+    k_plr_rank<<<dim3((unsigned)((D.K + kRankThreads - 1) / kRankThreads), (unsigned)((D.K + kRankJ - 1) / kRankJ)),
+                 kRankThreads, 0, s>>>(D, rank);
+    k_plr_sample<<<1, kPlrThreads, sizeof(SampleSmem), s>>>(D, rank, key, n, omr, rho, lut, iter, slots, levels,
+                                                             maxret, score, err);
     return 0;
 }
 
