@@ -377,7 +377,7 @@ constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses th
 #ifdef AMZ_PLR_STATS
 // [0] sequential candidates (warp 0), [1] of them in place, [2] bulk runs, [3] bulk
 // candidates, [4] insert_runs calls, [5] insert passes, [6] candidates consumed by runs,
-// [7] relevant candidates, [8] calls
+// [7] relevant candidates, [8] calls, [9] bottom-cache rebuilds
 __device__ unsigned long long g_plr_stats[16];
 #define PLR_STAT(k_, v_) atomicAdd(&g_plr_stats[k_], (unsigned long long)(v_))
 extern "C" int amz_debug_plr_stats(void *host, int reset) {
@@ -401,6 +401,7 @@ struct CandChunk {
     int32_t tf[kChunk];
     int32_t im[kChunk];
 };
+
 // Insert runs (whole CTA): relevant candidates from r0 on that are certainly new (no key
 // match at kernel start, first of their key in the batch), until the first one that is
 // not.  With free slots as virtual entries of score -inf (evicted in slot order) the
@@ -439,11 +440,10 @@ struct SortedEntries {
     uint64_t ekey[kPlrMaxK];  // score keys of the buffer (virtual free slots = 0), eviction order
     int32_t eslot[kPlrMaxK];
 };
+constexpr int kCache = 64;  // bottom cache entries (two per lane of warp 0)
 struct UpdSmem {
-    uint64_t hk[kPlrMaxK];  // heap: order-preserving score key (score_key)
-    uint64_t ht[kPlrMaxK];  // heap: relative tie key (last - lmin) << bq | (seq - qmin)
-    int hslot[kPlrMaxK];    // heap entry -> buffer slot
-    int pos[kPlrMaxK];      // buffer slot -> heap entry
+    uint64_t key[kPlrMaxK];  // slot -> order-preserving score key (score_key)
+    uint64_t tie[kPlrMaxK];  // slot -> relative tie key (last - lmin) << bq | (seq - qmin)
     union {
         uint32_t hash[kHash];
         CandChunk chunk;
@@ -458,6 +458,15 @@ struct UpdSmem {
         SortedEntries e;
     } r1;
     uint32_t evicted[kRunM / 32];  // insert run: acceptances evicted again inside the pass
+    // bottom cache: the kCache smallest (key, tie) entries of the buffer (warp 0 keeps it
+    // in registers while it replays candidates; rebuilt by the CTA when invalid)
+    int cslot[kCache];
+    uint64_t ckey[kCache];
+    uint64_t ctie[kCache];
+    uint8_t sel[kPlrMaxK];  // cache rebuild: selected slots
+    int hist[256];
+    int sel_b, sel_below, sel_cnt;
+    int cvalid;
     double mlow;
     int64_t next_seq;
     int64_t lmin, qmin, lmax, qmax, last_max0;
@@ -467,7 +476,7 @@ struct UpdSmem {
     int full;
     int size;
     int rcur;      // next chunk position for warp 0
-    int action;    // 0 = chunk done, 1 = bulk in-place run [rcur, arg), 2 = insert run [rcur, rcur + arg)
+    int action;    // 0 = chunk done, 1 = bulk in-place run [rcur, arg), 2 = insert run, 3 = rebuild the cache
     int arg;
     int run_ok;
     int flag_first;
@@ -492,11 +501,8 @@ __device__ __forceinline__ uint64_t tie_pack(const UpdSmem &S, int64_t last, int
     const uint64_t q = (uint64_t)seq - (uint64_t)S.qmin;
     return S.bq >= 64 ? q : ((((uint64_t)last - (uint64_t)S.lmin) << S.bq) | q);
 }
-__device__ __forceinline__ void heap_put(UpdSmem &S, int h, uint64_t k, uint64_t t, int slot) {
-    S.hk[h] = k;
-    S.ht[h] = t;
-    S.hslot[h] = slot;
-    S.pos[slot] = h;
+__device__ __forceinline__ bool ukey_le(uint64_t ka, uint64_t ta, uint64_t kb, uint64_t tb) {
+    return ka < kb || (ka == kb && ta <= tb);
 }
 // lanes whose bit is set in `eq` compete; narrows `eq` to the lanes holding the minimum of v
 __device__ __forceinline__ unsigned warp_argmin_word(unsigned eq, uint32_t v, int lane) {
@@ -504,90 +510,137 @@ __device__ __forceinline__ unsigned warp_argmin_word(unsigned eq, uint32_t v, in
     const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, in ? v : 0xFFFFFFFFu);
     return __ballot_sync(0xFFFFFFFFu, in && v == m);
 }
-// 64-ary min-heap (children of h are 64h+1 .. 64h+64; up to 4160 entries -> 2 levels below
-// the root).  The entry x = (xk, xt, xs) is sifted from the hole h: at each level lane l
-// loads children 64h+1+2l and 64h+2+2l and keeps the smaller, then a ballot of "child < x"
-// and a redux arg-min over the lanes; the winning lane moves its child into the hole.
-// Whole warp, uniform control flow.
-__device__ __forceinline__ void sift_down_w(UpdSmem &S, int h, int n, uint64_t xk, uint64_t xt, int xs, int lane) {
-    while (true) {
-        const int c0 = 64 * h + 1 + 2 * lane;
-        uint64_t ck = ~0ull, ct = ~0ull;
-        int cs = 0, cc = c0;
-        const bool valid = c0 < n;
-        if (valid) {
-            ck = S.hk[c0];
-            ct = S.ht[c0];
-            cs = S.hslot[c0];
-            if (c0 + 1 < n) {
-                const uint64_t k1 = S.hk[c0 + 1], t1 = S.ht[c0 + 1];
-                if (ukey_lt(k1, t1, ck, ct)) {
-                    ck = k1;
-                    ct = t1;
-                    cs = S.hslot[c0 + 1];
-                    cc = c0 + 1;
-                }
+// The lane holding the lexicographic minimum (or, with mx, maximum) of (k, t) among the
+// lanes with `has`, or -1.  (key, tie) pairs are unique, so the winner is unique.
+__device__ __forceinline__ int warp_lex_pick(bool has, uint64_t k, uint64_t t, bool mx, int lane) {
+    unsigned eq = __ballot_sync(0xFFFFFFFFu, has);
+    if (!eq) return -1;
+    const uint64_t kk = mx ? ~k : k, tt = mx ? ~t : t;
+    eq = warp_argmin_word(eq, (uint32_t)(kk >> 32), lane);
+    if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)kk, lane);
+    if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)(tt >> 32), lane);
+    if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)tt, lane);
+    return __ffs(eq) - 1;
+}
+
+// The bottom cache in warp 0's registers: lane l holds entries l (.0) and l + 32 (.1);
+// slot < 0 = free.  Invariant while valid: every buffer entry outside the cache is
+// larger than the cache maximum (cmk, cmt), and the cache is not empty.
+struct BottomCache {
+    int s0, s1;
+    uint64_t k0, k1, t0, t1;
+    uint64_t mk, mt;  // maximum (uniform)
+    bool valid;       // uniform
+
+    __device__ __forceinline__ void load(const UpdSmem &S, int lane) {
+        s0 = S.cslot[lane];
+        s1 = S.cslot[lane + 32];
+        k0 = S.ckey[lane];
+        k1 = S.ckey[lane + 32];
+        t0 = S.ctie[lane];
+        t1 = S.ctie[lane + 32];
+        valid = S.cvalid != 0;
+        if (valid) refresh_max(lane);
+    }
+    __device__ __forceinline__ void store(UpdSmem &S, int lane) const {
+        S.cslot[lane] = s0;
+        S.cslot[lane + 32] = s1;
+        S.ckey[lane] = k0;
+        S.ckey[lane + 32] = k1;
+        S.ctie[lane] = t0;
+        S.ctie[lane + 32] = t1;
+        if (lane == 0) S.cvalid = valid ? 1 : 0;
+    }
+    // this lane's extreme of its two entries (mx: maximum); which = 0 / 1
+    __device__ __forceinline__ bool local(bool mx, uint64_t &k, uint64_t &t, int &which) const {
+        const bool a = s0 >= 0, b = s1 >= 0;
+        if (a && (!b || (mx ? !ukey_le(k0, t0, k1, t1) : ukey_le(k0, t0, k1, t1)))) {
+            k = k0;
+            t = t0;
+            which = 0;
+        } else {
+            k = k1;
+            t = t1;
+            which = 1;
+        }
+        return a || b;
+    }
+    // recompute the maximum; an empty cache becomes invalid
+    __device__ __forceinline__ void refresh_max(int lane) {
+        uint64_t k, t;
+        int w;
+        const bool has = local(true, k, t, w);
+        const int win = warp_lex_pick(has, k, t, true, lane);
+        if (win < 0) {
+            valid = false;
+            return;
+        }
+        mk = __shfl_sync(0xFFFFFFFFu, k, win);
+        mt = __shfl_sync(0xFFFFFFFFu, t, win);
+    }
+    // the minimum entry: its slot, key and (lane, which)
+    __device__ __forceinline__ int argmin(int lane, uint64_t &mink, int &wl, int &ww) const {
+        uint64_t k, t;
+        int w;
+        const bool has = local(false, k, t, w);
+        wl = warp_lex_pick(has, k, t, false, lane);
+        ww = __shfl_sync(0xFFFFFFFFu, w, wl);
+        mink = __shfl_sync(0xFFFFFFFFu, k, wl);
+        const int sl = ww ? s1 : s0;
+        return __shfl_sync(0xFFFFFFFFu, sl, wl);
+    }
+    __device__ __forceinline__ void remove_at(int wl, int ww, int lane) {
+        if (lane == wl) {
+            if (ww)
+                s1 = -1;
+            else
+                s0 = -1;
+        }
+    }
+    // the entry holding slot s: (lane, which), or lane -1
+    __device__ __forceinline__ void find(int s, int &wl, int &ww) const {
+        const unsigned f0 = __ballot_sync(0xFFFFFFFFu, s0 == s), f1 = __ballot_sync(0xFFFFFFFFu, s1 == s);
+        if (f0) {
+            wl = __ffs(f0) - 1;
+            ww = 0;
+        } else if (f1) {
+            wl = __ffs(f1) - 1;
+            ww = 1;
+        } else {
+            wl = -1;
+            ww = 0;
+        }
+    }
+    // insert (s, k, t) <= the maximum; a full cache first drops its maximum (which then
+    // lies outside, above the new maximum)
+    __device__ __forceinline__ void insert(int s, uint64_t k, uint64_t t, int lane) {
+        unsigned f0 = __ballot_sync(0xFFFFFFFFu, s0 < 0), f1 = __ballot_sync(0xFFFFFFFFu, s1 < 0);
+        if (!(f0 | f1)) {
+            uint64_t xk, xt;
+            int w;
+            local(true, xk, xt, w);
+            const int win = warp_lex_pick(true, xk, xt, true, lane);
+            const int ww = __shfl_sync(0xFFFFFFFFu, w, win);
+            remove_at(win, ww, lane);
+            f0 = __ballot_sync(0xFFFFFFFFu, s0 < 0);
+            f1 = __ballot_sync(0xFFFFFFFFu, s1 < 0);
+        }
+        const int wl = f0 ? __ffs(f0) - 1 : __ffs(f1) - 1;
+        const int ww = f0 ? 0 : 1;
+        if (lane == wl) {
+            if (ww) {
+                s1 = s;
+                k1 = k;
+                t1 = t;
+            } else {
+                s0 = s;
+                k0 = k;
+                t0 = t;
             }
         }
-        unsigned eq = __ballot_sync(0xFFFFFFFFu, valid && ukey_lt(ck, ct, xk, xt));
-        if (eq == 0u) break;
-        eq = warp_argmin_word(eq, (uint32_t)(ck >> 32), lane);
-        if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)ck, lane);
-        if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)(ct >> 32), lane);
-        if (__popc(eq) > 1) eq = warp_argmin_word(eq, (uint32_t)ct, lane);
-        const int win = __ffs(eq) - 1;
-        if (lane == win) heap_put(S, h, ck, ct, cs);
-        h = __shfl_sync(0xFFFFFFFFu, cc, win);
+        refresh_max(lane);
     }
-    if (lane == 0) heap_put(S, h, xk, xt, xs);
-    __syncwarp();
-}
-__device__ __forceinline__ void sift_up_w(UpdSmem &S, int h, uint64_t xk, uint64_t xt, int xs, int lane) {
-    while (h > 0) {
-        const int p = (h - 1) >> 6;
-        const uint64_t pk = S.hk[p], pt = S.ht[p];
-        if (!ukey_lt(xk, xt, pk, pt)) break;
-        const int ps = S.hslot[p];
-        if (lane == 0) heap_put(S, h, pk, pt, ps);
-        h = p;
-    }
-    if (lane == 0) heap_put(S, h, xk, xt, xs);
-    __syncwarp();
-}
-// one thread (heapify: disjoint subtrees per level)
-__device__ __forceinline__ void heap_down_t(UpdSmem &S, int h, int n) {
-    const uint64_t xk = S.hk[h], xt = S.ht[h];
-    const int xs = S.hslot[h];
-    while (true) {
-        const int c0 = 64 * h + 1;
-        if (c0 >= n) break;
-        const int ce = c0 + 64 < n ? c0 + 64 : n;
-        int m = c0;
-        uint64_t mk = S.hk[c0], mt = S.ht[c0];
-        for (int c = c0 + 1; c < ce; c++) {
-            const uint64_t k = S.hk[c], t = S.ht[c];
-            if (ukey_lt(k, t, mk, mt)) {
-                m = c;
-                mk = k;
-                mt = t;
-            }
-        }
-        if (!ukey_lt(mk, mt, xk, xt)) break;
-        heap_put(S, h, mk, mt, S.hslot[m]);
-        h = m;
-    }
-    heap_put(S, h, xk, xt, xs);
-}
-// whole CTA: rebuild the heap property over entries [0, n) (level starts 0, 1, 65, 4161)
-__device__ __forceinline__ void heapify_cta(UpdSmem &S, int n) {
-    const int starts[4] = {0, 1, 65, 4161};
-    for (int lv = 2; lv >= 0; lv--) {
-        __syncthreads();
-        const int l0 = starts[lv], l1 = min(starts[lv + 1], n);
-        for (int h = l0 + (int)threadIdx.x; h < l1; h += blockDim.x) heap_down_t(S, h, n);
-    }
-    __syncthreads();
-}
+};
 
 // the buffer slot candidate r of the staged chunk updates in place, or -1
 __device__ __forceinline__ int cand_present(const UpdSmem &S, const UpdScratch &W, int r) {
@@ -670,6 +723,91 @@ __device__ __forceinline__ int block_excl_count(bool flag, int &excl, int *wscan
     return tot;
 }
 
+// Whole CTA: the kCache smallest (key, tie) among slots [0, n) into the cache arrays, by
+// a most-significant-digit radix select over the 128-bit values (8-bit digits; stops as
+// soon as the remaining bucket fits exactly).
+__device__ void cache_rebuild(UpdSmem &S, int n, int *wscan) {
+    const int tid = threadIdx.x;
+    const int c = n < kCache ? n : kCache;
+    uint64_t pk = 0, pt = 0, mk = 0, mt = 0;  // prefix value / mask of the bytes fixed so far
+    int need = c;
+    for (int i = tid; i < n; i += blockDim.x) S.sel[i] = 0;
+    __syncthreads();
+    for (int d = 15; d >= 0 && need > 0; d--) {
+        for (int i = tid; i < 256; i += blockDim.x) S.hist[i] = 0;
+        __syncthreads();
+        const int sh = 8 * (d & 7);
+        for (int i = tid; i < n; i += blockDim.x) {
+            if (S.sel[i]) continue;
+            const uint64_t k = S.key[i], t = S.tie[i];
+            if ((k & mk) != pk || (t & mt) != pt) continue;
+            atomicAdd(&S.hist[(int)(((d >= 8 ? k : t) >> sh) & 0xFFu)], 1);
+        }
+        __syncthreads();
+        if (tid < 32) {  // bucket b holding the need-th value
+            int v[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                v[j] = S.hist[tid * 8 + j];
+                tot += v[j];
+            }
+            int inc = tot;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+                if (tid >= o) inc += y;
+            }
+            int before = inc - tot;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if (before < need && before + v[j] >= need) {
+                    S.sel_b = tid * 8 + j;
+                    S.sel_below = before;
+                    S.sel_cnt = v[j];
+                }
+                before += v[j];
+            }
+        }
+        __syncthreads();
+        const int b = S.sel_b, below = S.sel_below, cnt = S.sel_cnt;
+        const uint64_t byte = (uint64_t)b << sh;
+        for (int i = tid; i < n; i += blockDim.x) {  // buckets below b are in
+            if (S.sel[i]) continue;
+            const uint64_t k = S.key[i], t = S.tie[i];
+            if ((k & mk) != pk || (t & mt) != pt) continue;
+            const int bb = (int)(((d >= 8 ? k : t) >> sh) & 0xFFu);
+            if (bb < b || (bb == b && cnt == need - below)) S.sel[i] = 1;
+        }
+        if (d >= 8) {
+            pk |= byte;
+            mk |= 0xFFull << sh;
+        } else {
+            pt |= byte;
+            mt |= 0xFFull << sh;
+        }
+        need = cnt == need - below ? 0 : need - below;
+        __syncthreads();
+    }
+    // compact the selected slots into the cache
+    for (int i = tid; i < kCache; i += blockDim.x) S.cslot[i] = -1;
+    __syncthreads();
+    int off = 0;
+    for (int base = 0; base < n; base += blockDim.x) {
+        const int i = base + tid;
+        const bool in = i < n && S.sel[i];
+        int e = 0;
+        const int tot = block_excl_count(in, e, wscan);
+        if (in) {
+            S.cslot[off + e] = i;
+            S.ckey[off + e] = S.key[i];
+            S.ctie[off + e] = S.tie[i];
+        }
+        off += tot;
+    }
+    __syncthreads();
+    if (tid == 0) S.cvalid = c > 0 ? 1 : 0;
+    __syncthreads();
+}
+
 __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__restrict__ cscore, int64_t iter,
                            int r0, int rend, int E, int *wscan) {
     // E = buffer capacity K: sort items [0, E) are the buffer (stored + virtual free
@@ -684,9 +822,9 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
         unsigned long long tmax = 0ull;
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            const int i = tid * 4 + k;  // heap position for i < size0, free slot i otherwise
-            keys[k] = i < size0 ? S.ht[i] : (unsigned long long)i;  // virtual: slot order
-            vals[k] = i < size0 ? S.hslot[i] : i;
+            const int i = tid * 4 + k;  // slot (stored for i < size0, free otherwise)
+            keys[k] = i < size0 ? S.tie[i] : (unsigned long long)i;  // virtual: slot order
+            vals[k] = i;
             tmax = keys[k] > tmax ? keys[k] : tmax;
         }
         if (tid == 0) S.tie_max = 0ull;
@@ -699,7 +837,7 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const int slot = vals[k];
-            keys[k] = slot < size0 ? S.hk[S.pos[slot]] : (slot < E ? 0ull : ~0ull);
+            keys[k] = slot < size0 ? S.key[slot] : (slot < E ? 0ull : ~0ull);
         }
         RunSort(S.r1.sort).Sort(keys, vals);
         __syncthreads();
@@ -849,8 +987,8 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
                     continue;
                 }
                 const int slot = R.aslot[j];
-                const int h = slot < size_cur ? S.pos[slot] : slot;  // free slots fill heap positions in order
-                heap_put(S, h, R.lk[li], tie_pack(S, iter, seq0 + j), slot);
+                S.key[slot] = R.lk[li];
+                S.tie[slot] = tie_pack(S, iter, seq0 + j);
                 S.owner[slot] = cj;
                 S.src[slot] = cj;
                 S.mr_src[slot] = cj;
@@ -924,7 +1062,8 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
         }
     }
     __syncthreads();
-    heapify_cta(S, S.size);
+    if (tid == 0) S.cvalid = 0;  // the bottom cache is rebuilt when next needed
+    __syncthreads();
     return pos - r0;
 }
 
@@ -1030,10 +1169,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     double my_min = __longlong_as_double(0x7FF0000000000000ll);  // +inf
     for (int i = tid; i < size0; i += blockDim.x) {
         const double sc = D.score[i];
-        S.hk[i] = score_key(sc);
-        S.ht[i] = tie_pack(S, D.last[i], D.seq[i]);
-        S.hslot[i] = i;
-        S.pos[i] = i;
+        S.key[i] = score_key(sc);
+        S.tie[i] = tie_pack(S, D.last[i], D.seq[i]);
         my_min = fmin(my_min, sc);
         uint4 w;
         uint32_t p0, p1;
@@ -1071,8 +1208,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         for (int k = 1; k < (int)(blockDim.x >> 5); k++) m = fmin(m, wmin[k]);
         S.mlow = m;
     }
-    // ---- heapify, level-parallel (all sift-downs of one level touch disjoint subtrees) ----
-    heapify_cta(S, size0);
+    if (tid == 0) S.cvalid = 0;
+    __syncthreads();
     // ---- B: relevant candidates, compacted in order (block-wide, chunk by chunk) ----
     for (int64_t base = 0; base < n; base += blockDim.x) {
         const int64_t c = base + tid;
@@ -1121,6 +1258,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             int64_t next_seq = S.next_seq;
             const bool run_ok = S.run_ok > 0;
             int r = 0, scan_end = 0, pscan_end = 0, action = 0, arg = 0;
+            BottomCache bc;
+            bc.load(S, lane);
             // candidate fields are prefetched one ahead (the replaced bit and the twin's
             // keyslot are read after the previous candidate is applied)
             int c_n = 0, f_n = 0, im_n = -1;
@@ -1167,31 +1306,63 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 if (lane == 0) PLR_STAT(0, 1);
                 if (present >= 0) {
                     if (lane == 0) PLR_STAT(1, 1);  // identical level: score / max_return in place (tb unchanged)
-                    const int h = S.pos[present];
-                    const uint64_t ok = S.hk[h], ot = S.ht[h];
+                    const int s2 = present;
+                    const uint64_t st = S.tie[s2];
                     __syncwarp();
-                    if (lane == 0) S.mr_src[present] = c;
-                    if (sk < ok)
-                        sift_up_w(S, h, sk, ot, present, lane);
-                    else if (sk > ok)
-                        sift_down_w(S, h, size, sk, ot, present, lane);
+                    if (lane == 0) {
+                        S.key[s2] = sk;
+                        S.mr_src[s2] = c;
+                    }
+                    if (bc.valid) {  // keep the bottom cache exact
+                        int wl, ww;
+                        bc.find(s2, wl, ww);
+                        const bool low = ukey_le(sk, st, bc.mk, bc.mt);
+                        if (wl >= 0) {
+                            if (lane == wl) {
+                                if (ww)
+                                    bc.k1 = sk;
+                                else
+                                    bc.k0 = sk;
+                            }
+                            if (!low) bc.remove_at(wl, ww, lane);  // it rose above the cache: outside now
+                            bc.refresh_max(lane);
+                        } else if (low) {
+                            bc.insert(s2, sk, st, lane);
+                        }
+                    }
                     __syncwarp();
                     continue;
                 }
                 const uint64_t tbn = tie_pack(S, iter, next_seq);
                 int slot;
                 if (size < K) {  // fill
-                    slot = size;
-                    const int h = size++;
+                    slot = size++;
                     __syncwarp();
-                    sift_up_w(S, h, sk, tbn, slot, lane);
+                    if (lane == 0) {
+                        S.key[slot] = sk;
+                        S.tie[slot] = tbn;
+                    }
+                    if (bc.valid && ukey_le(sk, tbn, bc.mk, bc.mt)) bc.insert(slot, sk, tbn, lane);
                 } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
-                    if (!(sk > S.hk[0])) continue;
-                    slot = S.hslot[0];
+                    if (!bc.valid) {  // the CTA rebuilds the cache, then this candidate again
+                        action = 3;
+                        break;
+                    }
+                    uint64_t mink;
+                    int wl, ww;
+                    const int ms = bc.argmin(lane, mink, wl, ww);
+                    if (!(sk > mink)) continue;
+                    slot = ms;
                     const int ow = S.owner[slot];
                     __syncwarp();
-                    if (lane == 0 && ow >= 0) W.keyslot[ow] = -1;
-                    sift_down_w(S, 0, size, sk, tbn, slot, lane);
+                    if (lane == 0) {
+                        if (ow >= 0) W.keyslot[ow] = -1;
+                        S.key[slot] = sk;
+                        S.tie[slot] = tbn;
+                    }
+                    bc.remove_at(wl, ww, lane);
+                    bc.refresh_max(lane);  // empty -> invalid (rebuilt before the next eviction)
+                    if (bc.valid && ukey_le(sk, tbn, bc.mk, bc.mt)) bc.insert(slot, sk, tbn, lane);
                 }
                 if (lane == 0) {
                     S.owner[slot] = f;
@@ -1204,6 +1375,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 next_seq++;
             }
             __syncwarp();
+            bc.store(S, lane);
             if (lane == 0) {
                 S.size = size;
                 S.next_seq = next_seq;
@@ -1218,6 +1390,12 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             base += cn;
             continue;
         }
+        if (action == 3) {  // the bottom cache: the kCache smallest entries, by radix select
+            if (tid == 0) PLR_STAT(9, 1);
+            cache_rebuild(S, S.size, wscan);
+            base += lo;
+            continue;
+        }
         if (action == 1) {  // bulk in-place run [lo, arg)
             if (tid == 0) {
                 PLR_STAT(2, 1);
@@ -1229,9 +1407,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             __syncthreads();
             for (int i = lo + tid; i < hi; i += blockDim.x) {
                 const int p = cand_present(S, W, i);
-                if (S.mr_src[p] == S.u.chunk.cid[i]) S.hk[S.pos[p]] = score_key(S.u.chunk.sc[i]);
+                if (S.mr_src[p] == S.u.chunk.cid[i]) S.key[p] = score_key(S.u.chunk.sc[i]);
             }
-            heapify_cta(S, S.size);
+            __syncthreads();
+            if (tid == 0) S.cvalid = 0;
             base += hi;
             continue;
         }
@@ -1246,12 +1425,11 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         }
     }
     __syncthreads();
-    // ---- epilogue: scatter the heap back to slots, deferred level / max_return copies ----
+    // ---- epilogue: tie keys back to last_sampled / seq, deferred level / max_return copies ----
     const int fsize = S.size;
     const uint64_t qmask = S.bq >= 64 ? ~0ull : ((1ull << S.bq) - 1ull);
-    for (int h = tid; h < fsize; h += blockDim.x) {
-        const int slot = S.hslot[h];
-        const uint64_t tb = S.ht[h];
+    for (int slot = tid; slot < fsize; slot += blockDim.x) {
+        const uint64_t tb = S.tie[slot];
         D.last[slot] = (int64_t)((S.bq >= 64 ? 0ull : (tb >> S.bq)) + (uint64_t)S.lmin);
         D.seq[slot] = (int64_t)((tb & qmask) + (uint64_t)S.qmin);
         if (S.src[slot] >= 0) D.levels[slot] = cand[S.src[slot]];

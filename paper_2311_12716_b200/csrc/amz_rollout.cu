@@ -30,6 +30,9 @@
 #ifndef AMZ_DYN8_MINB
 #define AMZ_DYN8_MINB 3
 #endif
+#ifndef AMZ_DYN8_TRACK
+#define AMZ_DYN8_TRACK false
+#endif
 #ifndef AMZ_DYN2_MINB
 #define AMZ_DYN2_MINB 1
 #endif
@@ -392,6 +395,9 @@ __device__ __forceinline__ void build_move_table(const uint32_t *board, int L, u
 template <int LPW>
 struct DynOcc {
     static constexpr int kMinBlocks = LPW >= 8 ? AMZ_DYN8_MINB : (LPW <= 2 ? AMZ_DYN2_MINB : 1);
+    // sampler variant: element tracking (lowest latency) where the per-warp chain bounds
+    // the rollout; swap-list read-off (fewest instructions) in the many-wave large batch
+    static constexpr bool kTrack = LPW >= 8 ? AMZ_DYN8_TRACK : true;
 };
 template <int LPW, int WPC>
 __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions, int mode,
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G
                     }
                     DYN_ACC2(1, c_key);
                     DYN_T0(c_smp);
-                    warp_sample_each<true>(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
+                    warp_sample_each<DynOcc<LPW>::kTrack>(need, k0, k1, G, S.samp, m, ar, acol, ad, gr, gc);
                     DYN_ACC(5, c_smp);
 #ifdef AMZ_DYN_PROF
                     if (lane == 0) g_dyn_prof[(int64_t)blockIdx.x * WPC + warp][7] += __popc(need);
