@@ -561,9 +561,11 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_step": e32_ms / args.steps, "host_enqueue_ms_per_step": host32_ms,
                 "inputs": "actions u8 [T, B] + values f32 [T, B] + last values f32 [B] (the policy's output dtype, "
                           "widened to f64 in-kernel like the reference's value.double(), agents/ppo.py:96)",
-                "mode": "DRIterationGraph(host_io=True): one graph replay per step; its H2D of the NEXT step's pinned "
-                        "inputs runs on two side branches (two DMA engines) concurrent with this step's kernels, the "
-                        "D2H of scores | max returns ends the replay; one timed region over all K steps",
+                "mode": "DRIterationGraph(host_io=True): one graph replay per step; the H2D of the NEXT step's "
+                        "pinned inputs is a copy kernel (amz_copy_h2d: reads the pinned buffer through its unified "
+                        "address) on a side branch forked after the reset kernel, concurrent with the dynamics / "
+                        "render / GAE kernels; the D2H of scores | max returns ends the replay; one timed region over "
+                        "all K steps",
                 "l2": "not flushed between e2e steps: every step's inputs are copied fresh from pinned host memory and "
                       "its 54 MB of outputs overwrite the previous step's (with_l2_flush: a 256 MB write before every "
                       "step, inside the timed region)",

@@ -228,6 +228,11 @@ int amz_env_rollout_iter(amz_env_t *env, int T, const uint8_t *actions_dev, cons
                          const uint32_t *iter_dev, uint8_t *view_dev, uint8_t *dir_dev, double *reward_dev,
                          uint8_t *done_dev, uint8_t *final_view_dev, uint8_t *final_dir_dev, void *stream);
 int amz_iter_advance(uint32_t *iter_dev, uint32_t by, void *stream);
+/* Host -> device copy by a kernel (`ctas` CTAs of 256 threads, 0 = 64) reading pinned host
+ * memory (amz_host_alloc) through its unified address: the input feed of a captured
+ * DR-iteration graph (graph.DRIterationGraph), at the PCIe link rate beside the step's
+ * kernels.  Both buffers 16-byte aligned. */
+int amz_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int ctas, void *stream);
 
 int amz_env_observe(amz_env_t *env, uint8_t *view_dev, int64_t *dir_dev, void *stream);
 

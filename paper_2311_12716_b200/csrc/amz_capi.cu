@@ -418,6 +418,14 @@ int amz_env_reset_dr_iter(amz_env_t *e, const amz_seed_t *root, const uint32_t *
     return cuda_status("env_reset_dr_iter");
 }
 
+int amz_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int ctas, void *stream) {
+    if (!dst_dev || !src_host) return fail(AMZ_ECONFIG, "null argument");
+    if ((((uintptr_t)dst_dev) | ((uintptr_t)src_host)) & 15u) return fail(AMZ_ECONFIG, "copy buffers must be 16-byte aligned");
+    if (bytes == 0) return 0;
+    launch_copy_h2d(dst_dev, src_host, bytes, ctas > 0 ? ctas : 64, (cudaStream_t)stream);
+    return cuda_status("copy_h2d");
+}
+
 int amz_iter_advance(uint32_t *iter_dev, uint32_t by, void *stream) {
     if (!iter_dev) return fail(AMZ_ECONFIG, "null argument");
     launch_iter_advance(iter_dev, by, (cudaStream_t)stream);

@@ -405,6 +405,36 @@ int launch_env_reset(const Geo &G, const EnvDev &E, const amz_level_t *lv, const
 
 __global__ void k_iter_advance(uint32_t *iter, uint32_t by) { *iter += by; }
 
+// Host -> device copy of pinned host memory by a kernel reading it through its unified
+// address (16-byte loads across PCIe, many in flight).  Used for the per-step input feed
+// of a captured graph: a memcpy node whose source is host memory made the driver read
+// that buffer at ~23 GB/s (eager and graph alike, once captured), this kernel moves it at
+// the link rate, concurrently with the step's kernels.
+__global__ void __launch_bounds__(256) k_copy_h2d(uint4 *__restrict__ dst, const uint4 *__restrict__ src, int64_t n16,
+                                                 uint8_t *__restrict__ dst_tail, const uint8_t *__restrict__ src_tail,
+                                                 int tail) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {  // four 16-byte loads in flight per thread
+        const uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+        dst[i] = a;
+        dst[i + stride] = b;
+        dst[i + 2 * stride] = c;
+        dst[i + 3 * stride] = d;
+    }
+    for (; i < n16; i += stride) dst[i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
+}
+
+int launch_copy_h2d(void *dst, const void *src, size_t bytes, int ctas, cudaStream_t s) {
+    const int64_t n16 = (int64_t)(bytes / 16);
+    const int tail = (int)(bytes - (size_t)n16 * 16);
+    k_copy_h2d<<<ctas, 256, 0, s>>>(reinterpret_cast<uint4 *>(dst), reinterpret_cast<const uint4 *>(src), n16,
+                                    reinterpret_cast<uint8_t *>(dst) + n16 * 16,
+                                    reinterpret_cast<const uint8_t *>(src) + n16 * 16, tail);
+    return 0;
+}
+
 int launch_iter_advance(uint32_t *iter, uint32_t by, cudaStream_t s) {
     k_iter_advance<<<1, 1, 0, s>>>(iter, by);
     return 0;

@@ -74,6 +74,7 @@ int launch_teacher_levels(int64_t B, const uint4 *mask, const uint4 *st, amz_lev
 int launch_policy_head(const void *logits, int dtype, int64_t B, int A, uint64_t k0, uint64_t k1,
                        const amz_seed_t *prefix_dev, const uint32_t *step_dev, int greedy, int64_t lane0, int64_t *act64,
                        uint8_t *act8, double *logp, cudaStream_t s);
+int launch_copy_h2d(void *dst, const void *src, size_t bytes, int ctas, cudaStream_t s);
 int launch_iter_advance(uint32_t *iter, uint32_t by, cudaStream_t s);
 int launch_env_reset_dr(const Geo &G, const EnvDev &E, const amz_seed_t &prefix, const amz_seed_t *wrap,
                         amz_level_t *spec, uint32_t *spec_step, uint8_t *view, int64_t *dirs, cudaStream_t s);

@@ -51,7 +51,7 @@ class DRIterationGraph:
 
     def __init__(self, benv: VectorBatchEnv, root_rng, T: int, params, gamma: float, lam: float,
                  score_fn: str = "maxmc", value_dtype=None, host_io: bool = False, overlap: bool = True,
-                 copy_streams: int = 1):
+                 copy_streams: int = 1, copy_ctas: int = 64):
         torch = _torch()
         if not isinstance(benv, VectorBatchEnv):
             raise ContractViolation("DRIterationGraph needs a VectorBatchEnv")
@@ -67,7 +67,8 @@ class DRIterationGraph:
         self.root_pfx = self.root.seed_prefix()
         self.host_io = host_io
         self.overlap = overlap and host_io
-        self.copy_streams = max(1, min(2, int(copy_streams)))
+        self.copy_streams = 1
+        self.copy_ctas = int(copy_ctas)
         T, B, dev, v = self.T, self.B, self.dev, self.p.agent_view_size
         self.it_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.next_it = 0
@@ -101,13 +102,18 @@ class DRIterationGraph:
         self._pending_h2d = False
 
     # -- one step's kernels on the current stream ------------------------------------
-    def _kernels(self, inp):
+    def _kernels(self, inp, after_reset=None):
+        """The step's kernels on the current stream; ``after_reset()`` runs right after the
+        reset kernel is enqueued (the overlapped input copy forks there: the reset fills
+        every SM's register file, the dynamics kernel leaves room beside it)."""
         torch = self.torch
         lanes = self.benv._ensure(self.p)
         o = self.out
         st = lanes.stream()
         _lib.call("amz_env_reset_dr_iter", lanes.handle, ctypes.byref(self.root_pfx), _lib.ptr(self.it_dev),
                   _lib.ptr(o["reset_view"]), _lib.ptr(o["reset_dir"]), st)
+        if after_reset is not None:
+            after_reset()
         _lib.call("amz_env_rollout_iter", lanes.handle, self.T, _lib.ptr(inp["actions"]), ctypes.byref(self.root_pfx),
                   _lib.ptr(self.it_dev), _lib.ptr(o["view"]), _lib.ptr(o["dir"]), _lib.ptr(o["rewards"]),
                   _lib.ptr(o["dones"]), _lib.ptr(o["final_view"]), _lib.ptr(o["final_dir"]), st)
@@ -122,22 +128,14 @@ class DRIterationGraph:
                 "actions": raw[nv + nl:].view(T, B)}
 
     def _h2d(self, k, streams=None):
-        """Copy the pinned staging into input slot k: two halves, one per copy stream
-        (two DMA engines) when ``streams`` are given, else on the current stream."""
+        """Copy the pinned staging into input slot k with ``amz_copy_h2d`` (a kernel
+        reading the pinned buffer through its unified address: measured 46 GB/s, where a
+        graph memcpy node from the same host buffer ran at 19-50 GB/s from one box to the
+        next), on the given side stream (or the current one)."""
         torch = self.torch
-        dst, src = self._raw[k], self._host_raw
-        half = (self._nbytes // 2) & ~15
-        if streams is None or len(streams) == 1:
-            if streams is None:
-                dst.copy_(src, non_blocking=True)
-            else:
-                with torch.cuda.stream(streams[0]):
-                    dst.copy_(src, non_blocking=True)
-            return
-        for i, st in enumerate(streams):
-            with torch.cuda.stream(st):
-                sl = slice(0, half) if i == 0 else slice(half, self._nbytes)
-                dst[sl].copy_(src[sl], non_blocking=True)
+        st = streams[0] if streams else torch.cuda.current_stream(self.dev)
+        _lib.call("amz_copy_h2d", self._raw[k].data_ptr(), self._host_raw.data_ptr(), self._nbytes, self.copy_ctas,
+                  st.cuda_stream)
 
     def capture(self):
         """Warm up (allocates the rollout scratch) and capture the graph(s)."""
@@ -156,14 +154,16 @@ class DRIterationGraph:
                     cur = torch.cuda.current_stream(self.dev)
                     if self.host_io and not self.overlap:
                         self._h2d(k)
+                    sides = []
                     if self.overlap:
-                        # next step's inputs on two side branches (two DMA engines),
-                        # concurrent with this step's kernels
-                        sides = [torch.cuda.Stream(device=self.dev) for _ in range(self.copy_streams)]
-                        for sd in sides:
-                            sd.wait_stream(cur)
-                        self._h2d(k ^ 1, sides)
-                    self._kernels(self.inputs[k])
+                        # the next step's inputs on a side branch forked after the reset,
+                        # concurrent with the dynamics / render / GAE kernels
+                        sides = [torch.cuda.Stream(device=self.dev, priority=-5)]
+
+                        def fork(k=k, sides=sides, cur=cur):
+                            sides[0].wait_stream(cur)
+                            self._h2d(k ^ 1, sides)
+                    self._kernels(self.inputs[k], fork if self.overlap else None)
                     if self.host_io:
                         self.host_result.copy_(self.res, non_blocking=True)
                     if self.overlap:
