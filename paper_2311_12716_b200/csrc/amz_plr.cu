@@ -377,7 +377,7 @@ constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses th
 #ifdef AMZ_PLR_STATS
 // [0] sequential candidates (warp 0), [1] of them in place, [2] bulk runs, [3] bulk
 // candidates, [4] insert_runs calls, [5] insert passes, [6] candidates consumed by runs,
-// [7] relevant candidates, [8] calls, [9] bottom-cache rebuilds
+// [7] relevant candidates, [8] calls, [9] bottom-cache rebuilds, [10] warp-batched in-place candidates
 __device__ unsigned long long g_plr_stats[16];
 #define PLR_STAT(k_, v_) atomicAdd(&g_plr_stats[k_], (unsigned long long)(v_))
 extern "C" int amz_debug_plr_stats(void *host, int reset) {
@@ -464,6 +464,7 @@ struct UpdSmem {
     uint64_t ckey[kCache];
     uint64_t ctie[kCache];
     uint8_t sel[kPlrMaxK];  // cache rebuild: selected slots
+    uint8_t incache[kPlrMaxK];  // slot is in the bottom cache (meaningful while cvalid)
     int hist[256];
     int sel_b, sel_below, sel_cnt;
     int cvalid;
@@ -531,8 +532,10 @@ struct BottomCache {
     uint64_t k0, k1, t0, t1;
     uint64_t mk, mt;  // maximum (uniform)
     bool valid;       // uniform
+    uint8_t *flag;    // UpdSmem::incache
 
-    __device__ __forceinline__ void load(const UpdSmem &S, int lane) {
+    __device__ __forceinline__ void load(UpdSmem &S, int lane) {
+        flag = S.incache;
         s0 = S.cslot[lane];
         s1 = S.cslot[lane + 32];
         k0 = S.ckey[lane];
@@ -591,6 +594,7 @@ struct BottomCache {
     }
     __device__ __forceinline__ void remove_at(int wl, int ww, int lane) {
         if (lane == wl) {
+            flag[ww ? s1 : s0] = 0;
             if (ww)
                 s1 = -1;
             else
@@ -628,6 +632,7 @@ struct BottomCache {
         const int wl = f0 ? __ffs(f0) - 1 : __ffs(f1) - 1;
         const int ww = f0 ? 0 : 1;
         if (lane == wl) {
+            flag[s] = 1;
             if (ww) {
                 s1 = s;
                 k1 = k;
@@ -731,7 +736,10 @@ __device__ void cache_rebuild(UpdSmem &S, int n, int *wscan) {
     const int c = n < kCache ? n : kCache;
     uint64_t pk = 0, pt = 0, mk = 0, mt = 0;  // prefix value / mask of the bytes fixed so far
     int need = c;
-    for (int i = tid; i < n; i += blockDim.x) S.sel[i] = 0;
+    for (int i = tid; i < kPlrMaxK; i += blockDim.x) {
+        S.sel[i] = 0;
+        S.incache[i] = 0;
+    }
     __syncthreads();
     for (int d = 15; d >= 0 && need > 0; d--) {
         for (int i = tid; i < 256; i += blockDim.x) S.hist[i] = 0;
@@ -800,6 +808,7 @@ __device__ void cache_rebuild(UpdSmem &S, int n, int *wscan) {
             S.cslot[off + e] = i;
             S.ckey[off + e] = S.key[i];
             S.ctie[off + e] = S.tie[i];
+            S.incache[i] = 1;
         }
         off += tot;
     }
@@ -1271,6 +1280,48 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 im_n = S.u.chunk.im[r];
             }
             for (; r < cn; r++) {
+                // Warp-batched fast path: the leading stretch of "simple" candidates -- in
+                // place (key present), slot outside the bottom cache and new key above the
+                // cache maximum -- changes neither presence nor the cache, so the stretch
+                // is applied at once (the last candidate per slot wins)
+                {
+                    const int i = r + lane;
+                    bool simple = false;
+                    int ps = -1, ci = 0;
+                    uint64_t ski = 0;
+                    if (i < cn) {
+                        ci = S.u.chunk.cid[i];
+                        const int imi = S.u.chunk.im[i], fi = S.u.chunk.tf[i];
+                        if (imi >= 0 && !((S.replaced[imi >> 5] >> (imi & 31)) & 1u))
+                            ps = imi;
+                        else if (fi != ci)
+                            ps = W.keyslot[fi];
+                        if (ps >= 0) {
+                            ski = score_key(S.u.chunk.sc[i]);
+                            simple = !bc.valid || (!S.incache[ps] && !ukey_le(ski, S.tie[ps], bc.mk, bc.mt));
+                        }
+                    }
+                    const unsigned bad = ~__ballot_sync(0xFFFFFFFFu, simple);
+                    const int k = bad ? __ffs(bad) - 1 : 32;
+                    if (k > 0) {
+                        const bool act = lane < k;
+                        const unsigned grp = __match_any_sync(0xFFFFFFFFu, act ? ps : -1 - lane);
+                        if (act && 31 - __clz(grp) == lane) {  // last writer of its slot
+                            S.key[ps] = ski;
+                            S.mr_src[ps] = ci;
+                        }
+                        if (lane == 0) PLR_STAT(10, k);
+                        __syncwarp();
+                        r += k - 1;  // the loop's r++ moves past the stretch
+                        if (r + 1 < cn) {
+                            c_n = S.u.chunk.cid[r + 1];
+                            sc_n = S.u.chunk.sc[r + 1];
+                            f_n = S.u.chunk.tf[r + 1];
+                            im_n = S.u.chunk.im[r + 1];
+                        }
+                        continue;
+                    }
+                }
                 const int c = c_n, f = f_n, im = im_n;
                 const double sc = sc_n;
                 if (r + 1 < cn) {

@@ -26,7 +26,7 @@ last = torch.rand((L,), generator=g, device="cuda", dtype=torch.float64) * 0.2
 fn = _lib.lib().amz_debug_plr_stats
 buf = (ctypes.c_ulonglong * 16)()
 names = ["seq", "seq_inplace", "bulk_runs", "bulk_cands", "insert_calls", "insert_passes", "run_cands", "relevant",
-         "calls", "cache_rebuilds"]
+         "calls", "cache_rebuilds", "batched"]
 for it in range(6):
     fn(buf, 1)
     r = plr.iteration(it, acts, vals, last)
