@@ -377,13 +377,15 @@ constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses th
 #ifdef AMZ_PLR_STATS
 // [0] sequential candidates (warp 0), [1] of them in place, [2] bulk runs, [3] bulk
 // candidates, [4] insert_runs calls, [5] insert passes, [6] candidates consumed by runs,
-// [7] relevant candidates, [8] calls, [9] bottom-cache rebuilds, [10] warp-batched in-place candidates
-__device__ unsigned long long g_plr_stats[16];
+// [7] relevant candidates, [8] calls, [9] bottom-cache rebuilds, [10] warp-batched candidates,
+// [11] cycles of phase B, [12] cycles of phase C, [13] batch steps, [14] cycles in batch steps
+__device__ unsigned long long g_plr_stats[32];
 #define PLR_STAT(k_, v_) atomicAdd(&g_plr_stats[k_], (unsigned long long)(v_))
+#define PLR_CLK(v_) const long long v_ = clock64()
 extern "C" int amz_debug_plr_stats(void *host, int reset) {
     int rc = (int)cudaMemcpyFromSymbol(host, g_plr_stats, sizeof(g_plr_stats));
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[32] = {};
         cudaMemcpyToSymbol(g_plr_stats, z, sizeof(z));
     }
     return rc;
@@ -391,6 +393,9 @@ extern "C" int amz_debug_plr_stats(void *host, int reset) {
 #else
 #define PLR_STAT(k_, v_) \
     do {                 \
+    } while (0)
+#define PLR_CLK(v_) \
+    do {            \
     } while (0)
 #endif
 constexpr int kRunMin = 96;   // shorter insert runs stay on the sequential warp path
@@ -526,11 +531,18 @@ __device__ __forceinline__ int warp_lex_pick(bool has, uint64_t k, uint64_t t, b
 
 // The bottom cache in warp 0's registers: lane l holds entries l (.0) and l + 32 (.1);
 // slot < 0 = free.  Invariant while valid: every buffer entry outside the cache is
-// larger than the cache maximum (cmk, cmt), and the cache is not empty.
+// larger than the cache maximum, and the cache is not empty.  The maximum and the
+// minimum (value and position) are kept as warp-uniform state, so an eviction reads
+// its victim without a warp reduction and only the operations that remove an extreme
+// pay one (warp_lex_pick).
 struct BottomCache {
     int s0, s1;
     uint64_t k0, k1, t0, t1;
-    uint64_t mk, mt;  // maximum (uniform)
+    uint64_t mk, mt;  // maximum (uniform) ...
+    int xl, xw;       // ... at lane xl, entry xw
+    uint64_t nk, nt;  // minimum (uniform) ...
+    int nl, nw, ns;   // ... at lane nl, entry nw, buffer slot ns
+    int n;            // entries (uniform)
     bool valid;       // uniform
     uint8_t *flag;    // UpdSmem::incache
 
@@ -543,7 +555,14 @@ struct BottomCache {
         t0 = S.ctie[lane];
         t1 = S.ctie[lane + 32];
         valid = S.cvalid != 0;
-        if (valid) refresh_max(lane);
+        mk = mt = nk = nt = 0;
+        xl = xw = nl = nw = 0;
+        ns = -1;
+        n = __popc(__ballot_sync(0xFFFFFFFFu, s0 >= 0)) + __popc(__ballot_sync(0xFFFFFFFFu, s1 >= 0));
+        if (valid) {
+            refresh_max(lane);
+            refresh_min(lane);
+        }
     }
     __device__ __forceinline__ void store(UpdSmem &S, int lane) const {
         S.cslot[lane] = s0;
@@ -568,29 +587,25 @@ struct BottomCache {
         }
         return a || b;
     }
-    // recompute the maximum; an empty cache becomes invalid
+    // recompute the maximum / minimum of a non-empty cache
     __device__ __forceinline__ void refresh_max(int lane) {
         uint64_t k, t;
         int w;
         const bool has = local(true, k, t, w);
-        const int win = warp_lex_pick(has, k, t, true, lane);
-        if (win < 0) {
-            valid = false;
-            return;
-        }
-        mk = __shfl_sync(0xFFFFFFFFu, k, win);
-        mt = __shfl_sync(0xFFFFFFFFu, t, win);
+        xl = warp_lex_pick(has, k, t, true, lane);
+        mk = __shfl_sync(0xFFFFFFFFu, k, xl);
+        mt = __shfl_sync(0xFFFFFFFFu, t, xl);
+        xw = __shfl_sync(0xFFFFFFFFu, w, xl);
     }
-    // the minimum entry: its slot, key and (lane, which)
-    __device__ __forceinline__ int argmin(int lane, uint64_t &mink, int &wl, int &ww) const {
+    __device__ __forceinline__ void refresh_min(int lane) {
         uint64_t k, t;
         int w;
         const bool has = local(false, k, t, w);
-        wl = warp_lex_pick(has, k, t, false, lane);
-        ww = __shfl_sync(0xFFFFFFFFu, w, wl);
-        mink = __shfl_sync(0xFFFFFFFFu, k, wl);
-        const int sl = ww ? s1 : s0;
-        return __shfl_sync(0xFFFFFFFFu, sl, wl);
+        nl = warp_lex_pick(has, k, t, false, lane);
+        nk = __shfl_sync(0xFFFFFFFFu, k, nl);
+        nt = __shfl_sync(0xFFFFFFFFu, t, nl);
+        nw = __shfl_sync(0xFFFFFFFFu, w, nl);
+        ns = __shfl_sync(0xFFFFFFFFu, w ? s1 : s0, nl);
     }
     __device__ __forceinline__ void remove_at(int wl, int ww, int lane) {
         if (lane == wl) {
@@ -600,6 +615,15 @@ struct BottomCache {
             else
                 s0 = -1;
         }
+        n--;
+    }
+    // drop the minimum (its slot is being evicted); an emptied cache becomes invalid
+    __device__ __forceinline__ void pop_min(int lane) {
+        remove_at(nl, nw, lane);
+        if (n == 0)
+            valid = false;
+        else
+            refresh_min(lane);  // the maximum is another entry: unchanged
     }
     // the entry holding slot s: (lane, which), or lane -1
     __device__ __forceinline__ void find(int s, int &wl, int &ww) const {
@@ -615,20 +639,12 @@ struct BottomCache {
             ww = 0;
         }
     }
-    // insert (s, k, t) <= the maximum; a full cache first drops its maximum (which then
-    // lies outside, above the new maximum)
+    // insert (s, k, t) below the maximum; a full cache first drops its maximum (which
+    // then lies outside, above the new maximum)
     __device__ __forceinline__ void insert(int s, uint64_t k, uint64_t t, int lane) {
-        unsigned f0 = __ballot_sync(0xFFFFFFFFu, s0 < 0), f1 = __ballot_sync(0xFFFFFFFFu, s1 < 0);
-        if (!(f0 | f1)) {
-            uint64_t xk, xt;
-            int w;
-            local(true, xk, xt, w);
-            const int win = warp_lex_pick(true, xk, xt, true, lane);
-            const int ww = __shfl_sync(0xFFFFFFFFu, w, win);
-            remove_at(win, ww, lane);
-            f0 = __ballot_sync(0xFFFFFFFFu, s0 < 0);
-            f1 = __ballot_sync(0xFFFFFFFFu, s1 < 0);
-        }
+        const bool drop = n == 2 * 32;
+        if (drop) remove_at(xl, xw, lane);
+        const unsigned f0 = __ballot_sync(0xFFFFFFFFu, s0 < 0), f1 = __ballot_sync(0xFFFFFFFFu, s1 < 0);
         const int wl = f0 ? __ffs(f0) - 1 : __ffs(f1) - 1;
         const int ww = f0 ? 0 : 1;
         if (lane == wl) {
@@ -643,7 +659,46 @@ struct BottomCache {
                 t0 = t;
             }
         }
-        refresh_max(lane);
+        n++;
+        if (drop) refresh_max(lane);
+        if (ukey_le(k, t, nk, nt)) {  // the new minimum
+            nk = k;
+            nt = t;
+            nl = wl;
+            nw = ww;
+            ns = s;
+        }
+    }
+    // the cached entry (wl, ww) of slot s takes key k (its tie t unchanged): it stays if
+    // still below the maximum, else it leaves the cache
+    __device__ __forceinline__ void rekey(int s, int wl, int ww, uint64_t k, uint64_t t, int lane) {
+        const bool was_max = wl == xl && ww == xw, was_min = wl == nl && ww == nw;
+        if (ukey_le(k, t, mk, mt)) {
+            if (lane == wl) {
+                if (ww)
+                    k1 = k;
+                else
+                    k0 = k;
+            }
+            if (was_max) refresh_max(lane);
+            if (was_min) {
+                refresh_min(lane);
+            } else if (ukey_le(k, t, nk, nt)) {
+                nk = k;
+                nt = t;
+                nl = wl;
+                nw = ww;
+                ns = s;
+            }
+        } else {  // rose above the maximum: outside now
+            remove_at(wl, ww, lane);
+            if (n == 0) {
+                valid = false;
+                return;
+            }
+            if (was_max) refresh_max(lane);
+            if (was_min) refresh_min(lane);
+        }
     }
 };
 
@@ -1219,6 +1274,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     }
     if (tid == 0) S.cvalid = 0;
     __syncthreads();
+    PLR_CLK(clk_b);
     // ---- B: relevant candidates, compacted in order (block-wide, chunk by chunk) ----
     for (int64_t base = 0; base < n; base += blockDim.x) {
         const int64_t c = base + tid;
@@ -1237,6 +1293,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     // A skipped first occurrence is never inserted (score <= mlow), so its later twins,
     // which are always relevant, correctly find no entry for the key (keyslot = -1).
 
+    PLR_CLK(clk_c);
+    if (tid == 0) PLR_STAT(11, clk_c - clk_b);
     // ---- C: ordered replay (warp 0); bulk in-place runs and insert runs by the CTA ----
     // In-place updates never change which later candidates find their key (only fills and
     // evictions do), so warp 0 scans ahead for the run of consecutive in-place candidates
@@ -1262,6 +1320,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             S.u.chunk.im[i] = W.init_match[c];
         }
         __syncthreads();
+        PLR_CLK(clk_w0);
         if (tid < 32) {
             int size = S.size;
             int64_t next_seq = S.next_seq;
@@ -1279,16 +1338,32 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 f_n = S.u.chunk.tf[r];
                 im_n = S.u.chunk.im[r];
             }
+#ifdef AMZ_PLR_STATS
+            long long clk_sc = 0;
+#endif
             for (; r < cn; r++) {
+#ifdef AMZ_PLR_STATS
+                if (clk_sc && lane == 0) {
+                    PLR_STAT(20, clock64() - clk_sc);
+                    PLR_STAT(21, 1);
+                }
+                clk_sc = 0;
+#endif
+                int present;  // candidate r's in-place slot or -1 (lane 0 of the batch probe)
                 // Warp-batched fast path: the leading stretch of "simple" candidates -- in
                 // place (key present), slot outside the bottom cache and new key above the
                 // cache maximum -- changes neither presence nor the cache, so the stretch
                 // is applied at once (the last candidate per slot wins)
                 {
+                    PLR_CLK(clk_bt);
                     const int i = r + lane;
                     bool simple = false;
                     int ps = -1, ci = 0;
                     uint64_t ski = 0;
+                    // an absent key is certainly rejected (a no-op) when the buffer is full and
+                    // its score does not beat the cache minimum, which no simple op changes
+                    const bool rej_ok = bc.valid && size >= K;
+                    const uint64_t mink = bc.nk;
                     if (i < cn) {
                         ci = S.u.chunk.cid[i];
                         const int imi = S.u.chunk.im[i], fi = S.u.chunk.tf[i];
@@ -1296,21 +1371,27 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                             ps = imi;
                         else if (fi != ci)
                             ps = W.keyslot[fi];
-                        if (ps >= 0) {
-                            ski = score_key(S.u.chunk.sc[i]);
+                        ski = score_key(S.u.chunk.sc[i]);
+                        if (ps >= 0)
                             simple = !bc.valid || (!S.incache[ps] && !ukey_le(ski, S.tie[ps], bc.mk, bc.mt));
-                        }
+                        else
+                            simple = rej_ok && !(ski > mink);
                     }
+                    present = __shfl_sync(0xFFFFFFFFu, ps, 0);
                     const unsigned bad = ~__ballot_sync(0xFFFFFFFFu, simple);
                     const int k = bad ? __ffs(bad) - 1 : 32;
                     if (k > 0) {
-                        const bool act = lane < k;
+                        const bool act = lane < k && ps >= 0;  // rejected absent keys change nothing
                         const unsigned grp = __match_any_sync(0xFFFFFFFFu, act ? ps : -1 - lane);
                         if (act && 31 - __clz(grp) == lane) {  // last writer of its slot
                             S.key[ps] = ski;
                             S.mr_src[ps] = ci;
                         }
-                        if (lane == 0) PLR_STAT(10, k);
+                        if (lane == 0) {
+                            PLR_STAT(10, k);
+                            PLR_STAT(13, 1);
+                            PLR_STAT(14, clock64() - clk_bt);
+                        }
                         __syncwarp();
                         r += k - 1;  // the loop's r++ moves past the stretch
                         if (r + 1 < cn) {
@@ -1322,6 +1403,9 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                         continue;
                     }
                 }
+#ifdef AMZ_PLR_STATS
+                clk_sc = clock64();
+#endif
                 const int c = c_n, f = f_n, im = im_n;
                 const double sc = sc_n;
                 if (r + 1 < cn) {
@@ -1340,12 +1424,11 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     }
                     pscan_end = r + L;
                 }
-                int present = -1;
-                if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) present = im;
-                if (present < 0 && f != c) present = W.keyslot[f];
                 // only an in-place candidate can open a run worth applying in bulk
                 if (present >= 0 && r >= scan_end) {
+                    PLR_CLK(clk_ir);
                     const int L = inplace_run(S, W, r, cn, lane);
+                    if (lane == 0) PLR_STAT(15, clock64() - clk_ir);
                     if (L >= kBulkRun) {
                         action = 1;
                         arg = r + L;
@@ -1355,6 +1438,12 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 }
                 const uint64_t sk = score_key(sc);
                 if (lane == 0) PLR_STAT(0, 1);
+#ifdef AMZ_PLR_STATS
+                if (lane == 0) PLR_STAT(22, clock64() - clk_sc);
+#endif
+#ifdef AMZ_PLR_STATS
+                const long long clk_body = clock64();
+#endif
                 if (present >= 0) {
                     if (lane == 0) PLR_STAT(1, 1);  // identical level: score / max_return in place (tb unchanged)
                     const int s2 = present;
@@ -1367,21 +1456,15 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     if (bc.valid) {  // keep the bottom cache exact
                         int wl, ww;
                         bc.find(s2, wl, ww);
-                        const bool low = ukey_le(sk, st, bc.mk, bc.mt);
-                        if (wl >= 0) {
-                            if (lane == wl) {
-                                if (ww)
-                                    bc.k1 = sk;
-                                else
-                                    bc.k0 = sk;
-                            }
-                            if (!low) bc.remove_at(wl, ww, lane);  // it rose above the cache: outside now
-                            bc.refresh_max(lane);
-                        } else if (low) {
+                        if (wl >= 0)
+                            bc.rekey(s2, wl, ww, sk, st, lane);
+                        else if (ukey_le(sk, st, bc.mk, bc.mt))
                             bc.insert(s2, sk, st, lane);
-                        }
                     }
                     __syncwarp();
+#ifdef AMZ_PLR_STATS
+                    if (lane == 0) PLR_STAT(23, clock64() - clk_body);
+#endif
                     continue;
                 }
                 const uint64_t tbn = tie_pack(S, iter, next_seq);
@@ -1394,14 +1477,19 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                         S.tie[slot] = tbn;
                     }
                     if (bc.valid && ukey_le(sk, tbn, bc.mk, bc.mt)) bc.insert(slot, sk, tbn, lane);
+#ifdef AMZ_PLR_STATS
+                    if (lane == 0) { PLR_STAT(24, clock64() - clk_body); PLR_STAT(25, 1); }
+#endif
                 } else {  // evict the (score, last_sampled, seq) minimum iff strictly better
                     if (!bc.valid) {  // the CTA rebuilds the cache, then this candidate again
                         action = 3;
                         break;
                     }
-                    uint64_t mink;
-                    int wl, ww;
-                    const int ms = bc.argmin(lane, mink, wl, ww);
+                    const uint64_t mink = bc.nk;
+                    const int ms = bc.ns;
+#ifdef AMZ_PLR_STATS
+                    if (lane == 0) { PLR_STAT(26, clock64() - clk_body); PLR_STAT(27, 1); }
+#endif
                     if (!(sk > mink)) continue;
                     slot = ms;
                     const int ow = S.owner[slot];
@@ -1411,9 +1499,11 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                         S.key[slot] = sk;
                         S.tie[slot] = tbn;
                     }
-                    bc.remove_at(wl, ww, lane);
-                    bc.refresh_max(lane);  // empty -> invalid (rebuilt before the next eviction)
+                    bc.pop_min(lane);  // empty -> invalid (rebuilt before the next eviction)
                     if (bc.valid && ukey_le(sk, tbn, bc.mk, bc.mt)) bc.insert(slot, sk, tbn, lane);
+#ifdef AMZ_PLR_STATS
+                    if (lane == 0) { PLR_STAT(28, clock64() - clk_body); PLR_STAT(29, 1); }
+#endif
                 }
                 if (lane == 0) {
                     S.owner[slot] = f;
@@ -1436,6 +1526,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             }
         }
         __syncthreads();
+        if (tid == 0) {
+            PLR_STAT(16, clock64() - clk_w0);
+            PLR_STAT(17, 1);
+        }
         const int lo = S.rcur, action = S.action, arg = S.arg;
         if (action == 0) {
             base += cn;
@@ -1443,7 +1537,9 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         }
         if (action == 3) {  // the bottom cache: the kCache smallest entries, by radix select
             if (tid == 0) PLR_STAT(9, 1);
+            PLR_CLK(clk_rb);
             cache_rebuild(S, S.size, wscan);
+            if (tid == 0) PLR_STAT(18, clock64() - clk_rb);
             base += lo;
             continue;
         }
@@ -1467,7 +1563,9 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         }
         // insert run [base + lo, base + lo + arg)
         {
+            PLR_CLK(clk_in);
             const int used = insert_runs(S, W, cscore, iter, base + lo, nrel, K, wscan);
+            if (tid == 0) PLR_STAT(19, clock64() - clk_in);
             if (tid == 0) {
                 PLR_STAT(4, 1);
                 PLR_STAT(6, used);
@@ -1476,6 +1574,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         }
     }
     __syncthreads();
+    PLR_CLK(clk_e);
+    if (tid == 0) PLR_STAT(12, clk_e - clk_c);
     // ---- epilogue: tie keys back to last_sampled / seq, deferred level / max_return copies ----
     const int fsize = S.size;
     const uint64_t qmask = S.bq >= 64 ? ~0ull : ((1ull << S.bq) - 1ull);
