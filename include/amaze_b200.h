@@ -101,10 +101,12 @@ int amz_abi_version(void);
 const char *amz_last_error(void);
 int amz_validate_params(const amz_params_t *p);
 
-/* Pinned host staging memory (cudaHostAlloc, portable) for the trajectory feed: the
- * host->device copies of actions/values run at full PCIe rate from it (the reference
- * keeps these arrays in numpy memory, agents/rollout.py:19-70).  Free with
- * amz_host_free.  bytes = 0 gives NULL. */
+/* Pinned host staging memory for the trajectory feed (the reference keeps these arrays
+ * in numpy memory, agents/rollout.py:19-70): 2 MB transparent-huge-page mappings
+ * registered with cudaHostRegister (portable), falling back to cudaHostAlloc; the
+ * host->device copies run at the PCIe rate from it where CPU-written 4 KB pinned pages
+ * read at a quarter to a half of it.  AMZ_HOST_ALLOC=cuda forces cudaHostAlloc.  Free
+ * with amz_host_free.  bytes = 0 gives NULL. */
 int amz_host_alloc(size_t bytes, void **out);
 int amz_host_free(void *p);
 
@@ -233,6 +235,10 @@ int amz_iter_advance(uint32_t *iter_dev, uint32_t by, void *stream);
  * DR-iteration graph (graph.DRIterationGraph), at the PCIe link rate beside the step's
  * kernels.  Both buffers 16-byte aligned. */
 int amz_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int ctas, void *stream);
+/* Device -> host by the same kernel (`ctas` CTAs, 0 = 8) storing into pinned host memory
+ * through its unified address: the result read-back of a captured DR-iteration graph
+ * without a copy-engine node (which would queue behind the next step's H2D). */
+int amz_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int ctas, void *stream);
 
 int amz_env_observe(amz_env_t *env, uint8_t *view_dev, int64_t *dir_dev, void *stream);
 

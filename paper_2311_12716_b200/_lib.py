@@ -69,6 +69,7 @@ _SIGS = {
     "amz_env_rollout_iter": ([P, I32, P, ctypes.POINTER(AmzSeed), P, P, P, P, P, P, P, VP], I32),
     "amz_iter_advance": ([P, U32, VP], I32),
     "amz_copy_h2d": ([P, P, ctypes.c_size_t, I32, VP], I32),
+    "amz_copy_d2h": ([P, P, ctypes.c_size_t, I32, VP], I32),
     "amz_env_observe": ([P, P, P, VP], I32),
     "amz_env_levels": ([P, P, VP], I32),
     "amz_env_state": ([P, P, VP], I32),

@@ -2,9 +2,13 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
+#include <sys/mman.h>
 
+#include <mutex>
 #include <new>
+#include <unordered_map>
 
 #include "amz_internal.h"
 
@@ -132,10 +136,47 @@ int amz_validate_params(const amz_params_t *p) {
     return 0;
 }
 
+// Pinned host memory.  Preferred: an anonymous mapping backed by 2 MB transparent huge
+// pages, registered with cudaHostRegister.  On the B200 hosts measured, the GPU reads
+// CPU-written cudaHostAlloc (4 KB) pages at 11-25 GB/s (copy engine / copy kernel) while
+// the same bytes on 2 MB pages stream at 49-53 GB/s: each 4 KB page costs the DMA path a
+// translation.  Falls back to cudaHostAlloc when THP or registration is unavailable (or
+// AMZ_HOST_ALLOC=cuda).
+namespace {
+constexpr size_t kHuge = size_t(2) << 20;
+std::mutex g_host_mu;
+std::unordered_map<void *, size_t> g_host_maps;  // THP blocks -> mapped length
+
+void *thp_alloc(size_t bytes) {
+    const char *mode = getenv("AMZ_HOST_ALLOC");
+    if (mode && strcmp(mode, "cuda") == 0) return nullptr;
+    const size_t len = (bytes + kHuge - 1) & ~(kHuge - 1);
+    void *raw = mmap(nullptr, len + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (raw == MAP_FAILED) return nullptr;
+    const uintptr_t r = (uintptr_t)raw, a = (r + kHuge - 1) & ~(uintptr_t)(kHuge - 1);
+    if (a > r) munmap(raw, a - r);  // trim to a 2 MB-aligned [a, a + len)
+    if (r + len + kHuge > a + len) munmap((void *)(a + len), r + len + kHuge - (a + len));
+    void *p = (void *)a;
+#ifdef MADV_HUGEPAGE
+    madvise(p, len, MADV_HUGEPAGE);
+#endif
+    memset(p, 0, len);  // fault the huge pages in before pinning
+    if (cudaHostRegister(p, len, cudaHostRegisterPortable) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, len);
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    g_host_maps[p] = len;
+    return p;
+}
+}  // namespace
+
 int amz_host_alloc(size_t bytes, void **out) {
     if (!out) return fail(AMZ_ECONFIG, "null argument");
     *out = nullptr;
     if (bytes == 0) return 0;
+    if ((*out = thp_alloc(bytes)) != nullptr) return 0;
     if (cudaHostAlloc(out, bytes, cudaHostAllocPortable) != cudaSuccess) {
         cudaGetLastError();
         *out = nullptr;
@@ -145,7 +186,23 @@ int amz_host_alloc(size_t bytes, void **out) {
 }
 
 int amz_host_free(void *p) {
-    if (p && cudaFreeHost(p) != cudaSuccess) {
+    if (!p) return 0;
+    size_t len = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        auto it = g_host_maps.find(p);
+        if (it != g_host_maps.end()) {
+            len = it->second;
+            g_host_maps.erase(it);
+        }
+    }
+    if (len) {
+        const bool ok = cudaHostUnregister(p) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+        munmap(p, len);
+        return ok ? 0 : fail(AMZ_ECUDA, "cudaHostUnregister failed");
+    }
+    if (cudaFreeHost(p) != cudaSuccess) {
         cudaGetLastError();
         return fail(AMZ_ECUDA, "cudaFreeHost failed");
     }
@@ -424,6 +481,14 @@ int amz_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, int ctas, vo
     if (bytes == 0) return 0;
     launch_copy_h2d(dst_dev, src_host, bytes, ctas > 0 ? ctas : 64, (cudaStream_t)stream);
     return cuda_status("copy_h2d");
+}
+
+int amz_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, int ctas, void *stream) {
+    if (!dst_host || !src_dev) return fail(AMZ_ECONFIG, "null argument");
+    if ((((uintptr_t)dst_host) | ((uintptr_t)src_dev)) & 15u) return fail(AMZ_ECONFIG, "copy buffers must be 16-byte aligned");
+    if (bytes == 0) return 0;
+    launch_copy_h2d(dst_host, src_dev, bytes, ctas > 0 ? ctas : 8, (cudaStream_t)stream);  // same kernel, UVA both ways
+    return cuda_status("copy_d2h");
 }
 
 int amz_iter_advance(uint32_t *iter_dev, uint32_t by, void *stream) {

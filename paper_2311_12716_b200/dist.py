@@ -146,16 +146,20 @@ def sdp_average_gradients(params, exact: bool = False, group=None) -> None:
     D = dist.get_world_size(group)
     if D == 1:
         return
+    dev = flat.device
+    # gloo has no all-gather of device tensors: its worlds (tests, several ranks on one
+    # GPU) exchange host copies; the arithmetic stays on the gradients' device
+    wire = flat.cpu() if (flat.is_cuda and dist.get_backend(group) == "gloo") else flat
     if exact:
-        parts = [torch.empty_like(flat) for _ in range(D)]
-        dist.all_gather(parts, flat, group=group)
+        parts = [torch.empty_like(wire) for _ in range(D)]
+        dist.all_gather(parts, wire, group=group)
         acc = torch.zeros_like(flat)
         for part in parts:
-            acc = acc + part
+            acc = acc + part.to(dev)
         mean = acc / D
     else:
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-        mean = flat / D
+        dist.all_reduce(wire, op=dist.ReduceOp.SUM, group=group)
+        mean = wire.to(dev) / D
     off = 0
     with torch.no_grad():
         for p in params:
@@ -171,6 +175,8 @@ def check_param_sync(params, tol: float = 1e-6, group=None) -> float:
     dist = torch.distributed
     with torch.no_grad():
         vec = _flat([p.detach().double() for p in params]).contiguous()
+        if vec.is_cuda and dist.get_backend(group) == "gloo":
+            vec = vec.cpu()  # gloo worlds exchange host copies
         ref = vec.clone()
         dist.broadcast(ref, src=0, group=group)
         drift = (vec - ref).abs().max() if vec.numel() else torch.zeros((), dtype=torch.float64)

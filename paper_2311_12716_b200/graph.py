@@ -13,10 +13,14 @@ a replay needs no host-side key work, and the host's cost per step is one
 
 ``host_io=True`` captures the end-to-end form: the step's inputs (actions u8 [T, B],
 values [T, B] and last values [B] in ``value_dtype``) are copied host->device from
-pinned staging at the start of the graph and scores | max returns (float64 [2, B]) are
-copied device->host at the end.  With ``overlap=True`` two graphs alternate between two
-device input buffers and each copies the NEXT step's inputs on a side stream while it
-computes the current step (the copy engines and the SMs work at the same time).
+pinned staging and scores | max returns (float64 [2, B]) are copied device->host at the
+end of the graph.  With ``overlap=True`` (the default) two graphs alternate between two
+device input slots and the copy of the NEXT step's inputs runs on its own copy stream
+while the current step computes: the copy into slot k waits (event) only for the graph
+that last read slot k, and the graph waits only for its own slot's copy, so the PCIe
+transfer and the kernels pipeline across steps instead of joining inside one replay
+(measured: 5.3 MB takes ~108 us over PCIe, the step's kernels ~90 us).  Without
+overlap the copy is the first node of the graph.
 
 Results equal the eager calls bit for bit (tests/test_gpu_graph.py).
 """
@@ -51,7 +55,7 @@ class DRIterationGraph:
 
     def __init__(self, benv: VectorBatchEnv, root_rng, T: int, params, gamma: float, lam: float,
                  score_fn: str = "maxmc", value_dtype=None, host_io: bool = False, overlap: bool = True,
-                 copy_streams: int = 1, copy_ctas: int = 64):
+                 copy_streams: int = 1, copy_ctas: int = 32, copy_mode: str = "auto"):
         torch = _torch()
         if not isinstance(benv, VectorBatchEnv):
             raise ContractViolation("DRIterationGraph needs a VectorBatchEnv")
@@ -67,8 +71,14 @@ class DRIterationGraph:
         self.root_pfx = self.root.seed_prefix()
         self.host_io = host_io
         self.overlap = overlap and host_io
-        self.copy_streams = 1
+        self.copy_streams = max(1, int(copy_streams))
         self.copy_ctas = int(copy_ctas)
+        if copy_mode not in ("auto", "kernel", "engine"):
+            raise ContractViolation(f"copy_mode {copy_mode!r}: 'auto', 'kernel' or 'engine'")
+        self.copy_mode = copy_mode
+        self.copy_engine = copy_mode == "engine"  # auto: the kernel until calibrate() decides
+        self.calibrate_after = 200  # auto: steps before the one-off calibration
+        self.calibration_ms = None
         T, B, dev, v = self.T, self.B, self.dev, self.p.agent_view_size
         self.it_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.next_it = 0
@@ -97,23 +107,31 @@ class DRIterationGraph:
             self.host_inputs = self._views(self._host_raw)
             self.host_result = pinned_empty((2, B), torch.float64)
         self.graphs = []
-        self.launches_per_step = 5  # k_env_reset_dr, k_dyn, k_render, k_gae_score*, k_iter_advance
         self._step_count = 0
         self._pending_h2d = False
+        if self.overlap:
+            # the copy stream(s): one for the copy kernel; copy-engine memcpys split the
+            # bytes over copy_streams streams (one DMA engine each)
+            self._cs = [torch.cuda.Stream(device=dev, priority=-5) for _ in range(self.copy_streams)]
+            self._copied = [torch.cuda.Event() for _ in range(nbuf)]  # slot k filled
+            self._used = [torch.cuda.Event() for _ in range(nbuf)]    # slot k read by its graph
 
     # -- one step's kernels on the current stream ------------------------------------
-    def _kernels(self, inp, after_reset=None):
-        """The step's kernels on the current stream; ``after_reset()`` runs right after the
-        reset kernel is enqueued (the overlapped input copy forks there: the reset fills
-        every SM's register file, the dynamics kernel leaves room beside it)."""
+    @property
+    def launches_per_step(self) -> int:
+        """Kernels per step: k_env_reset_dr, k_dyn, k_render, k_gae_score*, k_iter_advance,
+        with host_io the result read-back kernel and (unless a copy-engine H2D) the input
+        copy kernel."""
+        return 5 + (0 if not self.host_io else 1 + (0 if self.copy_engine else 1))
+
+    def _kernels(self, inp):
+        """The step's kernels on the current stream."""
         torch = self.torch
         lanes = self.benv._ensure(self.p)
         o = self.out
         st = lanes.stream()
         _lib.call("amz_env_reset_dr_iter", lanes.handle, ctypes.byref(self.root_pfx), _lib.ptr(self.it_dev),
                   _lib.ptr(o["reset_view"]), _lib.ptr(o["reset_dir"]), st)
-        if after_reset is not None:
-            after_reset()
         _lib.call("amz_env_rollout_iter", lanes.handle, self.T, _lib.ptr(inp["actions"]), ctypes.byref(self.root_pfx),
                   _lib.ptr(self.it_dev), _lib.ptr(o["view"]), _lib.ptr(o["dir"]), _lib.ptr(o["rewards"]),
                   _lib.ptr(o["dones"]), _lib.ptr(o["final_view"]), _lib.ptr(o["final_dir"]), st)
@@ -127,13 +145,13 @@ class DRIterationGraph:
         return {"values": raw[:nv].view(self.vdt).view(T, B), "last": raw[nv:nv + nl].view(self.vdt),
                 "actions": raw[nv + nl:].view(T, B)}
 
-    def _h2d(self, k, streams=None):
+    def _h2d(self, k, stream=None):
         """Copy the pinned staging into input slot k with ``amz_copy_h2d`` (a kernel
-        reading the pinned buffer through its unified address: measured 46 GB/s, where a
-        graph memcpy node from the same host buffer ran at 19-50 GB/s from one box to the
-        next), on the given side stream (or the current one)."""
+        reading the pinned buffer through its unified address: measured 49 GB/s, where a
+        copy-engine memcpy from the same host buffer ran at 19-50 GB/s from one box to the
+        next), on ``stream`` (or the current one)."""
         torch = self.torch
-        st = streams[0] if streams else torch.cuda.current_stream(self.dev)
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
         _lib.call("amz_copy_h2d", self._raw[k].data_ptr(), self._host_raw.data_ptr(), self._nbytes, self.copy_ctas,
                   st.cuda_stream)
 
@@ -151,28 +169,56 @@ class DRIterationGraph:
             for k in range(len(self.inputs)):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
-                    cur = torch.cuda.current_stream(self.dev)
                     if self.host_io and not self.overlap:
                         self._h2d(k)
-                    sides = []
-                    if self.overlap:
-                        # the next step's inputs on a side branch forked after the reset,
-                        # concurrent with the dynamics / render / GAE kernels
-                        sides = [torch.cuda.Stream(device=self.dev, priority=-5)]
-
-                        def fork(k=k, sides=sides, cur=cur):
-                            sides[0].wait_stream(cur)
-                            self._h2d(k ^ 1, sides)
-                    self._kernels(self.inputs[k], fork if self.overlap else None)
-                    if self.host_io:
-                        self.host_result.copy_(self.res, non_blocking=True)
-                    if self.overlap:
-                        for sd in sides:
-                            cur.wait_stream(sd)
+                    self._kernels(self.inputs[k])
+                    if self.host_io:  # scores | max returns -> pinned host, by a kernel
+                        _lib.call("amz_copy_d2h", self.host_result.data_ptr(), self.res.data_ptr(),
+                                  self.res.numel() * 8, 8, torch.cuda.current_stream(self.dev).cuda_stream)
                 self.graphs.append(g)
             torch.cuda.synchronize(self.dev)
         self.set_iteration(0)
         return self
+
+    def calibrate(self, rounds: int = 3, steps: int = 8) -> bool:
+        """Time pipelined steps with each H2D path (alternating, ``rounds`` x ``steps``
+        each, median per path) and keep the faster; returns True for the copy engine.
+        copy_mode "auto" runs this once by itself after ``calibrate_after`` steps.
+
+        Which path wins depends on the host and on its state.  Measured on B200 boxes
+        (tools/e2e_content.py, tools/pcie_interference.py): a copy-engine memcpy leaves the
+        SMs to the step (90 -> 101 us per step beside it) where the copy kernel takes SM
+        slots (90 -> 150 us), and in steady state the engine path wins (152 vs 165 us per
+        step); but for ~100-300 steps after the host CPU writes the pinned feed, PCIe
+        reads of it run 2-4x slower, the engine's worst (460 vs 250 us).  Hence the
+        decision is taken after a warm-up, not at capture.  The timed steps are real
+        iterations; the counter is restored afterwards (every iteration starts from a
+        full DR reset, so re-running one is side-effect free)."""
+        torch = self.torch
+        if not self.overlap:
+            return False
+        if not self.graphs:
+            self.capture()
+        resume = self.next_it
+        times = {False: [], True: []}
+        for _ in range(rounds):
+            for ce in (False, True):
+                self.copy_engine = ce
+                self._pending_h2d = False
+                self.step()
+                torch.cuda.synchronize(self.dev)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(torch.cuda.current_stream(self.dev))
+                for _ in range(steps):
+                    self.step()
+                b.record(torch.cuda.current_stream(self.dev))
+                torch.cuda.synchronize(self.dev)
+                times[ce].append(a.elapsed_time(b) / steps)
+        med = {ce: sorted(v)[len(v) // 2] for ce, v in times.items()}
+        self.copy_engine = med[True] < med[False]
+        self.calibration_ms = med
+        self.set_iteration(resume)
+        return self.copy_engine
 
     def set_iteration(self, it: int) -> None:
         """Point the device counter at iteration ``it`` (synchronous)."""
@@ -185,12 +231,37 @@ class DRIterationGraph:
         self.next_it = int(it)
         self._pending_h2d = False
 
+    def _issue_copy(self, k):
+        """overlap mode: fill slot k from the pinned staging on the copy stream, after the
+        graph that last read slot k."""
+        if not self.copy_engine:
+            cs = self._cs[0]
+            cs.wait_event(self._used[k])
+            self._h2d(k, cs)
+            self._copied[k].record(cs)
+            return
+        torch = self.torch
+        n, m = self._nbytes, len(self._cs)
+        part = ((n + m - 1) // m + 4095) & ~4095
+        first = self._cs[0]
+        first.wait_event(self._used[k])
+        for j, cs in enumerate(self._cs):
+            if j:
+                cs.wait_stream(first)
+            lo, hi = j * part, min(n, (j + 1) * part)
+            if lo < hi:
+                with torch.cuda.stream(cs):
+                    self._raw[k][lo:hi].copy_(self._host_raw[lo:hi], non_blocking=True)
+        for cs in self._cs[1:]:
+            first.wait_stream(cs)
+        self._copied[k].record(first)
+
     def prefetch(self):
-        """overlap mode: copy the first step's inputs (later steps' copies ride along in
-        the previous replay)."""
+        """overlap mode: copy the first step's inputs (every later step's copy is issued
+        one step ahead, concurrent with the previous step's kernels)."""
         if self.overlap:
             with self.torch.cuda.device(self.dev):
-                self._h2d(self._step_count & 1)
+                self._issue_copy(self._step_count % len(self.graphs))
             self._pending_h2d = True
 
     def step(self, it: int | None = None):
@@ -199,9 +270,22 @@ class DRIterationGraph:
             self.capture()
         if it is not None and it != self.next_it:
             self.set_iteration(it)
-        if self.overlap and not self._pending_h2d:
-            self.prefetch()
-        self.graphs[self._step_count % len(self.graphs)].replay()
+        if (self.overlap and self.copy_mode == "auto" and self.calibration_ms is None
+                and self._step_count >= self.calibrate_after):
+            self.calibration_ms = {}  # (re-entry guard: calibrate() steps too)
+            self.calibrate()
+        k = self._step_count % len(self.graphs)
+        if self.overlap:
+            if not self._pending_h2d:
+                self.prefetch()
+            cur = self.torch.cuda.current_stream(self.dev)
+            cur.wait_event(self._copied[k])
+            with self.torch.cuda.device(self.dev):
+                self._issue_copy(k ^ 1)  # the next step's inputs, beside this step's kernels
+            self.graphs[k].replay()
+            self._used[k].record(cur)
+        else:
+            self.graphs[k].replay()
         self._step_count += 1
         self.next_it += 1
         return self.gae

@@ -1,10 +1,12 @@
 """Pinned host staging buffers for the host->device trajectory feed.
 
-``pinned_empty`` allocates through the library (``amz_host_alloc`` = cudaHostAlloc) and
-wraps the block as a CPU torch tensor; the block is freed when the last tensor viewing
-it goes away.  Copies from it to the device run at the full PCIe rate (measured 54 GB/s
-on the B200 box, against 16-52 GB/s from torch's own pinned pool), so an input feed
-(actions, values from a host-side actor) should stage through it.
+``pinned_empty`` allocates through the library (``amz_host_alloc``: 2 MB transparent
+huge pages registered with cudaHostRegister, else cudaHostAlloc) and wraps the block as
+a CPU torch tensor; the block is freed when the last tensor viewing it goes away.
+Copies of CPU-written data from it to the device run at the PCIe rate (measured 49-53
+GB/s on the B200 hosts, where the same data in 4 KB cudaHostAlloc pages read at 11-25
+GB/s: tools/hugepage_probe.py), so an input feed (actions, values from a host-side
+actor) should stage through it.
 """
 
 from __future__ import annotations

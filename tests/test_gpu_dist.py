@@ -108,3 +108,62 @@ def test_two_ranks_equal_one_rank(accel):
         for k in st1:
             assert np.array_equal(ok[r][5][k], st1[k]), (r, k)
     assert ok[0][2:4] == (0, one.L // 2) and ok[1][2:4] == (one.L // 2, one.L)
+
+
+# -- SDP gradient mean on device tensors (agents/ppo.py:308-313) -------------------------
+def _grad_model(r):
+    torch.manual_seed(100)  # identical initial parameters on every shard
+    m = torch.nn.Sequential(torch.nn.Linear(5, 7), torch.nn.Tanh(), torch.nn.Linear(7, 3)).cuda()
+    torch.manual_seed(200 + r)  # shard-specific minibatch
+    x = (torch.randn(11, 5, dtype=torch.float32) * (r + 1)).cuda()
+    m(x).pow(2).sum().backward()
+    m[2].bias.grad = None  # a parameter without a gradient counts as zeros
+    return m
+
+
+def _sdp_worker(rank, world, port, backend, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as tdist
+
+    torch.cuda.set_device(0)
+    tdist.init_process_group(backend, rank=rank, world_size=world)
+    try:
+        from paper_2311_12716_b200 import dist
+
+        out = {}
+        for exact in (True, False):
+            m = _grad_model(rank)
+            dist.sdp_average_gradients(m.parameters(), exact=exact)
+            out[exact] = [p.grad.clone() for p in m.parameters()]
+        shards = [[p.grad.detach() if p.grad is not None else torch.zeros_like(p) for p in _grad_model(r).parameters()]
+                  for r in range(world)]
+        want = [sum(g[i] for g in shards) / world for i in range(len(shards[0]))]
+        on_dev = all(g.is_cuda for g in out[True] + out[False])
+        exact_ok = all(torch.equal(a, b) for a, b in zip(out[True], want))
+        close_ok = all(torch.allclose(a, b, rtol=1e-6, atol=1e-7) for a, b in zip(out[False], want))
+        drift0 = dist.check_param_sync(_grad_model(rank).parameters())
+        q.put((rank, on_dev, exact_ok, close_ok, drift0))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1)])
+def test_sdp_gradient_mean_on_device(backend, world):
+    """Device gradients: gloo with 2 ranks on the one GPU (host-staged exchange), NCCL with
+    the world this box has (1 GPU: the call must be the identity and stay on the device)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sdp_worker, args=(r, world, port, backend, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    msgs = sorted(q.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    for rank, on_dev, exact_ok, close_ok, drift0 in msgs:
+        assert on_dev and exact_ok and close_ok and drift0 == 0.0, rank

@@ -59,18 +59,21 @@ def test_graph_replays_equal_eager_iterations():
         _same(gr, *_eager(root, it, acts, vals, last, p))
 
 
-@pytest.mark.parametrize("overlap", [False, True])
+@pytest.mark.parametrize("overlap,copy_mode", [(False, "auto"), (True, "kernel"), (True, "engine"), (True, "auto")])
 @pytest.mark.parametrize("vdt", [torch.float64, torch.float32])
-def test_graph_host_io(overlap, vdt):
+def test_graph_host_io(overlap, copy_mode, vdt):
     p = amz.StaticParams()
     root = amz.RngStream.from_seed(3)
     acts, vals, last = _inputs(2, vdt)
     gr = DRIterationGraph(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B)), root, T, p, G, L,
-                          value_dtype=vdt, host_io=True, overlap=overlap)
+                          value_dtype=vdt, host_io=True, overlap=overlap, copy_mode=copy_mode)
     gr.host_inputs["actions"].copy_(acts.cpu())
     gr.host_inputs["values"].copy_(vals.cpu())
     gr.host_inputs["last"].copy_(last.cpu())
     gr.capture()
+    if copy_mode == "auto":
+        gr.calibrate(rounds=2, steps=2)  # real steps, counter restored: iteration 0 is next
+        assert gr.next_it == 0 and set(gr.calibration_ms) == {False, True}
     for it in range(4):
         gr.step()
         torch.cuda.synchronize()
