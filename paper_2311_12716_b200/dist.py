@@ -144,7 +144,10 @@ def sdp_average_gradients(params, exact: bool = False, group=None) -> None:
     grads = [p.grad.detach() if p.grad is not None else torch.zeros_like(p) for p in params]
     flat = _flat(grads).contiguous()
     D = dist.get_world_size(group)
-    if D == 1:
+    if D == 1:  # the mean of one shard; a missing gradient still reads as zeros
+        for p, g in zip(params, grads):
+            if p.grad is None:
+                p.grad = g
         return
     dev = flat.device
     # gloo has no all-gather of device tensors: its worlds (tests, several ranks on one

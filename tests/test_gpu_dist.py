@@ -126,7 +126,11 @@ def _sdp_worker(rank, world, port, backend, q):
     import torch.distributed as tdist
 
     torch.cuda.set_device(0)
-    tdist.init_process_group(backend, rank=rank, world_size=world)
+    try:
+        tdist.init_process_group(backend, rank=rank, world_size=world)
+    except Exception as e:  # report instead of leaving the parent waiting
+        q.put((rank, False, False, False, repr(e)))
+        return
     try:
         from paper_2311_12716_b200 import dist
 
@@ -143,6 +147,10 @@ def _sdp_worker(rank, world, port, backend, q):
         close_ok = all(torch.allclose(a, b, rtol=1e-6, atol=1e-7) for a, b in zip(out[False], want))
         drift0 = dist.check_param_sync(_grad_model(rank).parameters())
         q.put((rank, on_dev, exact_ok, close_ok, drift0))
+    except Exception as e:
+        import traceback
+
+        q.put((rank, False, False, False, traceback.format_exc()))
     finally:
         tdist.destroy_process_group()
 
@@ -161,9 +169,10 @@ def test_sdp_gradient_mean_on_device(backend, world):
     procs = [ctx.Process(target=_sdp_worker, args=(r, world, port, backend, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    msgs = sorted(q.get(timeout=300) for _ in range(world))
+    msgs = sorted((q.get(timeout=180) for _ in range(world)), key=lambda m: m[0])
     for pr in procs:
         pr.join(timeout=120)
-        assert pr.exitcode == 0
     for rank, on_dev, exact_ok, close_ok, drift0 in msgs:
-        assert on_dev and exact_ok and close_ok and drift0 == 0.0, rank
+        assert on_dev and exact_ok and close_ok and drift0 == 0.0, (rank, drift0)
+    for pr in procs:
+        assert pr.exitcode == 0
