@@ -302,6 +302,16 @@ int amz_plr_sample(amz_plr_t *plr, const amz_seed_t *key, int64_t n, double rho,
                    int64_t iter, int32_t *slots_dev, amz_level_t *levels_dev, double *max_ret_dev,
                    double *score_dev, void *stream);
 
+/* buffer_sample_levels with proportional prioritisation: P_S ~
+ * score^(1/temperature) (numpy's np.power; CUDA's pow is within 2 ulp of it, so draws
+ * equal the oracle's except where a uniform falls inside that rounding of a cdf
+ * boundary), mixed with the staleness term like amz_plr_sample.  NaN probabilities
+ * (a negative score, or every score 0: numpy's choice raises) give AMZ_ECONTRACT at
+ * amz_plr_size(). */
+int amz_plr_sample_proportional(amz_plr_t *plr, const amz_seed_t *key, int64_t n, double rho, double temperature,
+                                int64_t iter, int32_t *slots_dev, amz_level_t *levels_dev, double *max_ret_dev,
+                                double *score_dev, void *stream);
+
 /* ACCEL parent choice: indices of the q highest scores (ties -> lower index). */
 int amz_plr_top_q(const double *scores_dev, int64_t n, int q, int32_t *out_dev, void *stream);
 

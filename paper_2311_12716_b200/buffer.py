@@ -50,8 +50,8 @@ class PlrConfig:
             raise ConfigError(f"staleness_coef must be in [0, 1], got {self.staleness_coef}")
         if self.score_fn not in ("maxmc", "pvl"):
             raise ConfigError(f"unknown score_fn {self.score_fn!r}")
-        if self.prioritization != "rank":
-            raise ConfigError("only rank prioritisation is implemented on the GPU (paper Table 4)")
+        if self.prioritization not in ("rank", "proportional"):
+            raise ConfigError(f"unknown prioritization {self.prioritization!r}: 'rank' or 'proportional'")
         if not 1 <= self.buffer_size <= 4096:
             raise ConfigError(f"buffer_size must be in [1, 4096], got {self.buffer_size}")
         return self
@@ -118,9 +118,14 @@ class LevelBuffer:
                "max_returns": torch.empty(n, dtype=torch.float64, device=self.device),
                "scores": torch.empty(n, dtype=torch.float64, device=self.device)}
         seed = as_stream(rng).seed_prefix()
-        _lib.call("amz_plr_sample", self.handle, ctypes.byref(seed), n, float(self.cfg.staleness_coef),
-                  _lib.ptr(self.lut), int(it), _lib.ptr(out["slots"]), _lib.ptr(out["levels"]),
-                  _lib.ptr(out["max_returns"]), _lib.ptr(out["scores"]), self._stream())
+        if self.cfg.prioritization == "proportional":  # P_S ~ score^(1/beta)
+            _lib.call("amz_plr_sample_proportional", self.handle, ctypes.byref(seed), n,
+                      float(self.cfg.staleness_coef), float(self.cfg.temperature), int(it), _lib.ptr(out["slots"]),
+                      _lib.ptr(out["levels"]), _lib.ptr(out["max_returns"]), _lib.ptr(out["scores"]), self._stream())
+        else:
+            _lib.call("amz_plr_sample", self.handle, ctypes.byref(seed), n, float(self.cfg.staleness_coef),
+                      _lib.ptr(self.lut), int(it), _lib.ptr(out["slots"]), _lib.ptr(out["levels"]),
+                      _lib.ptr(out["max_returns"]), _lib.ptr(out["scores"]), self._stream())
         return out
 
     def decision(self, rng) -> bool:

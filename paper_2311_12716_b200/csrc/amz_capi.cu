@@ -768,9 +768,22 @@ int amz_plr_sample(amz_plr_t *b, const amz_seed_t *key, int64_t n, double rho, c
     DevGuard guard_(b->device);
     if (rho < 0.0 || rho > 1.0) return fail(AMZ_ECONFIG, "staleness_coef must be in [0, 1], got %g", rho);
     if (n <= 0) return 0;
-    launch_plr_sample(b->D, b->rank, *key, n, 1.0 - rho, rho, lut, iter, slots, levels, max_ret, score, b->err,
-                      (cudaStream_t)stream);
+    launch_plr_sample(b->D, b->rank, *key, n, 1.0 - rho, rho, lut, 0, 0.0, iter, slots, levels, max_ret, score,
+                      b->err, (cudaStream_t)stream);
     return cuda_status("plr_sample");
+}
+
+int amz_plr_sample_proportional(amz_plr_t *b, const amz_seed_t *key, int64_t n, double rho, double temperature,
+                                int64_t iter, int32_t *slots, amz_level_t *levels, double *max_ret, double *score,
+                                void *stream) {
+    if (!b || !key || (n > 0 && !slots)) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
+    if (rho < 0.0 || rho > 1.0) return fail(AMZ_ECONFIG, "staleness_coef must be in [0, 1], got %g", rho);
+    if (!(temperature > 0.0)) return fail(AMZ_ECONFIG, "temperature must be > 0, got %g", temperature);
+    if (n <= 0) return 0;
+    launch_plr_sample(b->D, b->rank, *key, n, 1.0 - rho, rho, nullptr, 1, 1.0 / temperature, iter, slots, levels,
+                      max_ret, score, b->err, (cudaStream_t)stream);
+    return cuda_status("plr_sample_proportional");
 }
 
 int amz_plr_top_q(const double *scores, int64_t n, int q, int32_t *out, void *stream) {
@@ -796,6 +809,8 @@ int amz_plr_size(amz_plr_t *b, int64_t *size, void *stream) {
         cudaStreamSynchronize(s);
         if (err & 4)
             return fail(AMZ_ECONTRACT, "buffer_update refused: last_sampled / seq spans exceed a 64-bit tie key");
+        if (err & 8)
+            return fail(AMZ_ECONTRACT, "proportional sampling: NaN probabilities (a negative score, or every score 0)");
         return fail(AMZ_ECONTRACT, "sampled from an empty level buffer");
     }
     return 0;

@@ -177,7 +177,8 @@ __device__ double block_pairwise_sum(const double *x, int n, PwTree &P) {
 //   1. ranks: one bitonic sort (1024 threads, 78 compare-exchange stages over the next
 //      power of two >= size) by (score desc, seq asc) -- the order numpy's lexsort of
 //      (seq, -score) gives (rank ties -> older insertion first)
-//   2. w = LUT[rank - 1] ((1/rank)^(1/beta), numpy's host LUT)
+//   2. w = LUT[rank - 1] ((1/rank)^(1/beta), numpy's host LUT); proportional:
+//      w = score^(1/beta)
 //   3. sum(w) in numpy's pairwise order
 //   4. P = (1-rho) w/sum(w) + rho st/sum(st); cdf = sequential cumsum (one thread: it is
 //      numpy's order) while the other warps draw the uniforms u_i = i-th random() of the
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(kRankThreads) k_plr_rank(PlrDev D, int32_t *__
 
 __global__ void __launch_bounds__(kPlrThreads, 1)
     k_plr_sample(PlrDev D, const int32_t *__restrict__ rank, amz_seed_t key, int64_t n, double one_minus_rho,
-                 double rho, const double *__restrict__ lut, int64_t iter, int32_t *__restrict__ slots_out,
-                 amz_level_t *__restrict__ levels_out, double *__restrict__ maxret_out,
+                 double rho, const double *__restrict__ lut, int prop, double inv_beta, int64_t iter,
+                 int32_t *__restrict__ slots_out, amz_level_t *__restrict__ levels_out, double *__restrict__ maxret_out,
                  double *__restrict__ score_out, int *__restrict__ err) {
     extern __shared__ __align__(16) uint8_t smraw[];
     SampleSmem &S = *reinterpret_cast<SampleSmem *>(smraw);
@@ -244,15 +245,24 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     __syncthreads();
     // ---- 2./3. weights and their pairwise sum (slot order) ----
     unsigned long long my_st = 0ull;
+    bool bad = false;
     for (int i = tid; i < size; i += blockDim.x) {
-        S.p[i] = lut[rank[i]];
+        if (prop) {  // proportional: score^(1/beta) (numpy's np.power; CUDA pow is within 2 ulp of it)
+            const double w = pow(D.score[i], inv_beta);
+            bad |= !(w >= 0.0);  // a negative score: numpy's choice rejects NaN probabilities
+            S.p[i] = w;
+        } else {
+            S.p[i] = lut[rank[i]];
+        }
         my_st += (unsigned long long)(iter - D.last[i]);
     }
+    if (bad) atomicOr(err, 8);
     for (int o = 16; o > 0; o >>= 1) my_st += __shfl_down_sync(0xFFFFFFFFu, my_st, o);
     if ((tid & 31) == 0) atomicAdd(&S.st_total, my_st);
     __syncthreads();
     SAMP_CLK(4);
     const double wsum = block_pairwise_sum(S.p, size, S.pw);
+    if (prop && tid == 0 && !(wsum > 0.0)) atomicOr(err, 8);  // every score 0: 0/0 probabilities
     const long long tot = (long long)S.st_total;
     SAMP_CLK(5);
     // ---- 4. P ----
@@ -1689,8 +1699,8 @@ size_t plr_sample_smem() { return sizeof(SampleSmem); }
 size_t plr_update_smem() { return sizeof(UpdSmem); }
 
 int launch_plr_sample(const PlrDev &D, int32_t *rank, const amz_seed_t &key, int64_t n, double omr, double rho,
-                      const double *lut, int64_t iter, int32_t *slots, amz_level_t *levels, double *maxret,
-                      double *score, int *err, cudaStream_t s) {
+                      const double *lut, int prop, double inv_beta, int64_t iter, int32_t *slots, amz_level_t *levels,
+                      double *maxret, double *score, int *err, cudaStream_t s) {
     static bool attr[kMaxDevices] = {};  // the attribute is per device
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1698,11 +1708,14 @@ int launch_plr_sample(const PlrDev &D, int32_t *rank, const amz_seed_t &key, int
         cudaFuncSetAttribute(k_plr_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SampleSmem));
         if (dev < kMaxDevices) attr[dev] = true;
     }
-    cudaMemsetAsync(rank, 0, (size_t)D.K * sizeof(int32_t), s);
-    k_plr_rank<<<dim3((unsigned)((D.K + kRankThreads - 1) / kRankThreads), (unsigned)((D.K + kRankJ - 1) / kRankJ)),
-                 kRankThreads, 0, s>>>(D, rank);
-    k_plr_sample<<<1, kPlrThreads, sizeof(SampleSmem), s>>>(D, rank, key, n, omr, rho, lut, iter, slots, levels,
-                                                             maxret, score, err);
+    if (!prop) {  // ranks only for rank prioritisation
+        cudaMemsetAsync(rank, 0, (size_t)D.K * sizeof(int32_t), s);
+        k_plr_rank<<<dim3((unsigned)((D.K + kRankThreads - 1) / kRankThreads),
+                          (unsigned)((D.K + kRankJ - 1) / kRankJ)),
+                     kRankThreads, 0, s>>>(D, rank);
+    }
+    k_plr_sample<<<1, kPlrThreads, sizeof(SampleSmem), s>>>(D, rank, key, n, omr, rho, lut, prop, inv_beta, iter, slots,
+                                                             levels, maxret, score, err);
     return 0;
 }
 

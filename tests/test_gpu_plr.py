@@ -12,6 +12,7 @@ from tests.helpers import records_to_rows, tensor_rows  # noqa: E402
 
 import paper_2311_12716_b200 as amz  # noqa: E402
 from paper_2311_12716_b200.buffer import AccelConfig, LevelBuffer, PlrConfig, top_q  # noqa: E402
+from paper_2311_12716_b200.errors import ContractViolation  # noqa: E402
 from paper_2311_12716_b200.level import records_to_tensor  # noqa: E402
 from paper_2311_12716_b200.plr import ParallelPLR  # noqa: E402
 
@@ -144,6 +145,44 @@ def test_sample_matches_numpy_choice(K, rho, beta):
         assert np.array_equal(tensor_rows(out["levels"]), records_to_rows(lv))
         assert np.array_equal(out["scores"].cpu().numpy(), ref.score[want])
     _assert_same(gpu, ref)
+
+
+@pytest.mark.parametrize("K,rho,beta", [(100, 0.0, 0.3), (4000, 0.3, 0.3), (777, 0.5, 1.0)])
+def test_sample_proportional_matches_numpy_choice(K, rho, beta):
+    """SPEC.md:367 proportional prioritisation: P_S ~ score^(1/beta).  The weights come
+    from CUDA's pow (within 2 ulp of numpy's np.power), so the probabilities are checked
+    to 1e-13 relative and the draws for equality (a uniform would have to land inside
+    that rounding of a cdf boundary to differ)."""
+    rng = np.random.default_rng(K + 1)
+    recs = _pool(K + 50, seed=2)
+    cfg = PlrConfig(buffer_size=K, staleness_coef=rho, temperature=beta, prioritization="proportional")
+    gpu = LevelBuffer(cfg)
+    ref = plr_np.LevelBuffer(K)
+    for it in range(3):
+        idx = rng.permutation(K + 50)[:K]
+        sc = rng.choice([0.0, 0.2, 0.2, 0.4, 0.9], K) * rng.uniform(0.5, 1, K)
+        gpu.update(records_to_tensor(recs[idx]), torch.from_numpy(sc), torch.from_numpy(sc), it)
+        ref.update(recs[idx], sc, sc, it)
+    ocfg = plr_np.PlrConfig(buffer_size=K, staleness_coef=rho, temperature=beta, prioritization="proportional")
+    w_gpu = torch.pow(torch.from_numpy(ref.score[:ref.size]).cuda(), 1.0 / beta).cpu().numpy()
+    w_np = np.power(ref.score[:ref.size], 1.0 / beta)
+    assert np.allclose(w_gpu, w_np, rtol=1e-13, atol=0)
+    for it in range(3, 7):
+        out = gpu.sample(amz.RngStream(13, (it, 2)), 2048, it)
+        want = ref.sample(13, (it, 2), 2048, ocfg, it)
+        assert np.array_equal(out["slots"].cpu().numpy(), want)
+        assert np.array_equal(out["scores"].cpu().numpy(), ref.score[want])
+    _assert_same(gpu, ref)
+
+
+def test_sample_proportional_rejects_nan_probabilities():
+    cfg = PlrConfig(buffer_size=16, prioritization="proportional")
+    gpu = LevelBuffer(cfg)
+    recs = _pool(16, seed=3)
+    gpu.update(records_to_tensor(recs), torch.full((16,), -0.5, dtype=torch.float64), torch.zeros(16, dtype=torch.float64), 0)
+    gpu.sample(amz.RngStream(1, (0,)), 8, 1)
+    with pytest.raises(ContractViolation):
+        gpu.size()
 
 
 def test_top_q():
