@@ -389,13 +389,13 @@ constexpr int kChunk = 1024;  // relevant candidates staged per round (reuses th
 // candidates, [4] insert_runs calls, [5] insert passes, [6] candidates consumed by runs,
 // [7] relevant candidates, [8] calls, [9] bottom-cache rebuilds, [10] warp-batched candidates,
 // [11] cycles of phase B, [12] cycles of phase C, [13] batch steps, [14] cycles in batch steps
-__device__ unsigned long long g_plr_stats[32];
+__device__ unsigned long long g_plr_stats[40];
 #define PLR_STAT(k_, v_) atomicAdd(&g_plr_stats[k_], (unsigned long long)(v_))
 #define PLR_CLK(v_) const long long v_ = clock64()
 extern "C" int amz_debug_plr_stats(void *host, int reset) {
     int rc = (int)cudaMemcpyFromSymbol(host, g_plr_stats, sizeof(g_plr_stats));
     if (reset) {
-        unsigned long long z[32] = {};
+        unsigned long long z[40] = {};
         cudaMemcpyToSymbol(g_plr_stats, z, sizeof(z));
     }
     return rc;
@@ -468,6 +468,12 @@ struct UpdSmem {
     int src[kPlrMaxK];     // candidate whose level the slot now holds (-1 = unchanged)
     int mr_src[kPlrMaxK];  // candidate whose score / max_return the slot now holds (-1 = unchanged)
     uint32_t replaced[kPlrMaxK / 32];
+    // keys present at kernel start whose slot was taken, then inserted again by a later
+    // twin: reslot[initial slot] = the slot holding the key now (-1 = absent), and
+    // origin[slot] = the initial slot of the key a slot holds (-1 = initial entry or a
+    // key new to the buffer) -- the replay twins' presence without the global keyslot
+    int16_t reslot[kPlrMaxK];
+    int16_t origin[kPlrMaxK];
     union {
         typename RunSort::TempStorage sort;
         SortedEntries e;
@@ -712,12 +718,14 @@ struct BottomCache {
     }
 };
 
+// the slot holding the key of candidate c (initial match im, twin-first f), or -1
+__device__ __forceinline__ int present_slot(const UpdSmem &S, const UpdScratch &W, int im, int f, int c) {
+    if (im >= 0) return ((S.replaced[im >> 5] >> (im & 31)) & 1u) ? (int)S.reslot[im] : im;
+    return f != c ? W.keyslot[f] : -1;  // a later twin of a level new to the buffer
+}
 // the buffer slot candidate r of the staged chunk updates in place, or -1
 __device__ __forceinline__ int cand_present(const UpdSmem &S, const UpdScratch &W, int r) {
-    const int im = S.u.chunk.im[r];
-    if (im >= 0 && !((S.replaced[im >> 5] >> (im & 31)) & 1u)) return im;
-    const int f = S.u.chunk.tf[r];
-    return f != S.u.chunk.cid[r] ? W.keyslot[f] : -1;
+    return present_slot(S, W, S.u.chunk.im[r], S.u.chunk.tf[r], S.u.chunk.cid[r]);
 }
 // certainly new at any point of the batch: no key match at kernel start, first of its key
 __device__ __forceinline__ bool cand_pure(const UpdSmem &S, int r) {
@@ -1023,6 +1031,8 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
                         atomicAdd(&S.n_virtual, 1);
                     } else if (S.owner[slot] >= 0) {
                         W.keyslot[S.owner[slot]] = -1;  // inserted earlier in this update: evicted
+                        const int og = S.origin[slot];
+                        if (og >= 0) S.reslot[og] = -1;
                     }
                 } else {
                     R.aslot[j] = -1;
@@ -1064,6 +1074,7 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
                 S.key[slot] = R.lk[li];
                 S.tie[slot] = tie_pack(S, iter, seq0 + j);
                 S.owner[slot] = cj;
+                S.origin[slot] = -1;  // run candidates are new to the buffer
                 S.src[slot] = cj;
                 S.mr_src[slot] = cj;
                 atomicOr(&S.replaced[slot >> 5], 1u << (slot & 31));
@@ -1201,6 +1212,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         S.owner[i] = -1;
         S.src[i] = -1;
         S.mr_src[i] = -1;
+        S.reslot[i] = -1;
+        S.origin[i] = -1;
     }
     if (tid == 0) {
         S.n_rel = 0;
@@ -1374,20 +1387,52 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     // its score does not beat the cache minimum, which no simple op changes
                     const bool rej_ok = bc.valid && size >= K;
                     const uint64_t mink = bc.nk;
+#ifdef AMZ_PLR_STATS
+                    bool gread = false;
+#endif
                     if (i < cn) {
+                        // branch-free where the lanes disagree (initial match or not, present
+                        // or not): every load issues, clamped, and selects pick the result
                         ci = S.u.chunk.cid[i];
                         const int imi = S.u.chunk.im[i], fi = S.u.chunk.tf[i];
-                        if (imi >= 0 && !((S.replaced[imi >> 5] >> (imi & 31)) & 1u))
-                            ps = imi;
-                        else if (fi != ci)
-                            ps = W.keyslot[fi];
+                        const int imc = imi < 0 ? 0 : imi;
+                        const uint32_t rw = S.replaced[imc >> 5];
+                        const int rs = S.reslot[imc];
                         ski = score_key(S.u.chunk.sc[i]);
-                        if (ps >= 0)
-                            simple = !bc.valid || (!S.incache[ps] && !ukey_le(ski, S.tie[ps], bc.mk, bc.mt));
-                        else
-                            simple = rej_ok && !(ski > mink);
+                        ps = ((rw >> (imc & 31)) & 1u) ? rs : imi;
+                        if (imi < 0) {
+                            ps = -1;
+                            if (fi != ci) ps = W.keyslot[fi];  // a later twin of a new level (rare)
+                        }
+#ifdef AMZ_PLR_STATS
+                        gread = imi < 0 && fi != ci;
+#endif
+                        const int pc = ps < 0 ? 0 : ps;
+                        const bool inc = S.incache[pc] != 0;
+                        const uint64_t tp = S.tie[pc];
+                        const bool sin = !bc.valid || (!inc && !ukey_le(ski, tp, bc.mk, bc.mt));
+                        const bool sab = rej_ok && !(ski > mink);
+                        simple = ps >= 0 ? sin : sab;
                     }
+#ifdef AMZ_PLR_STATS
+                    {
+                        const bool sv = __ballot_sync(0xFFFFFFFFu, simple) != 0;  // the chain settles here
+                        if (lane == 0) {
+                            PLR_STAT(32, clock64() - clk_bt + (sv ? 0 : 0));
+                            PLR_STAT(33, 1);
+                        }
+                    }
+#endif
                     present = __shfl_sync(0xFFFFFFFFu, ps, 0);
+#ifdef AMZ_PLR_STATS
+                    {
+                        const unsigned gr = __ballot_sync(0xFFFFFFFFu, gread);
+                        if (lane == 0) {
+                            PLR_STAT(30, gr != 0);
+                            PLR_STAT(31, 1);
+                        }
+                    }
+#endif
                     const unsigned bad = ~__ballot_sync(0xFFFFFFFFu, simple);
                     const int k = bad ? __ffs(bad) - 1 : 32;
                     if (k > 0) {
@@ -1502,10 +1547,11 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 #endif
                     if (!(sk > mink)) continue;
                     slot = ms;
-                    const int ow = S.owner[slot];
+                    const int ow = S.owner[slot], og = S.origin[slot];
                     __syncwarp();
                     if (lane == 0) {
                         if (ow >= 0) W.keyslot[ow] = -1;
+                        if (og >= 0) S.reslot[og] = -1;
                         S.key[slot] = sk;
                         S.tie[slot] = tbn;
                     }
@@ -1517,6 +1563,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 }
                 if (lane == 0) {
                     S.owner[slot] = f;
+                    S.origin[slot] = (int16_t)im;
+                    if (im >= 0) S.reslot[im] = (int16_t)slot;
                     S.replaced[slot >> 5] |= 1u << (slot & 31);
                     S.src[slot] = c;
                     S.mr_src[slot] = c;
