@@ -732,8 +732,11 @@ __device__ __forceinline__ bool cand_pure(const UpdSmem &S, int r) {
     return S.u.chunk.im[r] < 0 && S.u.chunk.tf[r] == S.u.chunk.cid[r];
 }
 // length of the run of consecutive in-place candidates starting at r (whole warp)
-__device__ __forceinline__ int inplace_run(const UpdSmem &S, const UpdScratch &W, int r, int cn, int lane) {
-    int L = 0;
+__device__ __forceinline__ int inplace_run(const UpdSmem &S, const UpdScratch &W, int r, int cn, int lane,
+                                           unsigned ok0) {
+    const unsigned fail0 = ~ok0;
+    if (fail0) return __ffs(fail0) - 1;
+    int L = 32;
     while (true) {
         const int i = r + L + lane;
         const bool pr = i < cn && cand_present(S, W, i) >= 0;
@@ -743,8 +746,11 @@ __device__ __forceinline__ int inplace_run(const UpdSmem &S, const UpdScratch &W
     }
 }
 // length of the run of consecutive certainly-new candidates starting at r (whole warp)
-__device__ __forceinline__ int pure_run(const UpdSmem &S, int r, int cn, int lane) {
-    int L = 0;
+// ok0: the first window's ballot (lanes r..r+31), when the caller already has it
+__device__ __forceinline__ int pure_run(const UpdSmem &S, int r, int cn, int lane, unsigned ok0) {
+    const unsigned fail0 = ~ok0;
+    if (fail0) return __ffs(fail0) - 1;
+    int L = 32;
     while (L < kRunMin) {
         const int i = r + L + lane;
         const bool pr = i < cn && cand_pure(S, i);
@@ -1373,6 +1379,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 clk_sc = 0;
 #endif
                 int present;  // candidate r's in-place slot or -1 (lane 0 of the batch probe)
+                unsigned pres_b, pure_b;  // the probe's lanes r..r+31: present / certainly new
                 // Warp-batched fast path: the leading stretch of "simple" candidates -- in
                 // place (key present), slot outside the bottom cache and new key above the
                 // cache maximum -- changes neither presence nor the cache, so the stretch
@@ -1380,7 +1387,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 {
                     PLR_CLK(clk_bt);
                     const int i = r + lane;
-                    bool simple = false;
+                    bool simple = false, prs = false;
                     int ps = -1, ci = 0;
                     uint64_t ski = 0;
                     // an absent key is certainly rejected (a no-op) when the buffer is full and
@@ -1396,6 +1403,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                         ci = S.u.chunk.cid[i];
                         const int imi = S.u.chunk.im[i], fi = S.u.chunk.tf[i];
                         const int imc = imi < 0 ? 0 : imi;
+                        prs = imi < 0 && fi == ci;  // certainly new
                         const uint32_t rw = S.replaced[imc >> 5];
                         const int rs = S.reslot[imc];
                         ski = score_key(S.u.chunk.sc[i]);
@@ -1424,6 +1432,8 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     }
 #endif
                     present = __shfl_sync(0xFFFFFFFFu, ps, 0);
+                    pres_b = __ballot_sync(0xFFFFFFFFu, i < cn && ps >= 0);
+                    pure_b = __ballot_sync(0xFFFFFFFFu, prs);
 #ifdef AMZ_PLR_STATS
                     {
                         const unsigned gr = __ballot_sync(0xFFFFFFFFu, gread);
@@ -1471,7 +1481,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 }
                 // a stretch of certainly-new candidates worth a parallel insert run
                 if (run_ok && im < 0 && f == c && r >= pscan_end) {
-                    const int L = pure_run(S, r, cn, lane);
+                    const int L = pure_run(S, r, cn, lane, pure_b);
                     if (L >= kRunMin) {
                         action = 2;
                         arg = L;
@@ -1482,7 +1492,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 // only an in-place candidate can open a run worth applying in bulk
                 if (present >= 0 && r >= scan_end) {
                     PLR_CLK(clk_ir);
-                    const int L = inplace_run(S, W, r, cn, lane);
+                    const int L = inplace_run(S, W, r, cn, lane, pres_b);
                     if (lane == 0) PLR_STAT(15, clock64() - clk_ir);
                     if (L >= kBulkRun) {
                         action = 1;
