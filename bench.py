@@ -47,19 +47,22 @@ ENV_BYTES_PER_STEP = 36  # action u8 + view 25 u8 + dir u8 + reward f64 + done u
 GAE_BYTES_PER_ELEM = 33  # r f64 + V f64 + done u8 in, A f64 + R f64 out
 
 
+PROFILE_ROUND = "r2y"  # the committed capture (tools/profile_round.sh + tools/summarize_round.py)
+
+
 def _traffic():
     """Per-launch DRAM bytes of the roofline kernels from the committed ncu capture."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r2l_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", f"{PROFILE_ROUND}_traffic.json")) as f:
             return json.load(f)
     except (OSError, ValueError):
         return {}
 
 
 def _write_peak():
-    """Measured write-only HBM stream rate (tools/bw_probe.py, profiles/r2l_bw.json)."""
+    """Measured write-only HBM stream rate (tools/bw_probe.py, profiles/<round>_bw.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r2l_bw.json")) as f:
+        with open(os.path.join(ROOT, "profiles", f"{PROFILE_ROUND}_bw.json")) as f:
             return float(json.load(f)["write_fill_GBs"])
     except (OSError, ValueError, KeyError):
         return None
@@ -593,7 +596,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": "k_env_rollout", "achieved": roll_gbs, "peak": peak, "unit": "GB/s",
                      "frac": roll_gbs / peak,
                      "traffic": _traffic().get("k_env_rollout", {}).get("dram_bytes"),
-                     "traffic_source": "profiles/r2l_traffic.json (ncu --set full, per launch)",
+                     "traffic_source": f"profiles/{PROFILE_ROUND}_traffic.json (ncu --set full, per launch)",
                      "peak_source": src,
                      "algorithmic_bytes": f"{ENV_BYTES_PER_STEP} B/env-step x {B * T} env-steps per launch",
                      "kernel_ms": roll,
@@ -762,11 +765,11 @@ def measure_large_batch(dev, B, T, iters, flush, peak):
     tr = _traffic().get("large_batch_rollout", {})
     wpk = _write_peak()
     out = {"lanes": B, "T": T, "rollout_ms": roll, "rollout_GBs": rg, "rollout_frac": rg / peak,
-           "rollout_traffic": tr.get("dram_bytes"), "traffic_source": "profiles/r2l_traffic.json",
+           "rollout_traffic": tr.get("dram_bytes"), "traffic_source": f"profiles/{PROFILE_ROUND}_traffic.json",
            "rollout_frac_of_write_stream": (rg / wpk) if wpk else None,
            "write_stream_note": "the rollout's bytes are 97% writes (view, dir, reward, done out; 1 B of action in); "
                                 "a write-only stream (torch fill_) reaches the write_stream_GBs figure on this B200 "
-                                "(profiles/r2l_bw.json), the copy peak above counts reads and writes",
+                                f"(profiles/{PROFILE_ROUND}_bw.json), the copy peak above counts reads and writes",
            "write_stream_GBs": wpk,
            "rollout_env_steps_per_s": B * T / (roll * 1e-3), "gae_score_ms": gae, "gae_score_GBs": gg,
            "gae_score_frac": gg / peak, "levels_scored_per_s": B / (gae * 1e-3)}

@@ -370,14 +370,27 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 //                     no key match and score <= m_low can never enter (the minimum never
 //                     drops below m_low), so it is skipped; everything else is
 //                     "relevant" and compacted in order.
-//   C  (one warp)     replays the relevant candidates in order against an indexed
-//                     64-ary min-heap of (score, tb) in shared memory (the stale-first
-//                     eviction order): an in-place update is one sift, an eviction is
-//                     replace-top + sift-down; level / max_return copies are deferred
-//                     to a parallel epilogue.  Two kinds of stretch leave warp 0 for
-//                     the whole CTA:
+//   C  (one warp)     replays the relevant candidates in order.  The buffer's
+//                     (score key, tb) live in flat shared arrays; the eviction order
+//                     needs only the bottom: a BOTTOM CACHE of the 64 smallest entries
+//                     sits in warp 0's registers (2 per lane) with its minimum and
+//                     maximum kept as warp-uniform values, and every entry outside it
+//                     is larger than its maximum.  An eviction takes the cached minimum
+//                     (one warp reduction refreshes it), an in-place update edits the
+//                     cache only if the entry is in it or drops below its maximum; an
+//                     emptied cache is rebuilt by the CTA (128-bit MSD radix select).
+//                     Warp-batched stretches: the leading run of candidates that change
+//                     neither presence nor the cache (in place outside the cache and
+//                     above its maximum; absent and not above the minimum of a full
+//                     buffer) is applied 32 at a time, the last writer per slot found
+//                     by match.any.  Presence of a candidate's key: its initial slot
+//                     while not replaced, else (a level present at kernel start that
+//                     was evicted and inserted again by a twin) the shared reslot map,
+//                     else (a later twin of a new level) the global keyslot.  Level /
+//                     max_return copies are deferred to a parallel epilogue.  Two kinds
+//                     of stretch leave warp 0 for the whole CTA:
 //     bulk in-place run (>= kBulkRun consecutive candidates whose level is present):
-//                     last writer per slot by atomicMax, heap rebuilt level-parallel;
+//                     last writer per slot by atomicMax;
 //     insert run (>= kRunMin consecutive candidates that are certainly new: no key
 //                     match at kernel start, first of their key in the batch):
 //                     a streaming top-K in parallel (k_plr_update comment below,
