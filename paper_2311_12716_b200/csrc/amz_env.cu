@@ -10,6 +10,7 @@
 // registers and the boards in shared memory for all T steps.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "amz_internal.h"
 #include "amz_render.cuh"
@@ -192,6 +193,68 @@ __global__ void __launch_bounds__(128, 7) k_env_reset_dr(Geo G, EnvDev E, amz_se
             store_level(spec + l, ms, ar, ac, ad, gr, gc);
             spec_step[l] = (uint32_t)(G.tep - 1);
         }
+    }
+}
+
+constexpr int64_t kThreadSamplerMin = 16384;  // levels per launch from which one thread per level wins
+
+// Thread-per-level DR reset (the throughput sampler, thread_sample_level): a CTA owns 32
+// lanes; warp 0 samples their levels (key prefix ++ [global lane]) and writes lane state,
+// board and observation per thread, warp 1 (with a wrapper key) their timeout levels
+// (key wrap ++ [tep - 1, global lane]).  Same levels as k_env_reset_dr (one warp per
+// level), at ~1/10 of its instructions per level.
+template <int V>
+__global__ void __launch_bounds__(64) k_env_reset_dr_t(Geo G, EnvDev E, amz_seed_t prefix, int prep, amz_seed_t wrap,
+                                                       amz_level_t *__restrict__ spec,
+                                                       uint32_t *__restrict__ spec_step, uint8_t *__restrict__ view,
+                                                       int64_t *__restrict__ dirs) {
+    __shared__ __align__(16) uint8_t arr[64 * kTSlice];
+    __shared__ __align__(16) uint8_t stage[32 * V * V];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 1 && !prep) return;
+    const int64_t l0 = (int64_t)blockIdx.x * 32, l = l0 + lane;
+    const bool live = l < E.B;
+    const uint32_t gl = E.lane_offset + (uint32_t)l;
+    uint64_t k0, k1;
+    {
+        amz_seed_t sd = warp == 0 ? prefix : wrap;
+        if (E.iter) {  // graph replay: root.fold_in(it).fold_in(0) (lanes) / .fold_in(1) (auto-reset stream)
+            seed_absorb(sd, *E.iter);
+            seed_absorb(sd, (uint32_t)warp);
+        }
+        if (warp == 1) seed_absorb(sd, (uint32_t)(G.tep - 1));
+        seed_absorb(sd, gl);
+        seed_key(sd, k0, k1);
+    }
+    Mask m;
+    int ar = 0, ac = 0, ad = 0, gr = 0, gc = 0;
+    thread_sample_level(k0, k1, G, arr + threadIdx.x * kTSlice, live, m, ar, ac, ad, gr, gc);
+    if (warp == 1) {
+        if (live) {
+            store_level(spec + l, m, ar, ac, ad, gr, gc);
+            spec_step[l] = (uint32_t)(G.tep - 1);
+        }
+        return;
+    }
+    if (live) {
+        LaneRec L;
+        L.s.r = L.hr = ar;
+        L.s.c = L.hc = ac;
+        L.s.d = L.hd = ad;
+        L.gr = gr;
+        L.gc = gc;
+        L.s.time = 0;
+        L.term = false;
+        E.st[l] = pack_st(L);
+        E.mask[l] = make_uint4(m.w[0], m.w[1], m.w[2], m.w[3]);
+        build_board(m, G, E.board + l, (int)E.B);
+        if (dirs) dirs[l] = ad;
+        if (view) lane_render<V>(ar, ac, ad, gr, gc, G.H, G.W, G.see, E.board + l, (int)E.B, stage + lane * V * V);
+    }
+    if (view) {
+        __syncwarp();
+        const int nv = (int)((E.B - l0) < 32 ? (E.B - l0) : 32);
+        warp_flush(stage, view + l0 * V * V, nv * V * V, lane);
     }
 }
 
@@ -445,8 +508,19 @@ int launch_env_reset_dr(const Geo &G, const EnvDev &E, const amz_seed_t &prefix,
     if (E.B <= 0) return 0;
     const amz_seed_t w = wrap ? *wrap : amz_seed_t{};
     const int prep = wrap != nullptr;
-    AMZ_DISPATCH_V(G.V, (k_env_reset_dr<VT><<<(unsigned)((E.B + 3) / 4), 128, 0, s>>>(G, E, prefix, prep, w, spec,
-                                                                                         spec_step, view, dirs)));
+    // one warp per level while the batch is small (latency: 4096 lanes 32 us vs 53 us for
+    // the thread sampler, which then has < 2 warps per SM), one thread per level beyond
+    // (throughput: 65536 lanes 113 us vs 369 us); AMZ_RESET_WARP=0/1 forces one
+    static const int forced = getenv("AMZ_RESET_WARP") ? atoi(getenv("AMZ_RESET_WARP")) : -1;
+    const bool warp_sampler = forced >= 0 ? forced != 0 : E.B < kThreadSamplerMin;
+    if (warp_sampler) {
+        AMZ_DISPATCH_V(G.V, (k_env_reset_dr<VT><<<(unsigned)((E.B + 3) / 4), 128, 0, s>>>(G, E, prefix, prep, w, spec,
+                                                                                             spec_step, view, dirs)));
+    } else {
+        AMZ_DISPATCH_V(G.V, (k_env_reset_dr_t<VT><<<(unsigned)((E.B + 31) / 32), 64, 0, s>>>(G, E, prefix, prep, w,
+                                                                                                spec, spec_step, view,
+                                                                                                dirs)));
+    }
     return 0;
 }
 

@@ -235,6 +235,109 @@ __device__ __forceinline__ void warp_sample_level(uint64_t k0, uint64_t k1, cons
     __syncwarp();
 }
 
+// ---------------------------------------------------------------------------------
+// Thread sampler: one level per thread, for throughput kernels (DR resets, batched level
+// generation).  The same stream consumption as warp_sample_level, as a word-driven state
+// machine: in each round every thread of the warp computes the next Philox block of its
+// own key (uniform control flow: block r for everyone in round r) and feeds its 8 words,
+// in numpy's order, through its draw state -- Lemire for the wall count, the masked
+// rejection of each Fisher-Yates step (the swap in the thread's slice of shared
+// memory), Lemire for goal / agent / heading.  A warp samples 32 levels with about the
+// instructions warp_sample_level spends on one.
+// ---------------------------------------------------------------------------------
+constexpr int kTSlice = 132;  // bytes of shared memory per thread (33 words: conflict-free same-index access)
+
+template <int kPhases>
+__device__ __forceinline__ void ts_settle(int &phase, int &i, uint32_t &n, uint32_t &thr, uint32_t (&res)[5], int ni,
+                                          uint32_t bound0) {
+    // advance past phases that draw nothing (Lemire with n <= 1: numpy returns low; a
+    // Fisher-Yates with no step left)
+#pragma unroll 1
+    while (phase < kPhases) {
+        if (phase == 1) {
+            if (i >= 1) return;
+            phase = 2;
+            continue;
+        }
+        n = phase == 0 ? bound0 : phase == 2 ? (uint32_t)ni - res[0] : phase == 3 ? (uint32_t)ni - res[0] - 1u : 4u;
+        if (n > 1u) {
+            thr = (0u - n) % n;
+            return;
+        }
+        res[phase] = 0u;
+        phase++;
+        if (phase == 1) i = ni - 1;
+    }
+}
+
+// arr: this thread's kTSlice-byte slice (4-byte aligned).  Threads with active = false
+// run the rounds idle and return nothing.
+__device__ __forceinline__ void thread_sample_level(uint64_t k0, uint64_t k1, const Geo &G, uint8_t *arr, bool active,
+                                                    Mask &mask, int &ar, int &ac, int &ad, int &gr, int &gc) {
+    const int ni = G.ni;
+    uint32_t *aw = reinterpret_cast<uint32_t *>(arr);
+#pragma unroll 8
+    for (int w = 0; w < 32; w++) aw[w] = 0x03020100u + 0x04040404u * (uint32_t)w;  // arange(ni) (+ padding)
+    int phase = active ? 0 : 5, i = 0;
+    uint32_t n = 0, thr = 0, res[5] = {0u, 0u, 0u, 0u, 0u};
+    ts_settle<5>(phase, i, n, thr, res, ni, (uint32_t)G.budget + 1u);
+    const unsigned am = __activemask();
+    // block r+1 is computed while block r's words are consumed (two independent chains)
+    uint64_t o[4];
+    philox_block(1, k0, k1, o[0], o[1], o[2], o[3]);
+    for (uint64_t blk = 1; __any_sync(am, phase < 5); blk++) {
+        uint64_t nx[4];
+        philox_block(blk + 1, k0, k1, nx[0], nx[1], nx[2], nx[3]);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const uint32_t w = (q & 1) ? (uint32_t)(o[q >> 1] >> 32) : (uint32_t)o[q >> 1];
+            if (phase == 1) {
+                const uint32_t v = w & (0xFFFFFFFFu >> __clz(i));
+                if (v <= (uint32_t)i) {
+                    const uint8_t a = arr[i], b = arr[v];
+                    arr[i] = b;
+                    arr[v] = a;
+                    if (--i < 1) ts_settle<5>(phase, i, n, thr, res, ni, 0u);
+                }
+            } else if (phase < 5) {
+                const uint64_t m = (uint64_t)w * n;
+                if ((uint32_t)m >= thr) {
+                    res[phase] = (uint32_t)(m >> 32);
+                    phase++;
+                    if (phase == 1) i = ni - 1;
+                    ts_settle<5>(phase, i, n, thr, res, ni, 0u);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) o[q] = nx[q];
+    }
+    if (!active) return;
+    // walls: the interior cells at positions [0, nw) of the permuted array
+    const uint32_t nw = res[0];
+    uint32_t m0 = 0u, m1 = 0u, m2 = 0u, m3 = 0u;
+    for (uint32_t k = 0; k < nw; k++) {
+        const uint32_t e = arr[k];
+        const uint32_t b = 1u << (e & 31u), qw = e >> 5;
+        m0 |= qw == 0u ? b : 0u;
+        m1 |= qw == 1u ? b : 0u;
+        m2 |= qw == 2u ? b : 0u;
+        m3 |= qw == 3u ? b : 0u;
+    }
+    mask.w[0] = m0;
+    mask.w[1] = m1;
+    mask.w[2] = m2;
+    mask.w[3] = m3;
+    // goal = free[gk], agent = (free without goal)[ak]; free = positions nw..ni-1
+    const uint32_t gk = res[2], ak = res[3];
+    const int goal = arr[nw + gk], agent = arr[nw + (ak < gk ? ak : ak + 1u)];
+    ad = (int)res[4];
+    gr = goal / G.iw + 1;
+    gc = goal % G.iw + 1;
+    ar = agent / G.iw + 1;
+    ac = agent % G.iw + 1;
+}
+
 // Every lane whose bit is set in `need` gets the level of its own key (k0, k1), one
 // warp-cooperative sample per requesting lane.
 template <bool kTrack = false>

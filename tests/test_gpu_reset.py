@@ -38,22 +38,23 @@ def _same_cursor(a, b):
     assert torch.equal(a.state.state_table(), b.state.state_table())
 
 
-@pytest.mark.parametrize("view", [3, 5, 9])
-def test_reset_matches_sample_then_reset(view):
+# B >= 16384 runs the thread-per-level reset kernel (k_env_reset_dr_t), smaller B the
+# warp-per-level one; both must equal sample_levels + reset_to_levels
+@pytest.mark.parametrize("view,B", [(3, 777), (5, 777), (9, 777), (3, 16500), (5, 20000), (9, 16384)])
+def test_reset_matches_sample_then_reset(view, B):
     p = amz.StaticParams(agent_view_size=view)
-    e1, r1, e2, r2 = _pair(p, 777, 31)
+    e1, r1, e2, r2 = _pair(p, B, 31)
     assert torch.equal(r1.observation["view"], r2.observation["view"])
     assert torch.equal(r1.observation["dir"], r2.observation["dir"])
     assert torch.equal(r1.state.state_table(), r2.state.state_table())
     assert torch.equal(e1.benv.lane_levels_tensor(r1.state), e2.benv.lane_levels_tensor(r2.state))
 
 
-@pytest.mark.parametrize("tep,T", [(20, 64), (9, 9), (5, 200)])
-def test_prepared_timeout_levels_match(tep, T):
+@pytest.mark.parametrize("tep,T,B", [(20, 64, 1500), (9, 9, 1500), (5, 200, 1500), (20, 32, 16400)])
+def test_prepared_timeout_levels_match(tep, T, B):
     """First RESAMPLE rollout after the fused reset (timeout levels prepared by the reset)
     equals the rollout after reset_to_levels (timeout levels from k_spec_levels)."""
     p = amz.StaticParams(max_episode_steps=tep)
-    B = 1500
     e1, r1, e2, r2 = _pair(p, B, 5)
     acts = torch.from_numpy(np.random.default_rng(2).integers(0, 3, (T, B)).astype(np.uint8)).cuda()
     t1, c1 = amz.rollout_actions(e1, r1, acts, p)
