@@ -1018,11 +1018,36 @@ __global__ void __launch_bounds__(128) k_sample_levels_w(Geo G, amz_seed_t prefi
     if (mine) store_level(out + i, m, ar, ac, ad, gr, gc);
 }
 
+// One thread per level (thread_sample_level) for large batches.
+__global__ void __launch_bounds__(64) k_sample_levels_t(Geo G, amz_seed_t prefix, uint32_t lane0,
+                                                        const uint32_t *__restrict__ lane_ids, int64_t n,
+                                                        amz_level_t *__restrict__ out) {
+    __shared__ __align__(16) uint8_t arr[64 * kTSlice];
+    const int64_t i = (int64_t)blockIdx.x * 64 + threadIdx.x;
+    if ((int64_t)blockIdx.x * 64 + (threadIdx.x & ~31) >= n) return;  // whole warps only
+    const bool mine = i < n;
+    uint64_t k0 = 0, k1 = 0;
+    if (mine) {
+        amz_seed_t sd = prefix;
+        seed_absorb(sd, lane_ids ? lane_ids[i] : lane0 + (uint32_t)i);
+        seed_key(sd, k0, k1);
+    }
+    Mask m;
+    int ar = 0, ac = 0, ad = 0, gr = 0, gc = 0;
+    thread_sample_level(k0, k1, G, arr + threadIdx.x * kTSlice, mine, m, ar, ac, ad, gr, gc);
+    if (mine) store_level(out + i, m, ar, ac, ad, gr, gc);
+}
+
 int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0, const uint32_t *ids, int64_t n,
                          amz_level_t *out, cudaStream_t s) {
     if (n <= 0) return 0;
-    k_sample_levels_w<<<(unsigned)((n + 4 * kGenLPW - 1) / (4 * kGenLPW)), 128, 0, s>>>(G, prefix, lane0, ids, n,
-                                                                                          out);
+    // one warp per level while the batch is small (latency), one thread per level from
+    // 16384 levels on (throughput; the same levels)
+    if (n >= 16384)
+        k_sample_levels_t<<<(unsigned)((n + 63) / 64), 64, 0, s>>>(G, prefix, lane0, ids, n, out);
+    else
+        k_sample_levels_w<<<(unsigned)((n + 4 * kGenLPW - 1) / (4 * kGenLPW)), 128, 0, s>>>(G, prefix, lane0, ids,
+                                                                                              n, out);
     return 0;
 }
 
