@@ -1224,6 +1224,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     const int tid = threadIdx.x, lane = tid & 31;
     const int K = (int)D.K;
     const int size0 = (int)D.meta[0];
+    PLR_CLK(clk_a);
     // ---- A: tie-key frame, buffer into the heap arrays + key hash ----
     for (int i = tid; i < kHash; i += blockDim.x) S.u.hash[i] = 0u;
     for (int i = tid; i < kPlrMaxK / 32; i += blockDim.x) S.replaced[i] = 0u;
@@ -1317,6 +1318,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
     if (tid == 0) S.cvalid = 0;
     __syncthreads();
     PLR_CLK(clk_b);
+    if (tid == 0) PLR_STAT(34, clk_b - clk_a);
     // ---- B: relevant candidates, compacted in order (block-wide, chunk by chunk) ----
     for (int64_t base = 0; base < n; base += blockDim.x) {
         const int64_t c = base + tid;
@@ -1675,6 +1677,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         D.meta[0] = fsize;
         D.meta[1] = S.next_seq;
     }
+#ifdef AMZ_PLR_STATS
+    __syncthreads();
+    if (tid == 0) PLR_STAT(35, clock64() - clk_e);
+#endif
 }
 
 // top-q replay lanes by score (ties -> lower lane index), single CTA
