@@ -22,7 +22,10 @@ if mode.endswith("nod2h"):  # diagnostic: the graphs without the result read-bac
     g.host_io = True
 else:
     g.capture()
-for _ in range(5):
+import time  # noqa: E402
+
+time.sleep(2.0)  # the freshly written pinned feed settles (see bench.py)
+for _ in range(300):
     g.step()
 torch.cuda.synchronize()
 
