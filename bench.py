@@ -902,7 +902,7 @@ def _relaunch(args):
         import torch
 
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and not os.environ.get("AMZ_BENCH_ONE_DEVICE"):
             raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
@@ -957,10 +957,18 @@ def main():
     else:
         import torch
 
+        # test hooks (the multi-rank code path on a 1-GPU box): AMZ_BENCH_ONE_DEVICE=1 puts
+        # every rank on cuda:0, AMZ_BENCH_BACKEND=gloo replaces NCCL (which refuses two ranks
+        # on one device); timings from such a run are not scaling numbers
+        dev_index = 0 if os.environ.get("AMZ_BENCH_ONE_DEVICE") else local_rank
+        backend = os.environ.get("AMZ_BENCH_BACKEND", "nccl")
         if world > 1:
-            torch.cuda.set_device(local_rank)
-            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        line = run_ours(args, rank, world, local_rank)
+            torch.cuda.set_device(dev_index)
+            if backend == "nccl":
+                torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+            else:
+                torch.distributed.init_process_group(backend)
+        line = run_ours(args, rank, world, dev_index)
         if world > 1:
             torch.distributed.destroy_process_group()
     if line is not None:
