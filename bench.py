@@ -683,7 +683,10 @@ def measure_plr_parallel(dev, n, T, accel, iters, flush, world, name, config_lab
            "buffer_size": 4000, "gamma": gamma, "lambda": lam, "staleness_coef": cfg.staleness_coef,
            "replay_rate": cfg.replay_rate, "iteration_ms": it_ms,
            "levels_scored_per_s": plr.L / (it_ms * 1e-3), "env_steps_per_s": plr.L * T / (it_ms * 1e-3),
-           "collective": "NCCL all_gather_into_tensor of 48-byte candidate records" if world > 1 else "none (1 rank)"}
+           "collective": (("NCCL all_gather_into_tensor of 48-byte candidate records"
+                           if torch.distributed.get_backend() == "nccl" else
+                           f"{torch.distributed.get_backend()} all_gather of 48-byte candidate records (host-staged)")
+                          if world > 1 else "none (1 rank)")}
     if world == 1 and n <= 4096:
         # the two buffer kernels on their own: an update with 4096 distinct new levels
         # (scores U(0,1): most evict -- the worst case) and one with 4000 replays of
