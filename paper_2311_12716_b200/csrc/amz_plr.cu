@@ -930,7 +930,12 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
         }
         if (tid == 0) S.tie_max = 0ull;
         __syncthreads();
-        atomicMax(&S.tie_max, tmax);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, tmax, o);
+            tmax = y > tmax ? y : tmax;
+        }
+        if ((tid & 31) == 0) atomicMax(&S.tie_max, tmax);  // one per warp (not 1024 on one word)
         __syncthreads();
         const int tbits = 64 - __clzll((long long)(S.tie_max | 1ull));
         RunSort(S.r1.sort).Sort(keys, vals, 0, tbits);
@@ -1246,8 +1251,12 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         S.qmax = D.meta[1] + n;
     }
     __syncthreads();
+#ifdef AMZ_PLR_STATS
+    if (tid == 0) PLR_STAT(36, clock64() - clk_a);
+#endif
     {
         long long lmn = iter, lmx = iter, qmn = S.qmin, lm0 = INT64_MIN;
+#pragma unroll 4
         for (int i = tid; i < size0; i += blockDim.x) {
             const long long l = D.last[i], q = D.seq[i];
             lmn = l < lmn ? l : lmn;
@@ -1255,10 +1264,22 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             lm0 = l > lm0 ? l : lm0;
             qmn = q < qmn ? q : qmn;
         }
-        atomicMin((long long *)&S.lmin, lmn);
-        atomicMax((long long *)&S.lmax, lmx);
-        atomicMax((long long *)&S.last_max0, lm0);
-        atomicMin((long long *)&S.qmin, qmn);
+        // warp reductions first: 1024 threads' 64-bit shared atomics on four words serialise
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long a = __shfl_xor_sync(0xFFFFFFFFu, lmn, o), b = __shfl_xor_sync(0xFFFFFFFFu, lmx, o);
+            const long long c = __shfl_xor_sync(0xFFFFFFFFu, lm0, o), d = __shfl_xor_sync(0xFFFFFFFFu, qmn, o);
+            lmn = a < lmn ? a : lmn;
+            lmx = b > lmx ? b : lmx;
+            lm0 = c > lm0 ? c : lm0;
+            qmn = d < qmn ? d : qmn;
+        }
+        if (lane == 0) {
+            atomicMin((long long *)&S.lmin, lmn);
+            atomicMax((long long *)&S.lmax, lmx);
+            atomicMax((long long *)&S.last_max0, lm0);
+            atomicMin((long long *)&S.qmin, qmn);
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -1273,19 +1294,47 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         if (tid == 0) atomicOr(err, 4);
         return;
     }
+#ifdef AMZ_PLR_STATS
+    if (tid == 0) PLR_STAT(37, clock64() - clk_a);
+#endif
     double my_min = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-    for (int i = tid; i < size0; i += blockDim.x) {
-        const double sc = D.score[i];
-        S.key[i] = score_key(sc);
-        S.tie[i] = tie_pack(S, D.last[i], D.seq[i]);
-        my_min = fmin(my_min, sc);
-        uint4 w;
-        uint32_t p0, p1;
-        level_key(D.levels + i, w, p0, p1);
-        uint32_t h = level_hash(w, p0 ^ (p1 << 24)) & (kHash - 1);
-        while (atomicCAS(&S.u.hash[h], 0u, (uint32_t)(i + 1)) != 0u) h = (h + 1) & (kHash - 1);
+    // keys, tie keys and the key hash.  The hash is built in two steps: every entry stores
+    // itself into its home slot (plain stores, one wins per slot), then only the losers
+    // insert by atomicCAS from the next slot on -- four times fewer shared atomics than a
+    // CAS per entry, which serialised (~12k cycles for K = 4000).  Linear probing stays
+    // valid: a loser's run from its home slot to its place is occupied when it lands.
+    static_assert(kPlrMaxK <= 4 * kPlrThreads, "four buffer entries per thread");
+    uint32_t hh[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int i = tid + k * kPlrThreads;
+        hh[k] = 0u;
+        if (i < size0) {
+            const double sc = D.score[i];
+            const long long la = D.last[i], sq = D.seq[i];
+            uint4 w;
+            uint32_t p0, p1;
+            level_key(D.levels + i, w, p0, p1);
+            S.key[i] = score_key(sc);
+            S.tie[i] = tie_pack(S, la, sq);
+            my_min = fmin(my_min, sc);
+            hh[k] = level_hash(w, p0 ^ (p1 << 24)) & (kHash - 1);
+            S.u.hash[hh[k]] = (uint32_t)(i + 1);
+        }
     }
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int i = tid + k * kPlrThreads;
+        if (i < size0 && S.u.hash[hh[k]] != (uint32_t)(i + 1)) {
+            uint32_t h = (hh[k] + 1u) & (kHash - 1);
+            while (atomicCAS(&S.u.hash[h], 0u, (uint32_t)(i + 1)) != 0u) h = (h + 1) & (kHash - 1);
+        }
+    }
+    __syncthreads();
+#ifdef AMZ_PLR_STATS
+    if (tid == 0) PLR_STAT(38, clock64() - clk_a);
+#endif
     for (int64_t c = tid; c < n; c += blockDim.x) {
         uint4 w;
         uint32_t p0, p1;

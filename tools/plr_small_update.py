@@ -46,7 +46,7 @@ for kind, n in (("new", 4), ("new", 64), ("inplace", 4), ("inplace", 4096), ("ne
     line = f"{kind} n={n}: {sorted(ts)[2]:.1f} us"
     if fn:
         fn(stats, 1)
-        line += f"  cyc A {stats[34]} B {stats[11]} C {stats[12]} epi {stats[35]} rebuild {stats[18]}x{stats[9]} warp0 {stats[16]}"
+        line += f"  cyc A {stats[34]} B {stats[11]} C {stats[12]} epi {stats[35]} rebuild {stats[18]}x{stats[9]} warp0 {stats[16]} A-marks {stats[36]},{stats[37]},{stats[38]}"
         if len(sys.argv) > 1:
             names = ["seq", "seq_inplace", "bulk_runs", "bulk_cands", "insert_calls", "insert_passes", "run_cands",
                      "relevant", "calls", "cache_rebuilds", "batched", "cyc_B", "cyc_C", "batch_steps", "cyc_batch"]
