@@ -107,6 +107,7 @@ class DRIterationGraph:
             self.host_inputs = self._views(self._host_raw)
             self.host_result = pinned_empty((2, B), torch.float64)
         self.graphs = []
+        self._iter_stream = torch.cuda.Stream(device=dev)  # the counter advance beside GAE
         self._step_count = 0
         self._pending_h2d = False
         if self.overlap:
@@ -125,19 +126,24 @@ class DRIterationGraph:
         return 5 + (0 if not self.host_io else 1 + (0 if self.copy_engine else 1))
 
     def _kernels(self, inp):
-        """The step's kernels on the current stream."""
+        """The step's kernels on the current stream; the iteration counter advances on a
+        side branch beside GAE (only the reset and the dynamics read it, both done by then)."""
         torch = self.torch
         lanes = self.benv._ensure(self.p)
         o = self.out
         st = lanes.stream()
+        cur = torch.cuda.current_stream(self.dev)
         _lib.call("amz_env_reset_dr_iter", lanes.handle, ctypes.byref(self.root_pfx), _lib.ptr(self.it_dev),
                   _lib.ptr(o["reset_view"]), _lib.ptr(o["reset_dir"]), st)
         _lib.call("amz_env_rollout_iter", lanes.handle, self.T, _lib.ptr(inp["actions"]), ctypes.byref(self.root_pfx),
                   _lib.ptr(self.it_dev), _lib.ptr(o["view"]), _lib.ptr(o["dir"]), _lib.ptr(o["rewards"]),
                   _lib.ptr(o["dones"]), _lib.ptr(o["final_view"]), _lib.ptr(o["final_dir"]), st)
+        side = self._iter_stream
+        side.wait_stream(cur)
+        _lib.call("amz_iter_advance", _lib.ptr(self.it_dev), 1, side.cuda_stream)
         gae_and_scores(o["rewards"], inp["values"], o["dones"], inp["last"], self.gamma, self.lam,
                        score_fn=self.score_fn, out=self.gae)
-        _lib.call("amz_iter_advance", _lib.ptr(self.it_dev), 1, st)
+        cur.wait_stream(side)
         del torch
 
     def _views(self, raw):
