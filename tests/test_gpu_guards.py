@@ -92,6 +92,29 @@ def test_level_and_buffer_outputs_stay_in_bounds():
     g.check()
 
 
+@pytest.mark.parametrize("n", [17, 4096, 16500])
+def test_level_generation_and_dr_reset_stay_in_bounds(n):
+    """Both level samplers (one warp per level below 16384, one thread per level from
+    there: k_sample_levels_w / _t, k_env_reset_dr / _t) write only their outputs."""
+    import ctypes
+
+    from paper_2311_12716_b200 import _lib
+
+    g = Guarded()
+    p = amz.StaticParams()
+    seed = amz.RngStream(1, (0,)).seed_prefix()
+    out = g((n, 8), torch.int32)
+    _lib.call("amz_sample_levels", ctypes.byref(p.c_struct()), ctypes.byref(seed), ctypes.c_uint32(0), None, n,
+              _lib.ptr(out), _lib.stream_handle("cuda"))
+    benv = amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, n))
+    lanes = benv._ensure(p)
+    view, dirs = g((n, 5, 5), torch.uint8), g((n,), torch.int64)
+    wrap = amz.RngStream(7, (1,)).seed_prefix()
+    _lib.call("amz_env_reset_dr", lanes.handle, ctypes.byref(seed), ctypes.byref(wrap), _lib.ptr(view), _lib.ptr(dirs),
+              lanes.stream())
+    g.check()
+
+
 def _rollout_digest(B, T, seed):
     p = amz.StaticParams()
     env = amz.AutoResetWrapper(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B)), amz.RESAMPLE)
