@@ -173,10 +173,25 @@ __global__ void __launch_bounds__(128, 7) k_env_reset_dr(Geo G, EnvDev E, amz_se
         }
     }
     __syncwarp();
-    if (lane == 0 && view) lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, sboard[warp], 1, stage[warp]);
-    __syncwarp();
-    if (view)
-        for (int j = lane; j < V * V; j += 32) view[l * V * V + j] = stage[warp][j];
+    if (view && G.see && V * V <= 32) {
+        // see-through: every cell is independent -- one lane per cell (the level is
+        // warp-uniform), instead of lane 0 rendering all V*V
+        if (lane < V * V) {
+            const int vr = lane / V, side = lane % V - V / 2, ahead = V - 1 - vr;
+            const int fr = dir_dr(L.s.d), fc = dir_dc(L.s.d);
+            const int cr = L.s.r + fr * ahead + fc * side, cc = L.s.c + fc * ahead - fr * side;
+            uint32_t code = 3u;  // off-grid
+            if (cr >= 0 && cr < G.H && cc >= 0 && cc < G.W)
+                code = (cr == L.gr && cc == L.gc) ? 2u : ((sboard[warp][cr] >> cc) & 1u);
+            view[l * V * V + lane] = (uint8_t)code;
+        }
+    } else {
+        if (lane == 0 && view)
+            lane_render<V>(L.s.r, L.s.c, L.s.d, L.gr, L.gc, G.H, G.W, G.see, sboard[warp], 1, stage[warp]);
+        __syncwarp();
+        if (view)
+            for (int j = lane; j < V * V; j += 32) view[l * V * V + j] = stage[warp][j];
+    }
     if (prep) {
         amz_seed_t sd = wrap;
         if (E.iter) {  // root.fold_in(it).fold_in(1): the iteration's auto-reset stream
