@@ -778,6 +778,29 @@ def measure_large_batch(dev, B, T, iters, flush, peak):
            "gae_score_frac": gg / peak, "levels_scored_per_s": B / (gae * 1e-3)}
     del wl
     torch.cuda.empty_cache()
+    # GAE + scores alone at 2^17 lanes (the HBM fraction at >= 2^17 lanes),
+    # synthetic rewards / dones / values of the configs' shape, L2 flushed before each
+    import paper_2311_12716_b200 as amz
+
+    B2 = 1 << 17
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    r = torch.rand((T, B2), generator=g, device=dev, dtype=torch.float64)
+    d = torch.rand((T, B2), generator=g, device=dev, dtype=torch.float64) < 1.0 / 250
+    r = torch.where(d, r, torch.zeros_like(r))
+    v = torch.rand((T, B2), generator=g, device=dev, dtype=torch.float64)
+    last = torch.rand((B2,), generator=g, device=dev, dtype=torch.float64)
+    gout = {"advantages": torch.empty_like(v), "returns": torch.empty_like(v),
+            "scores": torch.empty(B2, dtype=torch.float64, device=dev),
+            "max_returns": torch.empty(B2, dtype=torch.float64, device=dev)}
+    amz.gae_and_scores(r, v, d, last, GAMMA, LAMBDA, out=gout)
+    ms = _timed(lambda i: amz.gae_and_scores(r, v, d, last, GAMMA, LAMBDA, out=gout), iters + 2, flush, torch)
+    g2 = statistics.mean(ms)
+    gb2 = GAE_BYTES_PER_ELEM * B2 * T / (g2 * 1e-3) / 1e9
+    out["gae_score_131072"] = {"lanes": B2, "ms": g2, "GBs": gb2, "frac": gb2 / peak,
+                               "levels_scored_per_s": B2 / (g2 * 1e-3)}
+    del r, d, v, last, gout
+    torch.cuda.empty_cache()
     return out
 
 
