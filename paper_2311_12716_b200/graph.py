@@ -19,8 +19,14 @@ device input slots and the copy of the NEXT step's inputs runs on its own copy s
 while the current step computes: the copy into slot k waits (event) only for the graph
 that last read slot k, and the graph waits only for its own slot's copy, so the PCIe
 transfer and the kernels pipeline across steps instead of joining inside one replay
-(measured: 5.3 MB takes ~108 us over PCIe, the step's kernels ~90 us).  Without
-overlap the copy is the first node of the graph.
+(measured: 5.3 MB takes ~100 us over PCIe, the step's kernels ~135 us).  Host-side
+contract of that pipeline: ``step(k)`` starts copying ``host_inputs`` for step k+1, so
+the staging must hold step k+1's inputs when ``step(k)`` is called (the first step's
+inputs are copied by ``prefetch()``, which ``step`` calls if needed) and must not be
+rewritten until ``step(k+1)`` has been enqueued and the copy finished (synchronize, or
+keep two host stagings).  ``host_result`` holds step k's scores | max returns once the
+stream has passed step k.  Without overlap the copy is the first node of the graph and
+``host_inputs`` belong to the step being called.
 
 Results equal the eager calls bit for bit (tests/test_gpu_graph.py).
 """

@@ -59,14 +59,15 @@ def test_graph_replays_equal_eager_iterations():
         _same(gr, *_eager(root, it, acts, vals, last, p))
 
 
-@pytest.mark.parametrize("overlap,copy_mode", [(False, "auto"), (True, "kernel"), (True, "engine"), (True, "auto")])
+@pytest.mark.parametrize("overlap,copy_mode,streams", [(False, "auto", 1), (True, "kernel", 1), (True, "engine", 1),
+                                                       (True, "engine", 3), (True, "auto", 1)])
 @pytest.mark.parametrize("vdt", [torch.float64, torch.float32])
-def test_graph_host_io(overlap, copy_mode, vdt):
+def test_graph_host_io(overlap, copy_mode, streams, vdt):
     p = amz.StaticParams()
     root = amz.RngStream.from_seed(3)
     acts, vals, last = _inputs(2, vdt)
     gr = DRIterationGraph(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B)), root, T, p, G, L,
-                          value_dtype=vdt, host_io=True, overlap=overlap, copy_mode=copy_mode)
+                          value_dtype=vdt, host_io=True, overlap=overlap, copy_mode=copy_mode, copy_streams=streams)
     gr.host_inputs["actions"].copy_(acts.cpu())
     gr.host_inputs["values"].copy_(vals.cpu())
     gr.host_inputs["last"].copy_(last.cpu())
