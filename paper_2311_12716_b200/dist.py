@@ -83,6 +83,10 @@ def all_gather_records(rec):
 
 
 def gather_candidates(levels, scores, max_returns):
+    """Every rank's candidates in global lane order; a 1-rank world passes them through
+    (no record packing: it cost 6 device copies per iteration)."""
+    if world()[1] == 1:
+        return levels, scores, max_returns
     return unpack_candidates(all_gather_records(pack_candidates(levels, scores, max_returns)))
 
 
