@@ -502,6 +502,9 @@ struct UpdSmem {
     int hist[256];
     int sel_b, sel_below, sel_cnt;
     int cvalid;
+    uint64_t bmk, bmt;  // bulk run: the bottom cache's maximum
+    int bulk_bad;       // bulk run: updated entries that touch the cache ...
+    int bulk_list[kCache];  // ... and their slots
     double mlow;
     int64_t next_seq;
     int64_t lmin, qmin, lmax, qmax, last_max0;
@@ -1681,15 +1684,70 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 PLR_STAT(3, arg - lo);
             }
             const int hi = arg;
+            // the bottom cache survives the run if no updated entry is in it or lands at or
+            // below its maximum (every entry outside then still lies above the maximum)
+            const bool cv = S.cvalid != 0;
+            if (tid < 32 && cv) {
+                uint64_t k = 0, t = 0;
+                bool has = false;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int j = tid + 32 * h;
+                    if (S.cslot[j] >= 0) {
+                        const uint64_t kj = S.ckey[j], tj = S.ctie[j];
+                        if (!has || !ukey_le(kj, tj, k, t)) {
+                            k = kj;
+                            t = tj;
+                        }
+                        has = true;
+                    }
+                }
+                const int win = warp_lex_pick(has, k, t, true, tid);
+                if (tid == win) {
+                    S.bmk = k;
+                    S.bmt = t;
+                }
+            }
+            if (tid == 0) S.bulk_bad = 0;
             for (int i = lo + tid; i < hi; i += blockDim.x)
                 atomicMax(&S.mr_src[cand_present(S, W, i)], S.u.chunk.cid[i]);
             __syncthreads();
             for (int i = lo + tid; i < hi; i += blockDim.x) {
                 const int p = cand_present(S, W, i);
-                if (S.mr_src[p] == S.u.chunk.cid[i]) S.key[p] = score_key(S.u.chunk.sc[i]);
+                if (S.mr_src[p] == S.u.chunk.cid[i]) {
+                    const uint64_t nk = score_key(S.u.chunk.sc[i]);
+                    S.key[p] = nk;
+                    if (cv && (S.incache[p] || ukey_le(nk, S.tie[p], S.bmk, S.bmt))) {
+                        const int j = atomicAdd(&S.bulk_bad, 1);  // entries the cache must absorb
+                        if (j < kCache) S.bulk_list[j] = p;
+                    }
+                }
             }
             __syncthreads();
-            if (tid == 0) S.cvalid = 0;
+            const int nb = S.bulk_bad;
+            if (nb > kCache) {
+                if (tid == 0) S.cvalid = 0;  // too many: rebuilt when next needed
+            } else if (nb > 0 && tid < 32) {
+                // warp 0 replays them into the cache (a changed member: rekey; an outside
+                // entry now at or below the maximum: insert) -- a few warp operations each
+                // instead of the CTA-wide rebuild
+                BottomCache bc;
+                bc.load(S, tid);
+                for (int j = 0; j < nb && bc.valid; j++) {
+                    const int p = S.bulk_list[j];
+                    const uint64_t k = S.key[p], t = S.tie[p];
+                    int wl, ww;
+                    bc.find(p, wl, ww);
+                    if (wl >= 0)
+                        bc.rekey(p, wl, ww, k, t, tid);
+                    else if (ukey_le(k, t, bc.mk, bc.mt))
+                        bc.insert(p, k, t, tid);
+                }
+                __syncwarp();
+                bc.store(S, tid);
+            }
+            __syncthreads();
+            if (tid == 0 && nb > kCache) PLR_STAT(39, 1);
             base += hi;
             continue;
         }

@@ -26,7 +26,7 @@ last = torch.rand((L,), generator=g, device="cuda", dtype=torch.float64) * 0.2
 fn = _lib.lib().amz_debug_plr_stats
 buf = (ctypes.c_ulonglong * 40)()
 names = ["seq", "seq_inplace", "bulk_runs", "bulk_cands", "insert_calls", "insert_passes", "run_cands", "relevant",
-         "calls", "cache_rebuilds", "batched", "cyc_B", "cyc_C", "batch_steps", "cyc_batch", "cyc_inplace_scan", "cyc_warp0", "warp0_sections", "cyc_rebuild", "cyc_insert_runs", "cyc_scalar", "n_scalar", "cyc_scalar_pre", "cyc_inplace_body", "cyc_fill", "n_fill", "cyc_evict_argmin", "n_evict", "cyc_evict_full", "n_evict_acc", "probes_gread", "probes", "cyc_probe_eval", "n_probe_eval", "cyc_A", "cyc_epilogue"]
+         "calls", "cache_rebuilds", "batched", "cyc_B", "cyc_C", "batch_steps", "cyc_batch", "cyc_inplace_scan", "cyc_warp0", "warp0_sections", "cyc_rebuild", "cyc_insert_runs", "cyc_scalar", "n_scalar", "cyc_scalar_pre", "cyc_inplace_body", "cyc_fill", "n_fill", "cyc_evict_argmin", "n_evict", "cyc_evict_full", "n_evict_acc", "probes_gread", "probes", "cyc_probe_eval", "n_probe_eval_or_bulk_nocache", "cyc_A", "cyc_epilogue", "x36", "x37", "x38", "bulk_invalidating"]
 for it in range(6):
     fn(buf, 1)
     r = plr.iteration(it, acts, vals, last)
