@@ -1174,7 +1174,25 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
         }
     }
     __syncthreads();
-    if (tid == 0) S.cvalid = 0;  // the bottom cache is rebuilt when next needed
+    // the bottom cache straight from the sorted buffer (no radix-select rebuild): the
+    // remaining virtual free slots (key 0) sort first, then the real entries in (score,
+    // tie) order -- the first kCache of those
+    {
+        const int sz = S.size, first = E - sz, c = sz < kCache ? sz : kCache;
+        for (int i = tid; i < kPlrMaxK; i += blockDim.x) S.incache[i] = 0;
+        __syncthreads();
+        if (tid < kCache) {
+            int slot = -1;
+            if (tid < c) {
+                slot = S.r1.e.eslot[first + tid];
+                S.ckey[tid] = S.key[slot];
+                S.ctie[tid] = S.tie[slot];
+                S.incache[slot] = 1;
+            }
+            S.cslot[tid] = slot;
+        }
+        if (tid == 0) S.cvalid = c > 0 ? 1 : 0;
+    }
     __syncthreads();
     return pos - r0;
 }
