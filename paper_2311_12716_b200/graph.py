@@ -57,7 +57,13 @@ class DRIterationGraph:
     run in order (the graph advances its device counter), a jump costs one small
     synchronous copy.  Outputs live in ``self.out`` (trajectory tensors), ``self.gae``
     (advantages / returns / scores / max_returns) and, with ``host_io``, ``self.host_result``
-    (pinned float64 [2, B]: scores | max returns of the last completed step)."""
+    (pinned float64 [2, B]: scores | max returns of the last completed step).
+
+    host_io options: ``overlap`` pipelines the feed one step ahead on its own stream;
+    ``copy_mode`` picks the H2D path ("kernel": ``amz_copy_h2d`` with ``copy_ctas`` CTAs,
+    "engine": copy-engine memcpy split over ``copy_streams`` streams, "auto": the kernel
+    until ``calibrate()`` -- run once by itself after ``calibrate_after`` steps -- times
+    both and keeps the faster)."""
 
     def __init__(self, benv: VectorBatchEnv, root_rng, T: int, params, gamma: float, lam: float,
                  score_fn: str = "maxmc", value_dtype=None, host_io: bool = False, overlap: bool = True,
@@ -89,8 +95,8 @@ class DRIterationGraph:
         self.it_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.next_it = 0
         nbuf = 2 if self.overlap else 1
-        # one contiguous byte buffer per input slot (values | last values | actions), so the
-        # host->device copy is two large copies (one per DMA engine) instead of three
+        # one contiguous byte buffer per input slot (values | last values | actions): the
+        # host->device feed is one copy (or copy_streams pieces with the copy engine)
         es = torch.empty((), dtype=self.vdt).element_size()
         self._nv, self._nl, self._na = T * B * es, B * es, T * B
         self._nbytes = self._nv + self._nl + self._na
