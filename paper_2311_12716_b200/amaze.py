@@ -39,13 +39,19 @@ def _split_key(rng: RngStream):
     return RngStream(rng.entropy, rng.key[:-1]), rng.key[-1]
 
 
-def sample_levels(rng, n: int, params: StaticParams, lane0: int = 0, lane_ids=None, device=None):
-    """Levels for keys rng.key + (lane0 + i,) (or + (lane_ids[i],)) -> int32 [n, 8] on device."""
+def sample_levels(rng, n: int, params: StaticParams, lane0: int = 0, lane_ids=None, device=None, out=None):
+    """Levels for keys rng.key + (lane0 + i,) (or + (lane_ids[i],)) -> int32 [n, 8] on device
+    (into ``out``, a contiguous int32 [n, 8] device tensor, when given)."""
     torch = _torch()
     p = as_params(params).validate()
     rng = as_stream(rng)
-    dev = device or torch.device("cuda", torch.cuda.current_device())
-    out = torch.empty((n, 8), dtype=torch.int32, device=dev)
+    if out is not None:
+        if out.shape != (n, 8) or out.dtype != torch.int32 or not out.is_contiguous() or not out.is_cuda:
+            raise ContractViolation("out must be a contiguous int32 [n, 8] CUDA tensor")
+        dev = out.device
+    else:
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        out = torch.empty((n, 8), dtype=torch.int32, device=dev)
     ids = None
     if lane_ids is not None:
         ids = torch.as_tensor(lane_ids, device=dev).to(torch.int32).contiguous()
@@ -57,8 +63,10 @@ def sample_levels(rng, n: int, params: StaticParams, lane0: int = 0, lane_ids=No
     return out
 
 
-def mutate_levels(rng, parents, n_edits: int, params: StaticParams, lane0: int = 0, parent_idx=None, n=None):
-    """ACCEL edits: out[i] = mutate(parents[parent_idx[i]] or parents[i], key rng.key + (lane0+i,))."""
+def mutate_levels(rng, parents, n_edits: int, params: StaticParams, lane0: int = 0, parent_idx=None, n=None,
+                  out=None):
+    """ACCEL edits: out[i] = mutate(parents[parent_idx[i]] or parents[i], key rng.key + (lane0+i,))
+    (into ``out``, a contiguous int32 [n, 8] device tensor, when given)."""
     torch = _torch()
     p = as_params(params).validate()
     rng = as_stream(rng)
@@ -70,7 +78,10 @@ def mutate_levels(rng, parents, n_edits: int, params: StaticParams, lane0: int =
         n = idx.numel()
     elif n is None:
         n = parents.shape[0]
-    out = torch.empty((n, 8), dtype=torch.int32, device=parents.device)
+    if out is None:
+        out = torch.empty((n, 8), dtype=torch.int32, device=parents.device)
+    elif out.shape != (n, 8) or out.dtype != torch.int32 or not out.is_contiguous() or out.device != parents.device:
+        raise ContractViolation("out must be a contiguous int32 [n, 8] tensor on the parents' device")
     seed = rng.seed_prefix()
     _lib.call("amz_mutate_levels", ctypes.byref(p.c_struct()), ctypes.byref(seed), ctypes.c_uint32(lane0), n,
               _lib.ptr(parents.contiguous()), _lib.ptr(idx), int(n_edits), _lib.ptr(out),

@@ -108,15 +108,23 @@ class LevelBuffer:
         if n > 0:
             self.nonempty = True
 
-    def sample(self, rng, n: int, it: int):
-        """n replay draws -> dict(slots i32, levels [n, 8], max_returns f64, scores f64)."""
+    def sample(self, rng, n: int, it: int, out: dict | None = None):
+        """n replay draws -> dict(slots i32, levels [n, 8], max_returns f64, scores f64);
+        ``out`` may supply any of those tensors (contiguous, on the buffer's device) to be
+        written in place."""
         torch = _torch()
         if not self.nonempty:
             raise ContractViolation("cannot sample from an empty level buffer")
-        out = {"slots": torch.empty(n, dtype=torch.int32, device=self.device),
-               "levels": torch.empty((n, 8), dtype=torch.int32, device=self.device),
-               "max_returns": torch.empty(n, dtype=torch.float64, device=self.device),
-               "scores": torch.empty(n, dtype=torch.float64, device=self.device)}
+        want = {"slots": ((n,), torch.int32), "levels": ((n, 8), torch.int32),
+                "max_returns": ((n,), torch.float64), "scores": ((n,), torch.float64)}
+        given = dict(out or {})
+        for k, (shape, dt) in want.items():
+            t = given.get(k)
+            if t is not None and (tuple(t.shape) != shape or t.dtype != dt or not t.is_contiguous()
+                                  or t.device != self.device):
+                raise ContractViolation(f"out[{k!r}] must be a contiguous {dt} {list(shape)} tensor on {self.device}")
+        out = {k: (given[k] if given.get(k) is not None else torch.empty(shape, dtype=dt, device=self.device))
+               for k, (shape, dt) in want.items()}
         seed = as_stream(rng).seed_prefix()
         if self.cfg.prioritization == "proportional":  # P_S ~ score^(1/beta), SPEC.md:367
             _lib.call("amz_plr_sample_proportional", self.handle, ctypes.byref(seed), n,

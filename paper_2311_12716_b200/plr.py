@@ -87,6 +87,8 @@ class ParallelPLR:
             ids = torch.arange(lo, hi, device=dev, dtype=torch.int32)
             levels = sample_levels(itr.fold_in(1), hi - lo, self.p, lane_ids=ids, device=dev)
             return levels, torch.zeros(hi - lo, dtype=torch.float64, device=dev), 0
+        if self.world == 1:
+            return self._compose_local(itr, it)
         parts, priors = [], []
         # new lanes [0, n)
         a, b = max(lo, 0), min(hi, n)
@@ -111,6 +113,28 @@ class ParallelPLR:
                                            lane0=a - 2 * n, parent_idx=pidx))
                 priors.append(torch.zeros(b - a, dtype=torch.float64, device=dev))
         return torch.cat(parts), torch.cat(priors), n
+
+    def _compose_local(self, itr, it: int):
+        """compose() for a 1-rank world without staging copies: the new levels, the replay
+        draw (levels and prior max returns) and the mutants are written straight into
+        preallocated lane arrays (alternating between two sets, so an iteration's
+        ``IterationResult.levels`` stays valid through the next iteration); the prior of
+        new and mutant lanes is a zero region nothing writes."""
+        torch = _torch()
+        n, dev = self.n, self.device
+        if not hasattr(self, "_lane_bufs"):
+            self._lane_bufs = [(torch.empty((self.L, 8), dtype=torch.int32, device=dev),
+                                torch.zeros(self.L, dtype=torch.float64, device=dev)) for _ in range(2)]
+            if self.accel is not None:  # mutant j takes parent j mod q of the top-q replay lanes
+                self._pcycle = torch.arange(n, device=dev) % self.accel.subsample_size
+        lv, pr = self._lane_bufs[self.iterations & 1]
+        sample_levels(itr.fold_in(1), n, self.p, lane0=0, out=lv[:n])
+        rep = self.buffer.sample(itr.fold_in(2), n, it, out={"levels": lv[n:2 * n], "max_returns": pr[n:2 * n]})
+        if self.accel is not None:
+            top = top_q(rep["scores"], self.accel.subsample_size)
+            mutate_levels(itr.fold_in(3), lv[n:2 * n], self.accel.n_mutations, self.p, lane0=0,
+                          parent_idx=top[self._pcycle], out=lv[2 * n:3 * n])
+        return lv, pr, n
 
     # -- one iteration ---------------------------------------------------------------------
     def iteration(self, it: int, actions, values, last_values, out=None) -> IterationResult:
