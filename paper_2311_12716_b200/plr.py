@@ -223,10 +223,11 @@ class SequentialPLR:
         itr = self.root.fold_in(it)
         n, dev = self.n, self.device
         if not self.decide(it):
-            ids = torch.arange(0, n, device=dev, dtype=torch.int32)
-            levels = sample_levels(itr.fold_in(1), n, self.p, lane_ids=ids, device=dev)
-            traj, o = self._roll_score(self.env, itr.fold_in(4), levels, torch.zeros(n, dtype=torch.float64, device=dev),
-                                       actions, values, last_values, out)
+            levels = sample_levels(itr.fold_in(1), n, self.p, lane0=0, device=dev)
+            if not hasattr(self, "_zero_prior"):
+                self._zero_prior = torch.zeros(n, dtype=torch.float64, device=dev)  # read-only
+            traj, o = self._roll_score(self.env, itr.fold_in(4), levels, self._zero_prior, actions, values,
+                                       last_values, out)
             self.buffer.update(levels, o["scores"], o["max_returns"], it)
             return PerpResult("new", levels, o["scores"], o["max_returns"], None, traj, o["advantages"])
         rep = self.buffer.sample(itr.fold_in(2), n, it)
