@@ -54,7 +54,9 @@ class ParallelPLR:
     """PLR|| / ACCEL|| over n new lanes per iteration (L = 2n or 3n
     lanes globally, sharded over the torch.distributed world).  ``check_every`` > 0 runs
     the replica drift check (on-device buffer digest + one all-reduce, RunnerFault on a
-    mismatch) after every ``check_every``-th iteration when world > 1."""
+    mismatch) after every ``check_every``-th iteration when world > 1.  In a 1-rank
+    world the lane levels of an ``IterationResult`` live in internal double-buffered
+    arrays: valid until the iteration after next (clone to keep them longer)."""
 
     def __init__(self, n: int, params: StaticParams, cfg: PlrConfig, root_rng, accel: AccelConfig | None = None,
                  gamma: float = 0.995, lam: float = 0.95, device=None, check_every: int = 16):
