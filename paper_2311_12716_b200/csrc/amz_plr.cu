@@ -1532,11 +1532,11 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     const int k = bad ? __ffs(bad) - 1 : 32;
                     if (k > 0) {
                         const bool act = lane < k && ps >= 0;  // rejected absent keys change nothing
-                        const unsigned grp = __match_any_sync(0xFFFFFFFFu, act ? ps : -1 - lane);
-                        if (act && 31 - __clz(grp) == lane) {  // last writer of its slot
-                            S.key[ps] = ski;
-                            S.mr_src[ps] = ci;
-                        }
+                        // last writer per slot: candidate ids grow along the order, so the
+                        // slot's atomicMax is the last writer (match.any was slower here)
+                        if (act) atomicMax(&S.mr_src[ps], ci);
+                        __syncwarp();
+                        if (act && S.mr_src[ps] == ci) S.key[ps] = ski;
                         if (lane == 0) {
                             PLR_STAT(10, k);
                             PLR_STAT(13, 1);
