@@ -424,7 +424,7 @@ extern "C" int amz_debug_plr_stats(void *host, int reset) {
 constexpr int kRunMin = 96;   // shorter insert runs stay on the sequential warp path
 constexpr int kBulkRun = 64;  // shorter in-place runs stay on the sequential warp path
 struct CandChunk {
-    double sc[kChunk];
+    uint64_t sk[kChunk];  // score keys (score_key of the candidates' scores)
     int32_t cid[kChunk];
     int32_t tf[kChunk];
     int32_t im[kChunk];
@@ -1429,7 +1429,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
         for (int i = tid; i < cn; i += blockDim.x) {
             const int c = W.rel[base + i];
             S.u.chunk.cid[i] = c;
-            S.u.chunk.sc[i] = cscore[c];
+            S.u.chunk.sk[i] = score_key(cscore[c]);
             S.u.chunk.tf[i] = W.twin_first[c];
             S.u.chunk.im[i] = W.init_match[c];
         }
@@ -1445,10 +1445,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             // candidate fields are prefetched one ahead (the replaced bit and the twin's
             // keyslot are read after the previous candidate is applied)
             int c_n = 0, f_n = 0, im_n = -1;
-            double sc_n = 0.0;
+            uint64_t sk_n = 0ull;
             if (r < cn) {
                 c_n = S.u.chunk.cid[r];
-                sc_n = S.u.chunk.sc[r];
+                sk_n = S.u.chunk.sk[r];
                 f_n = S.u.chunk.tf[r];
                 im_n = S.u.chunk.im[r];
             }
@@ -1491,7 +1491,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                         prs = imi < 0 && fi == ci;  // certainly new
                         const uint32_t rw = S.replaced[imc >> 5];
                         const int rs = S.reslot[imc];
-                        ski = score_key(S.u.chunk.sc[i]);
+                        ski = S.u.chunk.sk[i];
                         ps = ((rw >> (imc & 31)) & 1u) ? rs : imi;
                         if (imi < 0) {
                             ps = -1;
@@ -1546,7 +1546,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                         r += k - 1;  // the loop's r++ moves past the stretch
                         if (r + 1 < cn) {
                             c_n = S.u.chunk.cid[r + 1];
-                            sc_n = S.u.chunk.sc[r + 1];
+                            sk_n = S.u.chunk.sk[r + 1];
                             f_n = S.u.chunk.tf[r + 1];
                             im_n = S.u.chunk.im[r + 1];
                         }
@@ -1557,10 +1557,10 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                 clk_sc = clock64();
 #endif
                 const int c = c_n, f = f_n, im = im_n;
-                const double sc = sc_n;
+                const uint64_t sk = sk_n;
                 if (r + 1 < cn) {
                     c_n = S.u.chunk.cid[r + 1];
-                    sc_n = S.u.chunk.sc[r + 1];
+                    sk_n = S.u.chunk.sk[r + 1];
                     f_n = S.u.chunk.tf[r + 1];
                     im_n = S.u.chunk.im[r + 1];
                 }
@@ -1586,7 +1586,6 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                     }
                     scan_end = r + L;
                 }
-                const uint64_t sk = score_key(sc);
                 if (lane == 0) PLR_STAT(0, 1);
 #ifdef AMZ_PLR_STATS
                 if (lane == 0) PLR_STAT(22, clock64() - clk_sc);
@@ -1733,7 +1732,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
             for (int i = lo + tid; i < hi; i += blockDim.x) {
                 const int p = cand_present(S, W, i);
                 if (S.mr_src[p] == S.u.chunk.cid[i]) {
-                    const uint64_t nk = score_key(S.u.chunk.sc[i]);
+                    const uint64_t nk = S.u.chunk.sk[i];
                     S.key[p] = nk;
                     if (cv && (S.incache[p] || ukey_le(nk, S.tie[p], S.bmk, S.bmt))) {
                         const int j = atomicAdd(&S.bulk_bad, 1);  // entries the cache must absorb
