@@ -1,5 +1,7 @@
 // amz_internal.h -- declarations shared by the .cu translation units (not part of the ABI).
 #pragma once
+#include <mutex>
+#include <unordered_map>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -8,6 +10,25 @@
 #include "amz_level.cuh"
 
 namespace amz {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size): made on
+// every launch it cost the rollout call ~0.4 ms of host time
+inline void ensure_dyn_smem(const void *kern, int bytes) {
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, int> done;  // (kernel, device) -> bytes already allowed
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t key = (uint64_t)(uintptr_t)kern ^ ((uint64_t)(uint32_t)dev << 52);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = done.find(key);
+        if (it != done.end() && it->second >= bytes) return;
+    }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    std::lock_guard<std::mutex> lk(mu);
+    int &b = done[key];
+    if (bytes > b) b = bytes;
+}
 
 // Programmatic dependent launch along the rollout chain (k_env_reset_dr -> k_dyn ->
 // k_render -> GAE): a dependent kernel is launched with launch_pdl, runs its

@@ -821,7 +821,7 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
                        uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, int spec_ready, cudaStream_t s) {
     const int use_lut = G.tep <= 4096;
     const size_t sm = (size_t)WPC * sizeof(DynSmem<LPW>) + (use_lut ? ((size_t)G.tep + 1) * 8 : 0);
-    cudaFuncSetAttribute(k_dyn<LPW, WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    ensure_dyn_smem((const void *)k_dyn<LPW, WPC>, (int)sm);
     const int avec = (E.B % 4 == 0) && ((((uintptr_t)actions) & 3u) == 0);
     if (mode == AMZ_RESET_RESAMPLE && !spec_ready)
         k_spec_levels<<<(unsigned)((E.B + 4 * kSpecLPW - 1) / (4 * kSpecLPW)), 128, 0, s>>>(G, E, T, wrap, step0, spec,

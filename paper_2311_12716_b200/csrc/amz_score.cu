@@ -748,13 +748,13 @@ static int launch_gae_score_t(int T, int64_t B, const double *r, const VT *v, co
     if ((gsel == 4 || (gsel == 0 && g3)) && do_gae && T <= kG4MaxT && B % 16 == 0 && aligned) {
         if (lw == 16 || gsel == 4) {
             const size_t sm = sizeof(G4Smem<16, VT>);
-            cudaFuncSetAttribute(k_gae_score4<16, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            ensure_dyn_smem((const void *)k_gae_score4<16, VT>, (int)sm);
             launch_pdl(k_gae_score4<16, VT>, dim3((unsigned)(B / 16)), dim3(128), sm, s, T, B, r, v, d, last, gamma, gl,
                        prior, score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol, P);
             return 0;
         }
         const size_t sm = sizeof(G4Smem<8, VT>);
-        cudaFuncSetAttribute(k_gae_score4<8, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        ensure_dyn_smem((const void *)k_gae_score4<8, VT>, (int)sm);
         launch_pdl(k_gae_score4<8, VT>, dim3((unsigned)(B / 8)), dim3(128), sm, s, T, B, r, v, d, last, gamma, gl, prior,
                    score_fn, disc, adv, ret, scores, maxret, s_eps, s_mean, s_max, s_sol, P);
         return 0;
@@ -762,7 +762,7 @@ static int launch_gae_score_t(int T, int64_t B, const double *r, const VT *v, co
     if (g7 && (gsel == 0 || gsel == 7)) {
         static const int m7 = getenv("AMZ_GAE_M") ? atoi(getenv("AMZ_GAE_M")) : 0;  // CTAs per SM (tuning)
         auto go = [&](auto kern, size_t sm) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            ensure_dyn_smem((const void *)kern, (int)sm);
             int dev = 0, nsm = 148, occ = 1;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
