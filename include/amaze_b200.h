@@ -114,6 +114,10 @@ int amz_host_free(void *p);
  * _int_to_uint32_array), key = RngStream key prefix words.  The full spawn key is
  * prefix ++ suffix with a non-empty suffix, so the run entropy is zero-padded to 4. */
 int amz_seed_prefix(const uint32_t *run, int n_run, const uint32_t *key, int n_key, amz_seed_t *out);
+/* Host only: the first Generator.random() of the stream (numpy's Philox of the key's
+ * SeedSequence: (first u64 >> 11) * 2^-53) -- the replay decision of
+ * buffer_sample_decision without building a numpy Generator. */
+int amz_stream_uniform(const amz_seed_t *prefix, double *out_host);
 
 /* DR levels: out[i] = sample_random_level(key = prefix ++ [lane_ids ? lane_ids[i] : lane0 + i]). */
 int amz_sample_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t lane0,

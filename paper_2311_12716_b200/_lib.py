@@ -42,6 +42,7 @@ _SIGS = {
     "amz_last_error": ([], ctypes.c_char_p),
     "amz_validate_params": ([ctypes.POINTER(AmzParams)], I32),
     "amz_seed_prefix": ([P, I32, P, I32, ctypes.POINTER(AmzSeed)], I32),
+    "amz_stream_uniform": ([ctypes.POINTER(AmzSeed), P], I32),
     "amz_sample_levels": ([ctypes.POINTER(AmzParams), ctypes.POINTER(AmzSeed), U32, P, I64, P, VP], I32),
     "amz_mutate_levels": ([ctypes.POINTER(AmzParams), ctypes.POINTER(AmzSeed), U32, I64, P, P, I32, P, VP], I32),
     "amz_check_levels": ([ctypes.POINTER(AmzParams), P, I64, ctypes.POINTER(ctypes.c_int64), VP], I32),

@@ -215,6 +215,15 @@ int amz_seed_prefix(const uint32_t *run, int n_run, const uint32_t *key, int n_k
     return 0;
 }
 
+int amz_stream_uniform(const amz_seed_t *prefix, double *out) {
+    if (!prefix || !out) return fail(AMZ_ECONFIG, "null argument");
+    uint64_t k0, k1, o0, o1, o2, o3;
+    seed_key(*prefix, k0, k1);
+    philox_block(1ull, k0, k1, o0, o1, o2, o3);  // numpy pre-increments the counter
+    *out = (double)(o0 >> 11) * (1.0 / 9007199254740992.0);
+    return 0;
+}
+
 int amz_sample_levels(const amz_params_t *p, const amz_seed_t *prefix, uint32_t lane0, const uint32_t *lane_ids,
                       int64_t n, amz_level_t *out, void *stream) {
     int rc = amz_validate_params(p);

@@ -120,3 +120,19 @@ def test_plr_perp_oracle_spec_examples():
     calls.clear()
     out = plr_np.plr_perp_iteration(buf2, 1, (), 1, 8, p, cfg, fake_rollout, accel=(4, 20))
     assert out["branch"] == "replay" and len(out["mutants"]) == 4 and calls == ["main", "mutants"]
+
+
+def test_stream_uniform_matches_numpy():
+    """amz_stream_uniform (host C) == numpy's first Generator.random() of the stream."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2311_12716_b200 import RngStream, _lib
+
+    for entropy, key in [(0, ()), (7, (3,)), (11, (5, 0)), (2 ** 40 + 3, (1, 2, 3)), (123456789, (2 ** 31 + 5, 9))]:
+        s = RngStream(entropy, key)
+        u = ctypes.c_double(0.0)
+        _lib.call("amz_stream_uniform", ctypes.byref(s.seed_prefix()), ctypes.byref(u))
+        want = np.random.Generator(np.random.Philox(np.random.SeedSequence(entropy=entropy, spawn_key=key))).random()
+        assert u.value == want, (entropy, key)
