@@ -45,3 +45,10 @@ cost("rollout_actions", lambda i: amz.rollout_actions(env, start, acts, P))
 cost("gae_and_scores", lambda i: amz.gae_and_scores(traj.rewards, vals, traj.dones, last, 0.995, 0.98))
 cost("buffer.update", lambda i: buf.update(lv, o["scores"], o["max_returns"], i + 1))
 cost("buffer.sample", lambda i: buf.sample(root.fold_in(i), n, i + 100))
+renv = amz.AutoResetWrapper(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, n)), amz.RESAMPLE)
+renv.reset(root, P)
+res0 = renv.reset(root, P)
+torch.cuda.synchronize()
+cost("DR reset (RESAMPLE)", lambda i: renv.reset(root.fold_in(i), P))
+cost("rollout RESAMPLE", lambda i: amz.rollout_actions(renv, res0, acts, P))
+cost("flush fill_ 256MB", lambda i: vals.fill_(0.5))
