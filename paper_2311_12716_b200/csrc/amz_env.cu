@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(128) k_mutate_levels(Geo G, amz_seed_t prefix,
                                                        const amz_level_t *__restrict__ parents,
                                                        const int32_t *__restrict__ pidx, int n_edits,
                                                        amz_level_t *__restrict__ out) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     amz_seed_t s = prefix;
@@ -84,6 +85,7 @@ template <int V>
 __global__ void __launch_bounds__(128) k_env_reset(Geo G, EnvDev E, const amz_level_t *__restrict__ levels,
                                                    const int64_t *__restrict__ lanes, int64_t n,
                                                    uint8_t *__restrict__ view, int64_t *__restrict__ dirs) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     __shared__ uint8_t stage[128 * V * V];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(128) k_env_observe(Geo G, EnvDev E, uint8_t *_
 }
 
 __global__ void k_env_levels(EnvDev E, amz_level_t *__restrict__ out) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= E.B) return;
     LaneRec L = unpack_st(E.st[l]);
@@ -454,7 +457,8 @@ int launch_mutate_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0,
                          const int32_t *pidx, int n_edits, amz_level_t *out, cudaStream_t s) {
     if (n <= 0) return 0;
     const int nt = lanes_per_cta(n);
-    k_mutate_levels<<<blocks_for(n, nt), nt, 0, s>>>(G, prefix, lane0, n, par, pidx, n_edits, out);
+    launch_pdl(k_mutate_levels, dim3((unsigned)blocks_for(n, nt)), dim3(nt), 0, s, G, prefix, lane0, n, par, pidx, n_edits,
+               out);
     return 0;
 }
 
@@ -477,7 +481,8 @@ int launch_check_levels(const Geo &G, const amz_level_t *lv, int64_t n, unsigned
 int launch_env_reset(const Geo &G, const EnvDev &E, const amz_level_t *lv, const int64_t *lanes, int64_t n,
                      uint8_t *view, int64_t *dirs, cudaStream_t s) {
     if (n <= 0) return 0;
-    AMZ_DISPATCH_V(G.V, (k_env_reset<VT><<<blocks_for(n, 128), 128, 0, s>>>(G, E, lv, lanes, n, view, dirs)));
+    AMZ_DISPATCH_V(G.V, (launch_pdl(k_env_reset<VT>, dim3((unsigned)blocks_for(n, 128)), dim3(128), 0, s, G, E, lv,
+                                    lanes, n, view, dirs)));
     return 0;
 }
 
@@ -546,7 +551,7 @@ int launch_env_observe(const Geo &G, const EnvDev &E, uint8_t *view, int64_t *di
 }
 
 int launch_env_levels(const EnvDev &E, amz_level_t *out, cudaStream_t s) {
-    if (E.B > 0) k_env_levels<<<blocks_for(E.B, 256), 256, 0, s>>>(E, out);
+    if (E.B > 0) launch_pdl(k_env_levels, dim3((unsigned)blocks_for(E.B, 256)), dim3(256), 0, s, E, out);
     return 0;
 }
 

@@ -209,6 +209,7 @@ __device__ __forceinline__ void rank_keys(const PlrDev &D, int j, uint64_t &k, u
     q = (uint64_t)D.seq[j] ^ 0x8000000000000000ull;     // signed -> unsigned order
 }
 __global__ void __launch_bounds__(kRankThreads) k_plr_rank(PlrDev D, int32_t *__restrict__ rank) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     __shared__ uint64_t sk[kRankJ];
     __shared__ uint64_t sq[kRankJ];
     const int size = (int)D.meta[0];
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
                  double rho, const double *__restrict__ lut, int prop, double inv_beta, int64_t iter,
                  int32_t *__restrict__ slots_out, amz_level_t *__restrict__ levels_out, double *__restrict__ maxret_out,
                  double *__restrict__ score_out, int *__restrict__ err) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     extern __shared__ __align__(16) uint8_t smraw[];
     SampleSmem &S = *reinterpret_cast<SampleSmem *>(smraw);
     const int tid = threadIdx.x;
@@ -1199,6 +1201,7 @@ __device__ int insert_runs(UpdSmem &S, const UpdScratch &W, const double *__rest
 
 __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W,
                                 int64_t hsize) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     // twin detection over candidates: global open-addressing table keeps min index
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
         uint4 w;
@@ -1223,6 +1226,7 @@ __global__ void k_plr_cand_prep(PlrDev D, const amz_level_t *__restrict__ cand, 
 }
 
 __global__ void k_plr_cand_twin(const amz_level_t *__restrict__ cand, int64_t n, UpdScratch W, int64_t hsize) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
         uint4 w;
         uint32_t p0, p1;
@@ -1244,6 +1248,7 @@ __device__ __forceinline__ int bits_for(uint64_t span) { return span ? 64 - __cl
 __global__ void __launch_bounds__(kPlrThreads, 1)
     k_plr_update(PlrDev D, const amz_level_t *__restrict__ cand, const double *__restrict__ cscore,
                  const double *__restrict__ cmax, int64_t n, int64_t iter, UpdScratch W, int *err) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     extern __shared__ __align__(16) uint8_t smraw[];
     UpdSmem &S = *reinterpret_cast<UpdSmem *>(smraw);
     __shared__ int wscan[33];
@@ -1809,6 +1814,7 @@ __global__ void __launch_bounds__(kPlrThreads, 1)
 
 // top-q replay lanes by score (ties -> lower lane index), single CTA
 __global__ void k_top_q(const double *__restrict__ scores, int64_t n, int q, int32_t *__restrict__ out) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     __shared__ double bs[32];
     __shared__ int bi[32];
     __shared__ int chosen[64];
@@ -1911,12 +1917,12 @@ int launch_plr_sample(const PlrDev &D, int32_t *rank, const amz_seed_t &key, int
     }
     if (!prop) {  // ranks only for rank prioritisation
         cudaMemsetAsync(rank, 0, (size_t)D.K * sizeof(int32_t), s);
-        k_plr_rank<<<dim3((unsigned)((D.K + kRankThreads - 1) / kRankThreads),
-                          (unsigned)((D.K + kRankJ - 1) / kRankJ)),
-                     kRankThreads, 0, s>>>(D, rank);
+        launch_pdl(k_plr_rank, dim3((unsigned)((D.K + kRankThreads - 1) / kRankThreads),
+                                   (unsigned)((D.K + kRankJ - 1) / kRankJ)),
+                   dim3(kRankThreads), 0, s, D, rank);
     }
-    k_plr_sample<<<1, kPlrThreads, sizeof(SampleSmem), s>>>(D, rank, key, n, omr, rho, lut, prop, inv_beta, iter, slots,
-                                                             levels, maxret, score, err);
+    launch_pdl(k_plr_sample, dim3(1), dim3(kPlrThreads), sizeof(SampleSmem), s, D, (const int32_t *)rank, key, n,
+               omr, rho, lut, prop, inv_beta, iter, slots, levels, maxret, score, err);
     return 0;
 }
 
@@ -1934,14 +1940,14 @@ int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs
     while (hsize < 2 * n) hsize <<= 1;
     cudaMemsetAsync(W.chash, 0, hsize * sizeof(uint32_t), s);
     const int g = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
-    k_plr_cand_prep<<<g, 256, 0, s>>>(D, cand, n, W, hsize);
-    k_plr_cand_twin<<<g, 256, 0, s>>>(cand, n, W, hsize);
-    k_plr_update<<<1, kPlrThreads, sizeof(UpdSmem), s>>>(D, cand, cs, cm, n, iter, W, err);
+    launch_pdl(k_plr_cand_prep, g, dim3(256), 0, s, D, cand, n, W, hsize);
+    launch_pdl(k_plr_cand_twin, g, dim3(256), 0, s, cand, n, W, hsize);
+    launch_pdl(k_plr_update, dim3(1), dim3(kPlrThreads), sizeof(UpdSmem), s, D, cand, cs, cm, n, iter, W, err);
     return 0;
 }
 
 int launch_top_q(const double *scores, int64_t n, int q, int32_t *out, cudaStream_t s) {
-    k_top_q<<<1, 256, 0, s>>>(scores, n, q, out);
+    launch_pdl(k_top_q, dim3(1), dim3(256), 0, s, scores, n, q, out);
     return 0;
 }
 

@@ -998,6 +998,7 @@ constexpr int kGenLPW = 1;
 __global__ void __launch_bounds__(128) k_sample_levels_w(Geo G, amz_seed_t prefix, uint32_t lane0,
                                                          const uint32_t *__restrict__ lane_ids, int64_t n,
                                                          amz_level_t *__restrict__ out) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     constexpr int LPW = kGenLPW;
     __shared__ __align__(16) WarpSampler X[4];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1022,6 +1023,7 @@ __global__ void __launch_bounds__(128) k_sample_levels_w(Geo G, amz_seed_t prefi
 __global__ void __launch_bounds__(64) k_sample_levels_t(Geo G, amz_seed_t prefix, uint32_t lane0,
                                                         const uint32_t *__restrict__ lane_ids, int64_t n,
                                                         amz_level_t *__restrict__ out) {
+    pdl_wait();  // PDL: the predecessor kernel has completed (its launch overlapped)
     __shared__ __align__(16) uint8_t arr[64 * kTSlice];
     const int64_t i = (int64_t)blockIdx.x * 64 + threadIdx.x;
     if ((int64_t)blockIdx.x * 64 + (threadIdx.x & ~31) >= n) return;  // whole warps only
@@ -1044,10 +1046,10 @@ int launch_sample_levels(const Geo &G, const amz_seed_t &prefix, uint32_t lane0,
     // one warp per level while the batch is small (latency), one thread per level from
     // 16384 levels on (throughput; the same levels)
     if (n >= 16384)
-        k_sample_levels_t<<<(unsigned)((n + 63) / 64), 64, 0, s>>>(G, prefix, lane0, ids, n, out);
+        launch_pdl(k_sample_levels_t, dim3((unsigned)((n + 63) / 64)), dim3(64), 0, s, G, prefix, lane0, ids, n, out);
     else
-        k_sample_levels_w<<<(unsigned)((n + 4 * kGenLPW - 1) / (4 * kGenLPW)), 128, 0, s>>>(G, prefix, lane0, ids,
-                                                                                              n, out);
+        launch_pdl(k_sample_levels_w, dim3((unsigned)((n + 4 * kGenLPW - 1) / (4 * kGenLPW))), dim3(128), 0, s, G,
+                   prefix, lane0, ids, n, out);
     return 0;
 }
 
