@@ -294,6 +294,12 @@ int amz_plr_destroy(amz_plr_t *plr);
  * New entries get last_sampled = insert iteration = iter. */
 int amz_plr_update(amz_plr_t *plr, const amz_level_t *levels_dev, const double *scores_dev,
                    const double *max_ret_dev, int64_t n, int64_t iter, void *stream);
+/* Build the twin table of the next update's candidates ahead of it (it depends on the
+ * candidate levels only), e.g. on a side stream while the candidates are being rolled
+ * out and scored; the next amz_plr_update with the same levels pointer and count skips
+ * that work.  The caller orders the streams: the update must wait for this call's stream,
+ * and this call for the previous update. */
+int amz_plr_prepare(amz_plr_t *plr, const amz_level_t *levels_dev, int64_t n, void *stream);
 
 /* buffer_sample_levels, rank prioritisation: n draws with replacement
  * = numpy Generator(key).choice(size, n, p=P), P = (1-rho) P_S + rho P_C,

@@ -83,6 +83,7 @@ _SIGS = {
     "amz_plr_create": ([I64, ctypes.POINTER(ctypes.c_void_p)], I32),
     "amz_plr_destroy": ([P], I32),
     "amz_plr_update": ([P, P, P, P, I64, I64, VP], I32),
+    "amz_plr_prepare": ([P, P, I64, VP], I32),
     "amz_plr_sample": ([P, ctypes.POINTER(AmzSeed), I64, D, P, I64, P, P, P, P, VP], I32),
     "amz_plr_sample_proportional": ([P, ctypes.POINTER(AmzSeed), I64, D, D, I64, P, P, P, P, VP], I32),
     "amz_plr_top_q": ([P, I64, I32, P, VP], I32),

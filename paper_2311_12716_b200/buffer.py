@@ -108,6 +108,17 @@ class LevelBuffer:
         if n > 0:
             self.nonempty = True
 
+    def prepare(self, levels, stream=None) -> None:
+        """Build the next update's candidate twin table now (``amz_plr_prepare``), on
+        ``stream`` (a torch stream; default the current one) -- e.g. on a side stream
+        while the candidates are rolled out.  The update with the same ``levels`` tensor
+        skips that work; the caller orders the streams (update after this, this after the
+        previous update)."""
+        torch = _torch()
+        lv = levels.to(self.device).to(torch.int32).contiguous()
+        st = stream.cuda_stream if stream is not None else self._stream()
+        _lib.call("amz_plr_prepare", self.handle, _lib.ptr(lv), lv.shape[0], st)
+
     def sample(self, rng, n: int, it: int, out: dict | None = None):
         """n replay draws -> dict(slots i32, levels [n, 8], max_returns f64, scores f64);
         ``out`` may supply any of those tensors (contiguous, on the buffer's device) to be

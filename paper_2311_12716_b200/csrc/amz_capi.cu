@@ -84,6 +84,9 @@ struct amz_plr {
     int32_t *rank = nullptr;  // [K] sampler scratch: rank - 1 of every entry
     UpdScratch W;
     int *err;
+    // candidates whose twin table amz_plr_prepare already built (consumed by the update)
+    const amz_level_t *prep_cand = nullptr;
+    int64_t prep_n = -1;
 };
 
 static int plr_scratch(amz_plr *b, int64_t n, cudaStream_t s) {
@@ -765,10 +768,29 @@ int amz_plr_update(amz_plr_t *b, const amz_level_t *levels, const double *scores
     if (n < 0) return fail(AMZ_ESHAPE, "negative candidate count");
     if (n > ((int64_t)1 << 30)) return fail(AMZ_ESHAPE, "too many candidates");
     cudaStream_t s = (cudaStream_t)stream;
+    const int prepared = b->prep_cand == levels && b->prep_n == n && n > 0;
+    b->prep_cand = nullptr;
+    b->prep_n = -1;
+    if (!prepared) {
+        int rc = plr_scratch(b, n, s);
+        if (rc) return rc;
+    }
+    launch_plr_update(b->D, levels, scores, max_ret, n, iter, b->W, b->err, s, prepared);
+    return cuda_status("plr_update");
+}
+
+int amz_plr_prepare(amz_plr_t *b, const amz_level_t *levels, int64_t n, void *stream) {
+    if (!b || (n > 0 && !levels)) return fail(AMZ_ECONFIG, "null argument");
+    DevGuard guard_(b->device);
+    if (n < 0) return fail(AMZ_ESHAPE, "negative candidate count");
+    if (n > ((int64_t)1 << 30)) return fail(AMZ_ESHAPE, "too many candidates");
+    cudaStream_t s = (cudaStream_t)stream;
     int rc = plr_scratch(b, n, s);
     if (rc) return rc;
-    launch_plr_update(b->D, levels, scores, max_ret, n, iter, b->W, b->err, s);
-    return cuda_status("plr_update");
+    launch_plr_prepare(b->D, levels, n, b->W, s);
+    b->prep_cand = levels;
+    b->prep_n = n;
+    return cuda_status("plr_prepare");
 }
 
 int amz_plr_sample(amz_plr_t *b, const amz_seed_t *key, int64_t n, double rho, const double *lut, int64_t iter,

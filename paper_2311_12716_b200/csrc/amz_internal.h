@@ -151,8 +151,9 @@ struct UpdScratch {
 int launch_plr_sample(const PlrDev &D, int32_t *rank, const amz_seed_t &key, int64_t n, double omr, double rho,
                       const double *lut, int prop, double inv_beta, int64_t iter, int32_t *slots, amz_level_t *levels,
                       double *maxret, double *score, int *err, cudaStream_t s);
+int launch_plr_prepare(const PlrDev &D, const amz_level_t *cand, int64_t n, const UpdScratch &W, cudaStream_t s);
 int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs, const double *cm, int64_t n,
-                      int64_t iter, const UpdScratch &W, int *err, cudaStream_t s);
+                      int64_t iter, const UpdScratch &W, int *err, cudaStream_t s, int prepared = 0);
 int launch_plr_digest(const PlrDev &D, int64_t *out, cudaStream_t s);
 int launch_top_q(const double *scores, int64_t n, int q, int32_t *out, cudaStream_t s);
 

@@ -1926,8 +1926,21 @@ int launch_plr_sample(const PlrDev &D, int32_t *rank, const amz_seed_t &key, int
     return 0;
 }
 
+// the candidates' twin table (k_plr_cand_prep / _twin): depends on the candidate levels
+// only, so it can run ahead of the update (amz_plr_prepare)
+int launch_plr_prepare(const PlrDev &D, const amz_level_t *cand, int64_t n, const UpdScratch &W, cudaStream_t s) {
+    if (n <= 0) return 0;
+    int64_t hsize = 1;
+    while (hsize < 2 * n) hsize <<= 1;
+    cudaMemsetAsync(W.chash, 0, hsize * sizeof(uint32_t), s);
+    const int g = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+    launch_pdl(k_plr_cand_prep, g, dim3(256), 0, s, D, cand, n, W, hsize);
+    launch_pdl(k_plr_cand_twin, g, dim3(256), 0, s, cand, n, W, hsize);
+    return 0;
+}
+
 int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs, const double *cm, int64_t n,
-                      int64_t iter, const UpdScratch &W, int *err, cudaStream_t s) {
+                      int64_t iter, const UpdScratch &W, int *err, cudaStream_t s, int prepared) {
     static bool attr[kMaxDevices] = {};  // the attribute is per device
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1936,12 +1949,7 @@ int launch_plr_update(const PlrDev &D, const amz_level_t *cand, const double *cs
         if (dev < kMaxDevices) attr[dev] = true;
     }
     if (n <= 0) return 0;
-    int64_t hsize = 1;
-    while (hsize < 2 * n) hsize <<= 1;
-    cudaMemsetAsync(W.chash, 0, hsize * sizeof(uint32_t), s);
-    const int g = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
-    launch_pdl(k_plr_cand_prep, g, dim3(256), 0, s, D, cand, n, W, hsize);
-    launch_pdl(k_plr_cand_twin, g, dim3(256), 0, s, cand, n, W, hsize);
+    if (!prepared) launch_plr_prepare(D, cand, n, W, s);
     launch_pdl(k_plr_update, dim3(1), dim3(kPlrThreads), sizeof(UpdSmem), s, D, cand, cs, cm, n, iter, W, err);
     return 0;
 }

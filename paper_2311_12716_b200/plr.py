@@ -142,12 +142,26 @@ class ParallelPLR:
     def iteration(self, it: int, actions, values, last_values, out=None) -> IterationResult:
         """actions uint8 [T, L_local], values f64 [T, L_local], last_values f64 [L_local]
         (the policy side's outputs for this rank's lanes)."""
+        torch = _torch()
         levels, prior, n_replay = self.compose(it)
+        side = None
+        if self.world == 1:
+            # the update's candidate twin table depends on the levels only: build it on a
+            # side stream beside the rollout (joined before the update)
+            if not hasattr(self, "_prep_stream"):
+                self._prep_stream = torch.cuda.Stream(device=self.device)
+            side = self._prep_stream
+            cur = torch.cuda.current_stream(self.device)
+            side.wait_stream(cur)
+            self.buffer.prepare(levels, stream=side)
         start = self.env.reset_to_levels(self.root.fold_in(it).fold_in(4), levels, self.p)
         traj, _ = rollout_actions(self.env, start, actions, self.p, out=out)
         o = gae_and_scores(traj.rewards, values, traj.dones, last_values, self.gamma, self.lam, prior,
                            self.cfg.score_fn, self.cfg.maxmc_discounted)
         g_levels, g_scores, g_max = dist.gather_candidates(levels, o["scores"], o["max_returns"])
+        if side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            levels.record_stream(side)
         self.buffer.update(g_levels, g_scores, g_max, it)
         self.iterations += 1
         if self.world > 1 and self.check_every > 0 and self.iterations % self.check_every == 0:
