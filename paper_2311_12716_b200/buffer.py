@@ -115,9 +115,14 @@ class LevelBuffer:
         skips that work; the caller orders the streams (update after this, this after the
         previous update)."""
         torch = _torch()
-        lv = levels.to(self.device).to(torch.int32).contiguous()
+        # the update recognises the prepared batch by its device pointer: a converted
+        # temporary could be freed and its address reused by another batch
+        if (levels.dtype != torch.int32 or not levels.is_contiguous() or levels.device != torch.device(self.device)
+                or levels.dim() != 2 or levels.shape[1] != 8):
+            raise ContractViolation("prepare() needs the update's own levels tensor: contiguous int32 [n, 8] "
+                                    f"on {self.device}, got {levels.dtype} {tuple(levels.shape)} on {levels.device}")
         st = stream.cuda_stream if stream is not None else self._stream()
-        _lib.call("amz_plr_prepare", self.handle, _lib.ptr(lv), lv.shape[0], st)
+        _lib.call("amz_plr_prepare", self.handle, _lib.ptr(levels), levels.shape[0], st)
 
     def sample(self, rng, n: int, it: int, out: dict | None = None):
         """n replay draws -> dict(slots i32, levels [n, 8], max_returns f64, scores f64);

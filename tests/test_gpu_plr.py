@@ -268,3 +268,31 @@ def test_update_insert_runs_match_oracle(K, n, digits):
             want = ref.sample(3, (it,), 64, plr_np.PlrConfig(buffer_size=K), it)
             assert np.array_equal(out["slots"].cpu().numpy(), want)
             _assert_same(gpu, ref)
+
+
+def test_prepare_then_update_matches_oracle():
+    """amz_plr_prepare on a side stream, then the update with the same batch, equals the
+    oracle; a prepared batch is consumed once and ignored by an update with another batch."""
+    K, n = 200, 600
+    rng = np.random.default_rng(7)
+    recs = _pool(900, seed=7)
+    gpu = LevelBuffer(PlrConfig(buffer_size=K))
+    ref = plr_np.LevelBuffer(K)
+    side = torch.cuda.Stream()
+    for it in range(6):
+        idx = rng.integers(0, len(recs), n)
+        sc = rng.choice([0.0, 0.1, 0.2, 0.5], n)
+        mx = rng.uniform(0, 1, n)
+        lv = records_to_tensor(recs[idx]).cuda()
+        if it % 3 == 2:  # prepared for a different batch: must not be used
+            other = records_to_tensor(recs[rng.integers(0, len(recs), n)]).cuda()
+            gpu.prepare(other)
+        else:
+            side.wait_stream(torch.cuda.current_stream())
+            gpu.prepare(lv, stream=side)
+            torch.cuda.current_stream().wait_stream(side)
+        gpu.update(lv, torch.from_numpy(sc), torch.from_numpy(mx), it)
+        ref.update(recs[idx], sc, mx, it)
+        _assert_same(gpu, ref)
+    with pytest.raises(ContractViolation):
+        gpu.prepare(lv.to(torch.int64))
