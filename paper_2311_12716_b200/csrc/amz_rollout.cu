@@ -857,6 +857,11 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
     __shared__ __align__(16) uint8_t s_dir[4][128];
     __shared__ __align__(16) uint8_t s_done[4][128];
     __shared__ uint64_t s_spread[32];
+    // see-through 5x5: each thread's current epoch board (16 line words) staged at a
+    // 17-word stride (conflict-free), so a view row is one LDS instead of an LDG whose 32
+    // lanes hit ~20 L1 lines (records are 80 B apart)
+    constexpr int kBS = (V == 5 && SEE) ? 17 : 1;
+    __shared__ uint32_t s_brd[128 * kBS];
     if (!(V == 5 && SEE)) init_spread(s_spread);
     const int tid = threadIdx.x;
     const int64_t tile = blockIdx.x;
@@ -881,6 +886,17 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
                     ep = pr >> 12;
                     rec = epochs + ((size_t)ep * B + l) * kRec;
                     gw = rec[16];
+                    if constexpr (V == 5 && SEE) {
+                        const uint4 *r4 = reinterpret_cast<const uint4 *>(rec);
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const uint4 x = __ldg(r4 + j);
+                            s_brd[tid * kBS + 4 * j] = x.x;
+                            s_brd[tid * kBS + 4 * j + 1] = x.y;
+                            s_brd[tid * kBS + 4 * j + 2] = x.z;
+                            s_brd[tid * kBS + 4 * j + 3] = x.w;
+                        }
+                    }
                 }
                 s_dir[k][tid] = (uint8_t)((pr >> 8) & 3);
                 s_done[k][tid] = (uint8_t)((pr >> 11) & 1u);
@@ -890,7 +906,7 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
                 uint32_t w[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
                 if (live)
                     render5_see_words(pr & 15, (pr >> 4) & 15, (pr >> 8) & 3, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W,
-                                      rec, w);
+                                      s_brd + tid * kBS, w);
                 store_obs25(s_view[k], tid, live, w);  // warp-collective
             } else {
                 if (live)
