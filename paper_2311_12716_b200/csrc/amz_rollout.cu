@@ -206,51 +206,46 @@ __device__ __forceinline__ void render_lane(int r, int c, int d, int gr, int gc,
 }
 
 
-// See-through 5x5 observation (the default view) with word-level arithmetic: a view row
-// is one board word (grid row for N/S headings, grid column for E/W), its 5-cell window
-// and in-grid mask become code bytes (3 off-grid, 1 wall, 0 empty) by two
-// multiply-spreads, the S/W mirror is one byte permute, the goal byte is patched into its
-// row (it is never off-grid or a wall).  The 25 bytes come back as 7 little-endian words.
-__device__ __forceinline__ void render5_see_words(int r, int c, int d, int gr, int gc, int H, int W,
-                                                  const uint32_t *board, uint32_t (&w)[7]) {
+// See-through 5x5 observation (the default view) with word-level arithmetic, from a
+// staged board (16 line words; any index is readable, so rows off the grid read line
+// L & 15 and are overwritten by the off-grid code).  A view row is one board word (grid
+// row for N/S headings, grid column for E/W); its 5-cell window becomes code bytes
+// (3 off-grid, 1 wall, 0 empty) by one multiply-spread, the S/W mirror is a byte
+// permute.  The off-grid codes of the observation's two row kinds (in-grid line:
+// the columns outside the grid; off-grid line: all five) are built once, a row is
+// (window bits * spread) | off-grid codes -- 3 | wall = 3, so neither the window nor the
+// line needs masking -- and the goal byte is NOT patched: the caller stores it at byte
+// offset *gpos (-1: not visible) after the row words.
+__device__ __forceinline__ void render5_see_rows(int r, int c, int d, int gr, int gc, int H, int W,
+                                                 const uint32_t *board, uint32_t (&w)[7], int &gpos) {
     const bool ns = (d & 1) == 0;
     const int sgn = (d == 0 || d == 3) ? -1 : 1;
     const int base = ns ? r : c, center = ns ? c : r;
     const uint32_t nlines = (uint32_t)(ns ? H : W);
     const int llen = ns ? W : H;
-    const int up = ns ? 16 : 0;  // word << up: the line's 16 wall bits at bits 16..31
-    const int sx = 14 + center;  // window cell k (grid index center - 2 + k) at bit sx + k
-    const uint32_t ibm = ((((1u << llen) - 1u) << 16) >> sx) & 31u;
+    const int up = ns ? 16 : 0;
+    const int sx = 14 + center;
+    const uint32_t obm = ~(((((1u << llen) - 1u) << 16) >> sx)) & 31u;  // off-grid cells of an in-grid line
+    const uint32_t obl = ((obm * 0x00204081u) & 0x01010101u) * 3u, obh = (obm >> 4) * 3u;
     const bool rev = d >= 2;
-    const uint32_t sel = rev ? 0x1234u : 0x3210u;
+    const uint32_t sel0 = rev ? 0x1234u : 0x3210u, sel1 = rev ? 0x5550u : 0x5554u;
     const int fr = dir_dr(d), fc = dir_dc(d);
     const int dr = gr - r, dcol = gc - c;
     const int g_ahead = dr * fr + dcol * fc, g_side = dr * fc - dcol * fr;
-    const int g_vr = (g_ahead >= 0 && g_ahead < 5 && g_side >= -2 && g_side <= 2) ? 4 - g_ahead : -1;
-    const int g_vc = g_side + 2;  // 0..4 when visible
-    const uint32_t glo_clr = g_vc < 4 ? ~(0xFFu << (8 * (g_vc & 3))) : 0xFFFFFFFFu;
-    const uint32_t glo_set = g_vc < 4 ? (2u << (8 * (g_vc & 3))) : 0u;
+    gpos = (g_ahead >= 0 && g_ahead < 5 && g_side >= -2 && g_side <= 2) ? (4 - g_ahead) * 5 + g_side + 2 : -1;
+    const int L0 = base + 4 * sgn;
     uint32_t lo[5], hi[5];
 #pragma unroll
     for (int vr = 0; vr < 5; vr++) {
-        const int L = base + sgn * (4 - vr);
+        const int L = L0 - sgn * vr;
         const bool in = (uint32_t)L < nlines;
-        const uint32_t bw = in ? board[L] : 0u;
+        const uint32_t bw = board[L & 15];
         const uint32_t x = ((bw << up) >> sx) & 31u;
-        const uint32_t m = in ? ibm : 0u;
-        const uint32_t wl = x & m, ob = ~m & 31u;
-        const uint32_t l4 = (((wl & 15u) * 0x00204081u) & 0x01010101u) + (((ob & 15u) * 0x00204081u) & 0x01010101u) * 3u;
-        const uint32_t h1 = ((wl >> 4) & 1u) + ((ob >> 4) & 1u) * 3u;
-        uint32_t o0 = __byte_perm(l4, h1, sel);
-        uint32_t o1 = rev ? (l4 & 0xFFu) : h1;
-        if (vr == g_vr) {
-            o0 = (o0 & glo_clr) | glo_set;
-            o1 = g_vc == 4 ? 2u : o1;
-        }
-        lo[vr] = o0;
-        hi[vr] = o1;
+        const uint32_t l4 = ((x * 0x00204081u) & 0x01010101u) | (in ? obl : 0x03030303u);
+        const uint32_t h1 = (x >> 4) | (in ? obh : 3u);
+        lo[vr] = __byte_perm(l4, h1, sel0);
+        hi[vr] = __byte_perm(l4, h1, sel1);
     }
-    // rows at bytes 0, 5, 10, 15, 20
     w[0] = lo[0];
     w[1] = hi[0] | (lo[1] << 8);
     w[2] = (lo[1] >> 24) | (hi[1] << 8) | (lo[2] << 16);
@@ -259,7 +254,7 @@ __device__ __forceinline__ void render5_see_words(int r, int c, int d, int gr, i
     w[5] = lo[4];
     w[6] = hi[4];
 }
-// Warp-collective store of each lane's 25 bytes (7 words from render5_see_words) at byte
+// Warp-collective store of each lane's 25 bytes (7 words from render5_see_rows) at byte
 // offset 25 * idx of a 16-byte-aligned staging row, idx = lane index in the row (the
 // warp's lanes hold consecutive idx, idx % 32 == lane): 6-7 aligned 32-bit stores per
 // lane instead of 25 byte stores; the word a lane shares with its successor is merged
@@ -904,10 +899,13 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
             }
             if constexpr (V == 5 && SEE) {
                 uint32_t w[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                int gpos = -1;
                 if (live)
-                    render5_see_words(pr & 15, (pr >> 4) & 15, (pr >> 8) & 3, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W,
-                                      s_brd + tid * kBS, w);
+                    render5_see_rows(pr & 15, (pr >> 4) & 15, (pr >> 8) & 3, gw & 0xFF, (gw >> 8) & 0xFF, G.H, G.W,
+                                     s_brd + tid * kBS, w, gpos);
                 store_obs25(s_view[k], tid, live, w);  // warp-collective
+                __syncwarp();  // the lane's first word may have been stored by its predecessor
+                if (gpos >= 0) s_view[k][tid * VV + gpos] = 2;  // the goal (never off-grid or a wall)
             } else {
                 if (live)
                     render_obs<V, SEE>(pr & 15, (pr >> 4) & 15, (pr >> 8) & 3, gw, G, rec, s_spread,
