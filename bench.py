@@ -47,7 +47,7 @@ ENV_BYTES_PER_STEP = 36  # action u8 + view 25 u8 + dir u8 + reward f64 + done u
 GAE_BYTES_PER_ELEM = 33  # r f64 + V f64 + done u8 in, A f64 + R f64 out
 
 
-PROFILE_ROUND = "r2h"  # the committed capture (tools/profile_round.sh + tools/summarize_round.py)
+PROFILE_ROUND = "r2x"  # the committed capture (tools/profile_round.sh + tools/summarize_round.py)
 
 
 def _traffic():
