@@ -155,9 +155,10 @@ class ParallelPLR:
             side.wait_stream(cur)
             self.buffer.prepare(levels, stream=side)
         start = self.env.reset_to_levels(self.root.fold_in(it).fold_in(4), levels, self.p)
-        traj, _ = rollout_actions(self.env, start, actions, self.p, out=out)
+        tout, gout = self._iteration_outputs(actions.shape[0], out)
+        traj, _ = rollout_actions(self.env, start, actions, self.p, out=tout)
         o = gae_and_scores(traj.rewards, values, traj.dones, last_values, self.gamma, self.lam, prior,
-                           self.cfg.score_fn, self.cfg.maxmc_discounted)
+                           self.cfg.score_fn, self.cfg.maxmc_discounted, out=gout)
         g_levels, g_scores, g_max = dist.gather_candidates(levels, o["scores"], o["max_returns"])
         if side is not None:
             torch.cuda.current_stream(self.device).wait_stream(side)
@@ -167,6 +168,29 @@ class ParallelPLR:
         if self.world > 1 and self.check_every > 0 and self.iterations % self.check_every == 0:
             self.check_replicas()
         return IterationResult(levels, o["scores"], o["max_returns"], n_replay, traj, o["advantages"])
+
+    def _iteration_outputs(self, T: int, out):
+        """Trajectory and GAE result tensors of this iteration: two persistent sets used in
+        turn (like the lane arrays of _compose_local, an IterationResult stays valid
+        through the next iteration), so an iteration allocates nothing; a caller's
+        ``out`` (rollout tensors) takes precedence."""
+        torch = _torch()
+        n, dev, v = self.hi - self.lo, self.device, self.p.agent_view_size
+        if getattr(self, "_out_T", None) != T:
+            self._out_T = T
+            self._out_sets = [({"view": torch.empty((T, n, v, v), dtype=torch.uint8, device=dev),
+                                "dir": torch.empty((T, n), dtype=torch.uint8, device=dev),
+                                "rewards": torch.empty((T, n), dtype=torch.float64, device=dev),
+                                "dones": torch.empty((T, n), dtype=torch.bool, device=dev),
+                                "final_view": torch.empty((n, v, v), dtype=torch.uint8, device=dev),
+                                "final_dir": torch.empty((n,), dtype=torch.uint8, device=dev)},
+                               {"advantages": torch.empty((T, n), dtype=torch.float64, device=dev),
+                                "returns": torch.empty((T, n), dtype=torch.float64, device=dev),
+                                "scores": torch.empty((n,), dtype=torch.float64, device=dev),
+                                "max_returns": torch.empty((n,), dtype=torch.float64, device=dev)})
+                              for _ in range(2)]
+        tout, gout = self._out_sets[self.iterations & 1]
+        return (out if out is not None else tout), gout
 
     def check_replicas(self) -> None:
         """Drift check now: every rank's buffer digest must agree (RunnerFault if not)."""
