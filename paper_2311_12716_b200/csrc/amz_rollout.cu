@@ -28,7 +28,7 @@
 #include "amz_sampler.cuh"
 
 #ifndef AMZ_DYN8_MINB
-#define AMZ_DYN8_MINB 3
+#define AMZ_DYN8_MINB 4
 #endif
 #ifndef AMZ_DYN8_TRACK
 #define AMZ_DYN8_TRACK false
@@ -321,10 +321,16 @@ __device__ __forceinline__ unsigned smid_() {
     } while (0)
 #endif
 
+// move-table rows per lane: 5 (the 4 headings + an identity row, so a turn is the same
+// byte load as a move: the shortest chain, for the latency-bound small batches) or 4
+// (LPW >= 8: a turn selects the old position instead -- 8 KB less shared memory per
+// CTA, which with <= 128 registers gives the many-wave large batch a 4th resident CTA)
+template <int LPW>
+constexpr int kMtRows = LPW >= 8 ? 4 : 5;
 template <int LPW>
 struct DynSmem {
     uint32_t board[16][LPW];
-    uint8_t mt[LPW][5][256];  // move table: position after a step, [heading or 4 = no move][pos]
+    uint8_t mt[LPW][kMtRows<LPW>][256];  // move table: position after a step, [heading (or 4 = no move)][pos]
     uint8_t act[2][ACH][LPW];
     uint32_t aw[LPW][ACH / 4 + 2];  // this chunk's actions per lane, 4 steps per word (+2 zero pad)
     uint32_t rec[LPW][ACH + 8];     // this chunk's step records per lane (+8: a batch stores all 8)
@@ -356,7 +362,7 @@ __device__ __forceinline__ void build_move_table(const uint32_t *board, int L, u
         cp[h] = col(c0 + 8 * h + 1);
     }
 #pragma unroll
-    for (int k = 0; k < 10; k++) {
+    for (int k = 0; k < 2 * kMtRows<LPW>; k++) {
         const int e = k >> 1, h = k & 1, c = c0 + 8 * h;
         const uint32_t base4 = (uint32_t)(r0 | (c << 4)) * 0x01010101u + 0x03020100u;
         uint32_t out = base4;
@@ -386,7 +392,8 @@ __device__ __forceinline__ void build_move_table(const uint32_t *board, int L, u
 }
 
 // resident CTAs per SM the register budget is sized for: the large-batch instantiation
-// (LPW 8) runs many waves, so it trades registers for a third resident CTA
+// (LPW 8) runs many waves, so it trades registers for a 4th resident CTA (128 registers,
+// no spills; with the 4-row move table its CTA fits 4 per SM in shared memory too)
 template <int LPW>
 struct DynOcc {
     static constexpr int kMinBlocks = LPW >= 8 ? AMZ_DYN8_MINB : (LPW <= 2 ? AMZ_DYN2_MINB : 1);
@@ -612,7 +619,12 @@ __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G
                 const uint32_t e = (ew[k >> 2] >> (8 * (k & 3))) & 0xFFu;
                 const uint32_t db = (dw[k >> 2] >> (8 * (k & 3))) & 0x3u;
                 rec[k] = pos | (db << 8) | hi;
-                pos = mtl[e * 256u + pos];
+                if constexpr (kMtRows<LPW> == 5) {
+                    pos = mtl[e * 256u + pos];
+                } else {
+                    const uint32_t np = mtl[(e & 3u) * 256u + pos];
+                    pos = e < 4u ? np : pos;
+                }
                 pkw[k >> 2] |= pos << (8 * (k & 3));
                 ev |= (unsigned)(pos == g) << k;
             }
@@ -814,7 +826,9 @@ template <int LPW, int WPC>
 static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *actions, int mode, const amz_seed_t &wrap,
                        uint32_t step0, double *reward, uint8_t *done, uint32_t *poses, uint32_t *epochs,
                        uint32_t *final_pose, amz_level_t *spec, uint32_t *spec_step, int spec_ready, cudaStream_t s) {
-    const int use_lut = G.tep <= 4096;
+    // the goal-reward table: small batches only (LPW >= 8 spends the shared memory on a
+    // 4th resident CTA; a goal reach is rare, its one division is off the step chain)
+    const int use_lut = G.tep <= 4096 && LPW < 8;
     const size_t sm = (size_t)WPC * sizeof(DynSmem<LPW>) + (use_lut ? ((size_t)G.tep + 1) * 8 : 0);
     ensure_dyn_smem((const void *)k_dyn<LPW, WPC>, (int)sm);
     const int avec = (E.B % 4 == 0) && ((((uintptr_t)actions) & 3u) == 0);
