@@ -70,6 +70,8 @@ struct EnvDev {
     // prefixes passed in are the ROOT stream's, and the kernels derive the iteration's
     // streams root.fold_in(*iter).fold_in(0) (lane levels) and .fold_in(1) (auto-reset)
     const uint32_t *iter = nullptr;
+    // work counter of the persistent large-batch dynamics (zeroed before each launch)
+    uint32_t *work = nullptr;
 };
 
 // numpy pairwise summation schedule (numpy/_core/src/umath/loops_utils.h.src

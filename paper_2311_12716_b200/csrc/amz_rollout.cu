@@ -400,6 +400,10 @@ struct DynOcc {
     // sampler variant: element tracking (lowest latency) where the per-warp chain bounds
     // the rollout; swap-list read-off (fewest instructions) in the many-wave large batch
     static constexpr bool kTrack = LPW >= 8 ? AMZ_DYN8_TRACK : true;
+    // persistent warps over a lane-group queue (the many-wave large batch): a warp takes
+    // the next group as soon as it finishes one, instead of a CTA holding its slot until
+    // its slowest warp is done (achieved occupancy 18% of the 25% resident at 65536 lanes)
+    static constexpr bool kPersist = LPW >= 8;
 };
 template <int LPW, int WPC>
 __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G, EnvDev E, int T, const uint8_t *__restrict__ actions, int mode,
@@ -424,9 +428,11 @@ __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G
         seed_absorb(wrap, 1u);
     }
     const int64_t B = E.B;
+    const int64_t ngroups = (B + LPW - 1) / LPW;
+    int64_t grp = (int64_t)blockIdx.x * WPC + warp;  // first group static, then the queue
+    for (; grp < ngroups;) {
     DYN_MARK(0);
-    const int64_t lane0 = ((int64_t)blockIdx.x * WPC + warp) * LPW;
-    if (lane0 >= B) return;
+    const int64_t lane0 = grp * LPW;
     const int64_t l = lane0 + lane;
     const bool live = lane < LPW && l < B;
     const int nv = (int)((B - lane0) < LPW ? (B - lane0) : LPW);
@@ -680,6 +686,12 @@ __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G
         }
     }
     DYN_MARK(3);
+    if (!DynOcc<LPW>::kPersist) break;
+    __syncwarp();  // every lane is done with the group's shared state
+    unsigned nxt = 0;
+    if (lane == 0) nxt = atomicAdd(E.work, 1u);
+    grp = (int64_t)gridDim.x * WPC + __shfl_sync(0xFFFFFFFFu, nxt, 0);
+    }
 }
 
 #ifdef AMZ_DYN_PROF
@@ -836,7 +848,17 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
         k_spec_levels<<<(unsigned)((E.B + 4 * kSpecLPW - 1) / (4 * kSpecLPW)), 128, 0, s>>>(G, E, T, wrap, step0, spec,
                                                                                            spec_step);
     const int64_t warps = (E.B + LPW - 1) / LPW;
-    launch_pdl(k_dyn<LPW, WPC>, dim3((unsigned)((warps + WPC - 1) / WPC)), dim3(32 * WPC), sm, s, G, E, T, actions,
+    int64_t ctas = (warps + WPC - 1) / WPC;
+    if (DynOcc<LPW>::kPersist) {  // one resident wave, the rest from the queue
+        static int nsm[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !nsm[dev]) cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev);
+        const int64_t wave = (int64_t)(dev >= 0 && dev < 64 && nsm[dev] ? nsm[dev] : 148) * DynOcc<LPW>::kMinBlocks;
+        if (ctas > wave) ctas = wave;
+        cudaMemsetAsync(E.work, 0, sizeof(uint32_t), s);
+    }
+    launch_pdl(k_dyn<LPW, WPC>, dim3((unsigned)ctas), dim3(32 * WPC), sm, s, G, E, T, actions,
                mode, wrap, step0, reward, done, poses, epochs, final_pose, (const amz_level_t *)spec,
                (const uint32_t *)spec_step, avec, use_lut);
 }
