@@ -419,6 +419,7 @@ int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->spec, b * sizeof(amz_level_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->spec_step, b * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.work, sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.gdone, ((b + 127) / 128) * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMemset(e->E.err, 0, 4 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->term, 0, 2 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->E.st, 0, b * sizeof(uint4));
@@ -443,6 +444,7 @@ int amz_env_destroy(amz_env_t *e) {
     cudaFree(e->spec);
     cudaFree(e->spec_step);
     cudaFree(e->E.work);
+    cudaFree(e->E.gdone);
     cudaFree(e->poses);
     cudaFree(e->epochs);
     delete e;

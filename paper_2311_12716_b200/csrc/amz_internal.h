@@ -72,6 +72,9 @@ struct EnvDev {
     const uint32_t *iter = nullptr;
     // work counter of the persistent large-batch dynamics (zeroed before each launch)
     uint32_t *work = nullptr;
+    // finished k_dyn warps per 128-lane group [ceil(B / 128)] (zeroed before each launch):
+    // the render takes a group's tiles once its warps are done, beside k_dyn's tail
+    uint32_t *gdone = nullptr;
 };
 
 // numpy pairwise summation schedule (numpy/_core/src/umath/loops_utils.h.src

@@ -427,6 +427,9 @@ __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G
         seed_absorb(wrap, *E.iter);
         seed_absorb(wrap, 1u);
     }
+    // the render may launch now: everything before this grid is complete (pdl_wait), every
+    // CTA of it is resident, and the render waits per lane group (E.gdone)
+    if (E.gdone) pdl_trigger();
     const int64_t B = E.B;
     const int64_t ngroups = (B + LPW - 1) / LPW;
     int64_t grp = (int64_t)blockIdx.x * WPC + warp;  // first group static, then the queue
@@ -686,6 +689,11 @@ __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G
         }
     }
     DYN_MARK(3);
+    if (E.gdone) {  // publish: this warp's poses, epoch records, final poses and lane state
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(E.gdone + (lane0 >> 7), 1u);
+    }
     if (!DynOcc<LPW>::kPersist) break;
     __syncwarp();  // every lane is done with the group's shared state
     unsigned nxt = 0;
@@ -858,6 +866,7 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
         if (ctas > wave) ctas = wave;
         cudaMemsetAsync(E.work, 0, sizeof(uint32_t), s);
     }
+    if (E.gdone) cudaMemsetAsync(E.gdone, 0, ((E.B + 127) / 128) * sizeof(uint32_t), s);
     launch_pdl(k_dyn<LPW, WPC>, dim3((unsigned)ctas), dim3(32 * WPC), sm, s, G, E, T, actions,
                mode, wrap, step0, reward, done, poses, epochs, final_pose, (const amz_level_t *)spec,
                (const uint32_t *)spec_step, avec, use_lut);
@@ -882,7 +891,8 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
                                                   const uint32_t *__restrict__ epochs, uint8_t *__restrict__ view,
                                                   uint8_t *__restrict__ dirs, double *__restrict__ reward,
                                                   uint8_t *__restrict__ done, uint8_t *__restrict__ fview,
-                                                  uint8_t *__restrict__ fdir, int bulk_ok, int64_t ng, int64_t nq) {
+                                                  uint8_t *__restrict__ fdir, int bulk_ok, int64_t ng, int64_t nq,
+                                                  const uint32_t *gdone, int lpw) {
     constexpr int VV = V * V;
     __shared__ __align__(128) uint8_t s_view[4][128 * VV];
     __shared__ __align__(16) uint8_t s_dir[4][128];
@@ -902,8 +912,28 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
     const bool live = l < B;
     const int nvalid = (int)((B - g * 128) < 128 ? (B - g * 128) : 128);
     const int nsteps = fin ? 1 : ((T - 4 * (int)q) < 4 ? (T - 4 * (int)q) : 4);
-    __syncthreads();
-    pdl_wait();  // poses / epochs from k_dyn
+    if (gdone) {
+        // this tile's lane group: all of its k_dyn warps have published (launched early by
+        // k_dyn's trigger, so the wait overlaps the dynamics' tail).  Bounded: a lost
+        // count leaves wrong outputs after ~4 s instead of a hung GPU
+        if (tid == 0) {
+            const uint32_t want = (uint32_t)((nvalid + lpw - 1) / lpw);
+            uint64_t t0 = 0, now = 0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            for (;;) {
+                uint32_t got;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(gdone + g) : "memory");
+                if (got >= want) break;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (now - t0 > 4000000000ull) break;
+                __nanosleep(200);
+            }
+        }
+        __syncthreads();
+    } else {
+        __syncthreads();
+        pdl_wait();  // poses / epochs from k_dyn
+    }
     uint4 pq = make_uint4(0u, 0u, 0u, 0u);
     if (live) pq = fin ? make_uint4(final_pose[l], 0u, 0u, 0u) : reinterpret_cast<const uint4 *>(poses)[q * B + l];
     uint32_t ep = 0xFFFFFFFFu, gw = 0u;
@@ -979,7 +1009,7 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
 template <int V, bool SEE>
 static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *poses, const uint32_t *final_pose,
                           const uint32_t *epochs, uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done,
-                          uint8_t *fview, uint8_t *fdir, cudaStream_t s) {
+                          uint8_t *fview, uint8_t *fdir, const uint32_t *gdone, int lpw, cudaStream_t s) {
     auto al16 = [](const void *p) { return p == nullptr || (((uintptr_t)p) & 15u) == 0; };
     static const int legacy = getenv("AMZ_RENDER_LEGACY") ? atoi(getenv("AMZ_RENDER_LEGACY")) : 0;
     if (!legacy) {
@@ -988,7 +1018,7 @@ static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *po
         const int64_t ng = (B + 127) / 128, nq = (T + 3) / 4;
         const int64_t nt = nq * ng + (fview ? ng : 0);
         launch_pdl(k_render_q<V, SEE>, dim3((unsigned)nt), dim3(128), 0, s, G, B, T, poses, final_pose, epochs, view,
-                   dirs, reward, done, fview, fdir, bulk, ng, nq);
+                   dirs, reward, done, fview, fdir, bulk, ng, nq, gdone, lpw);
         return;
     }
     const int bulk = al16(view) && al16(dirs) && al16(done) && al16(fview) && al16(fdir);
@@ -1008,6 +1038,7 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
     // every resample of any of its lanes, so small warps finish sooner.  AMZ_DYN_LPW
     // (4, 8, 16) overrides the choice for tuning runs (tools/dyn_lpw.sh).
     static const int forced = getenv("AMZ_DYN_LPW") ? atoi(getenv("AMZ_DYN_LPW")) : 0;
+    const int lpw = (forced == 2 || forced == 8 || forced == 16) ? forced : (E.B <= 148 * 8 * 16 ? 4 : 8);
     if (forced == 2)
         launch_dyn<2, 4>(G, E, T, actions, mode, wrap, step0, reward, done, poses, epochs, final_pose, spec, spec_step, spec_ready, s);
     else if (forced == 8)
@@ -1025,10 +1056,10 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
     case VV_:                                                                                               \
         if (G.see)                                                                                          \
             launch_render<VV_, true>(G, E.B, n, poses, final_pose, epochs, view, dirs, reward, done, fview, \
-                                     fdir, s);                                                              \
+                                     fdir, E.gdone, lpw, s);                                                \
         else                                                                                                \
             launch_render<VV_, false>(G, E.B, n, poses, final_pose, epochs, view, dirs, reward, done, fview, \
-                                      fdir, s);                                                             \
+                                      fdir, E.gdone, lpw, s);                                               \
         return 0;
     switch (G.V) {
         AMZ_RR(3)
