@@ -420,6 +420,9 @@ int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->spec_step, b * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.work, sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.gdone, ((b + 127) / 128) * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.gpass, ((b + 127) / 128) * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMemset(e->E.gdone, 0, ((b + 127) / 128) * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMemset(e->E.gpass, 0, ((b + 127) / 128) * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMemset(e->E.err, 0, 4 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->term, 0, 2 * sizeof(int));
     if (err == cudaSuccess) err = cudaMemset(e->E.st, 0, b * sizeof(uint4));
@@ -445,6 +448,7 @@ int amz_env_destroy(amz_env_t *e) {
     cudaFree(e->spec_step);
     cudaFree(e->E.work);
     cudaFree(e->E.gdone);
+    cudaFree(e->E.gpass);
     cudaFree(e->poses);
     cudaFree(e->epochs);
     delete e;

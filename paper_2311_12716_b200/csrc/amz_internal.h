@@ -75,6 +75,9 @@ struct EnvDev {
     // finished k_dyn warps per 128-lane group [ceil(B / 128)] (zeroed before each launch):
     // the render takes a group's tiles once its warps are done, beside k_dyn's tail
     uint32_t *gdone = nullptr;
+    // render tiles past their wait per group [ceil(B / 128)]: the last one re-zeroes both
+    // counters for the next rollout (no memset between the reset and k_dyn)
+    uint32_t *gpass = nullptr;
 };
 
 // numpy pairwise summation schedule (numpy/_core/src/umath/loops_utils.h.src

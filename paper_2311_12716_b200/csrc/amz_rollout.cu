@@ -866,7 +866,7 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
         if (ctas > wave) ctas = wave;
         cudaMemsetAsync(E.work, 0, sizeof(uint32_t), s);
     }
-    if (E.gdone) cudaMemsetAsync(E.gdone, 0, ((E.B + 127) / 128) * sizeof(uint32_t), s);
+
     launch_pdl(k_dyn<LPW, WPC>, dim3((unsigned)ctas), dim3(32 * WPC), sm, s, G, E, T, actions,
                mode, wrap, step0, reward, done, poses, epochs, final_pose, (const amz_level_t *)spec,
                (const uint32_t *)spec_step, avec, use_lut);
@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
                                                   uint8_t *__restrict__ dirs, double *__restrict__ reward,
                                                   uint8_t *__restrict__ done, uint8_t *__restrict__ fview,
                                                   uint8_t *__restrict__ fdir, int bulk_ok, int64_t ng, int64_t nq,
-                                                  const uint32_t *gdone, int lpw) {
+                                                  uint32_t *gdone, uint32_t *gpass, int lpw) {
     constexpr int VV = V * V;
     __shared__ __align__(128) uint8_t s_view[4][128 * VV];
     __shared__ __align__(16) uint8_t s_dir[4][128];
@@ -927,6 +927,14 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
                 if (now - t0 > 4000000000ull) break;
                 __nanosleep(200);
+            }
+            // the group's last tile past its wait zeroes the counters for the next rollout
+            // (every tile of this launch has read gdone[g] by then; the next k_dyn runs
+            // after this grid completes)
+            const uint32_t tiles = (uint32_t)(nq + (fview ? 1 : 0));
+            if (atomicAdd(gpass + g, 1u) == tiles - 1u) {
+                gdone[g] = 0u;
+                gpass[g] = 0u;
             }
         }
         __syncthreads();
@@ -1009,7 +1017,7 @@ __global__ void __launch_bounds__(128) k_render_q(Geo G, int64_t B, int T, const
 template <int V, bool SEE>
 static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *poses, const uint32_t *final_pose,
                           const uint32_t *epochs, uint8_t *view, uint8_t *dirs, double *reward, uint8_t *done,
-                          uint8_t *fview, uint8_t *fdir, const uint32_t *gdone, int lpw, cudaStream_t s) {
+                          uint8_t *fview, uint8_t *fdir, uint32_t *gdone, uint32_t *gpass, int lpw, cudaStream_t s) {
     auto al16 = [](const void *p) { return p == nullptr || (((uintptr_t)p) & 15u) == 0; };
     static const int legacy = getenv("AMZ_RENDER_LEGACY") ? atoi(getenv("AMZ_RENDER_LEGACY")) : 0;
     if (!legacy) {
@@ -1018,7 +1026,7 @@ static void launch_render(const Geo &G, int64_t B, int64_t n, const uint32_t *po
         const int64_t ng = (B + 127) / 128, nq = (T + 3) / 4;
         const int64_t nt = nq * ng + (fview ? ng : 0);
         launch_pdl(k_render_q<V, SEE>, dim3((unsigned)nt), dim3(128), 0, s, G, B, T, poses, final_pose, epochs, view,
-                   dirs, reward, done, fview, fdir, bulk, ng, nq, gdone, lpw);
+                   dirs, reward, done, fview, fdir, bulk, ng, nq, gdone, gpass, lpw);
         return;
     }
     const int bulk = al16(view) && al16(dirs) && al16(done) && al16(fview) && al16(fdir);
@@ -1056,10 +1064,10 @@ int launch_env_rollout(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
     case VV_:                                                                                               \
         if (G.see)                                                                                          \
             launch_render<VV_, true>(G, E.B, n, poses, final_pose, epochs, view, dirs, reward, done, fview, \
-                                     fdir, E.gdone, lpw, s);                                                \
+                                     fdir, E.gdone, E.gpass, lpw, s);                                                \
         else                                                                                                \
             launch_render<VV_, false>(G, E.B, n, poses, final_pose, epochs, view, dirs, reward, done, fview, \
-                                      fdir, E.gdone, lpw, s);                                               \
+                                      fdir, E.gdone, E.gpass, lpw, s);                                               \
         return 0;
     switch (G.V) {
         AMZ_RR(3)
