@@ -421,6 +421,7 @@ int amz_env_create(const amz_params_t *p, int64_t n_lanes, amz_env_t **out) {
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.work, sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.gdone, ((b + 127) / 128) * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMalloc((void **)&e->E.gpass, ((b + 127) / 128) * sizeof(uint32_t));
+    if (err == cudaSuccess) err = cudaMemset(e->E.work, 0, sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMemset(e->E.gdone, 0, ((b + 127) / 128) * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMemset(e->E.gpass, 0, ((b + 127) / 128) * sizeof(uint32_t));
     if (err == cudaSuccess) err = cudaMemset(e->E.err, 0, 4 * sizeof(int));

@@ -70,7 +70,7 @@ struct EnvDev {
     // prefixes passed in are the ROOT stream's, and the kernels derive the iteration's
     // streams root.fold_in(*iter).fold_in(0) (lane levels) and .fold_in(1) (auto-reset)
     const uint32_t *iter = nullptr;
-    // work counter of the persistent large-batch dynamics (zeroed before each launch)
+    // work counter of the persistent large-batch dynamics (the launch's last fetch re-zeroes it)
     uint32_t *work = nullptr;
     // finished k_dyn warps per 128-lane group [ceil(B / 128)] (zeroed before each launch):
     // the render takes a group's tiles once its warps are done, beside k_dyn's tail

@@ -400,7 +400,8 @@ struct DynOcc {
     // sampler variant: element tracking (lowest latency) where the per-warp chain bounds
     // the rollout; swap-list read-off (fewest instructions) in the many-wave large batch
     static constexpr bool kTrack = LPW >= 8 ? AMZ_DYN8_TRACK : true;
-    // persistent warps over a lane-group queue (the many-wave large batch): a warp takes
+    // persistent warps over a lane-group queue (the many-wave large batch; E.work, zero
+    // between launches): a warp takes
     // the next group as soon as it finishes one, instead of a CTA holding its slot until
     // its slowest warp is done (achieved occupancy 18% of the 25% resident at 65536 lanes)
     static constexpr bool kPersist = LPW >= 8;
@@ -697,7 +698,12 @@ __global__ void __launch_bounds__(32 * WPC, DynOcc<LPW>::kMinBlocks) k_dyn(Geo G
     if (!DynOcc<LPW>::kPersist) break;
     __syncwarp();  // every lane is done with the group's shared state
     unsigned nxt = 0;
-    if (lane == 0) nxt = atomicAdd(E.work, 1u);
+    if (lane == 0) {
+        nxt = atomicAdd(E.work, 1u);
+        // every warp's last fetch fails, so a launch makes exactly ngroups fetches: the
+        // one that returns ngroups - 1 is the last and re-zeroes the queue for the next
+        if ((int64_t)nxt == ngroups - 1) *E.work = 0u;
+    }
     grp = (int64_t)gridDim.x * WPC + __shfl_sync(0xFFFFFFFFu, nxt, 0);
     }
 }
@@ -864,7 +870,6 @@ static void launch_dyn(const Geo &G, const EnvDev &E, int T, const uint8_t *acti
         if (dev >= 0 && dev < 64 && !nsm[dev]) cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev);
         const int64_t wave = (int64_t)(dev >= 0 && dev < 64 && nsm[dev] ? nsm[dev] : 148) * DynOcc<LPW>::kMinBlocks;
         if (ctas > wave) ctas = wave;
-        cudaMemsetAsync(E.work, 0, sizeof(uint32_t), s);
     }
 
     launch_pdl(k_dyn<LPW, WPC>, dim3((unsigned)ctas), dim3(32 * WPC), sm, s, G, E, T, actions,
