@@ -107,3 +107,24 @@ def test_config5_parallel_plr_32768_lanes():
         assert np.array_equal(st["seq"][:size].cpu().numpy(), ref.seq[:size])
         assert np.array_equal(st["last_sampled"][:size].cpu().numpy(), ref.last_sampled[:size])
         assert np.array_equal(tensor_rows(st["levels"][:size]), records_to_rows(ref.levels[:size]))
+
+
+@pytest.mark.parametrize("B", [512, 20000])
+def test_successive_rollouts_reuse_the_env_counters(B):
+    """One env, several reset + rollout rounds of different lengths: the render's per-group
+    counters and (B > 18944) the persistent dynamics' work queue re-zero themselves between
+    launches, so every round equals the oracle."""
+    p = amz.StaticParams()
+    env = amz.AutoResetWrapper(amz.VectorBatchEnv(amz.MazeEnv(), amz.BatchShape(1, 1, B)), amz.RESAMPLE)
+    for rnd, T in enumerate((37, 256, 5, 100)):
+        seed = 40 + rnd
+        res = env.reset(amz.RngStream.from_seed(seed), p)
+        rng = np.random.default_rng(seed)
+        acts = rng.integers(0, 3, (T, B)).astype(np.uint8)
+        vals = rng.uniform(0, 1, (T, B))
+        last = rng.uniform(0, 1, B)
+        tr, cur = amz.rollout_actions(env, res, torch.from_numpy(acts).cuda(), p)
+        o = amz.gae_and_scores(tr.rewards, torch.from_numpy(vals).cuda(), tr.dones, torch.from_numpy(last).cuda(),
+                               GAMMA, LAM)
+        for lo, hi in ((0, 160), (B - 160, B)):
+            _check_window(seed, acts, vals, last, tr, cur, o, lo, hi)
